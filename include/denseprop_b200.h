@@ -1,0 +1,163 @@
+/*
+ * denseprop_b200.h -- C ABI of the B200-native dense whole-image propagation
+ * kernels (arXiv 1412.4526).  Library: paper_1412_4526_b200/libdenseprop_b200.so
+ * (sm_100a, built by `python -m paper_1412_4526_b200.build` or
+ * __graft_entry__.build()).
+ *
+ * Replaces the reference's single plugin boundary, `backend.kernels()`
+ * (pkg/src/denseprop/backend.py:47-48), whose modules export 7 functions
+ * (pkg/src/denseprop/_kernels.pyx:23-247, _kernels_py.py:19-126).  Each of
+ * those gets two entry points here:
+ *
+ *   dp_host_<name>  -- drop-in form: HOST pointers, one (C,H,W) map, the
+ *                      reference's argument meaning; synchronous.  This is what
+ *                      a ctypes/cffi backend module binds.
+ *   dp_<name>       -- device form: DEVICE pointers, a batch of n maps laid
+ *                      out (n, C, H, W) C-contiguous, enqueued on `stream`
+ *                      (a cudaStream_t; NULL = legacy default stream), with
+ *                      fused nonlinearity / gate / mask options.  The batched
+ *                      executor and the data-parallel trainer call these.
+ *
+ * Conventions
+ *  - dtype: DP_F32 or DP_F64; every float argument of a call has that type
+ *    (reference fused `floating` type, _kernels.pyx:18-20).  argmax maps are
+ *    int32 at the host API (value i*p + j, _kernels.pyx:143,165); device calls
+ *    may use 1-byte argmax (arg_bytes = 1) when p*p <= 256.
+ *  - dilation d >= 1, kernel / pool size >= 1; extent e = (k-1)*d + 1.
+ *  - Return value: DP_OK (0) or an error code; dp_last_error() (thread-local)
+ *    describes the last failure.  Bad shapes / arguments give DP_ERR_ARG and
+ *    leave outputs untouched (reference wrappers raise ValueError before
+ *    dispatch: forward.py:33-38, backward.py:136-146).
+ *  - Exactness: conv forward, conv data-gradient, both pools and relu are
+ *    bit-identical to the reference's compiled backend in fp32 and fp64 (same
+ *    per-entry operation order, no FMA contraction); tanh is within 1 ulp of
+ *    numpy; weight/bias gradients are deterministic (fixed-order split
+ *    reduction) and agree to reduction-order rounding.
+ */
+#ifndef DENSEPROP_B200_H
+#define DENSEPROP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP_ABI_VERSION 1
+
+enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
+/* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
+enum dp_nonlin { DP_IDENTITY = 0, DP_TANH = 1, DP_RELU = 2 };
+enum dp_status { DP_OK = 0, DP_ERR_ARG = 1, DP_ERR_CUDA = 2, DP_ERR_UNSUPPORTED = 3 };
+
+const char *dp_last_error(void);
+int dp_abi_version(void);
+/* number of visible CUDA devices, or -1 if the runtime cannot be initialised */
+int dp_device_count(void);
+
+/* ======================= host-pointer drop-in entry points =======================
+ * One feature map (C, H, W), C-contiguous, caller-owned input and output
+ * buffers (outputs are written, never read).  Synchronous.
+ */
+
+/* replaces conv_forward(x, w, b, dilation, threads)  -- _kernels.pyx:23-53
+ * x (cin,h,w), wt (cout,cin,k,k), b (cout) -> y (cout, h-e+1, w-e+1) */
+int dp_host_conv_forward(int dtype, const void *x, const void *wt, const void *b, void *y,
+                         int cin, int h, int w, int cout, int k, int d);
+
+/* replaces conv_backward_data(dy, w, dilation, threads) -- _kernels.pyx:56-91
+ * dy (cout,ho,wo), wt (cout,cin,k,k) -> dx (cin, ho+e-1, wo+e-1) */
+int dp_host_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx,
+                               int cout, int ho, int wo, int cin, int k, int d);
+
+/* replaces conv_backward_kernel(x, dy, kernel_size, dilation, threads) -- _kernels.pyx:94-130
+ * x (cin,hi,wi), dy (cout,hi-e+1,wi-e+1) -> dw (cout,cin,k,k), db (cout) */
+int dp_host_conv_backward_kernel(int dtype, const void *x, const void *dy, void *dw, void *db,
+                                 int cin, int hi, int wi, int cout, int k, int d);
+
+/* replaces maxpool_forward(x, p, dilation, threads) -- _kernels.pyx:133-166
+ * x (c,h,w) -> y (c,ho,wo), arg int32 (c,ho,wo) */
+int dp_host_maxpool_forward(int dtype, const void *x, void *y, int32_t *arg,
+                            int c, int h, int w, int p, int d);
+
+/* replaces maxpool_backward(dy, arg, p, dilation, hi, wi, threads) -- _kernels.pyx:169-191
+ * requires hi >= ho+e-1, wi >= wo+e-1 (rows/cols beyond receive 0) */
+int dp_host_maxpool_backward(int dtype, const void *dy, const int32_t *arg, void *dx,
+                             int c, int ho, int wo, int p, int d, int hi, int wi);
+
+/* replaces avgpool_forward(x, p, dilation, threads) -- _kernels.pyx:194-221 */
+int dp_host_avgpool_forward(int dtype, const void *x, void *y, int c, int h, int w, int p, int d);
+
+/* replaces avgpool_backward(dy, p, dilation, hi, wi, threads) -- _kernels.pyx:224-247 */
+int dp_host_avgpool_backward(int dtype, const void *dy, void *dx, int c, int ho, int wo,
+                             int p, int d, int hi, int wi);
+
+/* nonlin_forward / nonlin_backward (forward.py:69-76, backward.py:172-182; numpy
+ * in the reference, outside its boundary).  x_in is the nonlinearity INPUT. */
+int dp_host_nonlin_forward(int dtype, const void *x, void *y, int64_t count, int kind);
+int dp_host_nonlin_backward(int dtype, const void *dy, const void *x_in, void *dx,
+                            int64_t count, int kind);
+
+/* ========================= device-pointer batched entry points ====================== */
+
+/* y[n,cout,ho,wo] = act(b + sum_{c,i,j} w * x), act = `nonlin` (DP_IDENTITY = none) */
+int dp_conv_forward(int dtype, const void *x, const void *wt, const void *b, void *y,
+                    int n, int cin, int h, int w, int cout, int k, int d, int nonlin,
+                    void *stream);
+
+/* dx[n,cin,ho+e-1,wo+e-1] = conv_backward_data(dy); if gate != NULL,
+ * dx *= act'(.) where gate holds the OUTPUT of the nonlinearity `gate_kind`
+ * that produced this conv's input (tanh' = 1 - t*t, relu' = t > 0). */
+int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx,
+                          int n, int cout, int ho, int wo, int cin, int k, int d,
+                          const void *gate, int gate_kind, void *stream);
+
+/* workspace bytes for dp_conv_backward_kernel at this shape */
+size_t dp_conv_backward_kernel_workspace(int dtype, int n, int cin, int hi, int wi,
+                                         int cout, int k, int d);
+/* dw[cout,cin,k,k], db[cout] = sums over the n images and all pixels.
+ * Deterministic: fixed split + fixed-order reduction, no float atomics. */
+int dp_conv_backward_kernel(int dtype, const void *x, const void *dy, void *dw, void *db,
+                            int n, int cin, int hi, int wi, int cout, int k, int d,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
+/* y = act(maxpool(x)), arg = first row-major argmax (int32 or uint8 per arg_bytes) */
+int dp_maxpool_forward(int dtype, const void *x, void *y, void *arg, int arg_bytes,
+                       int n, int c, int h, int w, int p, int d, int nonlin, void *stream);
+/* dx[n,c,hi,wi] = gather of dy at recorded taps (descending tap order), then
+ * optional gate multiply as in dp_conv_backward_data */
+int dp_maxpool_backward(int dtype, const void *dy, const void *arg, int arg_bytes, void *dx,
+                        int n, int c, int ho, int wo, int p, int d, int hi, int wi,
+                        const void *gate, int gate_kind, void *stream);
+int dp_avgpool_forward(int dtype, const void *x, void *y, int n, int c, int h, int w,
+                       int p, int d, int nonlin, void *stream);
+int dp_avgpool_backward(int dtype, const void *dy, void *dx, int n, int c, int ho, int wo,
+                        int p, int d, int hi, int wi, const void *gate, int gate_kind,
+                        void *stream);
+
+/* elementwise nonlinearity; backward: x_is_output=0 -> x is the input
+ * (reference semantics), 1 -> x is the nonlinearity's output */
+int dp_nonlin_forward(int dtype, const void *x, void *y, int64_t count, int kind, void *stream);
+int dp_nonlin_backward(int dtype, const void *dy, const void *x, void *dx, int64_t count,
+                       int kind, int x_is_output, void *stream);
+
+/* error-map mask / loss layer (backward.py:110-118; squared-error delta cli.py:218):
+ * out[n,c,y,x] = mask[n,y,x] ? (target ? a - target : a) : 0, mask uint8 (n,h,w) */
+int dp_mask_delta(int dtype, const void *a, const void *target, const uint8_t *mask, void *out,
+                  int n, int c, int h, int w, void *stream);
+
+/* zero-pad (n,c,h,w) -> (n,c,h+top+bottom,w+left+right)  (forward.py:96-98) */
+int dp_pad(int dtype, const void *src, void *dst, int n, int c, int h, int w,
+           int top, int bottom, int left, int right, void *stream);
+/* crop window (top,left,h,w) of (n,c,hs,ws) -> (n,c,h,w)  (backward.py:218-222) */
+int dp_crop(int dtype, const void *src, void *dst, int n, int c, int hs, int ws,
+            int top, int left, int h, int w, void *stream);
+/* param -= lr * grad (plain SGD; the reference has no optimizer) */
+int dp_sgd_update(int dtype, void *param, const void *grad, int64_t count, double lr,
+                  void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DENSEPROP_B200_H */

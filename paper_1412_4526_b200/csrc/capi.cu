@@ -1,0 +1,599 @@
+// extern "C" entry points declared in include/denseprop_b200.h.
+//
+// Argument validation mirrors the reference wrappers (forward.py:27-38,
+// backward.py:136-146, 154-155): bad shapes are rejected before any launch
+// with DP_ERR_ARG and a message in dp_last_error().  The dp_host_* forms are
+// the drop-in replacements for the 7 `backend.kernels()` functions: they copy
+// host buffers to the device on a per-thread stream, run the batched kernel
+// with n = 1, copy the result back and synchronise.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "dp_common.cuh"
+
+namespace dp {
+
+// ---- kernels (defined in conv_direct.cu, conv_wgrad.cu, pool.cu, elementwise.cu)
+template <typename T>
+int conv_forward_t(const T *, const T *, const T *, T *, int, int, int, int, int, int, int, int,
+                   cudaStream_t);
+template <typename T>
+int conv_backward_data_t(const T *, const T *, T *, int, int, int, int, int, int, int,
+                         const T *, int, cudaStream_t);
+template <typename T>
+int conv_backward_kernel_t(const T *, const T *, T *, T *, int, int, int, int, int, int, int,
+                           void *, size_t, cudaStream_t);
+size_t wgrad_workspace_bytes(int elem, int n, int cin, int hi, int wi, int cout, int k, int d);
+template <typename T>
+int maxpool_forward_t(const T *, T *, void *, int, int, int, int, int, int, int, int,
+                      cudaStream_t);
+template <typename T>
+int maxpool_backward_t(const T *, const void *, int, T *, int, int, int, int, int, int, int,
+                       int, const T *, int, cudaStream_t);
+template <typename T>
+int avgpool_forward_t(const T *, T *, int, int, int, int, int, int, int, cudaStream_t);
+template <typename T>
+int avgpool_backward_t(const T *, T *, int, int, int, int, int, int, int, int, const T *, int,
+                       cudaStream_t);
+template <typename T>
+int nonlin_forward_t(const T *, T *, long long, int, cudaStream_t);
+template <typename T>
+int nonlin_backward_t(const T *, const T *, T *, long long, int, int, cudaStream_t);
+template <typename T>
+int mask_delta_t(const T *, const T *, const uint8_t *, T *, int, int, int, int, cudaStream_t);
+template <typename T>
+int pad_t(const T *, T *, int, int, int, int, int, int, int, int, cudaStream_t);
+template <typename T>
+int crop_t(const T *, T *, int, int, int, int, int, int, int, int, cudaStream_t);
+template <typename T>
+int sgd_t(T *, const T *, long long, double, cudaStream_t);
+
+// ---- error state
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(DP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return DP_OK;
+}
+
+static int cuda_ok(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return set_error(DP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return DP_OK;
+}
+
+static inline int esize(int dtype) { return dtype == DP_F64 ? 8 : 4; }
+
+static int check_dtype(int dtype) {
+    if (dtype != DP_F32 && dtype != DP_F64)
+        return set_error(DP_ERR_ARG, "dtype must be DP_F32 or DP_F64, got %d", dtype);
+    return DP_OK;
+}
+
+static int check_pos(const char *what, long long v) {
+    if (v < 1) return set_error(DP_ERR_ARG, "%s must be >= 1, got %lld", what, v);
+    return DP_OK;
+}
+
+static int check_nonlin(int kind) {
+    if (kind < DP_IDENTITY || kind > DP_RELU)
+        return set_error(DP_ERR_ARG, "unknown nonlinearity code %d", kind);
+    return DP_OK;
+}
+
+#define DP_TRY(expr)            \
+    do {                        \
+        int _rc = (expr);       \
+        if (_rc) return _rc;    \
+    } while (0)
+
+static int check_window(const char *what, int h, int w, int k, int d) {
+    DP_TRY(check_pos("kernel size", k));
+    DP_TRY(check_pos("dilation", d));
+    long long e = (long long)(k - 1) * d + 1;
+    if (h < e || w < e)
+        return set_error(DP_ERR_ARG, "%s: input %dx%d is smaller than the %lldx%lld dilated window",
+                         what, h, w, e, e);
+    return DP_OK;
+}
+
+// ---- per-thread stream + scratch for the host-pointer forms
+struct HostCtx {
+    cudaStream_t st = nullptr;
+    ~HostCtx() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+static thread_local HostCtx g_host;
+
+static int host_stream(cudaStream_t *out) {
+    if (!g_host.st) DP_TRY(cuda_ok(cudaStreamCreateWithFlags(&g_host.st, cudaStreamNonBlocking),
+                                   "cudaStreamCreate"));
+    *out = g_host.st;
+    return DP_OK;
+}
+
+struct DevBufs {
+    cudaStream_t st;
+    void *p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int n = 0;
+    explicit DevBufs(cudaStream_t s) : st(s) {}
+    ~DevBufs() {
+        for (int i = 0; i < n; ++i)
+            if (p[i]) cudaFreeAsync(p[i], st);
+        cudaStreamSynchronize(st);
+    }
+    int alloc(size_t bytes, void **out) {
+        void *q = nullptr;
+        DP_TRY(cuda_ok(cudaMallocAsync(&q, bytes ? bytes : 1, st), "cudaMallocAsync"));
+        p[n++] = q;
+        *out = q;
+        return DP_OK;
+    }
+    int up(const void *host, size_t bytes, void **out) {
+        DP_TRY(alloc(bytes, out));
+        return cuda_ok(cudaMemcpyAsync(*out, host, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    }
+};
+
+static int down(void *host, const void *dev, size_t bytes, cudaStream_t st) {
+    DP_TRY(cuda_ok(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st), "D2H"));
+    return DP_OK;
+}
+
+static int finish(cudaStream_t st) { return cuda_ok(cudaStreamSynchronize(st), "sync"); }
+
+#define DP_DISPATCH(dtype, CALL_F, CALL_D) ((dtype) == DP_F64 ? (CALL_D) : (CALL_F))
+
+}  // namespace dp
+
+using namespace dp;
+
+extern "C" {
+
+const char *dp_last_error(void) { return g_err; }
+int dp_abi_version(void) { return DP_ABI_VERSION; }
+int dp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return n;
+}
+
+// ============================== device-pointer forms ==============================
+
+int dp_conv_forward(int dtype, const void *x, const void *wt, const void *b, void *y, int n,
+                    int cin, int h, int w, int cout, int k, int d, int nonlin, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_nonlin(nonlin));
+    DP_TRY(check_window("dilated conv", h, w, k, d));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       conv_forward_t<float>((const float *)x, (const float *)wt,
+                                             (const float *)b, (float *)y, n, cin, h, w, cout,
+                                             k, d, nonlin, st),
+                       conv_forward_t<double>((const double *)x, (const double *)wt,
+                                              (const double *)b, (double *)y, n, cin, h, w,
+                                              cout, k, d, nonlin, st));
+}
+
+int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx, int n, int cout,
+                          int ho, int wo, int cin, int k, int d, const void *gate,
+                          int gate_kind, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("delta height", ho));
+    DP_TRY(check_pos("delta width", wo));
+    DP_TRY(check_pos("kernel size", k));
+    DP_TRY(check_pos("dilation", d));
+    DP_TRY(check_nonlin(gate_kind));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       conv_backward_data_t<float>((const float *)dy, (const float *)wt,
+                                                   (float *)dx, n, cout, ho, wo, cin, k, d,
+                                                   (const float *)gate, gate_kind, st),
+                       conv_backward_data_t<double>((const double *)dy, (const double *)wt,
+                                                    (double *)dx, n, cout, ho, wo, cin, k, d,
+                                                    (const double *)gate, gate_kind, st));
+}
+
+size_t dp_conv_backward_kernel_workspace(int dtype, int n, int cin, int hi, int wi, int cout,
+                                         int k, int d) {
+    if (check_dtype(dtype) || n < 1 || cin < 1 || cout < 1 || check_window("wgrad", hi, wi, k, d))
+        return 0;
+    return wgrad_workspace_bytes(esize(dtype), n, cin, hi, wi, cout, k, d);
+}
+
+int dp_conv_backward_kernel(int dtype, const void *x, const void *dy, void *dw, void *db, int n,
+                            int cin, int hi, int wi, int cout, int k, int d, void *workspace,
+                            size_t workspace_bytes, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(
+        dtype,
+        conv_backward_kernel_t<float>((const float *)x, (const float *)dy, (float *)dw,
+                                      (float *)db, n, cin, hi, wi, cout, k, d, workspace,
+                                      workspace_bytes, st),
+        conv_backward_kernel_t<double>((const double *)x, (const double *)dy, (double *)dw,
+                                       (double *)db, n, cin, hi, wi, cout, k, d, workspace,
+                                       workspace_bytes, st));
+}
+
+int dp_maxpool_forward(int dtype, const void *x, void *y, void *arg, int arg_bytes, int n, int c,
+                       int h, int w, int p, int d, int nonlin, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_nonlin(nonlin));
+    DP_TRY(check_window("dilated max pool", h, w, p, d));
+    if (arg_bytes != 4 && !(arg_bytes == 1 && p * p <= 256))
+        return set_error(DP_ERR_ARG, "arg_bytes must be 4 (or 1 when p*p <= 256)");
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       maxpool_forward_t<float>((const float *)x, (float *)y, arg, arg_bytes, n,
+                                                c, h, w, p, d, nonlin, st),
+                       maxpool_forward_t<double>((const double *)x, (double *)y, arg, arg_bytes,
+                                                 n, c, h, w, p, d, nonlin, st));
+}
+
+static int check_pool_bwd(int ho, int wo, int p, int d, int hi, int wi) {
+    DP_TRY(check_pos("delta height", ho));
+    DP_TRY(check_pos("delta width", wo));
+    DP_TRY(check_pos("pool size", p));
+    DP_TRY(check_pos("dilation", d));
+    long long e = (long long)(p - 1) * d + 1;
+    if (hi < ho + e - 1 || wi < wo + e - 1)
+        return set_error(DP_ERR_ARG, "pool backward: input %dx%d smaller than %lldx%lld", hi, wi,
+                         ho + e - 1, wo + e - 1);
+    return DP_OK;
+}
+
+int dp_maxpool_backward(int dtype, const void *dy, const void *arg, int arg_bytes, void *dx,
+                        int n, int c, int ho, int wo, int p, int d, int hi, int wi,
+                        const void *gate, int gate_kind, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_nonlin(gate_kind));
+    DP_TRY(check_pool_bwd(ho, wo, p, d, hi, wi));
+    if (arg_bytes != 4 && arg_bytes != 1)
+        return set_error(DP_ERR_ARG, "arg_bytes must be 1 or 4");
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       maxpool_backward_t<float>((const float *)dy, arg, arg_bytes, (float *)dx,
+                                                 n, c, ho, wo, p, d, hi, wi,
+                                                 (const float *)gate, gate_kind, st),
+                       maxpool_backward_t<double>((const double *)dy, arg, arg_bytes,
+                                                  (double *)dx, n, c, ho, wo, p, d, hi, wi,
+                                                  (const double *)gate, gate_kind, st));
+}
+
+int dp_avgpool_forward(int dtype, const void *x, void *y, int n, int c, int h, int w, int p,
+                       int d, int nonlin, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_nonlin(nonlin));
+    DP_TRY(check_window("dilated avg pool", h, w, p, d));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       avgpool_forward_t<float>((const float *)x, (float *)y, n, c, h, w, p, d,
+                                                nonlin, st),
+                       avgpool_forward_t<double>((const double *)x, (double *)y, n, c, h, w, p,
+                                                 d, nonlin, st));
+}
+
+int dp_avgpool_backward(int dtype, const void *dy, void *dx, int n, int c, int ho, int wo, int p,
+                        int d, int hi, int wi, const void *gate, int gate_kind, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_nonlin(gate_kind));
+    DP_TRY(check_pool_bwd(ho, wo, p, d, hi, wi));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       avgpool_backward_t<float>((const float *)dy, (float *)dx, n, c, ho, wo, p,
+                                                 d, hi, wi, (const float *)gate, gate_kind, st),
+                       avgpool_backward_t<double>((const double *)dy, (double *)dx, n, c, ho, wo,
+                                                  p, d, hi, wi, (const double *)gate,
+                                                  gate_kind, st));
+}
+
+int dp_nonlin_forward(int dtype, const void *x, void *y, int64_t count, int kind, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_nonlin(kind));
+    if (count < 0) return set_error(DP_ERR_ARG, "count must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       nonlin_forward_t<float>((const float *)x, (float *)y, count, kind, st),
+                       nonlin_forward_t<double>((const double *)x, (double *)y, count, kind,
+                                                st));
+}
+
+int dp_nonlin_backward(int dtype, const void *dy, const void *x, void *dx, int64_t count,
+                       int kind, int x_is_output, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_nonlin(kind));
+    if (count < 0) return set_error(DP_ERR_ARG, "count must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       nonlin_backward_t<float>((const float *)dy, (const float *)x,
+                                                (float *)dx, count, kind, x_is_output, st),
+                       nonlin_backward_t<double>((const double *)dy, (const double *)x,
+                                                 (double *)dx, count, kind, x_is_output, st));
+}
+
+int dp_mask_delta(int dtype, const void *a, const void *target, const uint8_t *mask, void *out,
+                  int n, int c, int h, int w, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_pos("height", h));
+    DP_TRY(check_pos("width", w));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       mask_delta_t<float>((const float *)a, (const float *)target, mask,
+                                           (float *)out, n, c, h, w, st),
+                       mask_delta_t<double>((const double *)a, (const double *)target, mask,
+                                            (double *)out, n, c, h, w, st));
+}
+
+int dp_pad(int dtype, const void *src, void *dst, int n, int c, int h, int w, int top,
+           int bottom, int left, int right, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    if (top < 0 || bottom < 0 || left < 0 || right < 0)
+        return set_error(DP_ERR_ARG, "padding margins must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       pad_t<float>((const float *)src, (float *)dst, n, c, h, w, top, bottom,
+                                    left, right, st),
+                       pad_t<double>((const double *)src, (double *)dst, n, c, h, w, top,
+                                     bottom, left, right, st));
+}
+
+int dp_crop(int dtype, const void *src, void *dst, int n, int c, int hs, int ws, int top,
+            int left, int h, int w, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    if (top < 0 || left < 0 || top + h > hs || left + w > ws)
+        return set_error(DP_ERR_ARG, "crop window leaves the %dx%d map", hs, ws);
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       crop_t<float>((const float *)src, (float *)dst, n, c, hs, ws, top, left,
+                                     h, w, st),
+                       crop_t<double>((const double *)src, (double *)dst, n, c, hs, ws, top,
+                                      left, h, w, st));
+}
+
+int dp_sgd_update(int dtype, void *param, const void *grad, int64_t count, double lr,
+                  void *stream) {
+    DP_TRY(check_dtype(dtype));
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype, sgd_t<float>((float *)param, (const float *)grad, count, lr, st),
+                       sgd_t<double>((double *)param, (const double *)grad, count, lr, st));
+}
+
+// ============================== host-pointer forms ==============================
+
+int dp_host_conv_forward(int dtype, const void *x, const void *wt, const void *b, void *y,
+                         int cin, int h, int w, int cout, int k, int d) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("dilated conv", h, w, k, d));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    int e = (k - 1) * d + 1, ho = h - e + 1, wo = w - e + 1;
+    int rc;
+    {
+        DevBufs B(st);
+        void *dx, *dw, *db, *dy;
+        DP_TRY(B.up(x, es * cin * h * w, &dx));
+        DP_TRY(B.up(wt, es * cout * cin * k * k, &dw));
+        DP_TRY(B.up(b, es * cout, &db));
+        DP_TRY(B.alloc(es * (size_t)cout * ho * wo, &dy));
+        rc = dp_conv_forward(dtype, dx, dw, db, dy, 1, cin, h, w, cout, k, d, DP_IDENTITY, st);
+        if (!rc) rc = down(y, dy, es * (size_t)cout * ho * wo, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx, int cout,
+                               int ho, int wo, int cin, int k, int d) {
+    DP_TRY(check_dtype(dtype));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    int e = (k - 1) * d + 1, hi = ho + e - 1, wi = wo + e - 1;
+    int rc;
+    {
+        DevBufs B(st);
+        void *ddy, *dw, *ddx;
+        DP_TRY(B.up(dy, es * cout * ho * wo, &ddy));
+        DP_TRY(B.up(wt, es * cout * cin * k * k, &dw));
+        DP_TRY(B.alloc(es * (size_t)cin * hi * wi, &ddx));
+        rc = dp_conv_backward_data(dtype, ddy, dw, ddx, 1, cout, ho, wo, cin, k, d, nullptr,
+                                   DP_IDENTITY, st);
+        if (!rc) rc = down(dx, ddx, es * (size_t)cin * hi * wi, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_conv_backward_kernel(int dtype, const void *x, const void *dy, void *dw, void *db,
+                                 int cin, int hi, int wi, int cout, int k, int d) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    int e = (k - 1) * d + 1, ho = hi - e + 1, wo = wi - e + 1;
+    size_t wsb = dp_conv_backward_kernel_workspace(dtype, 1, cin, hi, wi, cout, k, d);
+    int rc;
+    {
+        DevBufs B(st);
+        void *ddx, *ddy, *ddw, *ddb, *ws;
+        DP_TRY(B.up(x, es * cin * hi * wi, &ddx));
+        DP_TRY(B.up(dy, es * cout * ho * wo, &ddy));
+        DP_TRY(B.alloc(es * cout * cin * k * k, &ddw));
+        DP_TRY(B.alloc(es * cout, &ddb));
+        DP_TRY(B.alloc(wsb, &ws));
+        rc = dp_conv_backward_kernel(dtype, ddx, ddy, ddw, ddb, 1, cin, hi, wi, cout, k, d, ws,
+                                     wsb, st);
+        if (!rc) rc = down(dw, ddw, es * cout * cin * k * k, st);
+        if (!rc) rc = down(db, ddb, es * cout, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_maxpool_forward(int dtype, const void *x, void *y, int32_t *arg, int c, int h, int w,
+                            int p, int d) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_window("dilated max pool", h, w, p, d));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    int e = (p - 1) * d + 1, ho = h - e + 1, wo = w - e + 1;
+    size_t nout = (size_t)c * ho * wo;
+    int rc;
+    {
+        DevBufs B(st);
+        void *dx, *dy, *da;
+        DP_TRY(B.up(x, es * c * h * w, &dx));
+        DP_TRY(B.alloc(es * nout, &dy));
+        DP_TRY(B.alloc(4 * nout, &da));
+        rc = dp_maxpool_forward(dtype, dx, dy, da, 4, 1, c, h, w, p, d, DP_IDENTITY, st);
+        if (!rc) rc = down(y, dy, es * nout, st);
+        if (!rc) rc = down(arg, da, 4 * nout, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_maxpool_backward(int dtype, const void *dy, const int32_t *arg, void *dx, int c,
+                             int ho, int wo, int p, int d, int hi, int wi) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_pool_bwd(ho, wo, p, d, hi, wi));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    size_t nout = (size_t)c * ho * wo, nin = (size_t)c * hi * wi;
+    int rc;
+    {
+        DevBufs B(st);
+        void *ddy, *da, *ddx;
+        DP_TRY(B.up(dy, es * nout, &ddy));
+        DP_TRY(B.up(arg, 4 * nout, &da));
+        DP_TRY(B.alloc(es * nin, &ddx));
+        rc = dp_maxpool_backward(dtype, ddy, da, 4, ddx, 1, c, ho, wo, p, d, hi, wi, nullptr,
+                                 DP_IDENTITY, st);
+        if (!rc) rc = down(dx, ddx, es * nin, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_avgpool_forward(int dtype, const void *x, void *y, int c, int h, int w, int p,
+                            int d) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_window("dilated avg pool", h, w, p, d));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    int e = (p - 1) * d + 1, ho = h - e + 1, wo = w - e + 1;
+    size_t nout = (size_t)c * ho * wo;
+    int rc;
+    {
+        DevBufs B(st);
+        void *dx, *dy;
+        DP_TRY(B.up(x, es * c * h * w, &dx));
+        DP_TRY(B.alloc(es * nout, &dy));
+        rc = dp_avgpool_forward(dtype, dx, dy, 1, c, h, w, p, d, DP_IDENTITY, st);
+        if (!rc) rc = down(y, dy, es * nout, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_avgpool_backward(int dtype, const void *dy, void *dx, int c, int ho, int wo, int p,
+                             int d, int hi, int wi) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_pool_bwd(ho, wo, p, d, hi, wi));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t es = esize(dtype);
+    size_t nout = (size_t)c * ho * wo, nin = (size_t)c * hi * wi;
+    int rc;
+    {
+        DevBufs B(st);
+        void *ddy, *ddx;
+        DP_TRY(B.up(dy, es * nout, &ddy));
+        DP_TRY(B.alloc(es * nin, &ddx));
+        rc = dp_avgpool_backward(dtype, ddy, ddx, 1, c, ho, wo, p, d, hi, wi, nullptr,
+                                 DP_IDENTITY, st);
+        if (!rc) rc = down(dx, ddx, es * nin, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_nonlin_forward(int dtype, const void *x, void *y, int64_t count, int kind) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_nonlin(kind));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t bytes = esize(dtype) * (size_t)count;
+    int rc;
+    {
+        DevBufs B(st);
+        void *dx, *dy;
+        DP_TRY(B.up(x, bytes, &dx));
+        DP_TRY(B.alloc(bytes, &dy));
+        rc = dp_nonlin_forward(dtype, dx, dy, count, kind, st);
+        if (!rc) rc = down(y, dy, bytes, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+int dp_host_nonlin_backward(int dtype, const void *dy, const void *x_in, void *dx, int64_t count,
+                            int kind) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_nonlin(kind));
+    cudaStream_t st;
+    DP_TRY(host_stream(&st));
+    size_t bytes = esize(dtype) * (size_t)count;
+    int rc;
+    {
+        DevBufs B(st);
+        void *ddy, *dxin, *ddx;
+        DP_TRY(B.up(dy, bytes, &ddy));
+        DP_TRY(B.up(x_in, bytes, &dxin));
+        DP_TRY(B.alloc(bytes, &ddx));
+        rc = dp_nonlin_backward(dtype, ddy, dxin, ddx, count, kind, 0, st);
+        if (!rc) rc = down(dx, ddx, bytes, st);
+    }
+    return rc ? rc : finish(st);
+}
+
+}  // extern "C"

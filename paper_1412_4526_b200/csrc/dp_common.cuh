@@ -1,0 +1,66 @@
+// Shared device helpers for the denseprop B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/denseprop_b200.h"
+
+namespace dp {
+
+// ---------------------------------------------------------------------------
+// Exact-order arithmetic.  The reference builds with -ffp-contract=off
+// (pkg/setup.py:15): every multiply and add rounds separately.  The _rn
+// intrinsics are never contracted into FFMA/DFMA regardless of -fmad.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// tanh: fp32 evaluates in fp64 and rounds once (<= 0.5 ulp + tiny), so it is
+// within 1 ulp of numpy's float32 tanh (reference forward.py:71).
+__device__ __forceinline__ float dp_tanh(float x) { return (float)tanh((double)x); }
+__device__ __forceinline__ double dp_tanh(double x) { return tanh(x); }
+
+// relu == np.maximum(x, 0): returns x when x >= 0 (keeps -0.0) or x is NaN.
+template <typename T>
+__device__ __forceinline__ T dp_relu(T x) { return (x >= T(0) || x != x) ? x : T(0); }
+
+template <typename T>
+__device__ __forceinline__ T apply_nonlin(T v, int kind) {
+    if (kind == DP_TANH) return dp_tanh(v);
+    if (kind == DP_RELU) return dp_relu(v);
+    return v;
+}
+
+// Derivative factor from the nonlinearity OUTPUT t (the engine caches outputs):
+// tanh' = 1 - t*t (backward.py:176-177 computes it from t = tanh(x_in)),
+// relu' = (x_in > 0) == (t > 0) (backward.py:179).
+template <typename T>
+__device__ __forceinline__ T gate_from_output(T delta, T t, int kind) {
+    if (kind == DP_TANH) return mul_rn(delta, add_rn(T(1), -mul_rn(t, t)));
+    if (kind == DP_RELU) return mul_rn(delta, t > T(0) ? T(1) : T(0));
+    return delta;
+}
+
+template <typename T>
+__device__ __forceinline__ T neg_inf();
+template <>
+__device__ __forceinline__ float neg_inf<float>() { return __int_as_float(0xff800000); }
+template <>
+__device__ __forceinline__ double neg_inf<double>() {
+    return __longlong_as_double(0xfff0000000000000ULL);
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace dp
+
+// error state + launch checking, implemented in capi.cu
+namespace dp {
+int set_error(int code, const char *fmt, ...);
+int check_launch(const char *what);
+}  // namespace dp

@@ -1,0 +1,157 @@
+// Elementwise kernels: nonlinearity, error-map mask / loss, pad, crop, SGD.
+//
+// nonlin fwd/bwd ... reference forward.py:69-76 / backward.py:172-182 (numpy
+//                    there, outside the kernel boundary); relu and identity
+//                    are bit-exact, tanh within 1 ulp of numpy.
+// mask / loss ...... backward.py:110-118 (keep the selected pixels across all
+//                    channels, zero the rest) fused with the squared-error
+//                    delta output - target (cli.py:218).  A dense bitmap: the
+//                    cost is independent of the number of selected pixels
+//                    (tests/test_acceptance.py:144-158).
+// pad / crop ....... forward.py:96-98 (pad_rect with (lead, trail) margins),
+//                    backward.py:218-222 (crop of the input delta).
+#include "dp_common.cuh"
+
+namespace dp {
+
+template <typename T>
+__global__ void nonlin_fwd_kernel(const T *__restrict__ x, T *__restrict__ y, long long n,
+                                  int kind) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = apply_nonlin(x[i], kind);
+}
+
+template <typename T>
+__global__ void nonlin_bwd_kernel(const T *__restrict__ dy, const T *__restrict__ x,
+                                  T *__restrict__ dx, long long n, int kind, int x_is_output) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        T t = x[i];
+        if (!x_is_output && kind == DP_TANH) t = dp_tanh(t);
+        dx[i] = gate_from_output(dy[i], t, kind);
+    }
+}
+
+template <typename T>
+__global__ void mask_delta_kernel(const T *__restrict__ a, const T *__restrict__ target,
+                                  const uint8_t *__restrict__ mask, T *__restrict__ out,
+                                  long long total, int C, long long HW) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long px = i % HW;
+        long long img = i / HW / C;
+        T v = T(0);
+        if (mask[img * HW + px]) v = target ? add_rn(a[i], -target[i]) : a[i];
+        out[i] = v;
+    }
+}
+
+template <typename T>
+__global__ void pad_kernel(const T *__restrict__ src, T *__restrict__ dst, long long total,
+                           int h, int w, int Hp, int Wp, int top, int left) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        int xx = (int)(i % Wp);
+        long long t = i / Wp;
+        int yy = (int)(t % Hp);
+        long long plane = t / Hp;
+        int sy = yy - top, sx = xx - left;
+        T v = T(0);
+        if (sy >= 0 && sy < h && sx >= 0 && sx < w) v = src[(plane * h + sy) * w + sx];
+        dst[i] = v;
+    }
+}
+
+template <typename T>
+__global__ void crop_kernel(const T *__restrict__ src, T *__restrict__ dst, long long total,
+                            int hs, int ws, int top, int left, int h, int w) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        int xx = (int)(i % w);
+        long long t = i / w;
+        int yy = (int)(t % h);
+        long long plane = t / h;
+        dst[i] = src[(plane * hs + yy + top) * ws + xx + left];
+    }
+}
+
+template <typename T>
+__global__ void sgd_kernel(T *__restrict__ p, const T *__restrict__ g, long long n, T lr) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        p[i] = p[i] - lr * g[i];
+}
+
+static inline int grid_for(long long n) {
+    long long b = (n + 255) / 256;
+    if (b > 148LL * 32) b = 148LL * 32;
+    return (int)(b < 1 ? 1 : b);
+}
+
+template <typename T>
+int nonlin_forward_t(const T *x, T *y, long long n, int kind, cudaStream_t st) {
+    if (n == 0) return DP_OK;
+    nonlin_fwd_kernel<T><<<grid_for(n), 256, 0, st>>>(x, y, n, kind);
+    return check_launch("nonlin_fwd_kernel");
+}
+
+template <typename T>
+int nonlin_backward_t(const T *dy, const T *x, T *dx, long long n, int kind, int x_is_output,
+                      cudaStream_t st) {
+    if (n == 0) return DP_OK;
+    nonlin_bwd_kernel<T><<<grid_for(n), 256, 0, st>>>(dy, x, dx, n, kind, x_is_output);
+    return check_launch("nonlin_bwd_kernel");
+}
+
+template <typename T>
+int mask_delta_t(const T *a, const T *target, const uint8_t *mask, T *out, int n, int c, int h,
+                 int w, cudaStream_t st) {
+    long long total = (long long)n * c * h * w;
+    if (total == 0) return DP_OK;
+    mask_delta_kernel<T><<<grid_for(total), 256, 0, st>>>(a, target, mask, out, total, c,
+                                                          (long long)h * w);
+    return check_launch("mask_delta_kernel");
+}
+
+template <typename T>
+int pad_t(const T *src, T *dst, int n, int c, int h, int w, int top, int bottom, int left,
+          int right, cudaStream_t st) {
+    int Hp = h + top + bottom, Wp = w + left + right;
+    long long total = (long long)n * c * Hp * Wp;
+    if (total == 0) return DP_OK;
+    pad_kernel<T><<<grid_for(total), 256, 0, st>>>(src, dst, total, h, w, Hp, Wp, top, left);
+    return check_launch("pad_kernel");
+}
+
+template <typename T>
+int crop_t(const T *src, T *dst, int n, int c, int hs, int ws, int top, int left, int h, int w,
+           cudaStream_t st) {
+    long long total = (long long)n * c * h * w;
+    if (total == 0) return DP_OK;
+    crop_kernel<T><<<grid_for(total), 256, 0, st>>>(src, dst, total, hs, ws, top, left, h, w);
+    return check_launch("crop_kernel");
+}
+
+template <typename T>
+int sgd_t(T *p, const T *g, long long n, double lr, cudaStream_t st) {
+    if (n == 0) return DP_OK;
+    sgd_kernel<T><<<grid_for(n), 256, 0, st>>>(p, g, n, (T)lr);
+    return check_launch("sgd_kernel");
+}
+
+#define DP_EW_INST(T)                                                                         \
+    template int nonlin_forward_t<T>(const T *, T *, long long, int, cudaStream_t);           \
+    template int nonlin_backward_t<T>(const T *, const T *, T *, long long, int, int,         \
+                                      cudaStream_t);                                          \
+    template int mask_delta_t<T>(const T *, const T *, const uint8_t *, T *, int, int, int,   \
+                                 int, cudaStream_t);                                          \
+    template int pad_t<T>(const T *, T *, int, int, int, int, int, int, int, int,             \
+                          cudaStream_t);                                                      \
+    template int crop_t<T>(const T *, T *, int, int, int, int, int, int, int, int,            \
+                           cudaStream_t);                                                     \
+    template int sgd_t<T>(T *, const T *, long long, double, cudaStream_t);
+DP_EW_INST(float)
+DP_EW_INST(double)
+
+}  // namespace dp

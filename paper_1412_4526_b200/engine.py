@@ -1,0 +1,489 @@
+"""Device-resident executors for the dense plan (torch CUDA tensors + the C ABI).
+
+Two executors share the device entry points of libdenseprop_b200.so:
+
+* `run_forward` / `run_backward` -- unfused, every layer input materialised
+  (the reference ForwardCache keeps them all, forward.py:19-24); used by the
+  drop-in `dense_forward` / `dense_backward` and by per-layer parity tests.
+
+* `DenseNet` -- the throughput engine.  Batches of N images (N, C, H, W) in
+  HBM, conv/pool kernels with the following nonlinearity fused into their
+  epilogue (plan.fusion_groups()), backward kernels that apply the upstream
+  nonlinearity's derivative in their epilogue ("gate"), 1-byte argmax maps,
+  a masked squared-error loss kernel (cli.py:218 + backward.py:110-118),
+  all buffers preallocated so a whole step can be captured in a CUDA graph,
+  and one flat gradient bucket (the data-parallel all-reduce unit).
+
+torch supplies device memory, streams and graphs only; every arithmetic op of
+the path is one of this package's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .netspec import ConvLayerSpec, NonlinLayerSpec
+from .plan import DensePlan, DilatedConv, DilatedPool
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+_TORCH_DT = {}
+if torch is not None:
+    _TORCH_DT = {torch.float32: _lib.DP_F32, torch.float64: _lib.DP_F64}
+
+
+def _code(t) -> int:
+    try:
+        return _TORCH_DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"expected float32/float64 tensor, got {t.dtype}") from None
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _lib_dev():
+    return _lib.require_device()
+
+
+# ---------------------------------------------------------------------------
+# thin typed wrappers over the device C ABI (batched NCHW tensors)
+# ---------------------------------------------------------------------------
+
+class ops:
+    """Each method enqueues one kernel on the current torch stream."""
+
+    @staticmethod
+    def conv_forward(x, w, b, y, k, d, nonlin=_lib.DP_IDENTITY):
+        n, ci, h, wd = x.shape
+        _lib.check(_lib_dev().dp_conv_forward(_code(x), _ptr(x), _ptr(w), _ptr(b), _ptr(y), n,
+                                              ci, h, wd, w.shape[0], k, d, nonlin, _stream()),
+                   "conv_forward")
+
+    @staticmethod
+    def conv_backward_data(dy, w, dx, k, d, gate=None, gate_kind=_lib.DP_IDENTITY):
+        n, co, ho, wo = dy.shape
+        _lib.check(_lib_dev().dp_conv_backward_data(_code(dy), _ptr(dy), _ptr(w), _ptr(dx), n,
+                                                    co, ho, wo, w.shape[1], k, d, _ptr(gate),
+                                                    gate_kind if gate is not None else 0,
+                                                    _stream()), "conv_backward_data")
+
+    @staticmethod
+    def wgrad_workspace(x, co, k, d) -> int:
+        n, ci, hi, wi = x.shape
+        return int(_lib_dev().dp_conv_backward_kernel_workspace(_code(x), n, ci, hi, wi, co, k,
+                                                                d))
+
+    @staticmethod
+    def conv_backward_kernel(x, dy, dw, db, k, d, ws):
+        n, ci, hi, wi = x.shape
+        co = dy.shape[1]
+        _lib.check(_lib_dev().dp_conv_backward_kernel(_code(x), _ptr(x), _ptr(dy), _ptr(dw),
+                                                      _ptr(db), n, ci, hi, wi, co, k, d,
+                                                      _ptr(ws), ws.numel() * ws.element_size(),
+                                                      _stream()), "conv_backward_kernel")
+
+    @staticmethod
+    def maxpool_forward(x, y, arg, p, d, nonlin=_lib.DP_IDENTITY):
+        n, c, h, w = x.shape
+        _lib.check(_lib_dev().dp_maxpool_forward(_code(x), _ptr(x), _ptr(y), _ptr(arg),
+                                                 arg.element_size(), n, c, h, w, p, d, nonlin,
+                                                 _stream()), "maxpool_forward")
+
+    @staticmethod
+    def maxpool_backward(dy, arg, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY):
+        n, c, ho, wo = dy.shape
+        _lib.check(_lib_dev().dp_maxpool_backward(_code(dy), _ptr(dy), _ptr(arg),
+                                                  arg.element_size(), _ptr(dx), n, c, ho, wo, p,
+                                                  d, dx.shape[2], dx.shape[3], _ptr(gate),
+                                                  gate_kind if gate is not None else 0,
+                                                  _stream()), "maxpool_backward")
+
+    @staticmethod
+    def avgpool_forward(x, y, p, d, nonlin=_lib.DP_IDENTITY):
+        n, c, h, w = x.shape
+        _lib.check(_lib_dev().dp_avgpool_forward(_code(x), _ptr(x), _ptr(y), n, c, h, w, p, d,
+                                                 nonlin, _stream()), "avgpool_forward")
+
+    @staticmethod
+    def avgpool_backward(dy, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY):
+        n, c, ho, wo = dy.shape
+        _lib.check(_lib_dev().dp_avgpool_backward(_code(dy), _ptr(dy), _ptr(dx), n, c, ho, wo,
+                                                  p, d, dx.shape[2], dx.shape[3], _ptr(gate),
+                                                  gate_kind if gate is not None else 0,
+                                                  _stream()), "avgpool_backward")
+
+    @staticmethod
+    def nonlin_forward(x, y, kind):
+        _lib.check(_lib_dev().dp_nonlin_forward(_code(x), _ptr(x), _ptr(y), x.numel(), kind,
+                                                _stream()), "nonlin_forward")
+
+    @staticmethod
+    def nonlin_backward(dy, x, dx, kind, x_is_output=False):
+        _lib.check(_lib_dev().dp_nonlin_backward(_code(dy), _ptr(dy), _ptr(x), _ptr(dx),
+                                                 dy.numel(), kind, int(x_is_output), _stream()),
+                   "nonlin_backward")
+
+    @staticmethod
+    def mask_delta(a, mask, out, target=None):
+        n, c, h, w = a.shape
+        _lib.check(_lib_dev().dp_mask_delta(_code(a), _ptr(a), _ptr(target), _ptr(mask),
+                                            _ptr(out), n, c, h, w, _stream()), "mask_delta")
+
+    @staticmethod
+    def pad(src, dst, top, bottom, left, right):
+        n, c, h, w = src.shape
+        _lib.check(_lib_dev().dp_pad(_code(src), _ptr(src), _ptr(dst), n, c, h, w, top, bottom,
+                                     left, right, _stream()), "pad")
+
+    @staticmethod
+    def crop(src, dst, top, left):
+        n, c, hs, ws = src.shape
+        _lib.check(_lib_dev().dp_crop(_code(src), _ptr(src), _ptr(dst), n, c, hs, ws, top, left,
+                                      dst.shape[2], dst.shape[3], _stream()), "crop")
+
+    @staticmethod
+    def sgd(param, grad, lr):
+        _lib.check(_lib_dev().dp_sgd_update(_code(param), _ptr(param), _ptr(grad),
+                                            param.numel(), float(lr), _stream()), "sgd")
+
+
+def _nl(kind: str) -> int:
+    return _lib.NONLIN_CODE[kind]
+
+
+# ---------------------------------------------------------------------------
+# unfused executor (drop-in semantics)
+# ---------------------------------------------------------------------------
+
+def conv_params(plan: DensePlan, k: int, dtype, device):
+    w, b = plan.conv_weights(k, dtype)
+    return (torch.from_numpy(w).to(device, non_blocking=False),
+            torch.from_numpy(b).to(device, non_blocking=False))
+
+
+def run_forward(plan: DensePlan, x_padded, params=None):
+    """All plan layers on (N, C, H, W) padded input; returns (inputs, argmax, output).
+
+    argmax maps are int32 (the API type).  `params[k]` = (w, b) device tensors,
+    uploaded from the plan when not given.
+    """
+    dev, dt = x_padded.device, x_padded.dtype
+    np_dt = np.float32 if dt == torch.float32 else np.float64
+    x = x_padded
+    inputs, argmax = [], {}
+    for k, layer in enumerate(plan.layers):
+        inputs.append(x)
+        n, c, h, w = x.shape
+        if isinstance(layer, DilatedConv):
+            wt, b = params[k] if params else conv_params(plan, k, np_dt, dev)
+            e = layer.extent
+            y = torch.empty((n, layer.base.out_channels, h - e + 1, w - e + 1), dtype=dt,
+                            device=dev)
+            ops.conv_forward(x, wt, b, y, layer.base.kernel_size, layer.dilation)
+        elif isinstance(layer, DilatedPool):
+            e = layer.extent
+            y = torch.empty((n, c, h - e + 1, w - e + 1), dtype=dt, device=dev)
+            if layer.base.kind == "max":
+                arg = torch.empty(y.shape, dtype=torch.int32, device=dev)
+                ops.maxpool_forward(x, y, arg, layer.base.kernel_size, layer.dilation)
+                argmax[k] = arg
+            else:
+                ops.avgpool_forward(x, y, layer.base.kernel_size, layer.dilation)
+        else:
+            if layer.kind == "identity":
+                y = x
+            else:
+                y = torch.empty_like(x)
+                ops.nonlin_forward(x, y, _nl(layer.kind))
+        x = y
+    return inputs, argmax, x
+
+
+def run_backward(plan: DensePlan, inputs, argmax, delta, params=None, with_input_grad=False):
+    """Reverse sweep over (N, ...) tensors from an already-masked last-layer delta.
+
+    Returns ({k: (dw, db)}, input_delta_padded_or_None).  Gradients are sums over
+    the batch and all pixels (backward.py:190-191).
+    """
+    dev, dt = delta.device, delta.dtype
+    np_dt = np.float32 if dt == torch.float32 else np.float64
+    grads = {}
+    for k in range(len(plan.layers) - 1, -1, -1):
+        layer, x_in = plan.layers[k], inputs[k]
+        if isinstance(layer, DilatedConv):
+            wt, _ = params[k] if params else conv_params(plan, k, np_dt, dev)
+            kk, d = layer.base.kernel_size, layer.dilation
+            dw = torch.empty(wt.shape, dtype=dt, device=dev)
+            db = torch.empty((wt.shape[0],), dtype=dt, device=dev)
+            ws = torch.empty(max(1, ops.wgrad_workspace(x_in, wt.shape[0], kk, d)),
+                             dtype=torch.uint8, device=dev)
+            ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, ws)
+            grads[k] = (dw, db)
+            if k == 0 and not with_input_grad:
+                return grads, None
+            dx = torch.empty(x_in.shape, dtype=dt, device=dev)
+            ops.conv_backward_data(delta, wt, dx, kk, d)
+            delta = dx
+        elif isinstance(layer, DilatedPool):
+            dx = torch.empty(x_in.shape, dtype=dt, device=dev)
+            if layer.base.kind == "max":
+                ops.maxpool_backward(delta, argmax[k], dx, layer.base.kernel_size,
+                                     layer.dilation)
+            else:
+                ops.avgpool_backward(delta, dx, layer.base.kernel_size, layer.dilation)
+            delta = dx
+        else:
+            if layer.kind != "identity":
+                dx = torch.empty_like(delta)
+                ops.nonlin_backward(delta, x_in, dx, _nl(layer.kind), x_is_output=False)
+                delta = dx
+    return grads, delta
+
+
+# ---------------------------------------------------------------------------
+# fused throughput engine
+# ---------------------------------------------------------------------------
+
+@dataclass
+class _Group:
+    first: int                 # plan index of the conv/pool/nonlin
+    op: object                 # DilatedConv | DilatedPool | NonlinLayerSpec
+    act: str                   # fused trailing nonlinearity kind ("identity" if none)
+    out_shape: tuple           # (C, H, W) per image
+
+
+class DenseNet:
+    """Fused, preallocated dense engine for a batch of `batch` images of h x w.
+
+    Buffers live in HBM for the life of the object; `forward`, `loss_delta`,
+    `backward` and `sgd_step` only enqueue kernels on the current stream, so a
+    whole step can be captured with `capture_step()` and replayed as one graph.
+    """
+
+    def __init__(self, plan: DensePlan, batch: int, height: int, width: int,
+                 dtype=None, device="cuda", train=True):
+        if torch is None:
+            raise _lib.KernelUnavailable("torch is required for the device engine")
+        _lib.require_device()
+        self.plan, self.batch, self.h, self.w = plan, batch, height, width
+        self.dtype = dtype or torch.float32
+        self.device = torch.device(device)
+        self.train = train
+        self.np_dtype = np.float32 if self.dtype == torch.float32 else np.float64
+        shapes = plan.layer_shapes(height, width)
+        self.in_shape = shapes[0]
+        # ---- fusion groups
+        self.groups: list[_Group] = []
+        for g in plan.fusion_groups():
+            op = plan.layers[g[0]]
+            act = plan.layers[g[1]].kind if len(g) == 2 else "identity"
+            self.groups.append(_Group(g[0], op, act, shapes[g[-1] + 1]))
+        kw = dict(dtype=self.dtype, device=self.device)
+        N = batch
+        # ---- parameters and the flat gradient bucket (conv layers in order, w then b)
+        convs = [(k, l) for k, l in enumerate(plan.layers) if isinstance(l, DilatedConv)]
+        sizes = [l.base.weights.size + l.base.bias.size for _, l in convs]
+        total = int(sum(sizes))
+        self.param_flat = torch.empty(total, **kw)
+        self.grad_flat = torch.zeros(total, **kw) if train else None
+        self.params, self.grads = {}, {}
+        off = 0
+        for (k, l), _ in zip(convs, sizes):
+            nw, nb = l.base.weights.size, l.base.bias.size
+            wv = self.param_flat[off:off + nw].view(l.base.weights.shape)
+            bv = self.param_flat[off + nw:off + nw + nb]
+            self.params[k] = (wv, bv)
+            if train:
+                self.grads[k] = (self.grad_flat[off:off + nw].view(l.base.weights.shape),
+                                 self.grad_flat[off + nw:off + nw + nb])
+            off += nw + nb
+        self.load_weights_from_plan()
+        # ---- activations: x0 (padded input) and one output per group
+        self.x0 = torch.zeros((N,) + tuple(self.in_shape), **kw)
+        self.acts = [torch.empty((N,) + tuple(g.out_shape), **kw) for g in self.groups]
+        self.args = {}
+        for gi, g in enumerate(self.groups):
+            if isinstance(g.op, DilatedPool) and g.op.base.kind == "max":
+                p = g.op.base.kernel_size
+                adt = torch.uint8 if p * p <= 256 else torch.int32
+                self.args[gi] = torch.empty((N,) + tuple(g.out_shape), dtype=adt,
+                                            device=self.device)
+        self.output = self.acts[-1]
+        if train:
+            biggest = max([int(np.prod(s)) for s in shapes])
+            self._dbuf = [torch.empty(N * biggest, **kw), torch.empty(N * biggest, **kw)]
+            ws = 1
+            for gi, g in enumerate(self.groups):
+                if isinstance(g.op, DilatedConv):
+                    xin = self._group_input(gi)
+                    ws = max(ws, ops.wgrad_workspace(xin, g.op.base.out_channels,
+                                                     g.op.base.kernel_size, g.op.dilation))
+            self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
+            self.mask = torch.zeros((N, height, width), dtype=torch.uint8, device=self.device)
+            self.target = torch.zeros_like(self.output)
+            self.delta_last = torch.empty_like(self.output)
+        self.graph = None
+
+    # ------------------------------------------------------------- parameters
+    def load_weights_from_plan(self):
+        for k, (wv, bv) in self.params.items():
+            w, b = self.plan.conv_weights(k, self.np_dtype)
+            wv.copy_(torch.from_numpy(w))
+            bv.copy_(torch.from_numpy(b))
+
+    def weights_numpy(self):
+        return {k: (w.cpu().numpy(), b.cpu().numpy()) for k, (w, b) in self.params.items()}
+
+    # ------------------------------------------------------------- helpers
+    def _group_input(self, gi):
+        return self.x0 if gi == 0 else self.acts[gi - 1]
+
+    def _view(self, buf, shape):
+        n = int(np.prod(shape))
+        return buf[:n].view(shape)
+
+    # ------------------------------------------------------------- forward
+    def set_input(self, images):
+        """images: (N, C, h, w) device tensor -> zero-padded x0 (forward.py:96-98)."""
+        lead, trail = self.plan.lead_margin, self.plan.trail_margin
+        ops.pad(images, self.x0, lead, trail, lead, trail)
+
+    def forward(self, images=None):
+        if images is not None:
+            self.set_input(images)
+        for gi, g in enumerate(self.groups):
+            x, y = self._group_input(gi), self.acts[gi]
+            op, act = g.op, _nl(g.act)
+            if isinstance(op, DilatedConv):
+                wt, b = self.params[g.first]
+                ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
+            elif isinstance(op, DilatedPool):
+                if op.base.kind == "max":
+                    ops.maxpool_forward(x, y, self.args[gi], op.base.kernel_size, op.dilation,
+                                        act)
+                else:
+                    ops.avgpool_forward(x, y, op.base.kernel_size, op.dilation, act)
+            else:
+                if op.kind == "identity":
+                    y.copy_(x)
+                else:
+                    ops.nonlin_forward(x, y, _nl(op.kind))
+        return self.output
+
+    # ------------------------------------------------------------- loss / mask
+    def loss_delta(self, target=None, mask=None, delta=None):
+        """delta_last = mask ? (output - target) : 0, or mask ? delta : 0."""
+        m = self.mask if mask is None else mask
+        if delta is not None:
+            ops.mask_delta(delta, m, self.delta_last)
+        else:
+            t = self.target if target is None else target
+            ops.mask_delta(self.output, m, self.delta_last, target=t)
+        return self.delta_last
+
+    # ------------------------------------------------------------- backward
+    def backward(self, delta_last=None, with_input_grad=False):
+        """Reverse sweep from the masked delta; fills self.grad_flat (sums)."""
+        if not self.train:
+            raise RuntimeError("engine built with train=False")
+        delta = self.delta_last if delta_last is None else delta_last
+        last = self.groups[-1]
+        ping = 0
+        if last.act != "identity":
+            # a net ending in conv/pool + nonlin: undo the fused nonlinearity first
+            d2 = self._view(self._dbuf[ping], delta.shape)
+            ops.nonlin_backward(delta, self.acts[-1], d2, _nl(last.act), x_is_output=True)
+            delta, ping = d2, ping ^ 1
+        for gi in range(len(self.groups) - 1, -1, -1):
+            g = self.groups[gi]
+            x_in = self._group_input(gi)
+            prev = self.groups[gi - 1] if gi > 0 else None
+            gate, gk = None, 0
+            if prev is not None and prev.act != "identity":
+                gate, gk = x_in, _nl(prev.act)
+            op = g.op
+            if isinstance(op, DilatedConv):
+                wt, _ = self.params[g.first]
+                dw, db = self.grads[g.first]
+                kk, d = op.base.kernel_size, op.dilation
+                ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
+                if gi == 0 and not with_input_grad:
+                    return None
+                dx = self._view(self._dbuf[ping], x_in.shape)
+                ops.conv_backward_data(delta, wt, dx, kk, d, gate, gk)
+            elif isinstance(op, DilatedPool):
+                dx = self._view(self._dbuf[ping], x_in.shape)
+                if op.base.kind == "max":
+                    ops.maxpool_backward(delta, self.args[gi], dx, op.base.kernel_size,
+                                         op.dilation, gate, gk)
+                else:
+                    ops.avgpool_backward(delta, dx, op.base.kernel_size, op.dilation, gate, gk)
+            else:
+                dx = self._view(self._dbuf[ping], x_in.shape)
+                if op.kind == "identity":
+                    dx.copy_(delta)
+                else:
+                    ops.nonlin_backward(delta, x_in, dx, _nl(op.kind), x_is_output=False)
+                if gate is not None:
+                    # standalone nonlin after a fused group: apply that group's gate too
+                    ops.nonlin_backward(dx, x_in, dx, gk, x_is_output=True)
+            delta, ping = dx, ping ^ 1
+        return delta
+
+    def sgd_step(self, lr):
+        ops.sgd(self.param_flat, self.grad_flat, lr)
+
+    # ------------------------------------------------------------- whole step
+    def train_step(self, lr=0.0, allreduce=None):
+        """forward -> masked squared-error delta -> backward -> [allreduce] -> SGD."""
+        self.forward()
+        self.loss_delta()
+        self.backward()
+        if allreduce is not None:
+            allreduce(self.grad_flat)
+        if lr:
+            self.sgd_step(lr)
+
+    def capture(self, fn, warmup=2):
+        """Capture `fn()` (enqueue-only) into a CUDA graph; returns the graph."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    def conv_flops_per_image(self) -> dict:
+        """Algorithmic conv FLOPs per image: fwd, bwd (no layer-0 dgrad)."""
+        fwd = bwd = 0
+        for gi, g in enumerate(self.groups):
+            if isinstance(g.op, DilatedConv):
+                c_out, ho, wo = g.out_shape
+                cin = g.op.base.in_channels
+                f = 2 * c_out * cin * g.op.base.kernel_size ** 2 * ho * wo
+                fwd += f
+                bwd += f if gi == 0 else 2 * f
+        return {"fwd": fwd, "bwd": bwd}
+
+
+def ensure_nonlin_spec(layer) -> bool:
+    return isinstance(layer, NonlinLayerSpec)
+
+
+__all__ = ["ops", "run_forward", "run_backward", "DenseNet", "ConvLayerSpec"]

@@ -1,0 +1,122 @@
+"""Image-sharded data-parallel trainer (NCCL all-reduce over NVLink / NVSwitch).
+
+Images are independent units: each rank runs the fused dense
+engine on its shard, sums its GradientSet locally (the engine's flat gradient
+bucket), then ONE `all_reduce(SUM)` of that bucket per step.  SUM keeps the
+reference's unweighted-sum gradient semantics (backward.py:190-191,
+SPEC.md:446), so the all-reduced bucket equals the single-process GradientSet
+of all images.  Forward-only inference shards images with no collective.
+
+The bucket layout is the conv layers in plan order, weights then bias each,
+flattened -- `bucket_layout()` / `flatten()` / `unflatten()` below, shared by
+the engine (engine.DenseNet.grad_flat) and the CPU gloo tests.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .netspec import ConvLayerSpec, NetworkSpec
+from .plan import DensePlan
+
+
+def bucket_layout(spec: NetworkSpec):
+    """[(layer_index, w_shape, b_shape, offset)] for the flat gradient bucket."""
+    out, off = [], 0
+    for k, layer in enumerate(spec.layers):
+        if isinstance(layer, ConvLayerSpec):
+            out.append((k, tuple(layer.weights.shape), tuple(layer.bias.shape), off))
+            off += layer.weights.size + layer.bias.size
+    return out, off
+
+
+def flatten(spec: NetworkSpec, kernels, biases, dtype=np.float64) -> np.ndarray:
+    layout, total = bucket_layout(spec)
+    flat = np.zeros(total, dtype=dtype)
+    for k, ws, bs, off in layout:
+        nw = int(np.prod(ws))
+        flat[off:off + nw] = np.asarray(kernels[k]).ravel()
+        flat[off + nw:off + nw + int(np.prod(bs))] = np.asarray(biases[k]).ravel()
+    return flat
+
+
+def unflatten(spec: NetworkSpec, flat):
+    """flat bucket -> (kernel list, bias list) aligned with spec.layers (None elsewhere)."""
+    flat = np.asarray(flat)
+    layout, _ = bucket_layout(spec)
+    ks = [None] * len(spec.layers)
+    bs = [None] * len(spec.layers)
+    for k, wshape, bshape, off in layout:
+        nw, nb = int(np.prod(wshape)), int(np.prod(bshape))
+        ks[k] = flat[off:off + nw].reshape(wshape).copy()
+        bs[k] = flat[off + nw:off + nw + nb].reshape(bshape).copy()
+    return ks, bs
+
+
+def shard(n_images: int, rank: int, world: int) -> range:
+    """Contiguous image shard of this rank (balanced, deterministic)."""
+    base, extra = divmod(n_images, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def allreduce_sum(tensor, group=None):
+    """In-place SUM all-reduce of the gradient bucket (no-op when not distributed)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+    return tensor
+
+
+class DataParallelTrainer:
+    """One DenseNet per rank + bucket all-reduce + SGD, optionally as one CUDA graph.
+
+    The all-reduce stays outside the captured graph (NCCL calls are issued on
+    the same stream right after the graph replay), so graph replay and the
+    collective are ordered on one stream with no host synchronisation.
+    """
+
+    def __init__(self, plan: DensePlan, batch_per_rank: int, height: int, width: int,
+                 lr: float = 0.0, group=None, dtype=None, use_graph: bool = True):
+        import torch
+        import torch.distributed as dist
+
+        from .engine import DenseNet
+        self.net = DenseNet(plan, batch_per_rank, height, width, dtype=dtype, train=True)
+        self.group = group
+        self.lr = lr
+        self.distributed = dist.is_available() and dist.is_initialized()
+        if self.distributed and dist.get_world_size(group) > 1:
+            # every rank starts from rank 0's weights (seeded specs agree anyway)
+            dist.broadcast(self.net.param_flat, src=0, group=group)
+        self._graph = None
+        self._use_graph = use_graph
+        self._torch = torch
+
+    def load_batch(self, images, targets, masks):
+        n = self.net
+        n.set_input(images)
+        n.target.copy_(targets)
+        n.mask.copy_(masks)
+
+    def _compute(self):
+        n = self.net
+        n.forward()
+        n.loss_delta()
+        n.backward()
+
+    def step(self):
+        """forward + masked loss + backward [+ all-reduce] [+ SGD] on the loaded batch."""
+        if self._use_graph:
+            if self._graph is None:
+                self._graph = self.net.capture(self._compute)
+            self._graph.replay()
+        else:
+            self._compute()
+        allreduce_sum(self.net.grad_flat, self.group)
+        if self.lr:
+            self.net.sgd_step(self.lr)
+
+    def forward_only(self):
+        self.net.forward()
+        return self.net.output

@@ -24,3 +24,12 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """Build libdenseprop_b200.so in-tree if this checkout has not built it yet."""
+    from paper_1412_4526_b200 import build
+    if not os.path.exists(build.LIB):
+        build.build()
+    yield

@@ -1,0 +1,270 @@
+"""Whole-network parity of the B200 path (GPU).
+
+* drop-in `dense_forward` / `dense_backward` against the golden vectors of the
+  real reference (tests/golden/): bit-exact maps/argmax/input-delta for
+  relu/identity nets, toleranced where np.tanh's last bit or the weight-gradient
+  reduction order enters;
+* teacher-forced layers: each plan layer fed the reference's own layer input
+  reproduces the reference's output and argmax bit-for-bit;
+* the fused batched engine (DenseNet) against per-image oracle runs, the config
+  networks at full size against the oracle C port, and size-independent
+  properties (determinism, mask additivity) at the largest sizes;
+* dense == patch-by-patch scan on small cases.
+"""
+
+import numpy as np
+import pytest
+
+from golden_io import manifest, net_case, net_names, rel_err
+from oracle import engine_np, kernels_c
+from oracle.netdesc import read_spec
+
+pytestmark = pytest.mark.gpu
+
+TAGS = {"f32": np.float32, "f64": np.float64}
+# normwise tolerances (north star: fp32 rel err <= 1e-4)
+FWD_TOL = {"f32": 1e-5, "f64": 1e-12}
+GRAD_TOL = {"f32": 1e-4, "f64": 1e-10}
+
+
+@pytest.fixture(scope="module")
+def dp():
+    import paper_1412_4526_b200 as dp
+    return dp
+
+
+def _has_tanh(spec):
+    return any(getattr(l, "kind", None) == "tanh" for l in spec.layers)
+
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("name", net_names())
+def test_dropin_matches_reference(dp, name, tag):
+    meta = manifest()["nets"][name]
+    g = net_case(name, tag)
+    spec = dp.parse_spec(meta["spec"])
+    plan = dp.compile_plan(spec)
+    cache = dp.dense_forward(plan, g["image"])
+    exact = not _has_tanh(spec)
+    assert len(cache.inputs) == meta["n_layers"]
+    assert sorted(cache.argmax) == meta["argmax_layers"]
+    for k, x in enumerate(cache.inputs):
+        ref = g[f"in{k:02d}"]
+        assert x.shape == ref.shape and x.dtype == ref.dtype
+        if exact:
+            assert np.array_equal(x, ref), f"layer {k} input"
+        else:
+            assert rel_err(x, ref) < FWD_TOL[tag], f"layer {k} input"
+    if exact:
+        for k, a in cache.argmax.items():
+            assert np.array_equal(a, g[f"arg{k:02d}"])
+        assert np.array_equal(cache.output, g["output"])
+    else:
+        assert rel_err(cache.output, g["output"]) < FWD_TOL[tag]
+    for m in ("m5", "all"):
+        mask = dp.ErrorMask.from_bitmap(g[f"mask_{m}"])
+        grads = dp.dense_backward(plan, cache, g["delta"], mask, with_input_grad=True)
+        for k in range(len(spec.layers)):
+            if grads.kernel[k] is None:
+                assert f"{m}/dw{k:02d}" not in g
+                continue
+            assert grads.kernel[k].dtype == g["delta"].dtype
+            assert rel_err(grads.kernel[k], g[f"{m}/dw{k:02d}"]) < GRAD_TOL[tag]
+            assert rel_err(grads.bias[k], g[f"{m}/db{k:02d}"]) < GRAD_TOL[tag]
+        ref_in = g[f"{m}/input_delta"]
+        if exact:
+            assert np.array_equal(grads.input_delta, ref_in)
+        else:
+            assert rel_err(grads.input_delta, ref_in) < GRAD_TOL[tag]
+
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("name", net_names())
+def test_teacher_forced_layers_bit_exact(dp, name, tag):
+    """Each layer fed the reference's own input: conv/pool outputs and argmax bit-exact."""
+    from paper_1412_4526_b200.forward import run_plan_layer
+    meta = manifest()["nets"][name]
+    g = net_case(name, tag)
+    plan = dp.compile_plan(dp.parse_spec(meta["spec"]))
+    n = meta["n_layers"]
+    for k, layer in enumerate(plan.layers):
+        y, arg = run_plan_layer(plan, k, g[f"in{k:02d}"])
+        ref = g[f"in{k + 1:02d}"] if k + 1 < n else g["output"]
+        if getattr(layer, "kind", None) == "tanh":
+            assert rel_err(y, ref) < (1e-7 if tag == "f32" else 1e-15)
+        else:
+            assert np.array_equal(y, ref), f"layer {k}"
+        if arg is not None:
+            assert np.array_equal(arg, g[f"arg{k:02d}"])
+
+
+@pytest.mark.parametrize("name", ["mixed", "example", "plain_small", "even_patch", "rand1017",
+                                  "strided"])
+def test_gpu_dense_equals_patch_scan(dp, name):
+    meta = manifest()["nets"][name]
+    g = net_case(name, "f64")
+    plan = dp.compile_plan(dp.parse_spec(meta["spec"]))
+    net = read_spec(meta["spec"])
+    side = meta["side"]
+    pixels = [(y, x) for y in range(side) for x in range(0, side, 3)]
+    dense = dp.dense_forward(plan, g["image"]).output
+    scanned = engine_np.scan_forward(net, g["image"], pixels)
+    ys, xs = zip(*pixels)
+    assert np.max(np.abs(dense[:, ys, xs] - scanned[:, ys, xs])) < 1e-13
+
+
+def _c1_text(cin):
+    return (f"input channels={cin}\n"
+            f"conv out=16 in={cin} k=6 stride=1 weights=seed:1\n"
+            "pool kind=max k=2 stride=2\nnonlin kind=tanh\n"
+            "conv out=32 in=16 k=5 stride=1 weights=seed:2\n"
+            "pool kind=max k=2 stride=2\nnonlin kind=tanh\n"
+            "conv out=10 in=32 k=4 stride=1 weights=seed:3\n")
+
+
+C4_TEXT = ("input channels=3\n"
+           "conv out=48 in=3 k=5 stride=2 weights=seed:1\nnonlin kind=relu\n"
+           "conv out=64 in=48 k=3 stride=1 weights=seed:2\nnonlin kind=relu\n"
+           "pool kind=max k=2 stride=2\n"
+           "conv out=96 in=64 k=3 stride=1 weights=seed:3\nnonlin kind=relu\n"
+           "pool kind=max k=2 stride=2\n"
+           "conv out=128 in=96 k=3 stride=2 weights=seed:4\nnonlin kind=relu\n"
+           "pool kind=max k=2 stride=2\n"
+           "conv out=8 in=128 k=3 stride=1 weights=seed:5\n")
+
+
+def _engine_vs_oracle(dp, text, side, batch, dt, frac, seed=0, tol_f=None, tol_g=None):
+    import torch
+    from paper_1412_4526_b200.engine import DenseNet
+    spec = dp.parse_spec(text)
+    plan = dp.compile_plan(spec)
+    net = read_spec(text)
+    rng = np.random.default_rng(seed)
+    imgs = rng.uniform(-0.5, 0.5, (batch, spec.input_channels, side, side)).astype(dt)
+    co = spec.output_channels
+    targets = rng.uniform(-1, 1, (batch, co, side, side)).astype(dt)
+    masks = np.zeros((batch, side, side), dtype=np.uint8)
+    for b in range(batch):
+        k = max(1, int(frac * side * side))
+        flat = rng.choice(side * side, size=k, replace=False)
+        masks[b].flat[flat] = 1
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    eng = DenseNet(plan, batch, side, side, dtype=tdt)
+    eng.set_input(torch.from_numpy(imgs).cuda())
+    eng.target.copy_(torch.from_numpy(targets))
+    eng.mask.copy_(torch.from_numpy(masks))
+    eng.forward()
+    eng.loss_delta()
+    eng.backward()
+    torch.cuda.synchronize()
+    out = eng.output.cpu().numpy()
+    from paper_1412_4526_b200 import trainer
+    ks, bs = trainer.unflatten(spec, eng.grad_flat.cpu().numpy())
+    acc_k = [None] * len(spec.layers)
+    acc_b = [None] * len(spec.layers)
+    for b in range(batch):
+        cache = engine_np.dense_forward(net, imgs[b], kernels_c, threads=8)
+        assert rel_err(out[b], cache.output) < (tol_f or FWD_TOL["f32" if dt == np.float32 else "f64"])
+        delta = (cache.output - targets[b]).astype(dt)
+        kg, bg, _ = engine_np.dense_backward(net, cache, delta, masks[b].astype(bool), kernels_c,
+                                             threads=8)
+        for k in range(len(spec.layers)):
+            if kg[k] is not None:
+                acc_k[k] = kg[k].astype(np.float64) + (0 if acc_k[k] is None else acc_k[k])
+                acc_b[k] = bg[k].astype(np.float64) + (0 if acc_b[k] is None else acc_b[k])
+    for k in range(len(spec.layers)):
+        if acc_k[k] is not None:
+            tg = tol_g or GRAD_TOL["f32" if dt == np.float32 else "f64"]
+            assert rel_err(ks[k], acc_k[k]) < tg, f"dw layer {k}"
+            assert rel_err(bs[k], acc_b[k]) < tg, f"db layer {k}"
+    return eng
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_fused_engine_batch_small(dp, dt):
+    _engine_vs_oracle(dp, _c1_text(1), 40, 3, dt, 0.05)
+
+
+def test_fused_engine_mixed_pools(dp):
+    text = manifest()["nets"]["mixed"]["spec"]
+    _engine_vs_oracle(dp, text, 33, 2, np.float64, 0.2)
+    _engine_vs_oracle(dp, text, 33, 2, np.float32, 1.0)
+
+
+def test_config_c2_full_size(dp):
+    """c2: 3x256x256, forward + masked backward with 1% of pixels (BASELINE.json configs[1])."""
+    _engine_vs_oracle(dp, _c1_text(3), 256, 2, np.float32, 0.01)
+
+
+def test_config_c4_reduced_side(dp):
+    """c4 network (strided convs, relu) vs the oracle at side 160."""
+    _engine_vs_oracle(dp, C4_TEXT, 160, 1, np.float32, 0.02)
+
+
+def test_config_c4_full_size_properties(dp):
+    """c4 at 1024x1024: determinism and mask additivity (oracle too slow at this size)."""
+    import torch
+    from paper_1412_4526_b200.engine import DenseNet
+    spec = dp.parse_spec(C4_TEXT)
+    plan = dp.compile_plan(spec)
+    side = 1024
+    eng = DenseNet(plan, 1, side, side)
+    rng = np.random.default_rng(3)
+    img = torch.from_numpy(rng.uniform(-0.5, 0.5, (1, 3, side, side)).astype(np.float32)).cuda()
+    eng.set_input(img)
+    eng.target.copy_(torch.from_numpy(rng.uniform(-1, 1, (1, 8, side, side)).astype(np.float32)))
+    a = np.zeros((1, side, side), np.uint8)
+    b = np.zeros((1, side, side), np.uint8)
+    a.flat[rng.choice(side * side, 5000, replace=False)] = 1
+    b.flat[rng.choice(side * side, 5000, replace=False)] = 1
+    b[a == 1] = 0
+    grads = {}
+    for name, m in (("a", a), ("b", b), ("ab", a | b), ("a2", a)):
+        eng.mask.copy_(torch.from_numpy(m))
+        eng.forward()
+        eng.loss_delta()
+        eng.backward()
+        grads[name] = eng.grad_flat.double().cpu().numpy()
+        if name == "a":
+            out1 = eng.output.clone()
+    torch.cuda.synchronize()
+    assert np.array_equal(grads["a"], grads["a2"])                 # run-to-run bitwise
+    assert torch.equal(out1, eng.output)
+    assert rel_err(grads["a"] + grads["b"], grads["ab"]) < 1e-4    # linearity in the mask
+    assert np.isfinite(grads["ab"]).all() and np.abs(grads["ab"]).max() > 0
+
+
+def test_graph_capture_replays_same_step(dp):
+    import torch
+    from paper_1412_4526_b200.trainer import DataParallelTrainer
+    spec = dp.parse_spec(_c1_text(3))
+    plan = dp.compile_plan(spec)
+    tr = DataParallelTrainer(plan, 2, 64, 64, lr=0.0, use_graph=True)
+    rng = np.random.default_rng(1)
+    imgs = torch.from_numpy(rng.uniform(-0.5, 0.5, (2, 3, 64, 64)).astype(np.float32)).cuda()
+    tgts = torch.from_numpy(rng.uniform(-1, 1, (2, 10, 64, 64)).astype(np.float32)).cuda()
+    masks = torch.from_numpy((rng.random((2, 64, 64)) < 0.3).astype(np.uint8)).cuda()
+    tr.load_batch(imgs, tgts, masks)
+    tr.net.forward()
+    tr.net.loss_delta()
+    tr.net.backward()
+    eager = tr.net.grad_flat.clone()
+    tr.step()
+    tr.step()
+    torch.cuda.synchronize()
+    assert torch.equal(eager, tr.net.grad_flat)
+
+
+def test_dropin_errors(dp):
+    plan = dp.compile_plan(dp.parse_spec(manifest()["nets"]["example"]["spec"]))
+    with pytest.raises(ValueError, match="channels"):
+        dp.dense_forward(plan, np.zeros((2, 5, 5)))
+    with pytest.raises(TypeError):
+        dp.dense_forward(plan, np.zeros((1, 5, 5), dtype=np.int64))
+    cache = dp.dense_forward(plan, np.zeros((1, 5, 5)))
+    with pytest.raises(ValueError):
+        dp.dense_backward(plan, cache, np.zeros((1, 4, 4)), dp.ErrorMask.full(5, 5))
+    with pytest.raises(ValueError):
+        dp.dense_backward(plan, cache, np.zeros((1, 5, 5)), dp.ErrorMask.full(4, 4))
+    g = dp.dense_backward(plan, cache, np.ones((1, 5, 5)), dp.ErrorMask.of(5, 5, []))
+    assert g.max_abs() == 0.0

@@ -30,7 +30,7 @@
  *    dispatch: forward.py:33-38, backward.py:136-146).
  *  - Exactness: conv forward, conv data-gradient, both pools and relu are
  *    bit-identical to the reference's compiled backend in fp32 and fp64 (same
- *    per-entry operation order, no FMA contraction); tanh is within 1 ulp of
+ *    per-entry operation order, no FMA contraction); tanh is within 2 ulp of
  *    numpy; weight/bias gradients are deterministic (fixed-order split
  *    reduction) and agree to reduction-order rounding.
  */

@@ -21,13 +21,14 @@ __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, 
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 
 // tanh: fp32 evaluates in fp64 and rounds once (<= 0.5 ulp + tiny), so it is
-// within 1 ulp of numpy's float32 tanh (reference forward.py:71).
+// within 2 ulp of numpy's float32 tanh (reference forward.py:71).
 __device__ __forceinline__ float dp_tanh(float x) { return (float)tanh((double)x); }
 __device__ __forceinline__ double dp_tanh(double x) { return tanh(x); }
 
-// relu == np.maximum(x, 0): returns x when x >= 0 (keeps -0.0) or x is NaN.
+// relu == np.maximum(x, 0) bit for bit: x when x > 0 or x is NaN, else +0.0
+// (numpy returns the second operand on ties, so maximum(-0.0, 0) is +0.0).
 template <typename T>
-__device__ __forceinline__ T dp_relu(T x) { return (x >= T(0) || x != x) ? x : T(0); }
+__device__ __forceinline__ T dp_relu(T x) { return (x > T(0) || x != x) ? x : T(0); }
 
 template <typename T>
 __device__ __forceinline__ T apply_nonlin(T v, int kind) {

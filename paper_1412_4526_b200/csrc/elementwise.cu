@@ -2,7 +2,7 @@
 //
 // nonlin fwd/bwd ... reference forward.py:69-76 / backward.py:172-182 (numpy
 //                    there, outside the kernel boundary); relu and identity
-//                    are bit-exact, tanh within 1 ulp of numpy.
+//                    are bit-exact, tanh within 2 ulp of numpy.
 // mask / loss ...... backward.py:110-118 (keep the selected pixels across all
 //                    channels, zero the rest) fused with the squared-error
 //                    delta output - target (cli.py:218).  A dense bitmap: the

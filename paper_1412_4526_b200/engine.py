@@ -61,23 +61,54 @@ def _lib_dev():
 # thin typed wrappers over the device C ABI (batched NCHW tensors)
 # ---------------------------------------------------------------------------
 
+class _Rec:
+    """Counts kernel launches and, when profiling, brackets each call with CUDA events."""
+
+    def __init__(self, name, kernels, bound, work):
+        self.name, self.kernels, self.bound, self.work = name, kernels, bound, work
+
+    def __enter__(self):
+        ops.launches += self.kernels
+        if ops.profile is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e1 = torch.cuda.Event(enable_timing=True)
+            self.e0.record(torch.cuda.current_stream())
+        return self
+
+    def __exit__(self, *exc):
+        if ops.profile is not None and exc[0] is None:
+            self.e1.record(torch.cuda.current_stream())
+            ops.profile.append((self.name, self.bound, self.work, self.e0, self.e1))
+
+
+def _nbytes(*ts):
+    return sum(t.numel() * t.element_size() for t in ts if t is not None)
+
+
 class ops:
-    """Each method enqueues one kernel on the current torch stream."""
+    """Each method enqueues one kernel (two for the weight gradient) on the current
+    torch stream.  `ops.launches` counts launches; set `ops.profile = []` to record
+    (name, bound, algorithmic work, start event, end event) per call."""
+
+    launches = 0
+    profile = None
 
     @staticmethod
     def conv_forward(x, w, b, y, k, d, nonlin=_lib.DP_IDENTITY):
-        n, ci, h, wd = x.shape
-        _lib.check(_lib_dev().dp_conv_forward(_code(x), _ptr(x), _ptr(w), _ptr(b), _ptr(y), n,
-                                              ci, h, wd, w.shape[0], k, d, nonlin, _stream()),
-                   "conv_forward")
+        with _Rec('conv_forward', 1, 'tensor', 2 * y.numel() * x.shape[1] * k * k):
+            n, ci, h, wd = x.shape
+            _lib.check(_lib_dev().dp_conv_forward(_code(x), _ptr(x), _ptr(w), _ptr(b), _ptr(y), n,
+                                                  ci, h, wd, w.shape[0], k, d, nonlin, _stream()),
+                       "conv_forward")
 
     @staticmethod
     def conv_backward_data(dy, w, dx, k, d, gate=None, gate_kind=_lib.DP_IDENTITY):
-        n, co, ho, wo = dy.shape
-        _lib.check(_lib_dev().dp_conv_backward_data(_code(dy), _ptr(dy), _ptr(w), _ptr(dx), n,
-                                                    co, ho, wo, w.shape[1], k, d, _ptr(gate),
-                                                    gate_kind if gate is not None else 0,
-                                                    _stream()), "conv_backward_data")
+        with _Rec('conv_backward_data', 1, 'tensor', 2 * dy.numel() * w.shape[1] * k * k):
+            n, co, ho, wo = dy.shape
+            _lib.check(_lib_dev().dp_conv_backward_data(_code(dy), _ptr(dy), _ptr(w), _ptr(dx), n,
+                                                        co, ho, wo, w.shape[1], k, d, _ptr(gate),
+                                                        gate_kind if gate is not None else 0,
+                                                        _stream()), "conv_backward_data")
 
     @staticmethod
     def wgrad_workspace(x, co, k, d) -> int:
@@ -87,76 +118,87 @@ class ops:
 
     @staticmethod
     def conv_backward_kernel(x, dy, dw, db, k, d, ws):
-        n, ci, hi, wi = x.shape
-        co = dy.shape[1]
-        _lib.check(_lib_dev().dp_conv_backward_kernel(_code(x), _ptr(x), _ptr(dy), _ptr(dw),
-                                                      _ptr(db), n, ci, hi, wi, co, k, d,
-                                                      _ptr(ws), ws.numel() * ws.element_size(),
-                                                      _stream()), "conv_backward_kernel")
+        with _Rec('conv_backward_kernel', 2, 'tensor', 2 * dy.numel() * x.shape[1] * k * k):
+            n, ci, hi, wi = x.shape
+            co = dy.shape[1]
+            _lib.check(_lib_dev().dp_conv_backward_kernel(_code(x), _ptr(x), _ptr(dy), _ptr(dw),
+                                                          _ptr(db), n, ci, hi, wi, co, k, d,
+                                                          _ptr(ws), ws.numel() * ws.element_size(),
+                                                          _stream()), "conv_backward_kernel")
 
     @staticmethod
     def maxpool_forward(x, y, arg, p, d, nonlin=_lib.DP_IDENTITY):
-        n, c, h, w = x.shape
-        _lib.check(_lib_dev().dp_maxpool_forward(_code(x), _ptr(x), _ptr(y), _ptr(arg),
-                                                 arg.element_size(), n, c, h, w, p, d, nonlin,
-                                                 _stream()), "maxpool_forward")
+        with _Rec('maxpool_forward', 1, 'hbm', _nbytes(x, y, arg)):
+            n, c, h, w = x.shape
+            _lib.check(_lib_dev().dp_maxpool_forward(_code(x), _ptr(x), _ptr(y), _ptr(arg),
+                                                     arg.element_size(), n, c, h, w, p, d, nonlin,
+                                                     _stream()), "maxpool_forward")
 
     @staticmethod
     def maxpool_backward(dy, arg, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY):
-        n, c, ho, wo = dy.shape
-        _lib.check(_lib_dev().dp_maxpool_backward(_code(dy), _ptr(dy), _ptr(arg),
-                                                  arg.element_size(), _ptr(dx), n, c, ho, wo, p,
-                                                  d, dx.shape[2], dx.shape[3], _ptr(gate),
-                                                  gate_kind if gate is not None else 0,
-                                                  _stream()), "maxpool_backward")
+        with _Rec('maxpool_backward', 1, 'hbm', _nbytes(dy, arg, dx, gate)):
+            n, c, ho, wo = dy.shape
+            _lib.check(_lib_dev().dp_maxpool_backward(_code(dy), _ptr(dy), _ptr(arg),
+                                                      arg.element_size(), _ptr(dx), n, c, ho, wo, p,
+                                                      d, dx.shape[2], dx.shape[3], _ptr(gate),
+                                                      gate_kind if gate is not None else 0,
+                                                      _stream()), "maxpool_backward")
 
     @staticmethod
     def avgpool_forward(x, y, p, d, nonlin=_lib.DP_IDENTITY):
-        n, c, h, w = x.shape
-        _lib.check(_lib_dev().dp_avgpool_forward(_code(x), _ptr(x), _ptr(y), n, c, h, w, p, d,
-                                                 nonlin, _stream()), "avgpool_forward")
+        with _Rec('avgpool_forward', 1, 'hbm', _nbytes(x, y)):
+            n, c, h, w = x.shape
+            _lib.check(_lib_dev().dp_avgpool_forward(_code(x), _ptr(x), _ptr(y), n, c, h, w, p, d,
+                                                     nonlin, _stream()), "avgpool_forward")
 
     @staticmethod
     def avgpool_backward(dy, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY):
-        n, c, ho, wo = dy.shape
-        _lib.check(_lib_dev().dp_avgpool_backward(_code(dy), _ptr(dy), _ptr(dx), n, c, ho, wo,
-                                                  p, d, dx.shape[2], dx.shape[3], _ptr(gate),
-                                                  gate_kind if gate is not None else 0,
-                                                  _stream()), "avgpool_backward")
+        with _Rec('avgpool_backward', 1, 'hbm', _nbytes(dy, dx, gate)):
+            n, c, ho, wo = dy.shape
+            _lib.check(_lib_dev().dp_avgpool_backward(_code(dy), _ptr(dy), _ptr(dx), n, c, ho, wo,
+                                                      p, d, dx.shape[2], dx.shape[3], _ptr(gate),
+                                                      gate_kind if gate is not None else 0,
+                                                      _stream()), "avgpool_backward")
 
     @staticmethod
     def nonlin_forward(x, y, kind):
-        _lib.check(_lib_dev().dp_nonlin_forward(_code(x), _ptr(x), _ptr(y), x.numel(), kind,
-                                                _stream()), "nonlin_forward")
+        with _Rec('nonlin_forward', 1, 'hbm', _nbytes(x, y)):
+            _lib.check(_lib_dev().dp_nonlin_forward(_code(x), _ptr(x), _ptr(y), x.numel(), kind,
+                                                    _stream()), "nonlin_forward")
 
     @staticmethod
     def nonlin_backward(dy, x, dx, kind, x_is_output=False):
-        _lib.check(_lib_dev().dp_nonlin_backward(_code(dy), _ptr(dy), _ptr(x), _ptr(dx),
-                                                 dy.numel(), kind, int(x_is_output), _stream()),
-                   "nonlin_backward")
+        with _Rec('nonlin_backward', 1, 'hbm', _nbytes(dy, x, dx)):
+            _lib.check(_lib_dev().dp_nonlin_backward(_code(dy), _ptr(dy), _ptr(x), _ptr(dx),
+                                                     dy.numel(), kind, int(x_is_output), _stream()),
+                       "nonlin_backward")
 
     @staticmethod
     def mask_delta(a, mask, out, target=None):
-        n, c, h, w = a.shape
-        _lib.check(_lib_dev().dp_mask_delta(_code(a), _ptr(a), _ptr(target), _ptr(mask),
-                                            _ptr(out), n, c, h, w, _stream()), "mask_delta")
+        with _Rec('mask_delta', 1, 'hbm', _nbytes(a, mask, out, target)):
+            n, c, h, w = a.shape
+            _lib.check(_lib_dev().dp_mask_delta(_code(a), _ptr(a), _ptr(target), _ptr(mask),
+                                                _ptr(out), n, c, h, w, _stream()), "mask_delta")
 
     @staticmethod
     def pad(src, dst, top, bottom, left, right):
-        n, c, h, w = src.shape
-        _lib.check(_lib_dev().dp_pad(_code(src), _ptr(src), _ptr(dst), n, c, h, w, top, bottom,
-                                     left, right, _stream()), "pad")
+        with _Rec('pad', 1, 'hbm', _nbytes(src, dst)):
+            n, c, h, w = src.shape
+            _lib.check(_lib_dev().dp_pad(_code(src), _ptr(src), _ptr(dst), n, c, h, w, top, bottom,
+                                         left, right, _stream()), "pad")
 
     @staticmethod
     def crop(src, dst, top, left):
-        n, c, hs, ws = src.shape
-        _lib.check(_lib_dev().dp_crop(_code(src), _ptr(src), _ptr(dst), n, c, hs, ws, top, left,
-                                      dst.shape[2], dst.shape[3], _stream()), "crop")
+        with _Rec('crop', 1, 'hbm', 2 * _nbytes(dst)):
+            n, c, hs, ws = src.shape
+            _lib.check(_lib_dev().dp_crop(_code(src), _ptr(src), _ptr(dst), n, c, hs, ws, top, left,
+                                          dst.shape[2], dst.shape[3], _stream()), "crop")
 
     @staticmethod
     def sgd(param, grad, lr):
-        _lib.check(_lib_dev().dp_sgd_update(_code(param), _ptr(param), _ptr(grad),
-                                            param.numel(), float(lr), _stream()), "sgd")
+        with _Rec('sgd', 1, 'hbm', 3 * _nbytes(param)):
+            _lib.check(_lib_dev().dp_sgd_update(_code(param), _ptr(param), _ptr(grad),
+                                                param.numel(), float(lr), _stream()), "sgd")
 
 
 def _nl(kind: str) -> int:
@@ -465,9 +507,17 @@ class DenseNet:
                 fn()
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
+        before = ops.launches
         with torch.cuda.graph(g):
             fn()
+        self.graph_kernels = ops.launches - before
         return g
+
+    def activation_bytes(self) -> int:
+        ts = [self.x0] + list(self.acts) + list(self.args.values())
+        if self.train:
+            ts += list(self._dbuf) + [self._ws, self.target, self.delta_last, self.mask]
+        return _nbytes(*ts)
 
     def conv_flops_per_image(self) -> dict:
         """Algorithmic conv FLOPs per image: fwd, bwd (no layer-0 dgrad)."""
@@ -480,6 +530,40 @@ class DenseNet:
                 fwd += f
                 bwd += f if gi == 0 else 2 * f
         return {"fwd": fwd, "bwd": bwd}
+
+
+def profile_step(trainer, reps=5):
+    """Per-kernel CUDA-event durations of eager training steps (forward, loss, backward).
+
+    Returns {"kernels": [{name, bound, ms, flops|bytes, achieved}], "step_ms"}; the
+    k-th launch of every step is averaged over `reps` steps.
+    """
+    net = trainer.net if hasattr(trainer, "net") else trainer
+    ops.profile = []
+    try:
+        for _ in range(reps):
+            net.forward()
+            net.loss_delta()
+            net.backward()
+        torch.cuda.synchronize()
+        rec = ops.profile
+    finally:
+        ops.profile = None
+    per = len(rec) // reps
+    out = []
+    for i in range(per):
+        entries = rec[i::per]
+        ms = float(np.mean([e0.elapsed_time(e1) for _, _, _, e0, e1 in entries]))
+        name, bound, work = entries[0][:3]
+        item = {"name": f"{i:02d}:{name}", "bound": bound, "ms": ms}
+        if bound == "tensor":
+            item["flops"] = int(work)
+            item["tflops"] = work / (ms / 1e3) / 1e12 if ms > 0 else None
+        else:
+            item["bytes"] = int(work)
+            item["gbs"] = work / (ms / 1e3) / 1e9 if ms > 0 else None
+        out.append(item)
+    return {"kernels": out, "step_ms": float(sum(k["ms"] for k in out))}
 
 
 def ensure_nonlin_spec(layer) -> bool:

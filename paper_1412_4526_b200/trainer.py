@@ -117,6 +117,10 @@ class DataParallelTrainer:
         if self.lr:
             self.net.sgd_step(self.lr)
 
+    @property
+    def graph_kernel_count(self) -> int:
+        return getattr(self.net, "graph_kernels", 0)
+
     def forward_only(self):
         self.net.forward()
         return self.net.output

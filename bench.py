@@ -339,8 +339,10 @@ def main():
     roof.update({"kernel": top["name"], "ms_per_launch": top["ms"],
                  "share_of_step": top["ms"] / prof["step_ms"], "peak_source": peaks["source"],
                  "traffic": None,
-                 "note": "CUDA-core exact-order conv (FMUL+FADD, no FMA) measured against the "
-                         "dense bf16 tensor peak"})
+                 "note": ("tcgen05 kind::tf32 3xTF32 conv: algorithmic FLOPs (each MAC issues 3 "
+                          "TF32 MACs); peak = measured dense bf16 (TF32 dense is half of it)"
+                          if "_tc" in top["name"] else
+                          "CUDA-core conv measured against the dense bf16 tensor peak")})
 
     line = {
         "metric": METRIC, "value": value, "unit": "pixels/s", "n_gpus": world,
@@ -354,7 +356,9 @@ def main():
                    "parallelism": f"dp{world} (images sharded, NCCL all-reduce SUM)",
                    "l2": "working set >> L2 (activations %.1f GB per GPU)" %
                          (net.activation_bytes() / 1e9),
-                   "cuda_graph": tr._graph is not None},
+                   "cuda_graph": tr._graph is not None,
+                   "precision": net.precision,
+                   "conv_tiers": {str(k): v for k, v in net.kernel_plan().items()}},
         "forward": {"value": px_per_step / (ms_fwd / args.steps / 1e3), "unit": "pixels/s",
                     "ms_per_step": ms_fwd / args.steps},
         "e2e": {"value": px_per_step / (ms_e2e / args.steps / 1e3), "unit": "pixels/s",

@@ -113,6 +113,22 @@ int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx,
                           int n, int cout, int ho, int wo, int cin, int k, int d,
                           const void *gate, int gate_kind, void *stream);
 
+/* ---- fast tier: tcgen05 tensor cores, fp32 in/out, 3xTF32 products (~1e-7 relative
+ * to fp32; the reference tolerance for this path is 1e-4).  Same argument meaning as
+ * dp_conv_forward / dp_conv_backward_data; DP_F32 only.  `workspace` (16-byte
+ * aligned, dp_conv_fast_workspace bytes) receives the packed hi/lo weights.  Returns
+ * DP_ERR_UNSUPPORTED when the packed weights exceed the kernel's shared-memory budget
+ * (caller then uses the exact CUDA-core entry points). */
+size_t dp_conv_fast_workspace(int reduce_channels, int out_channels, int k);
+int dp_conv_fast_supported(int reduce_channels, int out_channels, int k);
+int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float *y, int n,
+                         int cin, int h, int w, int cout, int k, int d, int nonlin,
+                         void *workspace, size_t workspace_bytes, void *stream);
+int dp_conv_backward_data_fast(const float *dy, const float *wt, float *dx, int n, int cout,
+                               int ho, int wo, int cin, int k, int d, const float *gate,
+                               int gate_kind, void *workspace, size_t workspace_bytes,
+                               void *stream);
+
 /* workspace bytes for dp_conv_backward_kernel at this shape */
 size_t dp_conv_backward_kernel_workspace(int dtype, int n, int cin, int hi, int wi,
                                          int cout, int k, int d);

@@ -41,6 +41,12 @@ SIGNATURES = {
     "dp_conv_forward": (_i, [_i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp]),
     "dp_conv_backward_data": (_i, [_i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _i,
                                    _vp]),
+    "dp_conv_fast_workspace": (_sz, [_i, _i, _i]),
+    "dp_conv_fast_supported": (_i, [_i, _i, _i]),
+    "dp_conv_forward_fast": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _sz,
+                                  _vp]),
+    "dp_conv_backward_data_fast": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _i,
+                                        _vp, _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel": (_i, [_i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
                                      _sz, _vp]),

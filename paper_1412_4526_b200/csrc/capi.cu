@@ -25,6 +25,12 @@ template <typename T>
 int conv_backward_kernel_t(const T *, const T *, T *, T *, int, int, int, int, int, int, int,
                            void *, size_t, cudaStream_t);
 size_t wgrad_workspace_bytes(int elem, int n, int cin, int hi, int wi, int cout, int k, int d);
+size_t tc_conv_workspace(int R, int Q, int l);
+bool tc_conv_supported(int R, int Q, int l);
+int tc_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
+                    int, int, int, void *, size_t, cudaStream_t);
+int tc_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
+                          int, const float *, int, void *, size_t, cudaStream_t);
 template <typename T>
 int maxpool_forward_t(const T *, T *, void *, int, int, int, int, int, int, int, int,
                       cudaStream_t);
@@ -211,6 +217,44 @@ int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx, i
                        conv_backward_data_t<double>((const double *)dy, (const double *)wt,
                                                     (double *)dx, n, cout, ho, wo, cin, k, d,
                                                     (const double *)gate, gate_kind, st));
+}
+
+size_t dp_conv_fast_workspace(int reduce_channels, int out_channels, int k) {
+    if (reduce_channels < 1 || out_channels < 1 || k < 1) return 0;
+    return tc_conv_workspace(reduce_channels, out_channels, k);
+}
+
+int dp_conv_fast_supported(int reduce_channels, int out_channels, int k) {
+    if (reduce_channels < 1 || out_channels < 1 || k < 1) return 0;
+    return tc_conv_supported(reduce_channels, out_channels, k) ? 1 : 0;
+}
+
+int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float *y, int n,
+                         int cin, int h, int w, int cout, int k, int d, int nonlin,
+                         void *workspace, size_t workspace_bytes, void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_nonlin(nonlin));
+    DP_TRY(check_window("dilated conv", h, w, k, d));
+    return tc_conv_forward(x, wt, b, y, n, cin, h, w, cout, k, d, nonlin, workspace,
+                           workspace_bytes, (cudaStream_t)stream);
+}
+
+int dp_conv_backward_data_fast(const float *dy, const float *wt, float *dx, int n, int cout,
+                               int ho, int wo, int cin, int k, int d, const float *gate,
+                               int gate_kind, void *workspace, size_t workspace_bytes,
+                               void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("delta height", ho));
+    DP_TRY(check_pos("delta width", wo));
+    DP_TRY(check_pos("kernel size", k));
+    DP_TRY(check_pos("dilation", d));
+    DP_TRY(check_nonlin(gate_kind));
+    return tc_conv_backward_data(dy, wt, dx, n, cout, ho, wo, cin, k, d, gate, gate_kind,
+                                 workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t dp_conv_backward_kernel_workspace(int dtype, int n, int cin, int hi, int wi, int cout,

@@ -111,6 +111,31 @@ class ops:
                                                         _stream()), "conv_backward_data")
 
     @staticmethod
+    def fast_supported(reduce_c, out_c, k) -> bool:
+        return bool(_lib_dev().dp_conv_fast_supported(reduce_c, out_c, k))
+
+    @staticmethod
+    def fast_workspace(reduce_c, out_c, k) -> int:
+        return int(_lib_dev().dp_conv_fast_workspace(reduce_c, out_c, k))
+
+    @staticmethod
+    def conv_forward_fast(x, w, b, y, k, d, nonlin, ws):
+        with _Rec('conv_forward_tc', 2, 'tensor', 2 * y.numel() * x.shape[1] * k * k):
+            n, ci, h, wd = x.shape
+            _lib.check(_lib_dev().dp_conv_forward_fast(
+                _ptr(x), _ptr(w), _ptr(b), _ptr(y), n, ci, h, wd, w.shape[0], k, d, nonlin,
+                _ptr(ws), ws.numel() * ws.element_size(), _stream()), "conv_forward_fast")
+
+    @staticmethod
+    def conv_backward_data_fast(dy, w, dx, k, d, ws, gate=None, gate_kind=_lib.DP_IDENTITY):
+        with _Rec('conv_backward_data_tc', 2, 'tensor', 2 * dy.numel() * w.shape[1] * k * k):
+            n, co, ho, wo = dy.shape
+            _lib.check(_lib_dev().dp_conv_backward_data_fast(
+                _ptr(dy), _ptr(w), _ptr(dx), n, co, ho, wo, w.shape[1], k, d, _ptr(gate),
+                gate_kind if gate is not None else 0, _ptr(ws), ws.numel() * ws.element_size(),
+                _stream()), "conv_backward_data_fast")
+
+    @staticmethod
     def wgrad_workspace(x, co, k, d) -> int:
         n, ci, hi, wi = x.shape
         return int(_lib_dev().dp_conv_backward_kernel_workspace(_code(x), n, ci, hi, wi, co, k,
@@ -315,12 +340,19 @@ class DenseNet:
     """
 
     def __init__(self, plan: DensePlan, batch: int, height: int, width: int,
-                 dtype=None, device="cuda", train=True):
+                 dtype=None, device="cuda", train=True, precision="fast"):
+        """precision: "fast" runs fp32 convolutions on the tcgen05 tensor cores with
+        3xTF32 products (normwise ~1e-6 vs fp32; reference tolerance 1e-4) wherever the
+        layer fits the kernel, "exact" uses the CUDA-core kernels that reproduce the
+        reference bit for bit.  fp64 is always exact."""
         if torch is None:
             raise _lib.KernelUnavailable("torch is required for the device engine")
         _lib.require_device()
         self.plan, self.batch, self.h, self.w = plan, batch, height, width
         self.dtype = dtype or torch.float32
+        if precision not in ("fast", "exact"):
+            raise ValueError("precision must be 'fast' or 'exact'")
+        self.precision = precision if self.dtype == torch.float32 else "exact"
         self.device = torch.device(device)
         self.train = train
         self.np_dtype = np.float32 if self.dtype == torch.float32 else np.float64
@@ -376,7 +408,31 @@ class DenseNet:
             self.mask = torch.zeros((N, height, width), dtype=torch.uint8, device=self.device)
             self.target = torch.zeros_like(self.output)
             self.delta_last = torch.empty_like(self.output)
+        # ---- tensor-core (fast tier) plan per conv group: (forward ok, data-grad ok)
+        self.tc = {}
+        tc_ws = 16
+        for gi, g in enumerate(self.groups):
+            if isinstance(g.op, DilatedConv) and self.precision == "fast":
+                ci, co, kk = g.op.base.in_channels, g.op.base.out_channels, g.op.base.kernel_size
+                f_ok = ops.fast_supported(ci, co, kk)
+                b_ok = train and gi > 0 and ops.fast_supported(co, ci, kk)
+                self.tc[gi] = (f_ok, b_ok)
+                if f_ok:
+                    tc_ws = max(tc_ws, ops.fast_workspace(ci, co, kk))
+                if b_ok:
+                    tc_ws = max(tc_ws, ops.fast_workspace(co, ci, kk))
+        self._tc_ws = torch.empty(tc_ws, dtype=torch.uint8, device=self.device)
         self.graph = None
+
+    def kernel_plan(self):
+        """Which conv kernels run where: {plan layer: {"forward": tier, "data_grad": tier}}."""
+        out = {}
+        for gi, g in enumerate(self.groups):
+            if isinstance(g.op, DilatedConv):
+                f_ok, b_ok = self.tc.get(gi, (False, False))
+                out[g.first] = {"forward": "tcgen05-3xtf32" if f_ok else "exact",
+                                "data_grad": "tcgen05-3xtf32" if b_ok else "exact"}
+        return out
 
     # ------------------------------------------------------------- parameters
     def load_weights_from_plan(self):
@@ -410,7 +466,11 @@ class DenseNet:
             op, act = g.op, _nl(g.act)
             if isinstance(op, DilatedConv):
                 wt, b = self.params[g.first]
-                ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
+                if self.tc.get(gi, (False, False))[0]:
+                    ops.conv_forward_fast(x, wt, b, y, op.base.kernel_size, op.dilation, act,
+                                          self._tc_ws)
+                else:
+                    ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
             elif isinstance(op, DilatedPool):
                 if op.base.kind == "max":
                     ops.maxpool_forward(x, y, self.args[gi], op.base.kernel_size, op.dilation,
@@ -464,7 +524,10 @@ class DenseNet:
                 if gi == 0 and not with_input_grad:
                     return None
                 dx = self._view(self._dbuf[ping], x_in.shape)
-                ops.conv_backward_data(delta, wt, dx, kk, d, gate, gk)
+                if self.tc.get(gi, (False, False))[1]:
+                    ops.conv_backward_data_fast(delta, wt, dx, kk, d, self._tc_ws, gate, gk)
+                else:
+                    ops.conv_backward_data(delta, wt, dx, kk, d, gate, gk)
             elif isinstance(op, DilatedPool):
                 dx = self._view(self._dbuf[ping], x_in.shape)
                 if op.base.kind == "max":

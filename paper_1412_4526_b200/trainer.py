@@ -77,12 +77,14 @@ class DataParallelTrainer:
     """
 
     def __init__(self, plan: DensePlan, batch_per_rank: int, height: int, width: int,
-                 lr: float = 0.0, group=None, dtype=None, use_graph: bool = True):
+                 lr: float = 0.0, group=None, dtype=None, use_graph: bool = True,
+                 precision: str = "fast"):
         import torch
         import torch.distributed as dist
 
         from .engine import DenseNet
-        self.net = DenseNet(plan, batch_per_rank, height, width, dtype=dtype, train=True)
+        self.net = DenseNet(plan, batch_per_rank, height, width, dtype=dtype, train=True,
+                            precision=precision)
         self.group = group
         self.lr = lr
         self.distributed = dist.is_available() and dist.is_initialized()

@@ -134,7 +134,11 @@ C4_TEXT = ("input channels=3\n"
            "conv out=8 in=128 k=3 stride=1 weights=seed:5\n")
 
 
-def _engine_vs_oracle(dp, text, side, batch, dt, frac, seed=0, tol_f=None, tol_g=None):
+def _engine_vs_oracle(dp, text, side, batch, dt, frac, seed=0, tol_f=None, tol_g=None,
+                      precision="fast", oracle_f64=False):
+    """Fused engine vs per-image oracle runs.  oracle_f64 evaluates the oracle in fp64
+    (at large activations the fp32 reference's own sequential
+    weight-gradient sums drift by ~1e-4, so fp64 is the yardstick there)."""
     import torch
     from paper_1412_4526_b200.engine import DenseNet
     spec = dp.parse_spec(text)
@@ -150,7 +154,9 @@ def _engine_vs_oracle(dp, text, side, batch, dt, frac, seed=0, tol_f=None, tol_g
         flat = rng.choice(side * side, size=k, replace=False)
         masks[b].flat[flat] = 1
     tdt = torch.float32 if dt == np.float32 else torch.float64
-    eng = DenseNet(plan, batch, side, side, dtype=tdt)
+    eng = DenseNet(plan, batch, side, side, dtype=tdt, precision=precision)
+    if tol_f is None and precision == "fast" and dt == np.float32:
+        tol_f = 5e-5  # 3xTF32 tensor-core convs: fp32 reassociation-level differences
     eng.set_input(torch.from_numpy(imgs).cuda())
     eng.target.copy_(torch.from_numpy(targets))
     eng.mask.copy_(torch.from_numpy(masks))
@@ -164,9 +170,10 @@ def _engine_vs_oracle(dp, text, side, batch, dt, frac, seed=0, tol_f=None, tol_g
     acc_k = [None] * len(spec.layers)
     acc_b = [None] * len(spec.layers)
     for b in range(batch):
-        cache = engine_np.dense_forward(net, imgs[b], kernels_c, threads=8)
+        odt = np.float64 if oracle_f64 else dt
+        cache = engine_np.dense_forward(net, imgs[b].astype(odt), kernels_c, threads=8)
         assert rel_err(out[b], cache.output) < (tol_f or FWD_TOL["f32" if dt == np.float32 else "f64"])
-        delta = (cache.output - targets[b]).astype(dt)
+        delta = (cache.output - targets[b].astype(odt)).astype(odt)
         kg, bg, _ = engine_np.dense_backward(net, cache, delta, masks[b].astype(bool), kernels_c,
                                              threads=8)
         for k in range(len(spec.layers)):
@@ -182,8 +189,9 @@ def _engine_vs_oracle(dp, text, side, batch, dt, frac, seed=0, tol_f=None, tol_g
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-def test_fused_engine_batch_small(dp, dt):
-    _engine_vs_oracle(dp, _c1_text(1), 40, 3, dt, 0.05)
+@pytest.mark.parametrize("precision", ["fast", "exact"])
+def test_fused_engine_batch_small(dp, dt, precision):
+    _engine_vs_oracle(dp, _c1_text(1), 40, 3, dt, 0.05, precision=precision)
 
 
 def test_fused_engine_mixed_pools(dp):
@@ -194,12 +202,15 @@ def test_fused_engine_mixed_pools(dp):
 
 def test_config_c2_full_size(dp):
     """c2: 3x256x256, forward + masked backward with 1% of pixels (BASELINE.json configs[1])."""
-    _engine_vs_oracle(dp, _c1_text(3), 256, 2, np.float32, 0.01)
+    eng = _engine_vs_oracle(dp, _c1_text(3), 256, 2, np.float32, 0.01)
+    plan = eng.kernel_plan()
+    assert all(v["forward"] == "tcgen05-3xtf32" for v in plan.values())
+    _engine_vs_oracle(dp, _c1_text(3), 256, 1, np.float32, 0.01, precision="exact")
 
 
 def test_config_c4_reduced_side(dp):
     """c4 network (strided convs, relu) vs the oracle at side 160."""
-    _engine_vs_oracle(dp, C4_TEXT, 160, 1, np.float32, 0.02)
+    _engine_vs_oracle(dp, C4_TEXT, 160, 1, np.float32, 0.02, oracle_f64=True)
 
 
 def test_config_c4_full_size_properties(dp):

@@ -1,0 +1,105 @@
+"""Fast tier: tcgen05 3xTF32 conv (forward and data gradient) vs the exact tier (GPU).
+
+The exact CUDA-core kernels are bit-identical to the reference (test_gpu_kernels.py),
+so they are the yardstick here; the north-star tolerance for fp32 is 1e-4 normwise
+relative, and 3xTF32 should land near 1e-7.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# normwise; differences are fp32 reassociation of 1e2-1e3-term sums (~2e-6 seen)
+TOL = 5e-5
+
+SHAPES = [
+    # n, cin, cout, k, d, h, w
+    (2, 3, 16, 6, 1, 70, 75),       # c2 conv1 (Cin=3 -> one zero-padded chunk of 8)
+    (2, 16, 32, 5, 2, 62, 66),      # c2 conv2 (3-MMA mode, Npad=32)
+    (2, 32, 10, 4, 4, 61, 57),      # c2 conv3 (stacked mode, Q=10 -> Npad=16)
+    (1, 8, 8, 7, 8, 70, 71),        # FC head k=7 d=8
+    (1, 5, 20, 3, 16, 50, 40),      # large dilation, Npad=32 with Q=20
+    (3, 2, 3, 1, 5, 9, 9),          # 1x1 kernel, tiny image (MT clamps)
+    (1, 48, 64, 3, 2, 40, 45),      # c4-like L2: R=48, Q=64 (acc 64 cols)
+    (1, 12, 48, 5, 1, 33, 37),      # Npad=48
+]
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _rel(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).abs().max() / max(b.abs().max(), 1e-30))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_tc_forward_matches_exact(shape, act):
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    if not ops.fast_supported(ci, co, k):
+        pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
+    rng = np.random.default_rng(sum(shape) + act)
+    x = _t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
+    wt = _t(rng.uniform(-0.5, 0.5, (co, ci, k, k)).astype(np.float32))
+    b = _t(rng.uniform(-0.5, 0.5, co).astype(np.float32))
+    e = (k - 1) * d + 1
+    y_ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda")
+    y = torch.full_like(y_ref, float("nan"))
+    ops.conv_forward(x, wt, b, y_ref, k, d, act)
+    ws = torch.empty(ops.fast_workspace(ci, co, k), dtype=torch.uint8, device="cuda")
+    ops.conv_forward_fast(x, wt, b, y, k, d, act, ws)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
+    assert _rel(y, y_ref) < TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("gate_kind", [None, 1, 2])
+def test_tc_backward_data_matches_exact(shape, gate_kind):
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    if not ops.fast_supported(co, ci, k):
+        pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
+    rng = np.random.default_rng(sum(shape) + 7)
+    e = (k - 1) * d + 1
+    ho, wo = h - e + 1, w - e + 1
+    dy = _t(rng.uniform(-1, 1, (n, co, ho, wo)).astype(np.float32))
+    wt = _t(rng.uniform(-0.5, 0.5, (co, ci, k, k)).astype(np.float32))
+    gate = None
+    if gate_kind is not None:
+        gate = _t(np.tanh(rng.normal(size=(n, ci, h, w))).astype(np.float32))
+    dx_ref = torch.empty((n, ci, h, w), device="cuda")
+    dx = torch.full_like(dx_ref, float("nan"))
+    ops.conv_backward_data(dy, wt, dx_ref, k, d, gate, gate_kind or 0)
+    ws = torch.empty(ops.fast_workspace(co, ci, k), dtype=torch.uint8, device="cuda")
+    ops.conv_backward_data_fast(dy, wt, dx, k, d, ws, gate, gate_kind or 0)
+    torch.cuda.synchronize()
+    assert torch.isfinite(dx).all()
+    assert _rel(dx, dx_ref) < TOL
+
+
+def test_tc_deterministic_and_large_batch():
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    rng = np.random.default_rng(3)
+    x = _t(rng.uniform(-1, 1, (16, 16, 278, 278)).astype(np.float32))
+    wt = _t(rng.uniform(-0.5, 0.5, (32, 16, 5, 5)).astype(np.float32))
+    b = _t(rng.uniform(-0.5, 0.5, 32).astype(np.float32))
+    y1 = torch.empty((16, 32, 270, 270), device="cuda")
+    y2 = torch.empty_like(y1)
+    yr = torch.empty_like(y1)
+    ws = torch.empty(ops.fast_workspace(16, 32, 5), dtype=torch.uint8, device="cuda")
+    ops.conv_forward_fast(x, wt, b, y1, 5, 2, 1, ws)
+    ops.conv_forward_fast(x, wt, b, y2, 5, 2, 1, ws)
+    ops.conv_forward(x, wt, b, yr, 5, 2, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert _rel(y1, yr) < TOL

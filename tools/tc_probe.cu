@@ -79,13 +79,30 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// SWIZZLE_128B: 16B-chunk index (bits 4..6) ^= row-in-atom (bits 7..9)
+// SWIZZLE_128B: 16B-chunk index (bits 4..6) ^= row-in-atom (bits 7..9); SW32: bit 4 ^= bit 7
 __host__ __device__ inline uint32_t sw128(uint32_t off) { return off ^ (((off >> 7) & 7) << 4); }
+__host__ __device__ inline uint32_t sw32(uint32_t off) { return off ^ (((off >> 7) & 1) << 4); }
 
-// A: M=128 x K=8, MN-major SW128: m = h*32 + px, atom h at h*1024, K-row k at k*128.
-// B: N x K=8, K-major no-swizzle: core (g,kk) at g*256 + kk*128, row r at r*16, elem e.
-__device__ inline uint32_t a_off(int m, int k) {
-    return sw128((m >> 5) * 1024 + k * 128 + (m & 31) * 4);
+// A operand layouts (M=128 x K=8 tf32) -- mode:
+//  0 MN-major SW128   : m = blk*32 + px; atom blk at blk*1024 (LBO), K-row k at k*128
+//  1 K-major  SW32    : 8-row groups of 32B rows at 256B (SBO)
+//  2 K-major  INTERL. : core 8 rows x 16B; K halves at LBO=128, row groups at SBO=256
+//  3 MN-major INTERL. : core 4 MN x 8 K (16B rows); MN blocks at SBO=128
+__device__ inline uint32_t a_off(int mode, int m, int k) {
+    switch (mode) {
+        case 0: return sw128((m >> 5) * 1024 + k * 128 + (m & 31) * 4);
+        case 1: return sw32((m >> 3) * 256 + (m & 7) * 32 + k * 4);
+        case 2: return (m >> 3) * 256 + (k >> 2) * 128 + (m & 7) * 16 + (k & 3) * 4;
+        default: return (m >> 2) * 128 + k * 16 + (m & 3) * 4;
+    }
+}
+__device__ inline uint64_t a_desc(int mode, uint32_t base) {
+    switch (mode) {
+        case 0: return make_desc(base, 1024, 8192, 2);
+        case 1: return make_desc(base, 16, 256, 6);
+        case 2: return make_desc(base, 128, 256, 0);
+        default: return make_desc(base, 8192, 128, 0);
+    }
 }
 __device__ inline uint32_t b_off(int n, int k) {
     return (n >> 3) * 256 + (k >> 2) * 128 + (n & 7) * 16 + (k & 3) * 4;
@@ -98,20 +115,30 @@ struct ProbeArgs {
     int N;
     int reps;
     long long *cycles;
+    int mode;
+    int nacc;
 };
 
-template <int N>
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n .reg .b32 r;\n .reg .pred p;\n elect.sync r|p, 0xffffffff;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+    return pred;
+}
+
+template <int N, int NACC>
 __global__ void __launch_bounds__(128) mma_probe(ProbeArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    unsigned char *sA = smem;                      // 4 KB
-    unsigned char *sB = smem + 4096;               // N*32 B
+    unsigned char *sA = smem;                      // 4 KB (8 KB reserved)
+    unsigned char *sB = smem + 8192;               // N*32 B
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
     int tid = threadIdx.x, warp = tid >> 5;
+    const int mode = a.mode;
     for (int i = tid; i < 128 * 8; i += 128) {
         int m = i / 8, k = i % 8;
-        *(float *)(sA + a_off(m, k)) = a.A[i];
+        *(float *)(sA + a_off(mode, m, k)) = a.A[i];
     }
     for (int i = tid; i < N * 8; i += 128) {
         int n = i / 8, k = i % 8;
@@ -131,26 +158,30 @@ __global__ void __launch_bounds__(128) mma_probe(ProbeArgs a) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     uint32_t tm = tbase;
-    uint64_t ad = make_desc(smem_u32(sA), 1024, 8192, 2);
+    uint64_t ad = a_desc(mode, smem_u32(sA));
     uint64_t bd = make_desc(smem_u32(sB), 128, 256, 0);
-    constexpr uint32_t idesc = make_idesc(128, N, 1, 0);
-    long long t0 = 0, t1 = 0;
-    if (tid == 0) {
-        // correctness: single MMA
-        mma_tf32(tm, ad, bd, idesc, 0);
-        mma_commit(&bar);
+    const uint32_t idesc = make_idesc(128, N, (mode == 0 || mode == 3) ? 1 : 0, 0);
+    if (warp == 0) {
+        if (elect_one()) {
+            mma_tf32(tm, ad, bd, idesc, 0);
+            mma_commit(&bar);
+        }
+        __syncwarp();
         mbar_wait(&bar, 0);
-        // throughput: reps MMAs into the second half of TMEM
-        t0 = clock64();
-        for (int r = 0; r < a.reps; ++r) mma_tf32(tm + 256, ad, bd, idesc, r > 0);
-        mma_commit(&bar);
+        long long t0 = clock64();
+        for (int r = 0; r < 512 / NACC; ++r) {
+#pragma unroll
+            for (int q = 0; q < NACC; ++q)
+                if (elect_one()) mma_tf32(tm + 256 + q * N, ad, bd, idesc, r > 0);
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(&bar);
+        __syncwarp();
         mbar_wait(&bar, 1);
-        t1 = clock64();
-        a.cycles[0] = t1 - t0;
+        if (tid == 0) a.cycles[0] = clock64() - t0;
     }
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // read D: warp w owns lanes 32w..32w+31 (= rows m)
     for (int c0 = 0; c0 < N; c0 += 16) {
         float v[16];
         tmem_ld16(tm + ((uint32_t)(warp * 32) << 16) + c0, v);
@@ -199,8 +230,9 @@ static float tf32_rn(float x) {
     uint32_t lsb = (u >> 13) & 1; u += 0xFFF + lsb; u &= 0xFFFFE000u; memcpy(&x, &u, 4); return x;
 }
 
-template <int N>
-static void run_mma(const char *label) {
+template <int N, int NACC>
+static void run_mma(const char *label, int mode) {
+    const int nacc = NACC;
     std::vector<float> A(128 * 8), B(N * 8), D(128 * N);
     srand(7 + N);
     for (auto &v : A) v = (float)rand() / RAND_MAX * 2 - 1;
@@ -210,10 +242,10 @@ static void run_mma(const char *label) {
     CK(cudaMalloc(&dD, D.size() * 4)); CK(cudaMalloc(&dc, 8));
     CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
-    ProbeArgs a{dA, dB, dD, N, 512, dc};
-    int smem = 4096 + N * 32 + 1024;
-    CK(cudaFuncSetAttribute(mma_probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    mma_probe<N><<<1, 128, smem>>>(a);
+    ProbeArgs a{dA, dB, dD, N, 512, dc, mode, nacc};
+    int smem = 8192 + N * 32 + 1024;
+    CK(cudaFuncSetAttribute(mma_probe<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    mma_probe<N, NACC><<<1, 128, smem>>>(a);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     long long cyc;
@@ -232,8 +264,12 @@ static void run_mma(const char *label) {
             e_tr = fmax(e_tr, fabs(d - s_tr)); e_rn = fmax(e_rn, fabs(d - s_rn));
             e_raw = fmax(e_raw, fabs(d - s_raw)); scale = fmax(scale, fabs(s_raw));
         }
-    printf("%s N=%3d: maxerr vs trunc-tf32 %.3e, vs rn-tf32 %.3e, vs fp32 %.3e (scale %.2f); "
-           "%.2f cycles/MMA (512 back-to-back)\n", label, N, e_tr, e_rn, e_raw, scale,
+    printf("  D[0][0..2] = %g %g %g | fp32 ref %g %g %g\n", D[0], D[1], D[2],
+           A[0]*B[0]+A[1]*B[1]+A[2]*B[2]+A[3]*B[3]+A[4]*B[4]+A[5]*B[5]+A[6]*B[6]+A[7]*B[7],
+           A[0]*B[8]+A[1]*B[9]+A[2]*B[10]+A[3]*B[11]+A[4]*B[12]+A[5]*B[13]+A[6]*B[14]+A[7]*B[15],
+           A[0]*B[16]+A[1]*B[17]+A[2]*B[18]+A[3]*B[19]+A[4]*B[20]+A[5]*B[21]+A[6]*B[22]+A[7]*B[23]);
+    printf("%s nacc=%d mode=%d N=%3d: maxerr vs trunc-tf32 %.3e, vs rn-tf32 %.3e, vs fp32 %.3e (scale %.2f); "
+           "%.2f cycles/MMA (512 back-to-back)\n", label, nacc, mode, N, e_tr, e_rn, e_raw, scale,
            cyc / 512.0);
     cudaFree(dA); cudaFree(dB); cudaFree(dD); cudaFree(dc);
 }
@@ -242,17 +278,22 @@ int main() {
     int dev = 0; CK(cudaSetDevice(dev));
     cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
     printf("device %s, %d SMs, clock %d kHz\n", p.name, p.multiProcessorCount, p.clockRate);
-    run_mma<16>("mma");
-    run_mma<32>("mma");
-    run_mma<64>("mma");
-    run_mma<128>("mma");
-    run_mma<256>("mma");
+    for (int mode = 1; mode < 3; ++mode) {
+        run_mma<16, 1>("mma", mode); run_mma<16, 2>("mma", mode); run_mma<16, 4>("mma", mode);
+        run_mma<16, 8>("mma", mode);
+        run_mma<32, 1>("mma", mode); run_mma<32, 2>("mma", mode); run_mma<32, 4>("mma", mode);
+        run_mma<32, 8>("mma", mode);
+        run_mma<64, 1>("mma", mode); run_mma<64, 2>("mma", mode); run_mma<64, 4>("mma", mode);
+        run_mma<128, 1>("mma", mode); run_mma<128, 2>("mma", mode);
+        run_mma<256, 1>("mma", mode);
+    }
+    return 0;
 
     // ---- TMA probe
     EncodeFn encode = nullptr;
     cudaDriverEntryPointQueryResult q;
     CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q));
-    const int Nn = 2, C = 11, H = 13, W = 70;
+    const int Nn = 2, C = 11, H = 13, W = 72;
     std::vector<float> X((size_t)Nn * C * H * W);
     for (size_t i = 0; i < X.size(); ++i) X[i] = (float)i;
     float *dX, *dOut;

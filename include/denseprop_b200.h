@@ -129,6 +129,24 @@ int dp_conv_backward_data_fast(const float *dy, const float *wt, float *dx, int 
                                int gate_kind, void *workspace, size_t workspace_bytes,
                                void *stream);
 
+/* fast-tier weight/bias gradient: tcgen05 implicit GEMM (M = taps x channels, N = cout,
+ * K = pixels of all n images), operands staged by TMA, 3xTF32 products, split-K over
+ * the SMs with a fixed-order reduction (deterministic).  Same argument meaning as
+ * dp_conv_backward_kernel; DP_F32 only; cout <= 128.  `workspace` must be 256-byte
+ * aligned and hold dp_conv_backward_kernel_fast_workspace bytes. */
+int dp_conv_backward_kernel_fast_supported(int n, int cin, int hi, int wi, int cout, int k,
+                                           int d);
+size_t dp_conv_backward_kernel_fast_workspace(int n, int cin, int hi, int wi, int cout, int k,
+                                              int d);
+int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, float *db, int n,
+                                 int cin, int hi, int wi, int cout, int k, int d,
+                                 void *workspace, size_t workspace_bytes, void *stream);
+
+/* debugging aid: with DP_WG_TRACE set in the environment, the fast weight-gradient kernel
+ * records per-K-block clock64() timestamps of CTA 0 (256 blocks x 16 slots); this copies
+ * the last launch's record to host memory (synchronous). */
+int dp_debug_wgrad_trace(void *host, size_t bytes);
+
 /* workspace bytes for dp_conv_backward_kernel at this shape */
 size_t dp_conv_backward_kernel_workspace(int dtype, int n, int cin, int hi, int wi,
                                          int cout, int k, int d);

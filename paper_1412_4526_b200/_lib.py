@@ -47,6 +47,11 @@ SIGNATURES = {
                                   _vp]),
     "dp_conv_backward_data_fast": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _i,
                                         _vp, _sz, _vp]),
+    "dp_debug_wgrad_trace": (_i, [_vp, _sz]),
+    "dp_conv_backward_kernel_fast_supported": (_i, [_i, _i, _i, _i, _i, _i, _i]),
+    "dp_conv_backward_kernel_fast_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
+    "dp_conv_backward_kernel_fast": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
+                                          _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel": (_i, [_i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
                                      _sz, _vp]),

@@ -31,6 +31,11 @@ int tc_conv_forward(const float *, const float *, const float *, float *, int, i
                     int, int, int, void *, size_t, cudaStream_t);
 int tc_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
                           int, const float *, int, void *, size_t, cudaStream_t);
+bool tc_wgrad_supported(int, int, int, int, int, int, int);
+int wg_trace_copy(void *, size_t);
+size_t tc_wgrad_workspace(int, int, int, int, int, int, int);
+int tc_conv_backward_kernel(const float *, const float *, float *, float *, int, int, int, int,
+                            int, int, int, void *, size_t, cudaStream_t);
 template <typename T>
 int maxpool_forward_t(const T *, T *, void *, int, int, int, int, int, int, int, int,
                       cudaStream_t);
@@ -281,6 +286,31 @@ int dp_conv_backward_kernel(int dtype, const void *x, const void *dy, void *dw, 
         conv_backward_kernel_t<double>((const double *)x, (const double *)dy, (double *)dw,
                                        (double *)db, n, cin, hi, wi, cout, k, d, workspace,
                                        workspace_bytes, st));
+}
+
+int dp_conv_backward_kernel_fast_supported(int n, int cin, int hi, int wi, int cout, int k,
+                                           int d) {
+    if (n < 1 || cin < 1 || cout < 1 || check_window("wgrad", hi, wi, k, d)) return 0;
+    return tc_wgrad_supported(n, cin, hi, wi, cout, k, d) ? 1 : 0;
+}
+
+size_t dp_conv_backward_kernel_fast_workspace(int n, int cin, int hi, int wi, int cout, int k,
+                                              int d) {
+    if (n < 1 || cin < 1 || cout < 1 || check_window("wgrad", hi, wi, k, d)) return 0;
+    return tc_wgrad_workspace(n, cin, hi, wi, cout, k, d);
+}
+
+int dp_debug_wgrad_trace(void *host, size_t bytes) { return wg_trace_copy(host, bytes); }
+
+int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, float *db, int n,
+                                 int cin, int hi, int wi, int cout, int k, int d,
+                                 void *workspace, size_t workspace_bytes, void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
+                                   workspace_bytes, (cudaStream_t)stream);
 }
 
 int dp_maxpool_forward(int dtype, const void *x, void *y, void *arg, int arg_bytes, int n, int c,

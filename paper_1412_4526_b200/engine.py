@@ -81,6 +81,12 @@ class _Rec:
             ops.profile.append((self.name, self.bound, self.work, self.e0, self.e1))
 
 
+def _repitches(x, dy) -> int:
+    """Staging copies the tensor-core weight gradient launches: x always (16-byte row
+    pitch, (n, h, c, w) order, shifted copies), dy when its rows are not 16-byte aligned."""
+    return 1 + int(dy.shape[3] % 4 != 0)
+
+
 def _nbytes(*ts):
     return sum(t.numel() * t.element_size() for t in ts if t is not None)
 
@@ -150,6 +156,26 @@ class ops:
                                                           _ptr(db), n, ci, hi, wi, co, k, d,
                                                           _ptr(ws), ws.numel() * ws.element_size(),
                                                           _stream()), "conv_backward_kernel")
+
+    @staticmethod
+    def wgrad_fast_supported(x, co, k, d) -> bool:
+        n, ci, hi, wi = x.shape
+        return bool(_lib_dev().dp_conv_backward_kernel_fast_supported(n, ci, hi, wi, co, k, d))
+
+    @staticmethod
+    def wgrad_fast_workspace(x, co, k, d) -> int:
+        n, ci, hi, wi = x.shape
+        return int(_lib_dev().dp_conv_backward_kernel_fast_workspace(n, ci, hi, wi, co, k, d))
+
+    @staticmethod
+    def conv_backward_kernel_fast(x, dy, dw, db, k, d, ws):
+        with _Rec('conv_backward_kernel_tc', 2 + _repitches(x, dy), 'tensor',
+                  2 * dy.numel() * x.shape[1] * k * k):
+            n, ci, hi, wi = x.shape
+            co = dy.shape[1]
+            _lib.check(_lib_dev().dp_conv_backward_kernel_fast(
+                _ptr(x), _ptr(dy), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k, d, _ptr(ws),
+                ws.numel() * ws.element_size(), _stream()), "conv_backward_kernel_fast")
 
     @staticmethod
     def maxpool_forward(x, y, arg, p, d, nonlin=_lib.DP_IDENTITY):
@@ -398,12 +424,17 @@ class DenseNet:
         if train:
             biggest = max([int(np.prod(s)) for s in shapes])
             self._dbuf = [torch.empty(N * biggest, **kw), torch.empty(N * biggest, **kw)]
-            ws = 1
+            ws = 256
+            self.tc_wgrad = {}
             for gi, g in enumerate(self.groups):
                 if isinstance(g.op, DilatedConv):
                     xin = self._group_input(gi)
-                    ws = max(ws, ops.wgrad_workspace(xin, g.op.base.out_channels,
-                                                     g.op.base.kernel_size, g.op.dilation))
+                    co, kk, dd = g.op.base.out_channels, g.op.base.kernel_size, g.op.dilation
+                    fast = (self.precision == "fast" and
+                            ops.wgrad_fast_supported(xin, co, kk, dd))
+                    self.tc_wgrad[gi] = fast
+                    ws = max(ws, ops.wgrad_fast_workspace(xin, co, kk, dd) if fast else
+                             ops.wgrad_workspace(xin, co, kk, dd))
             self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
             self.mask = torch.zeros((N, height, width), dtype=torch.uint8, device=self.device)
             self.target = torch.zeros_like(self.output)
@@ -430,8 +461,10 @@ class DenseNet:
         for gi, g in enumerate(self.groups):
             if isinstance(g.op, DilatedConv):
                 f_ok, b_ok = self.tc.get(gi, (False, False))
+                w_ok = getattr(self, "tc_wgrad", {}).get(gi, False)
                 out[g.first] = {"forward": "tcgen05-3xtf32" if f_ok else "exact",
-                                "data_grad": "tcgen05-3xtf32" if b_ok else "exact"}
+                                "data_grad": "tcgen05-3xtf32" if b_ok else "exact",
+                                "weight_grad": "tcgen05-3xtf32" if w_ok else "cuda-core"}
         return out
 
     # ------------------------------------------------------------- parameters
@@ -520,7 +553,10 @@ class DenseNet:
                 wt, _ = self.params[g.first]
                 dw, db = self.grads[g.first]
                 kk, d = op.base.kernel_size, op.dilation
-                ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
+                if self.tc_wgrad.get(gi, False):
+                    ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws)
+                else:
+                    ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                 if gi == 0 and not with_input_grad:
                     return None
                 dx = self._view(self._dbuf[ping], x_in.shape)

@@ -103,3 +103,48 @@ def test_tc_deterministic_and_large_batch():
     torch.cuda.synchronize()
     assert torch.equal(y1, y2)
     assert _rel(y1, yr) < TOL
+
+
+WGRAD_SHAPES = [
+    # n, cin, cout, k, d, h, w   (x is (n, cin, h, w); dy is the valid-conv output size)
+    (2, 3, 16, 6, 1, 70, 75),       # c2 conv1: Cin=3 -> Cpad 8, odd widths (row re-pitch)
+    (2, 16, 32, 5, 2, 62, 66),      # c2 conv2: 4 tiles of 128 rows, Npad=32
+    (2, 32, 10, 4, 4, 61, 57),      # c2 conv3: 512 rows, Npad=16
+    (1, 48, 64, 3, 2, 40, 45),      # c4 L2-like: Cpad 48 (box 16), G=2 -> 2 tile groups
+    (1, 96, 128, 3, 8, 50, 52),     # c4 L8-like: Npad=128, G=1, 7 tile groups
+    (1, 128, 8, 3, 32, 70, 68),     # c4 head-like: large dilation, 9 tiles
+    (3, 2, 3, 1, 5, 9, 9),          # 1x1 kernel, tiny image (fewer K blocks than SMs)
+    (1, 12, 48, 5, 1, 33, 37),      # Npad=48 (G=3)
+    (4, 16, 32, 5, 2, 140, 140),    # larger batch, aligned widths (no re-pitch)
+]
+
+
+@pytest.mark.parametrize("shape", WGRAD_SHAPES)
+def test_tc_weight_gradient_matches_fp64(shape):
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    x = _t(np.random.default_rng(sum(shape)).uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
+    e = (k - 1) * d + 1
+    ho, wo = h - e + 1, w - e + 1
+    if not ops.wgrad_fast_supported(x, co, k, d):
+        pytest.skip("outside the tensor-core weight-gradient envelope")
+    rng = np.random.default_rng(sum(shape) + 1)
+    dy = _t(rng.uniform(-1, 1, (n, co, ho, wo)).astype(np.float32))
+    # ground truth: the exact-tier kernel in fp64 on the same (fp32-valued) inputs
+    dw64 = torch.empty((co, ci, k, k), dtype=torch.float64, device="cuda")
+    db64 = torch.empty(co, dtype=torch.float64, device="cuda")
+    ws64 = torch.empty(max(1, ops.wgrad_workspace(x.double(), co, k, d)), dtype=torch.uint8,
+                       device="cuda")
+    ops.conv_backward_kernel(x.double(), dy.double(), dw64, db64, k, d, ws64)
+    dw = torch.full((co, ci, k, k), float("nan"), device="cuda")
+    db = torch.full((co,), float("nan"), device="cuda")
+    ws = torch.empty(ops.wgrad_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+    ops.conv_backward_kernel_fast(x, dy, dw, db, k, d, ws)
+    dw2, db2 = torch.empty_like(dw), torch.empty_like(db)
+    ops.conv_backward_kernel_fast(x, dy, dw2, db2, k, d, ws)
+    torch.cuda.synchronize()
+    assert torch.isfinite(dw).all() and torch.isfinite(db).all()
+    assert torch.equal(dw, dw2) and torch.equal(db, db2)   # deterministic split-K
+    assert _rel(dw, dw64) < 1e-5, _rel(dw, dw64)
+    assert _rel(db, db64) < 1e-5, _rel(db, db64)

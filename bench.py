@@ -336,6 +336,11 @@ def main():
         achieved = top["bytes"] / (top["ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"]}
+    if top["bound"] == "tensor" and "_tc" in top["name"]:
+        # 3xTF32 issues 3 TF32 MACs per algorithmic MAC; dense TF32 is half of dense bf16
+        ceil = peaks["bf16_tflops"] / 2 / 3
+        roof["derived_3xtf32_ceiling_tflops"] = ceil
+        roof["frac_of_3xtf32_ceiling"] = roof["achieved"] / ceil
     roof.update({"kernel": top["name"], "ms_per_launch": top["ms"],
                  "share_of_step": top["ms"] / prof["step_ms"], "peak_source": peaks["source"],
                  "traffic": None,

@@ -48,7 +48,10 @@ extern "C" {
 
 enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
 /* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
-enum dp_nonlin { DP_IDENTITY = 0, DP_TANH = 1, DP_RELU = 2 };
+enum dp_nonlin { DP_IDENTITY = 0, DP_TANH = 1, DP_RELU = 2,
+                 /* fast tier: single-precision tanhf (<= 2 ulp); DP_TANH evaluates in
+                  * fp64 and rounds once so it stays within 2 ulp of numpy */
+                 DP_TANH_FAST = 3 };
 enum dp_status { DP_OK = 0, DP_ERR_ARG = 1, DP_ERR_CUDA = 2, DP_ERR_UNSUPPORTED = 3 };
 
 const char *dp_last_error(void);

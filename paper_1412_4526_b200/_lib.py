@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libdenseprop_b200.so")
 
 DP_F32, DP_F64 = 0, 1
-DP_IDENTITY, DP_TANH, DP_RELU = 0, 1, 2
+DP_IDENTITY, DP_TANH, DP_RELU, DP_TANH_FAST = 0, 1, 2, 3
 DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED = 0, 1, 2, 3
 NONLIN_CODE = {"identity": DP_IDENTITY, "tanh": DP_TANH, "relu": DP_RELU}
 ABI_VERSION = 1

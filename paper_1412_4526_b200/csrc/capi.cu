@@ -96,7 +96,7 @@ static int check_pos(const char *what, long long v) {
 }
 
 static int check_nonlin(int kind) {
-    if (kind < DP_IDENTITY || kind > DP_RELU)
+    if (kind < DP_IDENTITY || kind > DP_TANH_FAST)
         return set_error(DP_ERR_ARG, "unknown nonlinearity code %d", kind);
     return DP_OK;
 }

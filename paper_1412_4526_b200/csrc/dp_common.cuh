@@ -30,9 +30,13 @@ __device__ __forceinline__ double dp_tanh(double x) { return tanh(x); }
 template <typename T>
 __device__ __forceinline__ T dp_relu(T x) { return (x > T(0) || x != x) ? x : T(0); }
 
+__device__ __forceinline__ float dp_tanh_fast(float x) { return tanhf(x); }
+__device__ __forceinline__ double dp_tanh_fast(double x) { return tanh(x); }
+
 template <typename T>
 __device__ __forceinline__ T apply_nonlin(T v, int kind) {
     if (kind == DP_TANH) return dp_tanh(v);
+    if (kind == DP_TANH_FAST) return dp_tanh_fast(v);
     if (kind == DP_RELU) return dp_relu(v);
     return v;
 }
@@ -42,7 +46,8 @@ __device__ __forceinline__ T apply_nonlin(T v, int kind) {
 // relu' = (x_in > 0) == (t > 0) (backward.py:179).
 template <typename T>
 __device__ __forceinline__ T gate_from_output(T delta, T t, int kind) {
-    if (kind == DP_TANH) return mul_rn(delta, add_rn(T(1), -mul_rn(t, t)));
+    if (kind == DP_TANH || kind == DP_TANH_FAST)
+        return mul_rn(delta, add_rn(T(1), -mul_rn(t, t)));
     if (kind == DP_RELU) return mul_rn(delta, t > T(0) ? T(1) : T(0));
     return delta;
 }

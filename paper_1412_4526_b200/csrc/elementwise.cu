@@ -29,6 +29,7 @@ __global__ void nonlin_bwd_kernel(const T *__restrict__ dy, const T *__restrict_
          i += (long long)gridDim.x * blockDim.x) {
         T t = x[i];
         if (!x_is_output && kind == DP_TANH) t = dp_tanh(t);
+        if (!x_is_output && kind == DP_TANH_FAST) t = dp_tanh_fast(t);
         dx[i] = gate_from_output(dy[i], t, kind);
     }
 }

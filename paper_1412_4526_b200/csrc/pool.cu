@@ -2,7 +2,9 @@
 //
 // HBM-bound kernels; one thread per output (forward) or per input pixel
 // (backward), consecutive threads on consecutive columns so every tap read is
-// a coalesced row segment (shifted taps hit L1/L2).  Results are bit-identical
+// a coalesced row segment (shifted taps hit L1/L2).  Planes x pixels grid, no
+// 64-bit divides (the first version's per-thread 64-bit index math made these
+// kernels instruction bound at ~1 TB/s).  Results are bit-identical
 // to the compiled reference backend:
 //  * maxpool_forward  (_kernels.pyx:133-166): best = -inf, strict '>' scanning
 //    taps row-major, so the first tap wins ties and NaN never wins; argmax
@@ -19,134 +21,252 @@
 
 namespace dp {
 
-template <typename T, typename A>
-__global__ void maxpool_fwd_kernel(const T *__restrict__ x, T *__restrict__ y,
-                                   A *__restrict__ arg, long long total, int H, int W, int Ho,
-                                   int Wo, int p, int d, int act) {
-    long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    int v = (int)(idx % Wo);
-    long long t = idx / Wo;
-    int u = (int)(t % Ho);
-    long long plane = t / Ho;  // n*C + c
-    const T *src = x + plane * H * W + (long long)u * W + v;
-    T best = neg_inf<T>();
-    int bk = 0;
-    for (int i = 0; i < p; ++i) {
-        const T *row = src + (long long)i * d * W;
-        for (int j = 0; j < p; ++j) {
-            T xv = row[j * d];
-            if (xv > best) {
-                best = xv;
-                bk = i * p + j;
+// Indexing: grid.y (and grid.z for more than 65535 planes) = plane n*C + c, grid.x covers
+// the plane's Ho*Wo (or Hi*Wi) pixels; one 32-bit divide per thread gives (row, column).
+// Consecutive threads are consecutive columns, so every tap read and every store is a
+// coalesced row segment; a pixel's p^2 taps are re-read by neighbouring threads / rows
+// from L1/L2, so DRAM sees each map about once (HBM-bound by construction).
+__device__ __forceinline__ long long pool_plane() {
+    return (long long)blockIdx.z * gridDim.y + blockIdx.y;
+}
+
+// Max pool: 2-D tiles, block (32, 8), each thread 4 columns 32 apart (warp accesses stay
+// 128-byte row segments) so the index math and the plane/row bases are paid once per 4
+// outputs -- the one-output-per-thread version was issue bound at ~1.7 TB/s.
+constexpr int PT_X = 32, PT_Y = 8, PT_V = 4;  // tile: 128 columns x 8 rows
+
+template <typename T, typename A, int P>
+__global__ void __launch_bounds__(PT_X * PT_Y)
+    maxpool_fwd_tile(const T *__restrict__ x, T *__restrict__ y, A *__restrict__ arg, int H,
+                     int W, int Ho, int Wo, int p_rt, int d, int act, long long planes) {
+    const int u = blockIdx.y * PT_Y + threadIdx.y;
+    if (u >= Ho) return;
+    const int v0 = blockIdx.x * (PT_X * PT_V) + threadIdx.x;
+    for (long long plane = blockIdx.z; plane < planes; plane += gridDim.z) {
+        const T *src = x + (plane * H + u) * (long long)W;
+        T *yr = y + (plane * Ho + u) * (long long)Wo;
+        A *ar = arg + (plane * Ho + u) * (long long)Wo;
+        if (P == 2) {
+            // all 16 tap loads of the thread's 4 outputs issued before any compare
+            T t[PT_V][4];
+#pragma unroll
+            for (int k = 0; k < PT_V; ++k) {
+                const int v = v0 + k * PT_X;
+                const bool ok = v < Wo;
+                const T *s0 = src + (ok ? v : 0);
+                t[k][0] = __ldg(s0);
+                t[k][1] = __ldg(s0 + d);
+                t[k][2] = __ldg(s0 + (long long)d * W);
+                t[k][3] = __ldg(s0 + (long long)d * W + d);
+            }
+#pragma unroll
+            for (int k = 0; k < PT_V; ++k) {
+                const int v = v0 + k * PT_X;
+                if (v >= Wo) break;
+                T best = neg_inf<T>();
+                int bk = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (t[k][q] > best) {
+                        best = t[k][q];
+                        bk = q;
+                    }
+                yr[v] = apply_nonlin(best, act);
+                ar[v] = (A)bk;
+            }
+        } else {
+            const int p = p_rt;
+            for (int k = 0; k < PT_V; ++k) {
+                const int v = v0 + k * PT_X;
+                if (v >= Wo) break;
+                const T *s0 = src + v;
+                T best = neg_inf<T>();
+                int bk = 0;
+                for (int i = 0; i < p; ++i) {
+                    const T *row = s0 + (long long)i * d * W;
+                    for (int j = 0; j < p; ++j) {
+                        const T xv = __ldg(row + j * d);
+                        if (xv > best) {
+                            best = xv;
+                            bk = i * p + j;
+                        }
+                    }
+                }
+                yr[v] = apply_nonlin(best, act);
+                ar[v] = (A)bk;
             }
         }
     }
-    y[idx] = apply_nonlin(best, act);
-    arg[idx] = (A)bk;
 }
 
-template <typename T, typename A>
-__global__ void maxpool_bwd_kernel(const T *__restrict__ dy, const A *__restrict__ arg,
-                                   T *__restrict__ dx, const T *__restrict__ gate,
-                                   long long total, int Ho, int Wo, int Hi, int Wi, int p, int d,
-                                   int gate_kind) {
-    long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    int s = (int)(idx % Wi);
-    long long t = idx / Wi;
-    int r = (int)(t % Hi);
-    long long plane = t / Hi;
-    const T *dyp = dy + plane * Ho * Wo;
-    const A *ap = arg + plane * Ho * Wo;
-    T acc = T(0);
-    for (int i = p - 1; i >= 0; --i) {
-        int u = r - i * d;
-        if (u < 0 || u >= Ho) continue;
-        for (int j = p - 1; j >= 0; --j) {
-            int v = s - j * d;
-            if (v < 0 || v >= Wo) continue;
-            long long o = (long long)u * Wo + v;
-            if ((int)ap[o] == i * p + j) acc = add_rn(acc, dyp[o]);
+constexpr int PB_V = 2;  // backward: 2 pixels per thread (16 loads in flight, ~40 regs)
+
+template <typename T, typename A, int P>
+__global__ void __launch_bounds__(PT_X * PT_Y)
+    maxpool_bwd_tile(const T *__restrict__ dy, const A *__restrict__ arg, T *__restrict__ dx,
+                     const T *__restrict__ gate, int Ho, int Wo, int Hi, int Wi, int p_rt, int d,
+                     int gate_kind, long long planes) {
+    const int r = blockIdx.y * PT_Y + threadIdx.y;
+    if (r >= Hi) return;
+    const int s0 = blockIdx.x * (PT_X * PB_V) + threadIdx.x;
+    for (long long plane = blockIdx.z; plane < planes; plane += gridDim.z) {
+        const T *dyp = dy + plane * Ho * (long long)Wo;
+        const A *ap = arg + plane * Ho * (long long)Wo;
+        const long long q0 = (plane * Hi + r) * (long long)Wi;
+        if (P == 2) {
+            // candidate windows of input pixel (r, s): taps 3, 2, 1, 0 = outputs (r-d, s-d),
+            // (r-d, s), (r, s-d), (r, s) -- the reference's scatter (row-major (u, v)) order.
+            // All 32 (arg, dy) loads of the thread's 4 pixels issued before any compare.
+            const bool u1 = r - d >= 0 && r - d < Ho, u0 = r < Ho;
+            const long long o1 = (long long)(r - d) * Wo, o0 = (long long)r * Wo;
+            int av[PB_V][4];
+            T dv[PB_V][4];
+#pragma unroll
+            for (int k = 0; k < PB_V; ++k) {
+                const int s = s0 + k * PT_X;
+                const bool v1 = s - d >= 0 && s - d < Wo, v0 = s < Wo;
+                const bool ok[4] = {u1 && v1, u1 && v0, u0 && v1, u0 && v0};
+                const long long off[4] = {o1 + s - d, o1 + s, o0 + s - d, o0 + s};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    av[k][c] = ok[c] ? (int)__ldg(ap + off[c]) : -1;
+                    dv[k][c] = ok[c] ? __ldg(dyp + off[c]) : T(0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PB_V; ++k) {
+                const int s = s0 + k * PT_X;
+                if (s >= Wi) break;
+                T acc = T(0);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (av[k][c] == 3 - c) acc = add_rn(acc, dv[k][c]);
+                if (gate) acc = gate_from_output(acc, gate[q0 + s], gate_kind);
+                dx[q0 + s] = acc;
+            }
+        } else {
+            const int p = p_rt;
+            for (int k = 0; k < PB_V; ++k) {
+                const int s = s0 + k * PT_X;
+                if (s >= Wi) break;
+                T acc = T(0);
+                for (int i = p - 1; i >= 0; --i) {
+                    const int u = r - i * d;
+                    if (u < 0 || u >= Ho) continue;
+                    const A *arow = ap + (long long)u * Wo;
+                    const T *drow = dyp + (long long)u * Wo;
+                    for (int j = p - 1; j >= 0; --j) {
+                        const int v = s - j * d;
+                        if (v < 0 || v >= Wo) continue;
+                        if ((int)__ldg(arow + v) == i * p + j) acc = add_rn(acc, __ldg(drow + v));
+                    }
+                }
+                if (gate) acc = gate_from_output(acc, gate[q0 + s], gate_kind);
+                dx[q0 + s] = acc;
+            }
         }
     }
-    if (gate) acc = gate_from_output(acc, gate[idx], gate_kind);
-    dx[idx] = acc;
 }
 
 template <typename T>
-__global__ void avgpool_fwd_kernel(const T *__restrict__ x, T *__restrict__ y, long long total,
-                                   int H, int W, int Ho, int Wo, int p, int d, int act) {
-    long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    int v = (int)(idx % Wo);
-    long long t = idx / Wo;
-    int u = (int)(t % Ho);
-    long long plane = t / Ho;
+__global__ void __launch_bounds__(256) avgpool_fwd_kernel(const T *__restrict__ x,
+                                                          T *__restrict__ y, int H, int W, int Ho,
+                                                          int Wo, int p, int d, int act, long long planes) {
+    const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= Ho * Wo) return;
+    const long long plane = pool_plane();
+    if (plane >= planes) return;
+    const int u = pix / Wo, v = pix - u * Wo;
     const T *src = x + plane * H * W + (long long)u * W + v;
     T acc = T(0);
     for (int i = 0; i < p; ++i)
-        for (int j = 0; j < p; ++j) acc = add_rn(acc, src[(long long)i * d * W + j * d]);
-    y[idx] = apply_nonlin(div_rn(acc, T(p * p)), act);
+        for (int j = 0; j < p; ++j) acc = add_rn(acc, __ldg(src + (long long)i * d * W + j * d));
+    y[plane * Ho * Wo + pix] = apply_nonlin(div_rn(acc, T(p * p)), act);
 }
 
 template <typename T>
-__global__ void avgpool_bwd_kernel(const T *__restrict__ dy, T *__restrict__ dx,
-                                   const T *__restrict__ gate, long long total, int Ho, int Wo,
-                                   int Hi, int Wi, int p, int d, int gate_kind) {
-    long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    int s = (int)(idx % Wi);
-    long long t = idx / Wi;
-    int r = (int)(t % Hi);
-    long long plane = t / Hi;
+__global__ void __launch_bounds__(256) avgpool_bwd_kernel(const T *__restrict__ dy,
+                                                          T *__restrict__ dx,
+                                                          const T *__restrict__ gate, int Ho,
+                                                          int Wo, int Hi, int Wi, int p, int d,
+                                                          int gate_kind, long long planes) {
+    const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= Hi * Wi) return;
+    const long long plane = pool_plane();
+    if (plane >= planes) return;
+    const int r = pix / Wi, s = pix - r * Wi;
     const T *dyp = dy + plane * Ho * Wo;
     const T pp = T(p * p);
     T acc = T(0);
     for (int i = p - 1; i >= 0; --i) {
-        int u = r - i * d;
+        const int u = r - i * d;
         if (u < 0 || u >= Ho) continue;
         for (int j = p - 1; j >= 0; --j) {
-            int v = s - j * d;
+            const int v = s - j * d;
             if (v < 0 || v >= Wo) continue;
-            acc = add_rn(acc, div_rn(dyp[(long long)u * Wo + v], pp));
+            acc = add_rn(acc, div_rn(__ldg(dyp + u * Wo + v), pp));
         }
     }
-    if (gate) acc = gate_from_output(acc, gate[idx], gate_kind);
-    dx[idx] = acc;
+    const long long q = plane * Hi * Wi + pix;
+    if (gate) acc = gate_from_output(acc, gate[q], gate_kind);
+    dx[q] = acc;
 }
 
-static inline int blocks_for(long long total) { return ceil_div(total, 256); }
+// grid for `planes` planes of `pixels` pixels each (planes split over y and z)
+static inline dim3 pool_grid(long long planes, long long pixels) {
+    unsigned gy = (unsigned)(planes < 65535 ? planes : 65535);
+    unsigned gz = (unsigned)((planes + gy - 1) / gy);
+    return dim3((unsigned)((pixels + 255) / 256), gy, gz);
+}
+
 
 template <typename T>
 int maxpool_forward_t(const T *x, T *y, void *arg, int arg_bytes, int n, int c, int h, int w,
                       int p, int d, int act, cudaStream_t st) {
     int e = (p - 1) * d + 1;
     int ho = h - e + 1, wo = w - e + 1;
-    long long total = (long long)n * c * ho * wo;
-    if (total == 0) return DP_OK;
-    if (arg_bytes == 1)
-        maxpool_fwd_kernel<T, uint8_t><<<blocks_for(total), 256, 0, st>>>(
-            x, y, (uint8_t *)arg, total, h, w, ho, wo, p, d, act);
-    else
-        maxpool_fwd_kernel<T, int32_t><<<blocks_for(total), 256, 0, st>>>(
-            x, y, (int32_t *)arg, total, h, w, ho, wo, p, d, act);
-    return check_launch("maxpool_fwd_kernel");
+    long long planes = (long long)n * c;
+    if (planes == 0 || ho <= 0 || wo <= 0) return DP_OK;
+    dim3 blk(PT_X, PT_Y);
+    dim3 g(ceil_div(wo, PT_X * PT_V), ceil_div(ho, PT_Y),
+           (unsigned)(planes < 65535 ? planes : 65535));
+    if (arg_bytes == 1) {
+        if (p == 2)
+            maxpool_fwd_tile<T, uint8_t, 2><<<g, blk, 0, st>>>(x, y, (uint8_t *)arg, h, w, ho, wo,
+                                                               p, d, act, planes);
+        else
+            maxpool_fwd_tile<T, uint8_t, 0><<<g, blk, 0, st>>>(x, y, (uint8_t *)arg, h, w, ho, wo,
+                                                               p, d, act, planes);
+    } else {
+        maxpool_fwd_tile<T, int32_t, 0><<<g, blk, 0, st>>>(x, y, (int32_t *)arg, h, w, ho, wo, p,
+                                                           d, act, planes);
+    }
+    return check_launch("maxpool_fwd_tile");
 }
 
 template <typename T>
 int maxpool_backward_t(const T *dy, const void *arg, int arg_bytes, T *dx, int n, int c, int ho,
                        int wo, int p, int d, int hi, int wi, const T *gate, int gate_kind,
                        cudaStream_t st) {
-    long long total = (long long)n * c * hi * wi;
-    if (total == 0) return DP_OK;
-    if (arg_bytes == 1)
-        maxpool_bwd_kernel<T, uint8_t><<<blocks_for(total), 256, 0, st>>>(
-            dy, (const uint8_t *)arg, dx, gate, total, ho, wo, hi, wi, p, d, gate_kind);
-    else
-        maxpool_bwd_kernel<T, int32_t><<<blocks_for(total), 256, 0, st>>>(
-            dy, (const int32_t *)arg, dx, gate, total, ho, wo, hi, wi, p, d, gate_kind);
-    return check_launch("maxpool_bwd_kernel");
+    long long planes = (long long)n * c;
+    if (planes == 0 || hi <= 0 || wi <= 0) return DP_OK;
+    dim3 blk(PT_X, PT_Y);
+    dim3 g(ceil_div(wi, PT_X * PB_V), ceil_div(hi, PT_Y),
+           (unsigned)(planes < 65535 ? planes : 65535));
+    if (arg_bytes == 1) {
+        if (p == 2)
+            maxpool_bwd_tile<T, uint8_t, 2><<<g, blk, 0, st>>>(dy, (const uint8_t *)arg, dx, gate,
+                                                               ho, wo, hi, wi, p, d, gate_kind,
+                                                               planes);
+        else
+            maxpool_bwd_tile<T, uint8_t, 0><<<g, blk, 0, st>>>(dy, (const uint8_t *)arg, dx, gate,
+                                                               ho, wo, hi, wi, p, d, gate_kind,
+                                                               planes);
+    } else {
+        maxpool_bwd_tile<T, int32_t, 0><<<g, blk, 0, st>>>(dy, (const int32_t *)arg, dx, gate, ho,
+                                                           wo, hi, wi, p, d, gate_kind, planes);
+    }
+    return check_launch("maxpool_bwd_tile");
 }
 
 template <typename T>
@@ -154,20 +274,20 @@ int avgpool_forward_t(const T *x, T *y, int n, int c, int h, int w, int p, int d
                       cudaStream_t st) {
     int e = (p - 1) * d + 1;
     int ho = h - e + 1, wo = w - e + 1;
-    long long total = (long long)n * c * ho * wo;
-    if (total == 0) return DP_OK;
-    avgpool_fwd_kernel<T><<<blocks_for(total), 256, 0, st>>>(x, y, total, h, w, ho, wo, p, d,
-                                                             act);
+    long long planes = (long long)n * c;
+    if (planes == 0 || ho <= 0 || wo <= 0) return DP_OK;
+    dim3 g = pool_grid(planes, (long long)ho * wo);
+    avgpool_fwd_kernel<T><<<g, 256, 0, st>>>(x, y, h, w, ho, wo, p, d, act, planes);
     return check_launch("avgpool_fwd_kernel");
 }
 
 template <typename T>
 int avgpool_backward_t(const T *dy, T *dx, int n, int c, int ho, int wo, int p, int d, int hi,
                        int wi, const T *gate, int gate_kind, cudaStream_t st) {
-    long long total = (long long)n * c * hi * wi;
-    if (total == 0) return DP_OK;
-    avgpool_bwd_kernel<T><<<blocks_for(total), 256, 0, st>>>(dy, dx, gate, total, ho, wo, hi,
-                                                             wi, p, d, gate_kind);
+    long long planes = (long long)n * c;
+    if (planes == 0 || hi <= 0 || wi <= 0) return DP_OK;
+    dim3 g = pool_grid(planes, (long long)hi * wi);
+    avgpool_bwd_kernel<T><<<g, 256, 0, st>>>(dy, dx, gate, ho, wo, hi, wi, p, d, gate_kind, planes);
     return check_launch("avgpool_bwd_kernel");
 }
 

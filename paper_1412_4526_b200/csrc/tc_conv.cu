@@ -117,7 +117,7 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
 // line.  The exact tier's fp64-evaluated tanh unrolled over 16 outputs bloats the kernel
 // past the instruction cache and starves the producer / MMA warps (measured).
 __device__ __noinline__ float tc_act(float v, int kind) {
-    if (kind == DP_TANH) return tanhf(v);
+    if (kind == DP_TANH || kind == DP_TANH_FAST) return tanhf(v);
     if (kind == DP_RELU) return dp_relu(v);
     return v;
 }

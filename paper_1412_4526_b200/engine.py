@@ -497,6 +497,8 @@ class DenseNet:
         for gi, g in enumerate(self.groups):
             x, y = self._group_input(gi), self.acts[gi]
             op, act = g.op, _nl(g.act)
+            if act == _lib.DP_TANH and self.precision == "fast":
+                act = _lib.DP_TANH_FAST  # tanhf (<= 2 ulp) instead of the fp64 evaluation
             if isinstance(op, DilatedConv):
                 wt, b = self.params[g.first]
                 if self.tc.get(gi, (False, False))[0]:
@@ -514,7 +516,10 @@ class DenseNet:
                 if op.kind == "identity":
                     y.copy_(x)
                 else:
-                    ops.nonlin_forward(x, y, _nl(op.kind))
+                    kind = _nl(op.kind)
+                    if kind == _lib.DP_TANH and self.precision == "fast":
+                        kind = _lib.DP_TANH_FAST
+                    ops.nonlin_forward(x, y, kind)
         return self.output
 
     # ------------------------------------------------------------- loss / mask

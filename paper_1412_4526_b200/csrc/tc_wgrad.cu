@@ -45,8 +45,8 @@
 //
 // Roles (one CTA per SM):
 //   warps 0-7   converters, two groups of 4 (warp % 4 = TMEM lane quarter); group p
-//               handles slices ks = p, p+2 of every K block; group 0 also writes B_lo
-//               and accumulates db; both groups run the epilogue
+//               converts K blocks p, p+2, ... (B_lo, db, all slices of all tiles into one
+//               TMEM stage); both groups run the epilogue
 //   warp 8      TMA producer (one lane)
 //   warp 9      TMEM allocator + MMA issuer (one elected lane)
 #include <cuda.h>
@@ -66,7 +66,7 @@ constexpr int WG_MMA_WARP = 9;
 constexpr int WG_THREADS = 320;
 static_assert(WG_TMA_WARP == WG_CONV_WARPS && WG_THREADS == (WG_MMA_WARP + 1) * 32,
               "warp roles");
-constexpr int WG_MAX_G = 4;
+constexpr int WG_MAX_G = 2;
 constexpr int WG_MAX_SS = 8;
 constexpr int WG_MAX_TS = 16;
 constexpr int WG_KSTEPS = 4;          // K=8 slices per 32-pixel K block
@@ -89,7 +89,8 @@ struct TcWgradArgs {
     float *part;              // [splits][n_tiles*128][Npad]
     float *pdb;               // [splits][Npad]
     unsigned long long *trace;  // DP_WG_TRACE: per-K-block timestamps of CTA 0
-    int dbg;                  // DP_WG_DBG: 2 no MMA, 32 no converter work
+    int dbg;                  // DP_WG_DBG: 2 no MMA, 8 no x boxes, 32 no converter work,
+                              // 64 contiguous K ranges
 };
 
 #define WG_TRACE(A, KL, SLOT, COND)                                               \
@@ -121,7 +122,13 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
     const int g = blockIdx.x % a.n_groups, split = blockIdx.x / a.n_groups;
     const int tile0 = g * a.G;
     const int G = min(a.G, a.n_tiles - tile0);
-    const int nkb = (int)((a.kb_total - split + a.splits - 1) / a.splits);
+    // K blocks of split s: interleaved s, s + splits, ... (default) or, with DP_WG_DBG & 64,
+    // one contiguous range
+    const bool contig = (a.dbg & 64) != 0;
+    const long long kb_first = contig ? a.kb_total * split / a.splits : split;
+    const int kb_step = contig ? 1 : a.splits;
+    const int nkb = contig ? (int)(a.kb_total * (split + 1) / a.splits - kb_first)
+                           : (int)((a.kb_total - split + a.splits - 1) / a.splits);
     const int acc_cols = 2 * a.Npad;
     const int L = a.L4 * 4;
     int i_lo, n_i;
@@ -159,7 +166,7 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
             const int s = kl % a.SS;
             ptx::mbar_wait(&sempty[s], ((kl / a.SS) & 1) ^ 1);
             if (lane == 0) {
-                const long long kb = split + (long long)kl * a.splits;
+                const long long kb = kb_first + (long long)kl * kb_step;
                 const int vb = (int)(kb % a.nvb);
                 const long long tt = kb / a.nvb;
                 const int u = (int)(tt % a.Ho);
@@ -168,10 +175,12 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                 const int hh = img * a.Hi + u;
                 unsigned char *st = smem + (size_t)s * a.stage_bytes;
                 WG_TRACE(a, kl, 0, true);
-                ptx::mbar_expect_tx(&sfull[s], tx);
+                ptx::mbar_expect_tx(&sfull[s], (a.dbg & 8) ? (uint32_t)a.Npad * 128u : tx);
                 ptx::tma_load_4d(st, &tm_dy, v0, u, 0, img, &sfull[s]);
                 unsigned char *sa = st + a.b_bytes;
-                if (a.tap_mode) {
+                if (a.dbg & 8) {
+                    // bring-up: dy only
+                } else if (a.tap_mode) {
                     ptx::tma_load_5d(sa, &tm_x0, v0, 0, 0, i_lo, hh, &sfull[s]);
                 } else {
                     for (int b = 0, slot = 0; b < 4; ++b) {
@@ -188,33 +197,35 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
         }
     } else if (warp == WG_MMA_WARP) {
         // ================================ MMA issuer ================================
+        // One wait and one commit per K block (4 slices x G tiles x 2 MMAs): the issuing
+        // thread's wait / commit / fence sequence costs ~600 cycles of serial latency,
+        // so it is amortised over a whole K block rather than paid per K=8 slice.
         const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
         const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
         const uint32_t smem_base = ptx::smem_u32(smem);
-        int KS = 0;
         for (int kl = 0; kl < nkb; ++kl) {
             const int s = kl % a.SS;
+            const int ts = kl % a.TS;
             const uint32_t bhi = smem_base + (uint32_t)s * a.stage_bytes;
-            for (int ks = 0; ks < WG_KSTEPS; ++ks, ++KS) {
-                const int ts = KS % a.TS;
-                ptx::mbar_wait(&tfull[ts], (KS / a.TS) & 1);
-                ptx::tc_fence_after();
-                WG_TRACE(a, kl, 8 + ks, lane == 0);
-                if (ptx::elect_one()) {
+            ptx::mbar_wait(&tfull[ts], (kl / a.TS) & 1);
+            ptx::tc_fence_after();
+            WG_TRACE(a, kl, 8, lane == 0);
+            if (ptx::elect_one()) {
+                const uint32_t abase = a_base + (uint32_t)(ts * a.G * WG_KSTEPS * 16);
+                for (int ks = 0; ks < WG_KSTEPS; ++ks) {
                     const uint64_t dstack = ptx::smem_desc_sw128(bhi + ks * 32);
-                    const uint32_t abase = a_base + (uint32_t)(ts * a.G * 16);
                     for (int t = 0; t < ((a.dbg & 2) ? 0 : G); ++t) {
                         const uint32_t dcol = tmem + (uint32_t)(t * acc_cols);
-                        const uint32_t ahi = abase + t * 16, alo = ahi + 8;
-                        ptx::mma_tf32_ts(dcol, ahi, dstack, idesc_2n, KS > 0);
+                        const uint32_t ahi = abase + (uint32_t)((ks * a.G + t) * 16), alo = ahi + 8;
+                        ptx::mma_tf32_ts(dcol, ahi, dstack, idesc_2n, (kl | ks) > 0);
                         ptx::mma_tf32_ts(dcol, alo, dstack, idesc_n, 1);
                     }
-                    ptx::mma_commit(&tempty[ts]);
-                    if (ks == WG_KSTEPS - 1) ptx::mma_commit(&sempty[s]);
                 }
-                __syncwarp();
-                WG_TRACE(a, kl, 12 + (ks == WG_KSTEPS - 1), lane == 0 && ks >= WG_KSTEPS - 2);
+                ptx::mma_commit(&tempty[ts]);
+                ptx::mma_commit(&sempty[s]);
             }
+            __syncwarp();
+            WG_TRACE(a, kl, 9, lane == 0);
         }
         if (ptx::elect_one()) ptx::mma_commit(&accfull);
         __syncwarp();
@@ -253,16 +264,19 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
         float dbacc[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) dbacc[m] = 0.f;
-        for (int kl = 0; kl < nkb; ++kl) {
+        // group p converts K blocks kl = p, p + 2, ...: B_lo + db, then all 4 slices of every
+        // tile into TMEM stage kl % TS, one arrive per warp
+        for (int kl = grp; kl < nkb; kl += 2) {
             const int s = kl % a.SS;
+            const int ts = kl % a.TS;
             ptx::mbar_wait(&sfull[s], (kl / a.SS) & 1);
-            WG_TRACE(a, kl, 2, threadIdx.x == 0);
+            WG_TRACE(a, kl, 2, q == 0 && lane == 0);
             unsigned char *st = smem + (size_t)s * a.stage_bytes;
-            if (grp == 0) {
+            {
                 // B_lo = B_hi - trunc(B_hi) (elementwise; the swizzle is preserved) + db
                 const float4 *bh = reinterpret_cast<const float4 *>(st);
                 float4 *bl = reinterpret_cast<float4 *>(st + (uint32_t)a.Npad * 128);
-                const int tid = threadIdx.x;  // 0..127
+                const int tid = q * 32 + lane;  // 0..127 within the group
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
                     if (m >= dbn) break;
@@ -274,15 +288,14 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                                           ptx::tf32_lo(v.z), ptx::tf32_lo(v.w));
                 }
                 ptx::fence_proxy_async_smem();
-                WG_TRACE(a, kl, 3, threadIdx.x == 0);
+                WG_TRACE(a, kl, 3, q == 0 && lane == 0);
             }
             const unsigned char *sa = st + a.b_bytes;
-            for (int ks = grp; ks < WG_KSTEPS; ks += 2) {
-                const int KS = kl * WG_KSTEPS + ks;
-                const int ts = KS % a.TS;
-                ptx::mbar_wait(&tempty[ts], ((KS / a.TS) & 1) ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t tbase = a_base + lane_off + (uint32_t)(ts * a.G * 16);
+            ptx::mbar_wait(&tempty[ts], ((kl / a.TS) & 1) ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t tbase = a_base + lane_off + (uint32_t)(ts * a.G * WG_KSTEPS * 16);
+#pragma unroll
+            for (int ks = 0; ks < WG_KSTEPS; ++ks) {
 #pragma unroll
                 for (int t = 0; t < WG_MAX_G; ++t) {
                     if (t >= G || (a.dbg & 32)) break;
@@ -299,18 +312,19 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                     float lo[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) lo[k] = ptx::tf32_lo(hi[k]);
-                    ptx::tmem_st8(tbase + t * 16, hi);
-                    ptx::tmem_st8(tbase + t * 16 + 8, lo);
+                    const uint32_t col = tbase + (uint32_t)((ks * a.G + t) * 16);
+                    ptx::tmem_st8(col, hi);
+                    ptx::tmem_st8(col + 8, lo);
                 }
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tfull[ts]);
-                WG_TRACE(a, kl, 4 + ks, lane == 0 && q == 0);
             }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tfull[ts]);
+            WG_TRACE(a, kl, 4, lane == 0 && q == 0);
         }
-        // ---- db partial (group 0 threads own B rows (tid >> 3) + 16 m)
-        if (grp == 0 && g == 0) {
+        // ---- db partials (thread q*32+lane of each group owns B rows (tid >> 3) + 16 m)
+        if (g == 0) {
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
                 if (m >= dbn) break;
@@ -318,8 +332,9 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
                 v += __shfl_xor_sync(0xffffffffu, v, 2);
                 v += __shfl_xor_sync(0xffffffffu, v, 4);
-                const int row = (threadIdx.x >> 3) + 16 * m;
-                if ((lane & 7) == 0 && row < a.Npad) a.pdb[(size_t)split * a.Npad + row] = v;
+                const int row = ((q * 32 + lane) >> 3) + 16 * m;
+                if ((lane & 7) == 0 && row < a.Npad)
+                    a.pdb[((size_t)split * 2 + grp) * a.Npad + row] = v;
             }
         }
         // ---- epilogue: tiles t = grp, grp + 2, ... ; lane = row
@@ -375,7 +390,7 @@ __global__ void tc_wgrad_reduce(const float *__restrict__ part, const float *__r
     } else if (idx < total + Q) {
         const int o = (int)(idx - total);
         float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += pdb[(size_t)s * Npad + o];
+        for (int s = 0; s < 2 * splits; ++s) acc += pdb[(size_t)s * Npad + o];
         db[o] = acc;
     }
 }
@@ -405,12 +420,18 @@ __global__ void tc_stage_x(const float *__restrict__ src, float *__restrict__ ds
     }
 }
 
-// dy staging when its rows are not 16-byte aligned: (rows x w) -> (rows x wp), zero pad
-__global__ void tc_stage_dy(const float *__restrict__ src, float *__restrict__ dst, int w,
-                            int wp) {
-    const long long row = blockIdx.x;
+// dy staging: NCHW (n, o, h, w) -> (n, h, o, wp), zero pad.  A K block's dy box then
+// reads Npad lines wp floats apart instead of one line per channel plane (plane-strided
+// boxes measured ~4x slower here: every line opens a different DRAM page).
+__global__ void tc_stage_dy(const float *__restrict__ src, float *__restrict__ dst, int O, int H,
+                            int w, int wp) {
+    const long long row = blockIdx.x;  // (n, o, h)
+    const int h = (int)(row % H);
+    const long long no = row / H;
+    const int o = (int)(no % O);
+    const long long n = no / O;
     const float *s = src + row * w;
-    float *d = dst + row * wp;
+    float *d = dst + ((n * H + h) * O + o) * wp;
     for (int v = threadIdx.x; v < wp; v += blockDim.x) d[v] = v < w ? __ldg(s + v) : 0.f;
 }
 
@@ -462,15 +483,15 @@ static bool wg_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WgPl
     p.rows_total = k * k * p.Cpad;
     p.n_tiles = (p.rows_total + 127) / 128;
     const int acc_cols = 2 * p.Npad;
-    int G = 512 / (acc_cols + 64);
+    // TMEM: G tiles of accumulators + TS stages of one K block's A (4 slices x G x 16 cols)
+    int G = 512 / (acc_cols + 2 * WG_KSTEPS * 16);
     if (G > WG_MAX_G) G = WG_MAX_G;
     if (G < 1) return false;
     p.n_groups = (p.n_tiles + G - 1) / G;
     p.G = (p.n_tiles + p.n_groups - 1) / p.n_groups;
-    int TS = (512 - p.G * acc_cols) / (p.G * 16);
+    int TS = (512 - p.G * acc_cols) / (p.G * WG_KSTEPS * 16);
     if (TS > WG_MAX_TS) TS = WG_MAX_TS;
-    TS &= ~1;
-    if (TS < 4) return false;
+    if (TS < 2) return false;
     p.TS = TS;
     p.max_ni = 0;
     for (int g = 0; g < p.n_groups; ++g) {
@@ -511,10 +532,10 @@ static bool wg_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WgPl
     if (p.splits > p.kb_total) p.splits = (int)p.kb_total;
     p.wp_x = (wi + 3) / 4 * 4;
     p.wp_dy = (p.wo + 3) / 4 * 4;
-    p.stage_dy = p.wp_dy != p.wo;
+    p.stage_dy = p.wp_dy != p.wo;  // re-pitched (n, h, o, wp) only when rows are unaligned
     if ((long long)n * hi > (1LL << 31)) return false;
     p.part_bytes = align256((size_t)p.splits * p.n_tiles * 128 * p.Npad * 4);
-    p.pdb_bytes = align256((size_t)p.splits * p.Npad * 4);
+    p.pdb_bytes = align256((size_t)p.splits * 2 * p.Npad * 4);  // one row per converter group
     // tap-mode boxes may read up to (l-1)*d + 32 floats past a row's end (those columns
     // only meet zero dy); pad the staged copy so the last row stays inside it
     p.copy_bytes = align256((size_t)n * cin * hi * p.wp_x * 4 + ((size_t)(k - 1) * d + 64) * 4);
@@ -578,9 +599,6 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     if (((uintptr_t)ws & 255) != 0)
         return set_error(DP_ERR_ARG,
                          "tensor-core weight gradient: workspace must be 256-byte aligned");
-    const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
-    if (stage_dy && !p.stage_dy)
-        return set_error(DP_ERR_ARG, "weight gradient: dy must be 16-byte aligned");
     unsigned char *w8 = (unsigned char *)ws;
     TcWgradArgs a;
     a.part = (float *)w8;
@@ -591,22 +609,25 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
                                              (long long)(p.copy_bytes / 4));
     int rc = check_launch("tc_stage_x");
     if (rc) return rc;
+    const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
+    if (stage_dy && !p.stage_dy)
+        return set_error(DP_ERR_ARG, "weight gradient: dy must be 16-byte aligned");
     const float *dys = dy;
-    int dy_pitch = p.wo;
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
-        tc_stage_dy<<<n * cout * p.ho, 128, 0, st>>>(dy, dp_, p.wo, p.wp_dy);
+        tc_stage_dy<<<n * cout * p.ho, 128, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy);
         rc = check_launch("tc_stage_dy");
         if (rc) return rc;
         dys = dp_;
-        dy_pitch = p.wp_dy;
     }
     // ---- tensor maps
     CUtensorMap mx[4], mdy;
     {
-        const cuuint64_t rowb = (cuuint64_t)dy_pitch * 4;
+        // staged: (n, h, o, wp_dy); direct: NCHW with 16-byte rows
+        const cuuint64_t rowb = (cuuint64_t)(stage_dy ? p.wp_dy : p.wo) * 4;
         cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)p.ho, (cuuint64_t)cout, (cuuint64_t)n};
-        cuuint64_t str[3] = {rowb, rowb * p.ho, rowb * p.ho * cout};
+        cuuint64_t str[3] = {stage_dy ? rowb * cout : rowb, stage_dy ? rowb : rowb * p.ho,
+                             rowb * cout * p.ho};
         cuuint32_t box[4] = {32, 1, (cuuint32_t)p.Npad, 1};
         rc = wg_map(&mdy, dys, 4, dims, str, box, true);
         if (rc) return rc;

@@ -27,11 +27,11 @@ torch.cuda.synchronize()
 buf = np.zeros((256, 16), dtype=np.uint64)
 _lib.check(_lib.load().dp_debug_wgrad_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes))
 t0 = buf[0, 0]
-names = ["ld", "dyTMA", "sfull", "Blo", "cv0", "cv1", "cv2", "cv3", "mm0", "mm1", "mm2", "mm3",
-         "mmi2", "mmi3"]
+names = ["tma", "-", "sfull", "Blo", "cvdone", "-", "-", "-", "mmwait", "mmissued", "-", "-",
+         "-", "-", "-", "-"]
 print("K-block  " + " ".join(f"{n:>7}" for n in names))
 for kl in list(range(0, 12)) + list(range(100, 106)):
     row = buf[kl]
-    print(f"{kl:7d}  " + " ".join(f"{int(v) - int(t0):7d}" if v else "      -" for v in row[:14]))
-per = (int(buf[200, 12]) - int(buf[100, 12])) / 100 if buf[200, 12] and buf[100, 12] else 0
-print(f"steady-state cycles per K-block (MMA issue of last slice, kb 100->200): {per:.0f}")
+    print(f"{kl:7d}  " + " ".join(f"{int(v) - int(t0):7d}" if v else "      -" for v in row[:16]))
+per = (int(buf[200, 9]) - int(buf[100, 9])) / 100 if buf[200, 9] and buf[100, 9] else 0
+print(f"steady-state cycles per K-block (MMA issue, kb 100->200): {per:.0f}")

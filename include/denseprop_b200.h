@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DP_ABI_VERSION 1
+#define DP_ABI_VERSION 2
 
 enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
 /* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
@@ -120,10 +120,12 @@ int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx,
  * to fp32; the reference tolerance for this path is 1e-4).  Same argument meaning as
  * dp_conv_forward / dp_conv_backward_data; DP_F32 only.  `workspace` (16-byte
  * aligned, dp_conv_fast_workspace bytes) receives the packed hi/lo weights.  Returns
- * DP_ERR_UNSUPPORTED when the packed weights exceed the kernel's shared-memory budget
- * (caller then uses the exact CUDA-core entry points). */
+ * DP_ERR_UNSUPPORTED when the packed weights plus the input halo buffers (which grow with
+ * the dilation d) exceed the kernel's shared-memory budget -- check
+ * dp_conv_fast_supported(reduce, out, k, d) first; the caller then uses the exact
+ * CUDA-core entry points. */
 size_t dp_conv_fast_workspace(int reduce_channels, int out_channels, int k);
-int dp_conv_fast_supported(int reduce_channels, int out_channels, int k);
+int dp_conv_fast_supported(int reduce_channels, int out_channels, int k, int d);
 int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float *y, int n,
                          int cin, int h, int w, int cout, int k, int d, int nonlin,
                          void *workspace, size_t workspace_bytes, void *stream);
@@ -149,6 +151,8 @@ int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, flo
  * records per-K-block clock64() timestamps of CTA 0 (256 blocks x 16 slots); this copies
  * the last launch's record to host memory (synchronous). */
 int dp_debug_wgrad_trace(void *host, size_t bytes);
+/* same for the fast forward / data-gradient kernel with DP_TC_TRACE set (1024 K-steps x 8) */
+int dp_debug_conv_trace(void *host, size_t bytes);
 
 /* workspace bytes for dp_conv_backward_kernel at this shape */
 size_t dp_conv_backward_kernel_workspace(int dtype, int n, int cin, int hi, int wi,

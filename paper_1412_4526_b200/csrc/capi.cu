@@ -26,13 +26,14 @@ int conv_backward_kernel_t(const T *, const T *, T *, T *, int, int, int, int, i
                            void *, size_t, cudaStream_t);
 size_t wgrad_workspace_bytes(int elem, int n, int cin, int hi, int wi, int cout, int k, int d);
 size_t tc_conv_workspace(int R, int Q, int l);
-bool tc_conv_supported(int R, int Q, int l);
+bool tc_conv_supported(int R, int Q, int l, int d);
 int tc_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
                     int, int, int, void *, size_t, cudaStream_t);
 int tc_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
                           int, const float *, int, void *, size_t, cudaStream_t);
 bool tc_wgrad_supported(int, int, int, int, int, int, int);
 int wg_trace_copy(void *, size_t);
+int tc_trace_copy(void *, size_t);
 size_t tc_wgrad_workspace(int, int, int, int, int, int, int);
 int tc_conv_backward_kernel(const float *, const float *, float *, float *, int, int, int, int,
                             int, int, int, void *, size_t, cudaStream_t);
@@ -229,9 +230,9 @@ size_t dp_conv_fast_workspace(int reduce_channels, int out_channels, int k) {
     return tc_conv_workspace(reduce_channels, out_channels, k);
 }
 
-int dp_conv_fast_supported(int reduce_channels, int out_channels, int k) {
-    if (reduce_channels < 1 || out_channels < 1 || k < 1) return 0;
-    return tc_conv_supported(reduce_channels, out_channels, k) ? 1 : 0;
+int dp_conv_fast_supported(int reduce_channels, int out_channels, int k, int d) {
+    if (reduce_channels < 1 || out_channels < 1 || k < 1 || d < 1) return 0;
+    return tc_conv_supported(reduce_channels, out_channels, k, d) ? 1 : 0;
 }
 
 int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float *y, int n,
@@ -301,6 +302,7 @@ size_t dp_conv_backward_kernel_fast_workspace(int n, int cin, int hi, int wi, in
 }
 
 int dp_debug_wgrad_trace(void *host, size_t bytes) { return wg_trace_copy(host, bytes); }
+int dp_debug_conv_trace(void *host, size_t bytes) { return tc_trace_copy(host, bytes); }
 
 int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, float *db, int n,
                                  int cin, int hi, int wi, int cout, int k, int d,

@@ -14,28 +14,32 @@
 // results agree with fp32 up to summation order (~1e-6 normwise on 400-term sums; the
 // reference tolerance for this path is 1e-4).
 //
-// Data flow per CTA (persistent, one per SM, 13 warps):
-//   warps 0-7  producers, 2 groups x 4 warps: gather the A tiles of one K-step for all
-//              MT M tiles straight from the NCHW map (lane = output column -> coalesced
-//              128 B row segments; warp q of a group = pixel row q of every M tile =
-//              TMEM lane quarter q), split hi/lo in registers and write both into a
-//              TMEM stage with tcgen05.st.  Loads of the group's next K-step are issued
-//              before it waits for a free stage (register double buffering).  A never
-//              touches shared memory: SMEM-operand MMAs are SMEM-bandwidth bound
-//              (~128 B/cycle, tools/tc_probe.cu) while A-in-TMEM MMAs run at the
-//              tcgen05 floor (tools/tc_probe_ts.cu).
-//   warp 12    loads all packed weights (B, K-major, hi and lo) into shared memory
-//              once with bulk async copies (TMA engine), allocates TMEM, then issues
-//              the MMAs (one elected lane), one stage = one K-step = MT M tiles:
-//              A_hi x [B_hi|B_lo] (N = 2*Npad) + A_lo x B_hi   (Npad <= 16), or
-//              A_hi x B_hi + A_hi x B_lo + A_lo x B_hi          (Npad >= 32),
-//              and releases the stage with one tcgen05.commit.
-//   warps 8-11 epilogue: tcgen05.ld the accumulators (double-buffered in TMEM so the
-//              next tile's MMAs overlap), add bias + nonlinearity (forward) or apply
-//              the upstream nonlinearity's derivative (data gradient), store NCHW.
-// Synchronisation is per K-step (not per M tile): one mbarrier wait and one commit
-// amortised over MT*(2..3) MMAs -- the per-item barrier round trip (~100-400 cycles)
-// otherwise dominates the ~50-cycle MMA work of a skinny-N item.
+// Data flow per CTA (persistent, one per SM, 25 warps):
+//   warps 16-23 loaders: for every (tile, channel chunk) copy the input window the l^2
+//               taps need into a shared-memory "halo" buffer [8 ch][rows][cols] with
+//               coalesced loads (any alignment; zero-fill outside the map = the data
+//               gradient's padding).  Rows/columns are the halo (4*MT + (l-1)d rows,
+//               32 + (l-1)d columns) or, for large dilations, only the l tap rows /
+//               l*32 tap columns -- whichever is smaller.  Two or three buffers.
+//   warps 8-15  converters, 2 groups x 4 warps (warp % 4 = TMEM lane quarter = pixel row
+//               of every M tile): per K-step read the 8 channel values of their pixel
+//               from the halo buffer (lane = column -> bank-conflict-free LDS), split
+//               hi/lo in registers, write both into a TMEM stage with tcgen05.st.  The
+//               tap only moves the read window; every input element is fetched from
+//               global memory once per tile instead of l^2 times.
+//   warp 24     loads all packed weights (B, K-major, hi and lo) into shared memory once
+//               with bulk async copies, allocates TMEM, then issues the MMAs (one
+//               elected lane), one stage = one K-step = MT M tiles:
+//               A_hi x [B_hi|B_lo] (N = 2*Npad) + A_lo x B_hi   (Npad <= 16), or
+//               A_hi x B_hi + A_hi x B_lo + A_lo x B_hi          (Npad >= 32),
+//               and releases the stage with one tcgen05.commit.
+//   warps 0-7   epilogue, 2 per TMEM lane quarter (M tiles split by parity): tcgen05.ld
+//               the accumulators (double-buffered in TMEM so the next tile's MMAs
+//               overlap), add bias + nonlinearity (forward) or apply the upstream
+//               nonlinearity's derivative (data gradient), store NCHW.
+// Measured before this layout (tools/tc_trace.cu): producers that gathered A straight
+// from global memory spent ~2000 cycles per K-step on load latency, and a 4-warp
+// epilogue with out-of-line tanh stalled the MMA ~12k cycles per tile.
 #include <stdlib.h>
 
 #include "dp_common.cuh"
@@ -44,19 +48,19 @@
 namespace dp {
 
 constexpr int TC_MAX_STAGES = 16;
-constexpr int TC_GROUPS = 2;          // producer groups of 4 warps (one per TMEM lane quarter)
-constexpr int TC_MAX_MT = 4;          // M tiles per CTA tile
-// Warp roles, ordered by scheduling priority (the SM arbiter favours the highest warp
-// id): epilogue warps 0-3 (they mostly wait a whole tile), producers 4..4+4*GROUPS-1,
-// the MMA issuer last.  Role warp % 4 == TMEM lane quarter for epilogue and producers.
-constexpr int TC_EPI_WARP0 = 0;
-constexpr int TC_PROD_WARP0 = 4;
-constexpr int TC_PROD_WARPS = 4 * TC_GROUPS;
-constexpr int TC_MMA_WARP = TC_PROD_WARP0 + TC_PROD_WARPS;
+constexpr int TC_MAX_MT = 4;  // M tiles per CTA tile
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_CONV_WARP0 = 8;   // 2 groups x 4
+constexpr int TC_LOAD_WARP0 = 16;  // 8 loader warps
+constexpr int TC_LOAD_WARPS = 8;
+constexpr int TC_MMA_WARP = 24;
+constexpr int TC_MAX_HROWS = 128;  // halo buffer rows per channel
 constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;
-constexpr int TC_MIN_STAGES = 2 * TC_GROUPS;  // each group keeps 2 K-steps in flight
-static_assert(TC_PROD_WARP0 % 4 == 0, "producer warps must start on a lane-quarter boundary");
-constexpr int TC_MAX_SMEM = 200 * 1024;
+constexpr int TC_MIN_STAGES = 4;
+constexpr int TC_MAX_HB = 3;  // halo buffers (2 or 3, as shared memory allows)
+constexpr int TC_LB = 8;  // loader: buffer rows in flight per warp
+constexpr int TC_LC = 3;  // loader: 32-column groups per row (halo columns <= 96)
+constexpr int TC_SMEM_BUDGET = 220 * 1024;
 
 struct TcConvArgs {
     const float *in;     // (n, R, Hin, Win)
@@ -67,22 +71,18 @@ struct TcConvArgs {
     int R, Hin, Win, Q, Ho, Wo, l, d, pad, act, gate_kind;
     int n_rc, n_ks, Npad, MT, acc_cols, stages, tiles_x, tiles_y, total_tiles;
     uint32_t wbytes;
-#ifdef DP_TC_TRACE
-    unsigned long long *trace;  // per K-step timestamps of CTA 0 (tools/tc_trace.cu)
-    int dbg;                    // 1: no loads, 2: no MMAs, 4: no TMEM stores
-#endif
+    // halo buffer geometry: rows (RB-row blocks per tap row i, step RS in the converter),
+    // columns (CB-column blocks per tap column j, step CS)
+    int hrows, hcols, RB, RS, CB, CS, HB;
+    uint32_t hbytes;
+    unsigned long long *trace;  // DP_TC_TRACE: per-K-step clock64 stamps of CTA 0 (8 slots)
 };
 
-#ifdef DP_TC_TRACE
-#define TC_TRACE(A, KS, SLOT, COND)                                               \
-    do {                                                                          \
-        if ((COND) && blockIdx.x == 0 && (KS) < 512) (A).trace[(KS) * 8 + (SLOT)] = clock64(); \
+#define TC_TRACE(A, KS, SLOT, COND)                                                  \
+    do {                                                                             \
+        if ((A).trace && (COND) && blockIdx.x == 0 && (KS) < 1024)                   \
+            (A).trace[(KS) * 8 + (SLOT)] = clock64();                                \
     } while (0)
-#define TC_DBG(A, BIT) (((A).dbg & (BIT)) != 0)
-#else
-#define TC_TRACE(A, KS, SLOT, COND) do {} while (0)
-#define TC_DBG(A, BIT) false
-#endif
 
 // --------------------------------------------------------------------------------
 // weight packing: W(q, r, i, j) -> per K-step ks = (rc*l + i)*l + j two Npad x 8 tiles
@@ -113,172 +113,42 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
     }
 }
 
-// Epilogue nonlinearity of the fast tier: single-precision tanhf (<= 2 ulp) kept out of
-// line.  The exact tier's fp64-evaluated tanh unrolled over 16 outputs bloats the kernel
-// past the instruction cache and starves the producer / MMA warps (measured).
-__device__ __noinline__ float tc_act(float v, int kind) {
-    if (kind == DP_TANH || kind == DP_TANH_FAST) return tanhf(v);
+// Epilogue tanh: single-precision tanhf (<= 2 ulp) kept out of line so the unrolled
+// epilogue stays small (instruction cache); relu / identity are inlined.
+__device__ __noinline__ float tc_tanh(float v) { return tanhf(v); }
+__device__ __forceinline__ float tc_act(float v, int kind) {
+    if (kind == DP_TANH || kind == DP_TANH_FAST) return tc_tanh(v);
     if (kind == DP_RELU) return dp_relu(v);
     return v;
 }
 
-// One producer warp's view: gathers A tiles (8 channels x 32 columns of one pixel row
-// per M tile) from the NCHW map and commits them to TMEM stages.
-//
-// Every field is a register copy: addressing the kernel's parameter struct through a
-// pointer turns each field read into a slow generic load (measured ~3000 cycles per
-// K-step with tools/tc_trace.cu before this was fixed).  K-steps are decoded
-// incrementally: group p walks KS = p, p + TC_GROUPS, ... so (tile, rc, i, j) advance
-// by a fixed stride without integer division.
-struct TcProducer {
-    const float *in;
-    int q, lane, MT, stages, total_ks;
-    int n_ks, l, d, pad, Hin, Win, R, tiles_x, per_img;
-    uint32_t lane_off, a_base;
-    long long plane;
-    // cursor of the next K-step this warp loads
-    int cur_ks, cur_tile, cur_rc, cur_i, cur_j, cur_KS;
-#ifdef DP_TC_TRACE
-    unsigned long long *trace;
-    int dbg;
-#endif
-
-    __device__ __forceinline__ void init(const TcConvArgs &args, int q_, int grp, int lane_,
-                                         uint32_t a_base_, int per_img_) {
-        in = args.in;
-        q = q_;
-        lane = lane_;
-        a_base = a_base_;
-        per_img = per_img_;
-        MT = args.MT;
-        stages = args.stages;
-        n_ks = args.n_ks;
-        l = args.l;
-        d = args.d;
-        pad = args.pad;
-        Hin = args.Hin;
-        Win = args.Win;
-        R = args.R;
-        tiles_x = args.tiles_x;
-        lane_off = (uint32_t)(q * 32) << 16;
-        plane = (long long)Hin * Win;
-        const int my_tiles =
-            (args.total_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-        total_ks = my_tiles * n_ks;
-#ifdef DP_TC_TRACE
-        trace = args.trace;
-        dbg = args.dbg;
-#endif
-        // cursor at KS = grp
-        cur_KS = grp;
-        cur_tile = grp / n_ks;
-        cur_ks = grp - cur_tile * n_ks;
-        decode_ks();
-    }
-
-    __device__ __forceinline__ void decode_ks() {
-        const int ll = l * l;
-        cur_rc = cur_ks / ll;
-        const int tap = cur_ks - cur_rc * ll;
-        cur_i = tap / l;
-        cur_j = tap - cur_i * l;
-    }
-
-    // advance the cursor by TC_GROUPS K-steps (cheap: carries only)
-    __device__ __forceinline__ void advance() {
-        cur_KS += TC_GROUPS;
-        cur_ks += TC_GROUPS;
-        if (cur_ks >= n_ks) {
-            cur_ks -= n_ks;
-            ++cur_tile;
-            decode_ks();
-            return;
-        }
-        cur_j += TC_GROUPS;
-        while (cur_j >= l) {
-            cur_j -= l;
-            if (++cur_i == l) {
-                cur_i = 0;
-                ++cur_rc;
-            }
-        }
-    }
-
-    // load the A tiles of the cursor's K-step into v, then advance the cursor.
-    // Instruction-lean: the producers' issue rate, not memory, bounds this kernel
-    // (~1000 warp-instructions per K-step budget for ~235 tensor-core cycles), so the
-    // 32 loads share one 64-bit base, advance by 32-bit channel strides and use
-    // per-load predicates only.
-    __device__ __forceinline__ void load(float (&v)[TC_MAX_MT][8]) {
-        const bool live = cur_KS < total_ks;
-        const int tile = blockIdx.x + cur_tile * gridDim.x;
-        const int img = tile / per_img;
-        const int rem = tile - img * per_img;
-        const int ty = rem / tiles_x;
-        const int u0 = ty * 4 * MT, v0 = (rem - ty * tiles_x) * 32;
-        const int row0 = u0 + q + cur_i * d - pad;
-        const int col = v0 + lane + cur_j * d - pad;
-        const bool col_ok = live && col >= 0 && col < Win && !TC_DBG(*this, 1);
-        const int c0 = cur_rc * 8;
-        const int kmax = R - c0;  // channels of this chunk that exist (>= 1)
-        const uint32_t pl = (uint32_t)plane;
-        const float *base = in + ((long long)img * R + c0) * plane;
-        uint32_t off = (uint32_t)(row0 * Win + col);
-#pragma unroll
-        for (int mt = 0; mt < TC_MAX_MT; ++mt, off += 4u * (uint32_t)Win) {
-            const int row = row0 + 4 * mt;
-            const bool ok = mt < MT && col_ok && row >= 0 && row < Hin;
-            uint32_t o = off;
-#pragma unroll
-            for (int k = 0; k < 8; ++k, o += pl) {
-                float t = 0.f;
-                if (ok && k < kmax) t = __ldg(base + o);
-                v[mt][k] = t;
-            }
-        }
-        advance();
-    }
-
-    // K-step KS -> stage KS % stages: wait until the MMAs of K-step KS - stages finished,
-    // write hi/lo of every M tile, then one arrive (per warp) on the stage's full barrier.
-    __device__ __forceinline__ void commit(const float (&v)[TC_MAX_MT][8], int KS,
-                                           uint64_t *empty_bar, uint64_t *full_bar) const {
-        const int stage = KS % stages;
-        const uint32_t phase = (uint32_t)((KS / stages) & 1);
-        TC_TRACE(*this, KS, 0, lane == 0 && q == 0);
-        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-        TC_TRACE(*this, KS, 1, lane == 0 && q == 0);
-        ptx::tc_fence_after();
-        const uint32_t sbase = a_base + lane_off + (uint32_t)(stage * MT * 16);
-#pragma unroll
-        for (int mt = 0; mt < TC_MAX_MT; ++mt) {
-            if (mt >= MT) break;
-            float lo[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) lo[k] = ptx::tf32_lo(v[mt][k]);
-            if (!TC_DBG(*this, 4)) {
-                ptx::tmem_st8(sbase + mt * 16, v[mt]);
-                ptx::tmem_st8(sbase + mt * 16 + 8, lo);
-            }
-        }
-        ptx::tmem_wait_st();
-        TC_TRACE(*this, KS, 2, lane == 0 && q == 0);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
-    }
-};
+__device__ __forceinline__ void tc_tile_origin(const TcConvArgs &a, int tile, int &img, int &u0,
+                                               int &v0) {
+    const int per_img = a.tiles_x * a.tiles_y;
+    img = tile / per_img;
+    const int rem = tile - img * per_img;
+    const int ty = rem / a.tiles_x;
+    u0 = ty * 4 * a.MT;
+    v0 = (rem - ty * a.tiles_x) * 32;
+}
 
 template <bool STACKED, bool BWD>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *wsm = smem_raw;  // packed weights
+    unsigned char *wsm = smem_raw;             // packed weights
+    unsigned char *hsm = smem_raw + a.wbytes;  // HB halo buffers
     __shared__ uint64_t full_bar[TC_MAX_STAGES], empty_bar[TC_MAX_STAGES];
-    __shared__ uint64_t tfull_bar[2], tempty_bar[2], w_bar;
+    __shared__ uint64_t tfull_bar[2], tempty_bar[2], hfull[TC_MAX_HB], hempty[TC_MAX_HB], w_bar;
     __shared__ uint32_t s_tmem;
+    __shared__ int s_rowrel[TC_MAX_HROWS];  // halo row -> input row offset from u0 - pad
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int MT = a.MT;
+    const int ll = a.l * a.l;
+    for (int r = threadIdx.x; r < a.hrows; r += blockDim.x) {
+        const int ib = r / a.RB;
+        s_rowrel[r] = (r - ib * a.RB) + ib * a.d;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             ptx::mbar_init(&full_bar[s], 4);
@@ -286,7 +156,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull_bar[b], 1);
-            ptx::mbar_init(&tempty_bar[b], 4);
+            ptx::mbar_init(&tempty_bar[b], TC_EPI_WARPS);
+        }
+        for (int b = 0; b < a.HB; ++b) {
+            ptx::mbar_init(&hfull[b], TC_LOAD_WARPS);
+            ptx::mbar_init(&hempty[b], 8);
         }
         ptx::mbar_init(&w_bar, 1);
         ptx::mbar_fence_init();
@@ -298,28 +172,124 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
     const uint32_t tmem = s_tmem;
     // TMEM columns: [0, 2*MT*acc_cols) accumulators (2 tile buffers), then the A stages
     const uint32_t a_base = tmem + (uint32_t)(2 * MT * a.acc_cols);
-    const int per_img = a.tiles_x * a.tiles_y;
+    const long long plane_in = (long long)a.Hin * a.Win;
 
-    if (warp >= TC_PROD_WARP0 && warp < TC_PROD_WARP0 + TC_PROD_WARPS) {
-        // ============================ producers ============================
-        // K-steps are numbered per CTA in MMA order, KS = tile_seq * n_ks + ks; group p
-        // produces KS = p, p + TC_GROUPS, ...  Striding the CTA-global KS keeps each
-        // group's stage waits one parity round deep (unambiguous) and, with
-        // stages >= 2 * TC_GROUPS, deadlock-free.
-        TcProducer pr;
-        const int grp = (warp - TC_PROD_WARP0) >> 2;
-        pr.init(a, warp & 3, grp, lane, a_base, per_img);
-        float va[TC_MAX_MT][8], vb[TC_MAX_MT][8];
-        pr.load(va);  // K-step grp
-        pr.load(vb);  // K-step grp + TC_GROUPS
-        for (int KS = grp; KS < pr.total_ks; KS += 2 * TC_GROUPS) {
-            pr.commit(va, KS, empty_bar, full_bar);
-            TC_TRACE(a, KS, 6, lane == 0 && (warp & 3) == 0);
-            pr.load(va);  // K-step KS + 2 * TC_GROUPS
-            TC_TRACE(a, KS, 7, lane == 0 && (warp & 3) == 0);
-            if (KS + TC_GROUPS >= pr.total_ks) break;
-            pr.commit(vb, KS + TC_GROUPS, empty_bar, full_bar);
-            pr.load(vb);  // K-step KS + 3 * TC_GROUPS
+    if (warp >= TC_LOAD_WARP0 && warp < TC_MMA_WARP) {
+        // ============================ halo loaders ============================
+        // buffer rows (c, srow) are spread over the loader warps, lanes walk the columns:
+        // row srow holds input row u0 - pad + s_rowrel[srow], column scol holds input
+        // column v0 - pad + colrel (both fixed per kernel).  Coalesced LDG (lanes =
+        // consecutive columns) -> STS with TC_LB rows of loads in flight per warp.
+        // (4-byte cp.async measured ~43k cycles per chunk: LDGSTS throughput is per
+        // thread-op, not per byte.)
+        const int lw = warp - TC_LOAD_WARP0;
+        const int nrows = 8 * a.hrows;
+        int colrel[TC_LC];
+#pragma unroll
+        for (int cc = 0; cc < TC_LC; ++cc) {
+            const int scol = lane + 32 * cc;
+            const int jb = scol / a.CB;
+            colrel[cc] = scol < a.hcols ? (scol - jb * a.CB) + jb * a.d : -(1 << 29);
+        }
+        int g = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            int img, u0, v0;
+            tc_tile_origin(a, tile, img, u0, v0);
+            const int ub = u0 - a.pad, vb = v0 - a.pad;
+            for (int rc = 0; rc < a.n_rc; ++rc, ++g) {
+                const int hb = g % a.HB;
+                ptx::mbar_wait(&hempty[hb], ((g / a.HB) & 1) ^ 1);
+                TC_TRACE(a, g * ll, 0, lw == 0 && lane == 0);
+                float *buf = reinterpret_cast<float *>(hsm + (size_t)hb * a.hbytes);
+                const float *src_c = a.in + ((long long)img * a.R + rc * 8) * plane_in;
+                const int cvalid = min(8, a.R - rc * 8);
+                int c = 0, srow = lw;  // row = c * hrows + srow, advanced without divides
+                while (srow >= a.hrows) {
+                    srow -= a.hrows;
+                    ++c;
+                }
+                for (int row0 = lw; row0 < nrows; row0 += TC_LOAD_WARPS * TC_LB) {
+                    float v[TC_LB][TC_LC];
+                    int cb = c, sb = srow;
+#pragma unroll
+                    for (int b = 0; b < TC_LB; ++b) {
+                        const int grow = ub + s_rowrel[sb < a.hrows ? sb : 0];
+                        const bool rok = cb < cvalid && grow >= 0 && grow < a.Hin;
+                        const float *src_r =
+                            src_c + (long long)cb * plane_in + (long long)grow * a.Win + vb;
+#pragma unroll
+                        for (int cc = 0; cc < TC_LC; ++cc) {
+                            const int gcol = vb + colrel[cc];
+                            const bool ok = rok && gcol >= 0 && gcol < a.Win;
+                            v[b][cc] = ok ? __ldg(src_r + colrel[cc]) : 0.f;
+                        }
+                        sb += TC_LOAD_WARPS;
+                        while (sb >= a.hrows) {
+                            sb -= a.hrows;
+                            ++cb;
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < TC_LB; ++b) {
+                        const int row = row0 + b * TC_LOAD_WARPS;
+                        if (row >= nrows) break;
+                        float *dst_r = buf + (size_t)row * a.hcols;
+#pragma unroll
+                        for (int cc = 0; cc < TC_LC; ++cc) {
+                            const int scol = lane + 32 * cc;
+                            if (scol < a.hcols) dst_r[scol] = v[b][cc];
+                        }
+                    }
+                    c = cb;
+                    srow = sb;
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&hfull[hb]);
+                TC_TRACE(a, g * ll, 1, lw == 0 && lane == 0);
+            }
+        }
+    } else if (warp >= TC_CONV_WARP0 && warp < TC_LOAD_WARP0) {
+        // ============================ converters ============================
+        const int q = warp & 3, grp = (warp - TC_CONV_WARP0) >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const int cstride = a.hrows * a.hcols;  // floats between channels in a buffer
+        int KS = 0, g = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            for (int rc = 0; rc < a.n_rc; ++rc, ++g) {
+                const int hb = g % a.HB;
+                ptx::mbar_wait(&hfull[hb], (g / a.HB) & 1);
+                const float *buf = reinterpret_cast<const float *>(hsm + (size_t)hb * a.hbytes);
+                for (int tap = 0; tap < ll; ++tap, ++KS) {
+                    if ((KS & 1) != grp) continue;
+                    const int i = tap / a.l, j = tap - i * a.l;
+                    const int stage = KS % a.stages;
+                    TC_TRACE(a, KS, 2, q == 0 && lane == 0);
+                    ptx::mbar_wait(&empty_bar[stage], ((KS / a.stages) & 1) ^ 1);
+                    ptx::tc_fence_after();
+                    TC_TRACE(a, KS, 3, q == 0 && lane == 0);
+                    const uint32_t sbase = a_base + lane_off + (uint32_t)(stage * MT * 16);
+                    const float *p0 = buf + (i * a.RS + q) * a.hcols + lane + j * a.CS;
+#pragma unroll
+                    for (int mt = 0; mt < TC_MAX_MT; ++mt) {
+                        if (mt >= MT) break;
+                        const float *p = p0 + 4 * mt * a.hcols;
+                        float hi[8], lo[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) hi[k] = p[k * cstride];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) lo[k] = ptx::tf32_lo(hi[k]);
+                        ptx::tmem_st8(sbase + mt * 16, hi);
+                        ptx::tmem_st8(sbase + mt * 16 + 8, lo);
+                    }
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
+                    TC_TRACE(a, KS, 4, q == 0 && lane == 0);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&hempty[hb]);
+            }
         }
     } else if (warp == TC_MMA_WARP) {
         // ============================ weights + MMA issuer ============================
@@ -337,10 +307,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
         const uint32_t ks_bytes = (uint32_t)a.Npad * 64;  // hi + lo tiles
         const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
         const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
-        int stage = 0, buf = 0;
+        int stage = 0, buf = 0, mks = 0;
         uint32_t phase = 0, tphase = 0;
-        int tseq_mma = 0;
-        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x, ++tseq_mma) {
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tempty_bar[buf], tphase ^ 1);
             ptx::tc_fence_after();
             const uint32_t dbase = tmem + (uint32_t)(buf * MT * a.acc_cols);
@@ -350,13 +319,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
                 const uint64_t dlo = ptx::smem_desc(bhi + (uint32_t)a.Npad * 32, 128, 256);
                 const uint32_t sbase = a_base + (uint32_t)(stage * MT * 16);
                 const uint32_t acc = ks > 0;
-                const int KSg = tseq_mma * a.n_ks + ks;
-                TC_TRACE(a, KSg, 3, lane == 0);
+                TC_TRACE(a, mks, 5, lane == 0);
                 ptx::mbar_wait(&full_bar[stage], phase);
-                TC_TRACE(a, KSg, 4, lane == 0);
                 ptx::tc_fence_after();
+                TC_TRACE(a, mks, 6, lane == 0);
                 if (ptx::elect_one()) {
-                    for (int mt = 0; mt < (TC_DBG(a, 2) ? 0 : MT); ++mt) {
+                    for (int mt = 0; mt < MT; ++mt) {
                         const uint32_t ahi = sbase + mt * 16, alo = ahi + 8;
                         const uint32_t d = dbase + (uint32_t)(mt * a.acc_cols);
                         if (STACKED) {
@@ -370,8 +338,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
                     }
                     ptx::mma_commit(&empty_bar[stage]);
                 }
-                TC_TRACE(a, KSg, 5, lane == 0);
                 __syncwarp();
+                TC_TRACE(a, mks, 7, lane == 0);
+                ++mks;
                 if (++stage == a.stages) {
                     stage = 0;
                     phase ^= 1;
@@ -386,21 +355,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
         }
     } else {
         // ============================ epilogue ============================
-        const int q = warp & 3;
+        const int q = warp & 3, half = warp >> 2;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const long long ostride = (long long)a.Ho * a.Wo;
         int buf = 0;
         uint32_t tphase = 0;
         for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-            const int img = tile / per_img;
-            const int rem = tile - img * per_img;
-            const int u0 = (rem / a.tiles_x) * 4 * MT, v0 = (rem % a.tiles_x) * 32;
+            int img, u0, v0;
+            tc_tile_origin(a, tile, img, u0, v0);
             const int col = v0 + lane;
             ptx::mbar_wait_sleep(&tfull_bar[buf], tphase);
             ptx::tc_fence_after();
-            float *out_img = a.out + (long long)img * a.Q * a.Ho * a.Wo;
-            const float *gate_img =
-                a.gate ? a.gate + (long long)img * a.Q * a.Ho * a.Wo : nullptr;
-            for (int mt = 0; mt < MT; ++mt) {
+            const long long img_off = (long long)img * a.Q * ostride;
+            for (int mt = half; mt < MT; mt += 2) {
                 const int row = u0 + 4 * mt + q;
                 const bool inside = row < a.Ho && col < a.Wo;
                 const uint32_t dcol = tmem + lane_off + (uint32_t)((buf * MT + mt) * a.acc_cols);
@@ -410,19 +377,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
                     if (STACKED) ptx::tmem_ld16(dcol + a.Npad + o0, r2);
                     ptx::tmem_wait_ld();
                     if (!inside) continue;
-#pragma unroll
+                    const long long off0 = img_off + (long long)o0 * ostride +
+                                           (long long)row * a.Wo + col;
+#pragma unroll 4
                     for (int t = 0; t < 16; ++t) {
                         const int o = o0 + t;
                         if (o >= a.Q) break;
                         float val = __uint_as_float(r[t]);
                         if (STACKED) val += __uint_as_float(r2[t]);
-                        const long long off = ((long long)o * a.Ho + row) * a.Wo + col;
-                        if (!BWD) {
-                            val = tc_act(val + a.bias[o], a.act);
-                        } else if (gate_img) {
-                            val = gate_from_output(val, gate_img[off], a.gate_kind);
-                        }
-                        out_img[off] = val;
+                        const long long off = off0 + t * ostride;
+                        if (!BWD)
+                            val = tc_act(val + __ldg(a.bias + o), a.act);
+                        else if (a.gate)
+                            val = gate_from_output(val, __ldg(a.gate + off), a.gate_kind);
+                        a.out[off] = val;
                     }
                 }
             }
@@ -447,17 +415,48 @@ struct TcPlan {
     int Npad, n_rc, n_ks, MT, acc_cols, stages;
     bool stacked;
     size_t wbytes;
+    // halo geometry for the chosen MT
+    int hrows, hcols, RB, RS, CB, CS, HB;
+    size_t hbytes;
 };
 
+// halo buffer geometry for M tiles MT: per axis the full halo or only the l tap blocks,
+// whichever is smaller
+static void tc_halo(TcPlan &p, int l, int d) {
+    const int rh = 4 * p.MT + (l - 1) * d, rt = l * 4 * p.MT;
+    if (rh <= rt) {
+        p.hrows = rh;
+        p.RB = rh;
+        p.RS = d;
+    } else {
+        p.hrows = rt;
+        p.RB = 4 * p.MT;
+        p.RS = 4 * p.MT;
+    }
+    const int ch = 32 + (l - 1) * d, ct = l * 32;
+    if (ch <= ct) {
+        p.hcols = ch;
+        p.CB = ch;
+        p.CS = d;
+    } else {
+        p.hcols = ct;
+        p.CB = 32;
+        p.CS = 32;
+    }
+    p.hbytes = ((size_t)8 * p.hrows * p.hcols * 4 + 127) / 128 * 128;
+}
+
 // TMEM budget (512 columns): 2 * MT * acc_cols accumulator columns + stages * MT * 16
-// A columns, with stages >= TC_MIN_STAGES.  DP_TC_MT overrides the M tiles per CTA tile.
-static TcPlan tc_plan(int R, int Q, int l) {
+// A columns, with stages >= TC_MIN_STAGES; shared memory: packed weights + 2-3 halo
+// buffers.  DP_TC_MT caps the M tiles per CTA tile.
+static TcPlan tc_plan(int R, int Q, int l, int d) {
     TcPlan p;
     p.Npad = (Q + 15) / 16 * 16;
     p.n_rc = (R + 7) / 8;
     p.n_ks = p.n_rc * l * l;
     p.stacked = p.Npad <= 16;
     p.acc_cols = p.stacked ? 2 * p.Npad : p.Npad;
+    p.wbytes = ((size_t)p.n_ks * p.Npad * 64 + 127) / 128 * 128;
     int want = TC_MAX_MT;
     if (const char *e = getenv("DP_TC_MT")) {
         int v = atoi(e);
@@ -469,34 +468,57 @@ static TcPlan tc_plan(int R, int Q, int l) {
         int acc_total = 2 * mt * p.acc_cols;
         int st = (512 - acc_total) / (mt * 16);
         if (st > TC_MAX_STAGES) st = TC_MAX_STAGES;
-        if (acc_total < 512 && st >= TC_MIN_STAGES) {
-            p.MT = mt;
+        TcPlan t = p;
+        t.MT = mt;
+        tc_halo(t, l, d);
+        if (acc_total < 512 && st >= TC_MIN_STAGES && t.hcols <= 32 * TC_LC &&
+            t.hrows <= TC_MAX_HROWS &&
+            p.wbytes + 2 * t.hbytes <= (size_t)TC_SMEM_BUDGET) {
+            p = t;
             p.stages = st;
+            p.HB = p.wbytes + 3 * t.hbytes <= (size_t)TC_SMEM_BUDGET ? 3 : 2;
             break;
         }
     }
-    p.wbytes = (size_t)p.n_ks * p.Npad * 64;
+    if (p.MT == 0) {
+        p.MT = 1;
+        tc_halo(p, l, d);
+        p.MT = 0;
+    }
     return p;
 }
 
-size_t tc_conv_workspace(int R, int Q, int l) { return tc_plan(R, Q, l).wbytes; }
+size_t tc_conv_workspace(int R, int Q, int l) {
+    return ((size_t)(R + 7) / 8 * l * l * ((Q + 15) / 16 * 16) * 64 + 127) / 128 * 128;
+}
 
-bool tc_conv_supported(int R, int Q, int l) {
-    TcPlan p = tc_plan(R, Q, l);
-    return p.Npad <= 128 && p.MT >= 1 && p.wbytes <= (size_t)TC_MAX_SMEM;
+bool tc_conv_supported(int R, int Q, int l, int d) {
+    TcPlan p = tc_plan(R, Q, l, d);
+    return p.Npad <= 128 && p.MT >= 1;
 }
 
 static int g_num_sms = 0;
+static unsigned long long *g_tc_trace = nullptr;
+
+// debugging aid (tools/tc_trace.py): the last traced launch's timestamps
+int tc_trace_copy(void *host, size_t bytes) {
+    if (!g_tc_trace) return DP_ERR_ARG;
+    if (bytes > 1024 * 8 * 8) bytes = 1024 * 8 * 8;
+    return cudaMemcpy(host, g_tc_trace, bytes, cudaMemcpyDeviceToHost) == cudaSuccess
+               ? DP_OK
+               : DP_ERR_CUDA;
+}
 
 static int launch_tc(const float *in, const float *w, const float *bias, float *out,
                      const float *gate, int n, int R, int Hin, int Win, int Q, int Ho, int Wo,
                      int l, int d, int pad, int act, int gate_kind, bool bwd, void *ws,
                      size_t ws_bytes, cudaStream_t st) {
-    TcPlan p = tc_plan(R, Q, l);
-    if (!tc_conv_supported(R, Q, l))
+    TcPlan p = tc_plan(R, Q, l, d);
+    if (!(p.Npad <= 128 && p.MT >= 1))
         return set_error(DP_ERR_UNSUPPORTED,
-                         "tensor-core conv: weights need %zu B of shared memory (R=%d Q=%d k=%d)",
-                         p.wbytes, R, Q, l);
+                         "tensor-core conv: weights (%zu B) + halo buffers exceed shared "
+                         "memory (R=%d Q=%d k=%d d=%d)",
+                         p.wbytes, R, Q, l, d);
     if (ws == nullptr || ws_bytes < p.wbytes)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
                          p.wbytes);
@@ -513,6 +535,13 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    // fewer M tiles per CTA tile when the image is short (less padding waste)
+    const int rows_needed = (Ho + 3) / 4;
+    if (p.MT > rows_needed) {
+        p.MT = rows_needed;
+        tc_halo(p, l, d);
+        p.HB = p.wbytes + 3 * p.hbytes <= (size_t)TC_SMEM_BUDGET ? 3 : 2;
     }
     TcConvArgs a;
     a.in = in;
@@ -536,10 +565,6 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     a.Npad = p.Npad;
     a.MT = p.MT;
     a.stages = p.stages;
-    // fewer M tiles per CTA tile when the image is short (less padding waste); the
-    // stage count is kept (fewer A columns per stage only loosens the TMEM budget)
-    int rows_needed = (Ho + 3) / 4;
-    if (a.MT > rows_needed) a.MT = rows_needed;
     a.acc_cols = p.acc_cols;
     a.tiles_x = ceil_div(Wo, 32);
     a.tiles_y = ceil_div(Ho, 4 * a.MT);
@@ -547,8 +572,24 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     if (tt > 0x7fffffff) return set_error(DP_ERR_UNSUPPORTED, "tensor-core conv: too many tiles");
     a.total_tiles = (int)tt;
     a.wbytes = (uint32_t)p.wbytes;
+    a.hrows = p.hrows;
+    a.hcols = p.hcols;
+    a.RB = p.RB;
+    a.RS = p.RS;
+    a.CB = p.CB;
+    a.CS = p.CS;
+    a.hbytes = (uint32_t)p.hbytes;
+    a.HB = p.HB;
+    a.trace = nullptr;
+    if (getenv("DP_TC_TRACE")) {
+        static unsigned long long *buf = nullptr;
+        if (!buf && cudaMalloc(&buf, 1024 * 8 * 8) != cudaSuccess) buf = nullptr;
+        if (buf) cudaMemsetAsync(buf, 0, 1024 * 8 * 8, st);
+        a.trace = buf;
+        g_tc_trace = buf;
+    }
     int grid = a.total_tiles < g_num_sms ? a.total_tiles : g_num_sms;
-    size_t smem = p.wbytes;
+    size_t smem = p.wbytes + (size_t)p.HB * p.hbytes;
     void (*kern)(const TcConvArgs);
     if (p.stacked)
         kern = bwd ? tc_conv_kernel<true, true> : tc_conv_kernel<true, false>;

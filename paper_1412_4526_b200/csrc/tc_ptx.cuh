@@ -99,6 +99,11 @@ __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, uint
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)),
                  "l"(src), "r"(src_bytes) : "memory");
 }
+// 4-byte global -> shared copy (no alignment constraints beyond 4 B); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async4(void *dst_smem, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst_smem)),
+                 "l"(src), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }

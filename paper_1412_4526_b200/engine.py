@@ -117,8 +117,8 @@ class ops:
                                                         _stream()), "conv_backward_data")
 
     @staticmethod
-    def fast_supported(reduce_c, out_c, k) -> bool:
-        return bool(_lib_dev().dp_conv_fast_supported(reduce_c, out_c, k))
+    def fast_supported(reduce_c, out_c, k, d) -> bool:
+        return bool(_lib_dev().dp_conv_fast_supported(reduce_c, out_c, k, d))
 
     @staticmethod
     def fast_workspace(reduce_c, out_c, k) -> int:
@@ -445,8 +445,9 @@ class DenseNet:
         for gi, g in enumerate(self.groups):
             if isinstance(g.op, DilatedConv) and self.precision == "fast":
                 ci, co, kk = g.op.base.in_channels, g.op.base.out_channels, g.op.base.kernel_size
-                f_ok = ops.fast_supported(ci, co, kk)
-                b_ok = train and gi > 0 and ops.fast_supported(co, ci, kk)
+                dd = g.op.dilation
+                f_ok = ops.fast_supported(ci, co, kk, dd)
+                b_ok = train and gi > 0 and ops.fast_supported(co, ci, kk, dd)
                 self.tc[gi] = (f_ok, b_ok)
                 if f_ok:
                     tc_ws = max(tc_ws, ops.fast_workspace(ci, co, kk))

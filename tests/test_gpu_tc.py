@@ -23,6 +23,9 @@ SHAPES = [
     (3, 2, 3, 1, 5, 9, 9),          # 1x1 kernel, tiny image (MT clamps)
     (1, 48, 64, 3, 2, 40, 45),      # c4-like L2: R=48, Q=64 (acc 64 cols)
     (1, 12, 48, 5, 1, 33, 37),      # Npad=48
+    (1, 16, 8, 3, 32, 80, 90),      # d=32: tap-row / tap-column halo layout
+    (1, 8, 16, 7, 8, 60, 66),       # 7x7 FC-style head, d=8
+    (4, 3, 16, 6, 1, 20, 23),       # tiny images: one M tile, several images per CTA
 ]
 
 
@@ -43,7 +46,7 @@ def test_tc_forward_matches_exact(shape, act):
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
-    if not ops.fast_supported(ci, co, k):
+    if not ops.fast_supported(ci, co, k, d):
         pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
     rng = np.random.default_rng(sum(shape) + act)
     x = _t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
@@ -66,7 +69,7 @@ def test_tc_backward_data_matches_exact(shape, gate_kind):
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
-    if not ops.fast_supported(co, ci, k):
+    if not ops.fast_supported(co, ci, k, d):
         pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
     rng = np.random.default_rng(sum(shape) + 7)
     e = (k - 1) * d + 1

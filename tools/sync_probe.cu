@@ -75,6 +75,59 @@ __global__ void tma_lat(const __grid_constant__ CUtensorMap tm, int iters, int n
     }
 }
 
+// Skeleton of the tc_conv / tc_wgrad pipeline: 2 producer groups x 4 warps alternate K-steps,
+// S stages, one MMA warp waits full / commits empty.  No data, no MMAs.
+// flags: 1 producer uses tcgen05.wait::st + fences, 2 MMA uses tcgen05.commit (else arrive),
+//        4 MMA thread does tcgen05.fence::after_thread_sync
+__global__ void skeleton(int ksteps, int S, int flags, unsigned long long *out) {
+    __shared__ uint64_t full[16], empty[16];
+    __shared__ uint32_t s_tmem;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 4);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_fence_init();
+    }
+    if (warp == 8) ptx::tmem_alloc<32>(&s_tmem);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    unsigned long long t0 = clock64();
+    if (warp < 8) {
+        const int grp = warp >> 2;
+        for (int KS = grp; KS < ksteps; KS += 2) {
+            const int st = KS % S;
+            ptx::mbar_wait(&empty[st], ((KS / S) & 1) ^ 1);
+            if (flags & 1) {
+                ptx::tc_fence_after();
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&full[st]);
+        }
+    } else if (warp == 8) {
+        for (int KS = 0; KS < ksteps; ++KS) {
+            const int st = KS % S;
+            ptx::mbar_wait(&full[st], (KS / S) & 1);
+            if (flags & 4) ptx::tc_fence_after();
+            if (flags & 2) {
+                if (ptx::elect_one()) ptx::mma_commit(&empty[st]);
+                __syncwarp();
+            } else if (lane == 0) {
+                ptx::mbar_arrive(&empty[st]);
+            }
+        }
+    }
+    unsigned long long t1 = clock64();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 8) ptx::tmem_dealloc<32>(s_tmem);
+    if (threadIdx.x == 256) out[blockIdx.x] = (t1 - t0) / ksteps;
+}
+
 int main() {
     unsigned long long *d, h;
     cudaMalloc(&d, 8);
@@ -106,5 +159,14 @@ int main() {
         cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
         printf("TMA %d box(es) {32,1,32} issue->complete: %llu cycles (%s)\n", nb, h, cudaGetErrorString(e));
     }
+    for (int grid : {1, 148})
+        for (int S : {4, 8})
+            for (int flags : {0, 1, 2, 4, 7}) {
+                skeleton<<<grid, 288>>>(4000, S, flags, d);
+                cudaError_t e = cudaDeviceSynchronize();
+                cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+                printf("skeleton grid %3d S=%d flags=%d: %llu cycles per K-step (%s)\n", grid, S, flags, h,
+                       cudaGetErrorString(e));
+            }
     return 0;
 }

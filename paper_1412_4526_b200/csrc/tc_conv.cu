@@ -375,22 +375,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
                     uint32_t r[16], r2[16];
                     ptx::tmem_ld16(dcol + o0, r);
                     if (STACKED) ptx::tmem_ld16(dcol + a.Npad + o0, r2);
-                    ptx::tmem_wait_ld();
-                    if (!inside) continue;
                     const long long off0 = img_off + (long long)o0 * ostride +
                                            (long long)row * a.Wo + col;
-#pragma unroll 4
+                    const int nq = min(16, a.Q - o0);
+                    // gate / bias operands fetched while the TMEM loads are in flight
+                    float aux[16];
+                    if (BWD) {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t)
+                            aux[t] = (a.gate && inside && t < nq)
+                                         ? __ldg(a.gate + off0 + t * ostride) : 0.f;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t) aux[t] = t < nq ? __ldg(a.bias + o0 + t) : 0.f;
+                    }
+                    ptx::tmem_wait_ld();
+                    if (!inside) continue;
+#pragma unroll
                     for (int t = 0; t < 16; ++t) {
-                        const int o = o0 + t;
-                        if (o >= a.Q) break;
+                        if (t >= nq) break;
                         float val = __uint_as_float(r[t]);
                         if (STACKED) val += __uint_as_float(r2[t]);
-                        const long long off = off0 + t * ostride;
                         if (!BWD)
-                            val = tc_act(val + __ldg(a.bias + o), a.act);
+                            val = tc_act(val + aux[t], a.act);
                         else if (a.gate)
-                            val = gate_from_output(val, __ldg(a.gate + off), a.gate_kind);
-                        a.out[off] = val;
+                            val = gate_from_output(val, aux[t], a.gate_kind);
+                        a.out[off0 + t * ostride] = val;
                     }
                 }
             }

@@ -341,9 +341,17 @@ def main():
         ceil = peaks["bf16_tflops"] / 2 / 3
         roof["derived_3xtf32_ceiling_tflops"] = ceil
         roof["frac_of_3xtf32_ceiling"] = roof["achieved"] / ceil
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if top["name"] in tj.get("kernels", {}):
+            traffic = tj["kernels"][top["name"]]["dram_bytes"]
+            traffic_src = tj.get("source")
     roof.update({"kernel": top["name"], "ms_per_launch": top["ms"],
                  "share_of_step": top["ms"] / prof["step_ms"], "peak_source": peaks["source"],
-                 "traffic": None,
+                 "traffic": traffic, "traffic_source": traffic_src,
                  "note": ("tcgen05 kind::tf32 3xTF32 conv: algorithmic FLOPs (each MAC issues 3 "
                           "TF32 MACs); peak = measured dense bf16 (TF32 dense is half of it)"
                           if "_tc" in top["name"] else

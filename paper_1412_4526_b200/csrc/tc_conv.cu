@@ -50,6 +50,7 @@ namespace dp {
 constexpr int TC_MAX_STAGES = 16;
 constexpr int TC_MAX_MT = 4;  // M tiles per CTA tile
 constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_NGROUPS = 2;      // converter groups of 4 warps, K-steps round-robin
 constexpr int TC_CONV_WARP0 = 8;   // 2 groups x 4
 constexpr int TC_LOAD_WARP0 = 16;  // 8 loader warps
 constexpr int TC_LOAD_WARPS = 8;
@@ -198,7 +199,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
             const int ub = u0 - a.pad, vb = v0 - a.pad;
             for (int rc = 0; rc < a.n_rc; ++rc, ++g) {
                 const int hb = g % a.HB;
-                ptx::mbar_wait(&hempty[hb], ((g / a.HB) & 1) ^ 1);
+                // loaders idle most of a chunk: back off instead of spinning on issue slots
+                ptx::mbar_wait_sleep(&hempty[hb], ((g / a.HB) & 1) ^ 1);
                 TC_TRACE(a, g * ll, 0, lw == 0 && lane == 0);
                 float *buf = reinterpret_cast<float *>(hsm + (size_t)hb * a.hbytes);
                 const float *src_c = a.in + ((long long)img * a.R + rc * 8) * plane_in;
@@ -254,21 +256,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const int cstride = a.hrows * a.hcols;  // floats between channels in a buffer
         int KS = 0, g = 0;
+        int stage = 0, sphase = 0, hb = 0, hphase = 0, kmod = 0;  // incremental counters
         for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
             for (int rc = 0; rc < a.n_rc; ++rc, ++g) {
-                const int hb = g % a.HB;
-                ptx::mbar_wait(&hfull[hb], (g / a.HB) & 1);
+                ptx::mbar_wait(&hfull[hb], hphase);
                 const float *buf = reinterpret_cast<const float *>(hsm + (size_t)hb * a.hbytes);
+                int i = 0, j = 0;
                 for (int tap = 0; tap < ll; ++tap, ++KS) {
-                    if ((KS & 1) != grp) continue;
-                    const int i = tap / a.l, j = tap - i * a.l;
-                    const int stage = KS % a.stages;
+                    const bool mine = kmod == grp;
+                    const int cur_stage = stage, cur_phase = sphase;
+                    const int ci = i, cj = j;
+                    if (++kmod == TC_NGROUPS) kmod = 0;
+                    if (++stage == a.stages) {
+                        stage = 0;
+                        sphase ^= 1;
+                    }
+                    if (++j == a.l) {
+                        j = 0;
+                        ++i;
+                    }
+                    if (!mine) continue;
                     TC_TRACE(a, KS, 2, q == 0 && lane == 0);
-                    ptx::mbar_wait(&empty_bar[stage], ((KS / a.stages) & 1) ^ 1);
+                    ptx::mbar_wait(&empty_bar[cur_stage], cur_phase ^ 1);
                     ptx::tc_fence_after();
                     TC_TRACE(a, KS, 3, q == 0 && lane == 0);
-                    const uint32_t sbase = a_base + lane_off + (uint32_t)(stage * MT * 16);
-                    const float *p0 = buf + (i * a.RS + q) * a.hcols + lane + j * a.CS;
+                    const uint32_t sbase = a_base + lane_off + (uint32_t)(cur_stage * MT * 16);
+                    const float *p0 = buf + (ci * a.RS + q) * a.hcols + lane + cj * a.CS;
 #pragma unroll
                     for (int mt = 0; mt < TC_MAX_MT; ++mt) {
                         if (mt >= MT) break;
@@ -284,11 +297,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
                     ptx::tmem_wait_st();
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
+                    if (lane == 0) ptx::mbar_arrive(&full_bar[cur_stage]);
                     TC_TRACE(a, KS, 4, q == 0 && lane == 0);
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&hempty[hb]);
+                if (++hb == a.HB) {
+                    hb = 0;
+                    hphase ^= 1;
+                }
             }
         }
     } else if (warp == TC_MMA_WARP) {

@@ -57,7 +57,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
             : "r"(smem_u32(b)), "r"(parity)
             : "memory");
         if (done) return;
-        __nanosleep(256);
+        __nanosleep(512);
     }
 }
 

@@ -1,3 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_tc.py -q -x 2>&1 | tail -3
-timeout 300 python -m pytest tests/test_gpu_engine.py -q -x 2>&1 | tail -3
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/f4/bench.json 2> gpurun_out/f4/bench.err
+timeout 300 python -m pytest tests/test_gpu_tc.py -q -x 2>&1 | tail -2
+for c in "fwd 64,32,10,4,4,268" "fwd 64,16,32,5,2,278" "bwd 64,16,32,5,2,278" "bwd 64,32,10,4,4,268" "fwd 64,3,16,6,1,284"; do timeout 60 python tools/tc_trace.py $c | sed -n "1p;\$p"; done
+timeout 60 python tools/tc_trace.py fwd 64,16,32,5,2,278 | sed -n "12,18p"

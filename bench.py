@@ -303,21 +303,36 @@ def main():
         fwd_step(s)
     ms_fwd = timed(fwd_step, args.steps)
 
-    # ---- e2e through the public trainer API from pinned host buffers
+    # ---- e2e through the public trainer API from pinned host buffers: every step copies
+    # its images + targets + masks H2D (double-buffered: the copy of batch s+1 overlaps
+    # step s) and reads the gradient bucket back D2H
+    from paper_1412_4526_b200.trainer import H2DPipeline
     grad_host = torch.empty(net.grad_flat.shape, dtype=net.grad_flat.dtype).pin_memory()
-    stage = [torch.empty_like(t) for t in dpool[0]]
+    feed = H2DPipeline(tr, *dpool[0])
 
-    def e2e_step(s):
-        himgs, htgts, hmasks = hpool[s & 1]
-        for dst, src in zip(stage, (himgs, htgts, hmasks)):
-            dst.copy_(src, non_blocking=True)
-        tr.load_batch(*stage)
-        tr.step()
-        grad_host.copy_(net.grad_flat, non_blocking=True)
+    def e2e_run(steps):
+        feed.submit(*hpool[0])
+        for s in range(steps):
+            if s + 1 < steps:
+                feed.submit(*hpool[(s + 1) & 1])
+            feed.step()
+            grad_host.copy_(net.grad_flat, non_blocking=True)
 
-    for s in range(args.warmup):
-        e2e_step(s)
-    ms_e2e = timed(e2e_step, args.steps)
+    e2e_run(args.warmup)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    feed.copy_stream.wait_event(e0)  # every H2D copy of the run lies inside [e0, e1]
+    e2e_run(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
     h2d = sum(t.numel() * t.element_size() for t in hpool[0])
     d2h = grad_host.numel() * grad_host.element_size()
 

@@ -126,3 +126,55 @@ class DataParallelTrainer:
     def forward_only(self):
         self.net.forward()
         return self.net.output
+
+
+class H2DPipeline:
+    """Double-buffered host -> device input pipeline for `DataParallelTrainer`.
+
+    `submit(images, targets, masks)` copies a batch from pinned host memory into one of
+    two device staging slots on a dedicated copy stream; `step()` makes the compute
+    stream wait for the oldest submitted batch, loads it into the engine and runs one
+    training step.  Submitting batch s+1 before stepping batch s overlaps the H2D
+    transfer with the step's kernels.  A slot is reused only after the step that read
+    it has finished (event), so no batch is overwritten in flight.
+    """
+
+    def __init__(self, trainer, images_like, targets_like, masks_like):
+        import torch
+        self._torch = torch
+        self.tr = trainer
+        dev = trainer.net.device
+        self.slots = [tuple(torch.empty(t.shape, dtype=t.dtype, device=dev)
+                            for t in (images_like, targets_like, masks_like)) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        self._free_recorded = [False, False]
+        self._submitted = 0
+        self._consumed = 0
+
+    def submit(self, images, targets, masks):
+        torch = self._torch
+        k = self._submitted % 2
+        if self._submitted - self._consumed >= 2:
+            raise RuntimeError("H2DPipeline: both slots hold unconsumed batches")
+        with torch.cuda.stream(self.copy_stream):
+            if self._free_recorded[k]:
+                self.copy_stream.wait_event(self.free[k])
+            for dst, src in zip(self.slots[k], (images, targets, masks)):
+                dst.copy_(src, non_blocking=True)
+            self.ready[k].record(self.copy_stream)
+        self._submitted += 1
+
+    def step(self):
+        torch = self._torch
+        if self._consumed >= self._submitted:
+            raise RuntimeError("H2DPipeline: step() without a submitted batch")
+        k = self._consumed % 2
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self.ready[k])
+        self.tr.load_batch(*self.slots[k])
+        self.free[k].record(cur)
+        self._free_recorded[k] = True
+        self.tr.step()
+        self._consumed += 1

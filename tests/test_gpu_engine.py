@@ -329,3 +329,38 @@ def test_dropin_errors(dp):
         dp.dense_backward(plan, cache, np.zeros((1, 5, 5)), dp.ErrorMask.full(4, 4))
     g = dp.dense_backward(plan, cache, np.ones((1, 5, 5)), dp.ErrorMask.of(5, 5, []))
     assert g.max_abs() == 0.0
+
+
+def test_h2d_pipeline_matches_direct_steps(dp):
+    """The double-buffered host->device feeder gives the same gradients as loading each
+    batch synchronously (trainer.H2DPipeline, used by bench.py's e2e leg)."""
+    import torch
+    from paper_1412_4526_b200.trainer import DataParallelTrainer, H2DPipeline
+    spec = dp.parse_spec(_c1_text(3))
+    plan = dp.compile_plan(spec)
+    side, B = 40, 2
+    rng = np.random.default_rng(5)
+    host = []
+    for _ in range(3):
+        imgs = torch.from_numpy(rng.uniform(-0.5, 0.5, (B, 3, side, side)).astype(np.float32))
+        tgts = torch.from_numpy(rng.uniform(-1, 1, (B, 10, side, side)).astype(np.float32))
+        masks = torch.from_numpy((rng.random((B, side, side)) < 0.1).astype(np.uint8))
+        host.append(tuple(t.pin_memory() for t in (imgs, tgts, masks)))
+    direct = DataParallelTrainer(plan, B, side, side, lr=1e-3, use_graph=False)
+    ref = []
+    for h in host:
+        direct.load_batch(*(t.cuda() for t in h))
+        direct.step()
+        ref.append(direct.net.grad_flat.clone())
+    piped = DataParallelTrainer(plan, B, side, side, lr=1e-3, use_graph=True)
+    feed = H2DPipeline(piped, *(t.cuda() for t in host[0]))
+    got = []
+    feed.submit(*host[0])
+    for s in range(3):
+        if s + 1 < 3:
+            feed.submit(*host[s + 1])
+        feed.step()
+        got.append(piped.net.grad_flat.clone())
+    torch.cuda.synchronize()
+    for a, b in zip(got, ref):
+        assert torch.equal(a, b)

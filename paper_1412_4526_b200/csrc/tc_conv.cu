@@ -27,9 +27,10 @@
 //               hi/lo in registers, write both into a TMEM stage with tcgen05.st.  The
 //               tap only moves the read window; every input element is fetched from
 //               global memory once per tile instead of l^2 times.
-//   warp 24     loads all packed weights (B, K-major, hi and lo) into shared memory once
-//               with bulk async copies, allocates TMEM, then issues the MMAs (one
-//               elected lane), one stage = one K-step = MT M tiles:
+//   warp 24     streams the packed weights (B, K-major, hi and lo) through a 3-buffer
+//               ring with bulk async copies, one unit per (channel chunk, tap row),
+//               allocates TMEM, and issues the MMAs (one elected lane), one stage = one
+//               K-step = MT M tiles:
 //               A_hi x [B_hi|B_lo] (N = 2*Npad) + A_lo x B_hi   (Npad <= 16), or
 //               A_hi x B_hi + A_hi x B_lo + A_lo x B_hi          (Npad >= 32),
 //               and releases the stage with one tcgen05.commit.
@@ -62,6 +63,8 @@ constexpr int TC_MAX_HB = 3;  // halo buffers (2 or 3, as shared memory allows)
 constexpr int TC_LB = 8;  // loader: buffer rows in flight per warp
 constexpr int TC_LC = 3;  // loader: 32-column groups per row (halo columns <= 96)
 constexpr int TC_SMEM_BUDGET = 220 * 1024;
+constexpr int TC_WB = 3;       // streamed weight-unit ring (per channel chunk and tap row)
+constexpr int TC_MAX_WB = 64;  // resident mode: one buffer per unit
 
 struct TcConvArgs {
     const float *in;     // (n, R, Hin, Win)
@@ -72,6 +75,8 @@ struct TcConvArgs {
     int R, Hin, Win, Q, Ho, Wo, l, d, pad, act, gate_kind;
     int n_rc, n_ks, Npad, MT, acc_cols, stages, tiles_x, tiles_y, total_tiles;
     uint32_t wbytes;
+    uint32_t unit_bytes;  // packed weights of one (channel chunk, tap row): l K-steps
+    int nwb, resident;    // weight-unit buffers; resident: all units loaded once
     // halo buffer geometry: rows (RB-row blocks per tap row i, step RS in the converter),
     // columns (CB-column blocks per tap column j, step CS)
     int hrows, hcols, RB, RS, CB, CS, HB;
@@ -133,13 +138,14 @@ __device__ __forceinline__ void tc_tile_origin(const TcConvArgs &a, int tile, in
     v0 = (rem - ty * a.tiles_x) * 32;
 }
 
-template <bool STACKED, bool BWD>
+template <bool STACKED, bool BWD, bool STREAM>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *wsm = smem_raw;             // packed weights
-    unsigned char *hsm = smem_raw + a.wbytes;  // HB halo buffers
+    unsigned char *wsm = smem_raw;  // nwb weight-unit buffers
+    unsigned char *hsm = smem_raw + (size_t)a.nwb * a.unit_bytes;  // HB halo buffers
     __shared__ uint64_t full_bar[TC_MAX_STAGES], empty_bar[TC_MAX_STAGES];
-    __shared__ uint64_t tfull_bar[2], tempty_bar[2], hfull[TC_MAX_HB], hempty[TC_MAX_HB], w_bar;
+    __shared__ uint64_t tfull_bar[2], tempty_bar[2], hfull[TC_MAX_HB], hempty[TC_MAX_HB];
+    __shared__ uint64_t wfull[TC_MAX_WB], wempty[TC_MAX_WB];
     __shared__ uint32_t s_tmem;
     __shared__ int s_rowrel[TC_MAX_HROWS];  // halo row -> input row offset from u0 - pad
 
@@ -163,7 +169,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
             ptx::mbar_init(&hfull[b], TC_LOAD_WARPS);
             ptx::mbar_init(&hempty[b], 8);
         }
-        ptx::mbar_init(&w_bar, 1);
+        for (int b = 0; b < a.nwb; ++b) {
+            ptx::mbar_init(&wfull[b], 1);
+            ptx::mbar_init(&wempty[b], 1);
+        }
         ptx::mbar_fence_init();
     }
     if (warp == TC_MMA_WARP) ptx::tmem_alloc<512>(&s_tmem);
@@ -310,16 +319,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
         }
     } else if (warp == TC_MMA_WARP) {
         // ============================ weights + MMA issuer ============================
-        if (ptx::elect_one()) {
-            ptx::mbar_expect_tx(&w_bar, a.wbytes);
-            const unsigned char *src = reinterpret_cast<const unsigned char *>(a.wpack);
-            for (uint32_t off = 0; off < a.wbytes; off += 32768u) {
-                uint32_t n = a.wbytes - off < 32768u ? a.wbytes - off : 32768u;
-                ptx::bulk_g2s(wsm + off, src + off, n, &w_bar);
+        // The packed weights stream through a TC_WB-buffer ring in units of one (channel
+        // chunk, tap row) = l K-steps (bulk async copies, L2-resident across tiles), so
+        // wide layers fit (the whole weight set of e.g. a 96->128 3x3 layer is 884 KB).
+        // Unit v+1 is requested when unit v starts; its buffer was last used by unit
+        // v+2-TC_WB, whose MMAs have retired by then.
+        const int units_per_tile = a.n_rc * a.l;
+        const int my_tiles = (a.total_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int total_units = my_tiles * units_per_tile;
+        const unsigned char *wsrc = reinterpret_cast<const unsigned char *>(a.wpack);
+        // request the next unit (incremental ring position; no divides on the MMA path)
+        int rq = 0, rq_b = 0, rq_w = 0;  // next unit to request, its buffer, its weight unit
+        uint32_t rq_ph = 0;              // completions of wempty[rq_b] to wait for (parity)
+        auto request_next = [&]() {
+            if (rq >= total_units) return;
+            if (STREAM && rq >= TC_WB) ptx::mbar_wait(&wempty[rq_b], rq_ph ^ 1);
+            if (ptx::elect_one()) {
+                ptx::mbar_expect_tx(&wfull[rq_b], a.unit_bytes);
+                const unsigned char *src = wsrc + (size_t)rq_w * a.unit_bytes;
+                unsigned char *dst = wsm + (size_t)rq_b * a.unit_bytes;
+                for (uint32_t off = 0; off < a.unit_bytes; off += 32768u) {
+                    const uint32_t n = a.unit_bytes - off < 32768u ? a.unit_bytes - off : 32768u;
+                    ptx::bulk_g2s(dst + off, src + off, n, &wfull[rq_b]);
+                }
             }
+            __syncwarp();
+            ++rq;
+            if (++rq_w == units_per_tile) rq_w = 0;
+            if (++rq_b == a.nwb) {
+                rq_b = 0;
+                rq_ph ^= 1;
+            }
+        };
+        if (!STREAM) {
+            for (int v = 0; v < units_per_tile && v < total_units; ++v) request_next();
+        } else {
+            request_next();
         }
-        __syncwarp();
-        ptx::mbar_wait(&w_bar, 0);
+        int unit = 0, wb = 0;
+        uint32_t wph = 0;
         const uint32_t wsm_addr = ptx::smem_u32(wsm);
         const uint32_t ks_bytes = (uint32_t)a.Npad * 64;  // hi + lo tiles
         const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
@@ -330,8 +368,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
             ptx::mbar_wait(&tempty_bar[buf], tphase ^ 1);
             ptx::tc_fence_after();
             const uint32_t dbase = tmem + (uint32_t)(buf * MT * a.acc_cols);
-            for (int ks = 0; ks < a.n_ks; ++ks) {
-                const uint32_t bhi = wsm_addr + (uint32_t)ks * ks_bytes;
+            for (int ks = 0, kin = 0; ks < a.n_ks; ++ks) {
+                uint32_t bhi;
+                if (STREAM) {
+                    if (kin == 0) {  // first K-step of a weight unit
+                        request_next();
+                        ptx::mbar_wait(&wfull[wb], wph);
+                    }
+                    bhi = wsm_addr + (uint32_t)wb * a.unit_bytes + (uint32_t)kin * ks_bytes;
+                } else {
+                    // resident: all units were requested up front into consecutive buffers
+                    if (unit < units_per_tile && kin == 0) ptx::mbar_wait(&wfull[unit], 0);
+                    bhi = wsm_addr + (uint32_t)ks * ks_bytes;
+                }
                 const uint64_t dhi = ptx::smem_desc(bhi, 128, 256);
                 const uint64_t dlo = ptx::smem_desc(bhi + (uint32_t)a.Npad * 32, 128, 256);
                 const uint32_t sbase = a_base + (uint32_t)(stage * MT * 16);
@@ -354,8 +403,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
                         }
                     }
                     ptx::mma_commit(&empty_bar[stage]);
+                    if (STREAM && kin == a.l - 1) ptx::mma_commit(&wempty[wb]);
                 }
                 __syncwarp();
+                if (STREAM || unit < units_per_tile) {
+                    if (++kin == a.l) {
+                        kin = 0;
+                        ++unit;
+                        if (++wb == a.nwb) {
+                            wb = 0;
+                            wph ^= 1;
+                        }
+                    }
+                }
                 TC_TRACE(a, mks, 7, lane == 0);
                 ++mks;
                 if (++stage == a.stages) {
@@ -439,9 +499,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_kernel(const TcConvArgs
 // host side
 // --------------------------------------------------------------------------------
 struct TcPlan {
-    int Npad, n_rc, n_ks, MT, acc_cols, stages;
-    bool stacked;
-    size_t wbytes;
+    int Npad, n_rc, n_ks, MT, acc_cols, stages, nwb;
+    bool stacked, resident;
+    size_t wbytes, unit_bytes;
     // halo geometry for the chosen MT
     int hrows, hcols, RB, RS, CB, CS, HB;
     size_t hbytes;
@@ -484,6 +544,7 @@ static TcPlan tc_plan(int R, int Q, int l, int d) {
     p.stacked = p.Npad <= 16;
     p.acc_cols = p.stacked ? 2 * p.Npad : p.Npad;
     p.wbytes = ((size_t)p.n_ks * p.Npad * 64 + 127) / 128 * 128;
+    p.unit_bytes = (size_t)l * p.Npad * 64;  // one (channel chunk, tap row); multiple of 128
     int want = TC_MAX_MT;
     if (const char *e = getenv("DP_TC_MT")) {
         int v = atoi(e);
@@ -498,12 +559,17 @@ static TcPlan tc_plan(int R, int Q, int l, int d) {
         TcPlan t = p;
         t.MT = mt;
         tc_halo(t, l, d);
+        const int units = p.n_rc * l;
+        const bool res = units <= TC_MAX_WB &&
+                         (size_t)units * p.unit_bytes + 2 * t.hbytes <= (size_t)TC_SMEM_BUDGET;
+        const size_t wring = (size_t)(res ? units : TC_WB) * p.unit_bytes;
         if (acc_total < 512 && st >= TC_MIN_STAGES && t.hcols <= 32 * TC_LC &&
-            t.hrows <= TC_MAX_HROWS &&
-            p.wbytes + 2 * t.hbytes <= (size_t)TC_SMEM_BUDGET) {
+            t.hrows <= TC_MAX_HROWS && wring + 2 * t.hbytes <= (size_t)TC_SMEM_BUDGET) {
             p = t;
             p.stages = st;
-            p.HB = p.wbytes + 3 * t.hbytes <= (size_t)TC_SMEM_BUDGET ? 3 : 2;
+            p.resident = res;
+            p.nwb = res ? units : TC_WB;
+            p.HB = wring + 3 * t.hbytes <= (size_t)TC_SMEM_BUDGET ? 3 : 2;
             break;
         }
     }
@@ -568,7 +634,7 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     if (p.MT > rows_needed) {
         p.MT = rows_needed;
         tc_halo(p, l, d);
-        p.HB = p.wbytes + 3 * p.hbytes <= (size_t)TC_SMEM_BUDGET ? 3 : 2;
+        p.HB = (size_t)p.nwb * p.unit_bytes + 3 * p.hbytes <= (size_t)TC_SMEM_BUDGET ? 3 : 2;
     }
     TcConvArgs a;
     a.in = in;
@@ -599,6 +665,9 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     if (tt > 0x7fffffff) return set_error(DP_ERR_UNSUPPORTED, "tensor-core conv: too many tiles");
     a.total_tiles = (int)tt;
     a.wbytes = (uint32_t)p.wbytes;
+    a.unit_bytes = (uint32_t)p.unit_bytes;
+    a.nwb = p.nwb;
+    a.resident = p.resident ? 1 : 0;
     a.hrows = p.hrows;
     a.hcols = p.hcols;
     a.RB = p.RB;
@@ -616,12 +685,19 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
         g_tc_trace = buf;
     }
     int grid = a.total_tiles < g_num_sms ? a.total_tiles : g_num_sms;
-    size_t smem = p.wbytes + (size_t)p.HB * p.hbytes;
+    size_t smem = (size_t)p.nwb * p.unit_bytes + (size_t)p.HB * p.hbytes;
     void (*kern)(const TcConvArgs);
-    if (p.stacked)
-        kern = bwd ? tc_conv_kernel<true, true> : tc_conv_kernel<true, false>;
-    else
-        kern = bwd ? tc_conv_kernel<false, true> : tc_conv_kernel<false, false>;
+    if (p.resident) {
+        if (p.stacked)
+            kern = bwd ? tc_conv_kernel<true, true, false> : tc_conv_kernel<true, false, false>;
+        else
+            kern = bwd ? tc_conv_kernel<false, true, false> : tc_conv_kernel<false, false, false>;
+    } else {
+        if (p.stacked)
+            kern = bwd ? tc_conv_kernel<true, true, true> : tc_conv_kernel<true, false, true>;
+        else
+            kern = bwd ? tc_conv_kernel<false, true, true> : tc_conv_kernel<false, false, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess)

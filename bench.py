@@ -48,6 +48,22 @@ C2_TEXT = ("input channels=3\n"
            "conv out=10 in=32 k=4 stride=1 weights=seed:3\n")
 SIDE = 256
 MASK_FRAC = 0.01
+# BASELINE.json configs[2] / configs[3]
+C3_TEXT = ("input channels=3\n"
+           "conv out=50 in=3 k=6 stride=1 weights=seed:0\n"
+           "pool kind=max k=4 stride=4\nnonlin kind=tanh\n"
+           "conv out=50 in=50 k=3 stride=1 weights=seed:3\n"
+           "pool kind=max k=2 stride=2\nnonlin kind=tanh\n"
+           "conv out=8 in=50 k=7 stride=1 weights=seed:6\n")
+C4_TEXT = ("input channels=3\n"
+           "conv out=48 in=3 k=5 stride=2 weights=seed:1\nnonlin kind=relu\n"
+           "conv out=64 in=48 k=3 stride=1 weights=seed:2\nnonlin kind=relu\n"
+           "pool kind=max k=2 stride=2\n"
+           "conv out=96 in=64 k=3 stride=1 weights=seed:3\nnonlin kind=relu\n"
+           "pool kind=max k=2 stride=2\n"
+           "conv out=128 in=96 k=3 stride=2 weights=seed:4\nnonlin kind=relu\n"
+           "pool kind=max k=2 stride=2\n"
+           "conv out=8 in=128 k=3 stride=1 weights=seed:5\n")
 
 
 def _peaks():
@@ -204,6 +220,49 @@ def run_reference_arm(args, rank):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+def measure_config(text, side, batch, mask_frac, steps=5, warmup=2, seed=7):
+    """Device-timed fwd and fwd+masked-bwd throughput (pixels/s) of one net / image size on
+    this GPU: CUDA-graph replays over synthetic HBM-resident inputs (SGD included)."""
+    import torch
+    import paper_1412_4526_b200 as dp
+    from paper_1412_4526_b200.trainer import DataParallelTrainer
+    spec = dp.parse_spec(text)
+    plan = dp.compile_plan(spec)
+    rng = np.random.default_rng(seed)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    imgs = torch.rand((batch, spec.input_channels, side, side), device="cuda", generator=gen) - 0.5
+    tgts = torch.rand((batch, spec.output_channels, side, side), device="cuda", generator=gen)
+    masks = torch.from_numpy((rng.random((batch, side, side)) < mask_frac).astype(np.uint8)).cuda()
+    tr = DataParallelTrainer(plan, batch, side, side, lr=1e-9, use_graph=True)
+    net = tr.net
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    tr.load_batch(imgs, tgts, masks)
+    ms_train = timed(tr.step)
+    ms_fwd = timed(net.forward)
+    px = batch * side * side
+    tiers = net.kernel_plan()
+    out = {"side": side, "images": batch, "mask_fraction": mask_frac,
+           "train": px / (ms_train / 1e3), "forward": px / (ms_fwd / 1e3),
+           "ms_train": ms_train, "ms_forward": ms_fwd,
+           "conv_tiers": {str(k): v for k, v in tiers.items()}}
+    del tr, net
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -213,6 +272,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the image-size sweep and the c3 / c4 config lines")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -397,6 +458,20 @@ def main():
         "clocks": clocks,
     }
 
+    if rank == 0 and world == 1 and not args.no_sweep:
+        # "per image size" (BASELINE metric) and the other BASELINE configs, same GPU
+        sizes = []
+        for side, b in ((128, 256), (512, 16), (1024, 4)):
+            sizes.append(measure_config(C2_TEXT, side, b, MASK_FRAC))
+        line["sizes"] = {"net": "c2 (conv6/pool2/tanh/conv5/pool2/tanh/conv4, 3 ch)",
+                         "unit": "pixels/s", "points": sizes,
+                         "note": "train = fwd + 1%-masked bwd + SGD; 256 is the headline line"}
+        line["configs"] = {
+            "c3_512": dict(measure_config(C3_TEXT, 512, 4, 1.0),
+                           net="plain CNN1 (50,50,8), pool1 4x4, patch 69, full-image fwd/bwd"),
+            "c4_1024": dict(measure_config(C4_TEXT, 1024, 2, MASK_FRAC),
+                            net="5 conv (strides 2,1,1,2,1) / 3 max-pool, relu, patch 119"),
+        }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         f, b, kind = cpu_dense_step_seconds(threads, 1)

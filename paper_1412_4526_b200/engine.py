@@ -463,8 +463,11 @@ class DenseNet:
             if isinstance(g.op, DilatedConv):
                 f_ok, b_ok = self.tc.get(gi, (False, False))
                 w_ok = getattr(self, "tc_wgrad", {}).get(gi, False)
+                dg = "tcgen05-3xtf32" if b_ok else "exact"
+                if gi == 0:
+                    dg = "not needed"  # layer 0's input delta is not computed (backward.py:208)
                 out[g.first] = {"forward": "tcgen05-3xtf32" if f_ok else "exact",
-                                "data_grad": "tcgen05-3xtf32" if b_ok else "exact",
+                                "data_grad": dg,
                                 "weight_grad": "tcgen05-3xtf32" if w_ok else "cuda-core"}
         return out
 

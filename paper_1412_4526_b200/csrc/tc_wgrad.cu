@@ -114,7 +114,7 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                 const __grid_constant__ CUtensorMap tm_dy, const TcWgradArgs a) {
     extern __shared__ __align__(1024) unsigned char wg_smem_raw[];
     __shared__ uint64_t sfull[WG_MAX_SS], sempty[WG_MAX_SS];
-    __shared__ uint64_t tfull[WG_MAX_TS], tempty[WG_MAX_TS], accfull;
+    __shared__ uint64_t tfull[WG_MAX_TS], accfull;
     __shared__ uint32_t s_tmem;
 
     unsigned char *smem = (unsigned char *)(((uintptr_t)wg_smem_raw + 1023) & ~(uintptr_t)1023);
@@ -141,7 +141,6 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
         }
         for (int s = 0; s < a.TS; ++s) {
             ptx::mbar_init(&tfull[s], 4);
-            ptx::mbar_init(&tempty[s], 1);
         }
         ptx::mbar_init(&accfull, 1);
         ptx::mbar_fence_init();
@@ -203,11 +202,12 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
         const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
         const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
         const uint32_t smem_base = ptx::smem_u32(smem);
+        // ring positions kept incrementally: this thread's loop is the critical path
+        int s = 0, ts = 0;
+        uint32_t tph = 0;
         for (int kl = 0; kl < nkb; ++kl) {
-            const int s = kl % a.SS;
-            const int ts = kl % a.TS;
             const uint32_t bhi = smem_base + (uint32_t)s * a.stage_bytes;
-            ptx::mbar_wait(&tfull[ts], (kl / a.TS) & 1);
+            ptx::mbar_wait(&tfull[ts], tph);
             ptx::tc_fence_after();
             WG_TRACE(a, kl, 8, lane == 0);
             if (ptx::elect_one()) {
@@ -221,11 +221,18 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                         ptx::mma_tf32_ts(dcol, alo, dstack, idesc_n, 1);
                     }
                 }
-                ptx::mma_commit(&tempty[ts]);
+                // ONE commit per K block (a tcgen05.commit costs the issuing thread ~200-300
+                // cycles): sempty[s] also tells the converters that TMEM stage ts is free
+                // again -- they wait for the K block TS earlier (see below)
                 ptx::mma_commit(&sempty[s]);
             }
             __syncwarp();
             WG_TRACE(a, kl, 9, lane == 0);
+            if (++s == a.SS) s = 0;
+            if (++ts == a.TS) {
+                ts = 0;
+                tph ^= 1;
+            }
         }
         if (ptx::elect_one()) ptx::mma_commit(&accfull);
         __syncwarp();
@@ -291,7 +298,12 @@ tc_wgrad_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant
                 WG_TRACE(a, kl, 3, q == 0 && lane == 0);
             }
             const unsigned char *sa = st + a.b_bytes;
-            ptx::mbar_wait(&tempty[ts], ((kl / a.TS) & 1) ^ 1);
+            if (kl >= a.TS) {
+                // TMEM stage ts was last used by K block kl - TS; its MMAs are done when
+                // that block's SMEM stage is released (SS >= TS, so the parity is exact)
+                const int kp = kl - a.TS;
+                ptx::mbar_wait(&sempty[kp % a.SS], (kp / a.SS) & 1);
+            }
             ptx::tc_fence_after();
             const uint32_t tbase = a_base + lane_off + (uint32_t)(ts * a.G * WG_KSTEPS * 16);
 #pragma unroll
@@ -486,6 +498,10 @@ static bool wg_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WgPl
     // TMEM: G tiles of accumulators + TS stages of one K block's A (4 slices x G x 16 cols)
     int G = 512 / (acc_cols + 2 * WG_KSTEPS * 16);
     if (G > WG_MAX_G) G = WG_MAX_G;
+    if (const char *e = getenv("DP_WG_G")) {  // tile-group size override (experiments)
+        const int v = atoi(e);
+        if (v >= 1 && v < G) G = v;
+    }
     if (G < 1) return false;
     p.n_groups = (p.n_tiles + G - 1) / G;
     p.G = (p.n_tiles + p.n_groups - 1) / p.n_groups;
@@ -524,6 +540,7 @@ static bool wg_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WgPl
     if (SS > WG_MAX_SS) SS = WG_MAX_SS;
     if (SS < 2) return false;
     p.SS = SS;
+    if (p.TS > p.SS) p.TS = p.SS;  // TMEM-stage reuse is read off the SMEM-stage barriers
     p.nvb = (p.wo + 31) / 32;
     p.kb_total = (long long)n * p.ho * p.nvb;
     int sms = wg_num_sms();

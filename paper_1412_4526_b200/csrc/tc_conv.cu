@@ -119,6 +119,20 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
     }
 }
 
+int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, cudaStream_t st) {
+    const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 7) / 8, n_ks = n_rc * l * l;
+    const int total = n_ks * 2 * Npad * 8;
+    tc_pack_weights<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Q, R, l, Npad, n_rc, n_ks, bwd);
+    return check_launch("tc_pack_weights");
+}
+
+// flattened shared-memory-operand variant (tc_conv_flat.cu), preferred when it applies
+bool tf_conv_supported(int R, int Q, int l, int d);
+int tf_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
+                    int, int, int, void *, size_t, cudaStream_t);
+int tf_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
+                          int, const float *, int, void *, size_t, cudaStream_t);
+
 // Epilogue tanh: single-precision tanhf (<= 2 ulp) kept out of line so the unrolled
 // epilogue stays small (instruction cache); relu / identity are inlined.
 __device__ __noinline__ float tc_tanh(float v) { return tanhf(v); }
@@ -586,6 +600,7 @@ size_t tc_conv_workspace(int R, int Q, int l) {
 }
 
 bool tc_conv_supported(int R, int Q, int l, int d) {
+    if (tf_conv_supported(R, Q, l, d)) return true;
     TcPlan p = tc_plan(R, Q, l, d);
     return p.Npad <= 128 && p.MT >= 1;
 }
@@ -709,6 +724,8 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
 int tc_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,
                     int h, int wd, int cout, int k, int d, int act, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
+    if (tf_conv_supported(cin, cout, k, d))
+        return tf_conv_forward(x, w, b, y, n, cin, h, wd, cout, k, d, act, ws, ws_bytes, st);
     int e = (k - 1) * d + 1;
     return launch_tc(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k, d, 0, act,
                      0, false, ws, ws_bytes, st);
@@ -717,6 +734,9 @@ int tc_conv_forward(const float *x, const float *w, const float *b, float *y, in
 int tc_conv_backward_data(const float *dy, const float *w, float *dx, int n, int cout, int ho,
                           int wo, int cin, int k, int d, const float *gate, int gate_kind,
                           void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (tf_conv_supported(cout, cin, k, d))
+        return tf_conv_backward_data(dy, w, dx, n, cout, ho, wo, cin, k, d, gate, gate_kind, ws,
+                                     ws_bytes, st);
     int e = (k - 1) * d + 1;
     return launch_tc(dy, w, nullptr, dx, gate, n, cout, ho, wo, cin, ho + e - 1, wo + e - 1, k, d,
                      e - 1, 0, gate_kind, true, ws, ws_bytes, st);

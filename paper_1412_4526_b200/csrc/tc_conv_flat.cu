@@ -1,0 +1,429 @@
+// d-regularly sparse convolution on the tcgen05 tensor cores as a FLATTENED implicit GEMM
+// with both operands read by the tensor core from shared memory (fast tier, 3xTF32).
+//
+// Same maths and argument meaning as tc_conv.cu / conv_direct.cu:
+//   forward        y[o,u,v]  = b[o] + sum_{c,i,j} w[o,c,i,j] * x[c, u+i*d, v+j*d]
+//   data gradient  dx[c,y,x] = sum_{o,i,j} w[o,c,l-1-i,l-1-j] * dy_pad[o, y+i*d, x+j*d]
+// (reference _kernels.pyx:23-53 and :56-91).
+//
+// Flattening: on the (virtual, zero-padded) input grid of width Wv an output pixel (u, v)
+// is the flat index p = u*Wv + v, and tap (i, j) reads input flat index p + i*d*Wv + j*d.
+// 128 consecutive output flat indices are therefore 128 consecutive input records for
+// every tap, so one M=128 tile of the GEMM (M = pixels, N = output channels, K = 8
+// channels of one tap) is a plain shared-memory window -- no per-tap re-layout.  The
+// flat range covers the (l-1)*d wrap columns at the end of each row too; those outputs
+// are computed and discarded (waste (l-1)d / Wv, ~3% at 256-pixel rows).
+//
+// Shared-memory operand layouts (K-major, SWIZZLE_NONE core matrices):
+//   A (pixels): one halo unit = 4 planes [hi c0-3 | hi c4-7 | lo c0-3 | lo c4-7] of NR
+//       16-byte records (4 channels of one input pixel).  Element (m, k) of the A tile
+//       starting at record s is at s*16 + (m>>3)*128 + (m&7)*16 + (k>>2)*PLANE + (k&3)*4:
+//       descriptor SBO = 128, LBO = PLANE.  hi = raw fp32 bits (kind::tf32 truncates),
+//       lo = x - trunc(x), both produced once per element by the loaders.
+//   B (weights): tc_pack_weights' per-K-step [W_hi (Npad rows) | W_lo (Npad rows)].
+// 3xTF32 per K-step and M tile:  A_hi x [W_hi|W_lo] (N = 2 Npad) + A_lo x W_hi (N = Npad)
+// (Npad <= 128), else three N = Npad MMAs.  D columns [0, Npad) + [Npad, 2 Npad) summed
+// in the epilogue.
+//
+// Per CTA (persistent, one per SM, 17 warps):
+//   warps 8-15 loaders: per (tile, channel chunk rc, tap row i) unit fill one halo unit
+//              buffer: records f0 + i*d*Wv + [0, NR) of the 8 channels (coalesced LDG,
+//              lanes = consecutive pixels, zero outside the image / the padding), split
+//              hi/lo, four 16-byte STS per pixel; loader warp 0 also requests the unit's
+//              l K-steps of packed weights with one bulk async copy into the same buffer.
+//   warp 16    MMA issuer: per unit l taps x MT M tiles x 2 MMAs, one tcgen05.commit
+//              frees the unit buffer; one commit per tile hands the accumulators over.
+//   warps 0-7  epilogue (2 per TMEM lane quarter, M tiles by parity): tcgen05.ld, bias +
+//              nonlinearity (forward) or the upstream nonlinearity's derivative (data
+//              gradient), coalesced NCHW stores (lane = pixel).
+#include <stdlib.h>
+
+#include "dp_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace dp {
+
+int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, cudaStream_t st);
+
+constexpr int TF_EPI_WARPS = 8;
+constexpr int TF_LOAD_WARP0 = 8;
+constexpr int TF_LOAD_WARPS = 8;
+constexpr int TF_MMA_WARP = 16;
+constexpr int TF_THREADS = (TF_MMA_WARP + 1) * 32;
+constexpr int TF_MAX_MT = 4;
+constexpr int TF_MAX_HB = 6;
+constexpr int TF_LU = 3;  // loader: records per thread in flight (NR <= TF_LU * 256 per pass)
+constexpr int TF_SMEM_BUDGET = 220 * 1024;
+
+struct TfArgs {
+    const float *in;     // (n, R, Hin, Win)
+    const float *wpack;  // tc_pack_weights layout
+    const float *bias;   // (Q) forward, nullptr for the data gradient
+    float *out;          // (n, Q, Ho, Wo)
+    const float *gate;   // (n, Q, Ho, Wo) nonlinearity output, or nullptr
+    int R, Hin, Win;     // real input
+    int Wv, pad;         // virtual (zero-padded) grid width; offset of the real input in it
+    int Q, Ho, Wo, l, d, act, gate_kind;
+    int n_rc, Npad, MT, acc_cols, NR, HB;
+    uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
+    int tiles_per_img, total_tiles, flat_len;
+};
+
+__device__ __noinline__ float tf_tanh(float v) { return tanhf(v); }
+__device__ __forceinline__ float tf_act(float v, int kind) {
+    if (kind == DP_TANH || kind == DP_TANH_FAST) return tf_tanh(v);
+    if (kind == DP_RELU) return dp_relu(v);
+    return v;
+}
+
+template <bool STACKED, bool BWD>
+__global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ uint64_t ufull[TF_MAX_HB], uempty[TF_MAX_HB], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int MT = a.MT;
+    const int units = a.n_rc * a.l;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < a.HB; ++b) {
+            ptx::mbar_init(&ufull[b], TF_LOAD_WARPS + 1);  // + the weight copy's expect_tx
+            ptx::mbar_init(&uempty[b], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tfull[b], 1);
+            ptx::mbar_init(&tempty[b], TF_EPI_WARPS);
+        }
+        ptx::mbar_fence_init();
+    }
+    if (warp == TF_MMA_WARP) ptx::tmem_alloc<512>(&s_tmem);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
+        // ================================ loaders ================================
+        const int lw = warp - TF_LOAD_WARP0;
+        const long long plane_in = (long long)a.Hin * a.Win;
+        const unsigned char *wsrc = reinterpret_cast<const unsigned char *>(a.wpack);
+        int b = 0;
+        uint32_t uph = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            const int img = tile / a.tiles_per_img;
+            const int f0 = (tile - img * a.tiles_per_img) * MT * 128;
+            for (int rc = 0, wu = 0; rc < a.n_rc; ++rc) {
+                const float *src = a.in + ((long long)img * a.R + rc * 8) * plane_in;
+                const int cvalid = min(8, a.R - rc * 8);
+                for (int i = 0; i < a.l; ++i, ++wu) {
+                    ptx::mbar_wait_sleep(&uempty[b], uph ^ 1);
+                    unsigned char *ub = smem_raw + (size_t)b * a.ubytes;
+                    if (lw == 0) {
+                        if (ptx::elect_one()) {
+                            ptx::mbar_expect_tx(&ufull[b], a.wunit_bytes);
+                            const unsigned char *ws = wsrc + (size_t)wu * a.wunit_bytes;
+                            for (uint32_t off = 0; off < a.wunit_bytes; off += 32768u) {
+                                const uint32_t nb =
+                                    a.wunit_bytes - off < 32768u ? a.wunit_bytes - off : 32768u;
+                                ptx::bulk_g2s(ub + a.halo_bytes + off, ws + off, nb, &ufull[b]);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    const int gbase = f0 + i * a.d * a.Wv;
+                    for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += TF_LU * TF_LOAD_WARPS * 32) {
+                        float v[TF_LU][8];
+#pragma unroll
+                        for (int u = 0; u < TF_LU; ++u) {
+                            const int r = r0 + u * TF_LOAD_WARPS * 32;
+                            const int gf = gbase + r;
+                            const int yv = gf / a.Wv;
+                            const int y = yv - a.pad, x = gf - yv * a.Wv - a.pad;
+                            const bool ok = r < a.NR && y >= 0 && y < a.Hin && x >= 0 && x < a.Win;
+                            const float *p = src + (ok ? (long long)y * a.Win + x : 0);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k)
+                                v[u][k] = (ok && k < cvalid) ? __ldg(p + k * plane_in) : 0.f;
+                        }
+#pragma unroll
+                        for (int u = 0; u < TF_LU; ++u) {
+                            const int r = r0 + u * TF_LOAD_WARPS * 32;
+                            if (r >= a.NR) break;
+                            float4 *p0 = reinterpret_cast<float4 *>(ub) + r;
+                            const uint32_t ps = a.plane_bytes / 16;  // plane stride in float4
+                            p0[0] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                            p0[ps] = make_float4(v[u][4], v[u][5], v[u][6], v[u][7]);
+                            p0[2 * ps] = make_float4(ptx::tf32_lo(v[u][0]), ptx::tf32_lo(v[u][1]),
+                                                     ptx::tf32_lo(v[u][2]), ptx::tf32_lo(v[u][3]));
+                            p0[3 * ps] = make_float4(ptx::tf32_lo(v[u][4]), ptx::tf32_lo(v[u][5]),
+                                                     ptx::tf32_lo(v[u][6]), ptx::tf32_lo(v[u][7]));
+                        }
+                    }
+                    // generic-proxy stores -> visible to the tensor core (async proxy)
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&ufull[b]);
+                    if (++b == a.HB) {
+                        b = 0;
+                        uph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == TF_MMA_WARP) {
+        // ================================ MMA issuer ================================
+        const uint32_t hs = ptx::smem_u32(smem_raw);
+        const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
+        const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
+        const uint32_t ks_units = (uint32_t)(a.Npad * 64) >> 4;  // descriptor units = 16 B
+        const uint32_t wlo_units = (uint32_t)(a.Npad * 32) >> 4;
+        const uint32_t lo_units = (2 * a.plane_bytes) >> 4;
+        int b = 0, buf = 0;
+        uint32_t uph = 0, tph = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tempty[buf], tph ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t dbase = tmem + (uint32_t)(buf * MT * a.acc_cols);
+            for (int u = 0; u < units; ++u) {
+                ptx::mbar_wait(&ufull[b], uph);
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                    const uint32_t ubase = hs + (uint32_t)b * a.ubytes;
+                    const uint64_t a0 = ptx::smem_desc(ubase, a.plane_bytes, 128);
+                    const uint64_t b0 = ptx::smem_desc(ubase + a.halo_bytes, 128, 256);
+                    for (int j = 0; j < a.l; ++j) {
+                        const uint64_t bj = b0 + (uint64_t)(j * ks_units);
+                        const uint32_t acc = (u | j) != 0;
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * a.d);
+                            const uint32_t dd = dbase + (uint32_t)(mt * a.acc_cols);
+                            if (STACKED) {
+                                ptx::mma_tf32_ss(dd, ad, bj, idesc_2n, acc);
+                                ptx::mma_tf32_ss(dd, ad + lo_units, bj, idesc_n, 1);
+                            } else {
+                                ptx::mma_tf32_ss(dd, ad, bj, idesc_n, acc);
+                                ptx::mma_tf32_ss(dd, ad, bj + wlo_units, idesc_n, 1);
+                                ptx::mma_tf32_ss(dd, ad + lo_units, bj, idesc_n, 1);
+                            }
+                        }
+                    }
+                    ptx::mma_commit(&uempty[b]);
+                }
+                __syncwarp();
+                if (++b == a.HB) {
+                    b = 0;
+                    uph ^= 1;
+                }
+            }
+            if (ptx::elect_one()) ptx::mma_commit(&tfull[buf]);
+            __syncwarp();
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1;
+            }
+        }
+    } else {
+        // ================================ epilogue ================================
+        const int q = warp & 3, half = warp >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const long long ostride = (long long)a.Ho * a.Wo;
+        int buf = 0;
+        uint32_t tph = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            const int img = tile / a.tiles_per_img;
+            const int f0 = (tile - img * a.tiles_per_img) * MT * 128;
+            ptx::mbar_wait_sleep(&tfull[buf], tph);
+            ptx::tc_fence_after();
+            const long long img_off = (long long)img * a.Q * ostride;
+            for (int mt = half; mt < MT; mt += 2) {
+                const int p = f0 + mt * 128 + q * 32 + lane;
+                const int u = p / a.Wv, v = p - u * a.Wv;
+                const bool inside = p < a.flat_len && v < a.Wo;
+                const long long pix = img_off + (long long)u * a.Wo + v;
+                const uint32_t dcol =
+                    tmem + lane_off + (uint32_t)((buf * MT + mt) * a.acc_cols);
+                for (int o0 = 0; o0 < a.Npad; o0 += 16) {
+                    uint32_t r[16], r2[16];
+                    ptx::tmem_ld16(dcol + o0, r);
+                    if (STACKED) ptx::tmem_ld16(dcol + a.Npad + o0, r2);
+                    const long long off0 = pix + (long long)o0 * ostride;
+                    const int nq = min(16, a.Q - o0);
+                    float aux[16];
+                    if (BWD) {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t)
+                            aux[t] = (a.gate && inside && t < nq)
+                                         ? __ldg(a.gate + off0 + t * ostride) : 0.f;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t) aux[t] = t < nq ? __ldg(a.bias + o0 + t) : 0.f;
+                    }
+                    ptx::tmem_wait_ld();
+                    if (!inside) continue;
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) {
+                        if (t >= nq) break;
+                        float val = __uint_as_float(r[t]);
+                        if (STACKED) val += __uint_as_float(r2[t]);
+                        if (!BWD)
+                            val = tf_act(val + aux[t], a.act);
+                        else if (a.gate)
+                            val = gate_from_output(val, aux[t], a.gate_kind);
+                        a.out[off0 + t * ostride] = val;
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1;
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == TF_MMA_WARP) ptx::tmem_dealloc<512>(tmem);
+}
+
+// --------------------------------------------------------------------------------
+// host side
+// --------------------------------------------------------------------------------
+struct TfPlan {
+    int Npad, n_rc, MT, acc_cols, NR, HB;
+    bool stacked, ok;
+    uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
+};
+
+// M tiles per CTA tile: accumulators double-buffered in the 512 TMEM columns; unit
+// buffers (halo + one tap row of weights) as many as fit, at least two.
+static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt) {
+    TfPlan p;
+    p.Npad = (Q + 15) / 16 * 16;
+    p.n_rc = (R + 7) / 8;
+    p.stacked = 2 * p.Npad <= 256;
+    p.acc_cols = p.stacked ? 2 * p.Npad : p.Npad;
+    p.ok = p.Npad <= 256;
+    int mt = p.acc_cols <= 256 ? 256 / p.acc_cols : 1;
+    if (mt > TF_MAX_MT) mt = TF_MAX_MT;
+    if (const char *e = getenv("DP_TF_MT")) {
+        int v = atoi(e);
+        if (v >= 1 && v < mt) mt = v;
+    }
+    if (max_mt >= 1 && mt > max_mt) mt = max_mt;
+    p.MT = mt;
+    p.NR = (mt * 128 + (l - 1) * d + 7) / 8 * 8;
+    p.plane_bytes = (uint32_t)p.NR * 16;
+    p.halo_bytes = 4 * p.plane_bytes;
+    p.wunit_bytes = (uint32_t)(l * p.Npad * 64);
+    p.ubytes = (p.halo_bytes + p.wunit_bytes + 127) / 128 * 128;
+    long long hb = (long long)TF_SMEM_BUDGET / p.ubytes;
+    if (hb > TF_MAX_HB) hb = TF_MAX_HB;
+    p.HB = (int)hb;
+    p.ok = p.ok && p.HB >= 2 && (p.plane_bytes >> 4) < (1u << 14);
+    return p;
+}
+
+bool tf_conv_supported(int R, int Q, int l, int d) {
+    if (getenv("DP_TC_HALO")) return false;  // force the halo-buffer kernel (tc_conv.cu)
+    return tf_plan(R, Q, l, d, 0).ok;
+}
+
+static int g_tf_sms = 0;
+
+static int tf_launch(const float *in, const float *w, const float *bias, float *out,
+                     const float *gate, int n, int R, int Hin, int Win, int Q, int Ho, int Wo,
+                     int l, int d, int pad, int act, int gate_kind, bool bwd, void *ws,
+                     size_t ws_bytes, cudaStream_t st) {
+    const int Wv = Win + 2 * pad;
+    const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
+    // short images: fewer M tiles per CTA tile
+    const int max_mt = (int)((flat_len + 127) / 128);
+    TfPlan p = tf_plan(R, Q, l, d, max_mt);
+    if (!p.ok)
+        return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
+                         R, Q, l, d);
+    const size_t wbytes = (size_t)p.n_rc * l * p.wunit_bytes;
+    if (ws == nullptr || ws_bytes < wbytes)
+        return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
+                         wbytes);
+    if (((uintptr_t)ws & 15) != 0)
+        return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
+    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, st);
+    if (rc) return rc;
+    if (g_tf_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_tf_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_tf_sms <= 0) g_tf_sms = 148;
+    }
+    if ((long long)(Hin + 2 * pad) * Wv + p.NR > 0x7fffffffLL)
+        return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: image too large");
+    TfArgs a;
+    a.in = in;
+    a.wpack = (const float *)ws;
+    a.bias = bias;
+    a.out = out;
+    a.gate = gate;
+    a.R = R;
+    a.Hin = Hin;
+    a.Win = Win;
+    a.Wv = Wv;
+    a.pad = pad;
+    a.Q = Q;
+    a.Ho = Ho;
+    a.Wo = Wo;
+    a.l = l;
+    a.d = d;
+    a.act = act;
+    a.gate_kind = gate_kind;
+    a.n_rc = p.n_rc;
+    a.Npad = p.Npad;
+    a.MT = p.MT;
+    a.acc_cols = p.acc_cols;
+    a.NR = p.NR;
+    a.HB = p.HB;
+    a.plane_bytes = p.plane_bytes;
+    a.halo_bytes = p.halo_bytes;
+    a.wunit_bytes = p.wunit_bytes;
+    a.ubytes = p.ubytes;
+    a.flat_len = (int)flat_len;
+    a.tiles_per_img = (int)((flat_len + p.MT * 128 - 1) / (p.MT * 128));
+    const long long tt = (long long)n * a.tiles_per_img;
+    if (tt > 0x7fffffff) return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: too many tiles");
+    a.total_tiles = (int)tt;
+    if (a.total_tiles == 0) return DP_OK;
+    const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
+    const size_t smem = (size_t)p.HB * p.ubytes;
+    void (*kern)(const TfArgs);
+    if (p.stacked)
+        kern = bwd ? tc_conv_flat_kernel<true, true> : tc_conv_flat_kernel<true, false>;
+    else
+        kern = bwd ? tc_conv_flat_kernel<false, true> : tc_conv_flat_kernel<false, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+        return set_error(DP_ERR_CUDA, "tc_conv_flat: cudaFuncSetAttribute: %s",
+                         cudaGetErrorString(e));
+    kern<<<grid, TF_THREADS, smem, st>>>(a);
+    return check_launch("tc_conv_flat_kernel");
+}
+
+int tf_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,
+                    int h, int wd, int cout, int k, int d, int act, void *ws, size_t ws_bytes,
+                    cudaStream_t st) {
+    int e = (k - 1) * d + 1;
+    return tf_launch(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k, d, 0, act,
+                     0, false, ws, ws_bytes, st);
+}
+
+int tf_conv_backward_data(const float *dy, const float *w, float *dx, int n, int cout, int ho,
+                          int wo, int cin, int k, int d, const float *gate, int gate_kind,
+                          void *ws, size_t ws_bytes, cudaStream_t st) {
+    int e = (k - 1) * d + 1;
+    return tf_launch(dy, w, nullptr, dx, gate, n, cout, ho, wo, cin, ho + e - 1, wo + e - 1, k, d,
+                     e - 1, 0, gate_kind, true, ws, ws_bytes, st);
+}
+
+}  // namespace dp

@@ -617,6 +617,15 @@ int tc_trace_copy(void *host, size_t bytes) {
                : DP_ERR_CUDA;
 }
 
+// zeroed 1024 x 8 stamp buffer shared by both conv kernels' DP_TC_TRACE modes
+unsigned long long *tc_trace_buffer(cudaStream_t st) {
+    static unsigned long long *buf = nullptr;
+    if (!buf && cudaMalloc(&buf, 1024 * 8 * 8) != cudaSuccess) buf = nullptr;
+    if (buf) cudaMemsetAsync(buf, 0, 1024 * 8 * 8, st);
+    g_tc_trace = buf;
+    return buf;
+}
+
 static int launch_tc(const float *in, const float *w, const float *bias, float *out,
                      const float *gate, int n, int R, int Hin, int Win, int Q, int Ho, int Wo,
                      int l, int d, int pad, int act, int gate_kind, bool bwd, void *ws,
@@ -692,13 +701,7 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     a.hbytes = (uint32_t)p.hbytes;
     a.HB = p.HB;
     a.trace = nullptr;
-    if (getenv("DP_TC_TRACE")) {
-        static unsigned long long *buf = nullptr;
-        if (!buf && cudaMalloc(&buf, 1024 * 8 * 8) != cudaSuccess) buf = nullptr;
-        if (buf) cudaMemsetAsync(buf, 0, 1024 * 8 * 8, st);
-        a.trace = buf;
-        g_tc_trace = buf;
-    }
+    if (getenv("DP_TC_TRACE")) a.trace = tc_trace_buffer(st);
     int grid = a.total_tiles < g_num_sms ? a.total_tiles : g_num_sms;
     size_t smem = (size_t)p.nwb * p.unit_bytes + (size_t)p.HB * p.hbytes;
     void (*kern)(const TcConvArgs);

@@ -25,15 +25,18 @@
 // (Npad <= 128), else three N = Npad MMAs.  D columns [0, Npad) + [Npad, 2 Npad) summed
 // in the epilogue.
 //
-// Per CTA (persistent, one per SM, 17 warps):
-//   warps 8-15 loaders: per (tile, channel chunk rc, tap row i) unit fill one halo unit
+// Per CTA (persistent, one per SM, 13 warps):
+//   warps 4-11 loaders, 2 groups of 4 taking alternate units (a single group was
+//              latency-bound at ~2700 cycles per unit, above the MMA time):
+//              per (tile, channel chunk rc, tap row i) unit fill one halo unit
 //              buffer: records f0 + i*d*Wv + [0, NR) of the 8 channels (coalesced LDG,
 //              lanes = consecutive pixels, zero outside the image / the padding), split
 //              hi/lo, four 16-byte STS per pixel; loader warp 0 also requests the unit's
-//              l K-steps of packed weights with one bulk async copy into the same buffer.
-//   warp 16    MMA issuer: per unit l taps x MT M tiles x 2 MMAs, one tcgen05.commit
+//              l K-steps of packed weights with one bulk async copy into the same buffer
+//              (first warp of the group).
+//   warp 12    MMA issuer: per unit l taps x MT M tiles x 2 MMAs, one tcgen05.commit
 //              frees the unit buffer; one commit per tile hands the accumulators over.
-//   warps 0-7  epilogue (2 per TMEM lane quarter, M tiles by parity): tcgen05.ld, bias +
+//   warps 0-3  epilogue (one per TMEM lane quarter): tcgen05.ld, bias +
 //              nonlinearity (forward) or the upstream nonlinearity's derivative (data
 //              gradient), coalesced NCHW stores (lane = pixel).
 #include <stdlib.h>
@@ -44,15 +47,20 @@
 namespace dp {
 
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, cudaStream_t st);
+unsigned long long *tc_trace_buffer(cudaStream_t st);
 
-constexpr int TF_EPI_WARPS = 8;
-constexpr int TF_LOAD_WARP0 = 8;
+// 13 warps: registers are granted per 4 warps, so 13 warps (as 16) leave 128 registers
+// per thread for the loaders' 40 values in flight; 17 warps (as 20) would cap them at 96.
+constexpr int TF_EPI_WARPS = 4;
+constexpr int TF_LOAD_WARP0 = 4;
 constexpr int TF_LOAD_WARPS = 8;
-constexpr int TF_MMA_WARP = 16;
+constexpr int TF_MMA_WARP = 12;
 constexpr int TF_THREADS = (TF_MMA_WARP + 1) * 32;
 constexpr int TF_MAX_MT = 4;
 constexpr int TF_MAX_HB = 6;
-constexpr int TF_LU = 3;  // loader: records per thread in flight (NR <= TF_LU * 256 per pass)
+constexpr int TF_LGROUPS = 2;  // loader groups, alternate units (two units' loads in flight)
+constexpr int TF_LGW = TF_LOAD_WARPS / TF_LGROUPS;  // warps per loader group
+constexpr int TF_LU = 5;  // loader: records per thread in flight (NR <= TF_LU * 128 per pass)
 constexpr int TF_SMEM_BUDGET = 220 * 1024;
 
 struct TfArgs {
@@ -67,11 +75,21 @@ struct TfArgs {
     int n_rc, Npad, MT, acc_cols, NR, HB;
     uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
     int tiles_per_img, total_tiles, flat_len;
+    unsigned long long *trace;  // DP_TC_TRACE: per-unit clock64 stamps of CTA 0 (8 slots)
 };
 
-__device__ __noinline__ float tf_tanh(float v) { return tanhf(v); }
+// slots: 0/1 loader warp 0 unit start/end, 2/3/4 MMA wait/got/issued, 5/6 epilogue
+// tile wait/got (at the tile's first unit), 7 epilogue tile done
+#define TF_TRACE(A, U, SLOT, COND)                                                   \
+    do {                                                                             \
+        if ((A).trace && (COND) && blockIdx.x == 0 && (U) < 1024)                    \
+            (A).trace[(U) * 8 + (SLOT)] = clock64();                                 \
+    } while (0)
+
+// inlined so the 16 evaluations of an epilogue chunk interleave (an out-of-line call per
+// value serialised them: measured ~30k cycles per tile with 4 epilogue warps)
 __device__ __forceinline__ float tf_act(float v, int kind) {
-    if (kind == DP_TANH || kind == DP_TANH_FAST) return tf_tanh(v);
+    if (kind == DP_TANH || kind == DP_TANH_FAST) return tanhf(v);
     if (kind == DP_RELU) return dp_relu(v);
     return v;
 }
@@ -81,13 +99,16 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t ufull[TF_MAX_HB], uempty[TF_MAX_HB], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
+    __shared__ float s_bias[256];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int MT = a.MT;
     const int units = a.n_rc * a.l;
+    for (int o = threadIdx.x; o < a.Npad; o += blockDim.x)
+        s_bias[o] = (!BWD && o < a.Q) ? a.bias[o] : 0.f;
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.HB; ++b) {
-            ptx::mbar_init(&ufull[b], TF_LOAD_WARPS + 1);  // + the weight copy's expect_tx
+            ptx::mbar_init(&ufull[b], TF_LGW + 1);  // + the weight copy's expect_tx
             ptx::mbar_init(&uempty[b], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -104,10 +125,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
 
     if (warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
         // ================================ loaders ================================
-        const int lw = warp - TF_LOAD_WARP0;
+        const int lw = (warp - TF_LOAD_WARP0) % TF_LGW, grp = (warp - TF_LOAD_WARP0) / TF_LGW;
         const long long plane_in = (long long)a.Hin * a.Win;
         const unsigned char *wsrc = reinterpret_cast<const unsigned char *>(a.wpack);
-        int b = 0;
+        int b = 0, gu = 0;
         uint32_t uph = 0;
         for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
             const int img = tile / a.tiles_per_img;
@@ -115,8 +136,16 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
             for (int rc = 0, wu = 0; rc < a.n_rc; ++rc) {
                 const float *src = a.in + ((long long)img * a.R + rc * 8) * plane_in;
                 const int cvalid = min(8, a.R - rc * 8);
-                for (int i = 0; i < a.l; ++i, ++wu) {
+                for (int i = 0; i < a.l; ++i, ++wu, ++gu) {
+                    if ((gu % TF_LGROUPS) != grp) {  // the other group's unit
+                        if (++b == a.HB) {
+                            b = 0;
+                            uph ^= 1;
+                        }
+                        continue;
+                    }
                     ptx::mbar_wait_sleep(&uempty[b], uph ^ 1);
+                    TF_TRACE(a, gu, 0, lw == 0 && lane == 0);
                     unsigned char *ub = smem_raw + (size_t)b * a.ubytes;
                     if (lw == 0) {
                         if (ptx::elect_one()) {
@@ -131,11 +160,11 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         __syncwarp();
                     }
                     const int gbase = f0 + i * a.d * a.Wv;
-                    for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += TF_LU * TF_LOAD_WARPS * 32) {
+                    for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += TF_LU * TF_LGW * 32) {
                         float v[TF_LU][8];
 #pragma unroll
                         for (int u = 0; u < TF_LU; ++u) {
-                            const int r = r0 + u * TF_LOAD_WARPS * 32;
+                            const int r = r0 + u * TF_LGW * 32;
                             const int gf = gbase + r;
                             const int yv = gf / a.Wv;
                             const int y = yv - a.pad, x = gf - yv * a.Wv - a.pad;
@@ -147,7 +176,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         }
 #pragma unroll
                         for (int u = 0; u < TF_LU; ++u) {
-                            const int r = r0 + u * TF_LOAD_WARPS * 32;
+                            const int r = r0 + u * TF_LGW * 32;
                             if (r >= a.NR) break;
                             float4 *p0 = reinterpret_cast<float4 *>(ub) + r;
                             const uint32_t ps = a.plane_bytes / 16;  // plane stride in float4
@@ -163,6 +192,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&ufull[b]);
+                    TF_TRACE(a, gu, 1, lw == 0 && lane == 0);
                     if (++b == a.HB) {
                         b = 0;
                         uph ^= 1;
@@ -178,15 +208,17 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
         const uint32_t ks_units = (uint32_t)(a.Npad * 64) >> 4;  // descriptor units = 16 B
         const uint32_t wlo_units = (uint32_t)(a.Npad * 32) >> 4;
         const uint32_t lo_units = (2 * a.plane_bytes) >> 4;
-        int b = 0, buf = 0;
+        int b = 0, buf = 0, gu = 0;
         uint32_t uph = 0, tph = 0;
         for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tempty[buf], tph ^ 1);
             ptx::tc_fence_after();
             const uint32_t dbase = tmem + (uint32_t)(buf * MT * a.acc_cols);
-            for (int u = 0; u < units; ++u) {
+            for (int u = 0; u < units; ++u, ++gu) {
+                TF_TRACE(a, gu, 2, lane == 0);
                 ptx::mbar_wait(&ufull[b], uph);
                 ptx::tc_fence_after();
+                TF_TRACE(a, gu, 3, lane == 0);
                 if (ptx::elect_one()) {
                     const uint32_t ubase = hs + (uint32_t)b * a.ubytes;
                     const uint64_t a0 = ptx::smem_desc(ubase, a.plane_bytes, 128);
@@ -210,6 +242,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     ptx::mma_commit(&uempty[b]);
                 }
                 __syncwarp();
+                TF_TRACE(a, gu, 4, lane == 0);
                 if (++b == a.HB) {
                     b = 0;
                     uph ^= 1;
@@ -224,18 +257,20 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
         }
     } else {
         // ================================ epilogue ================================
-        const int q = warp & 3, half = warp >> 2;
+        const int q = warp & 3;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const long long ostride = (long long)a.Ho * a.Wo;
-        int buf = 0;
+        int buf = 0, gu = 0;
         uint32_t tph = 0;
-        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x, gu += units) {
             const int img = tile / a.tiles_per_img;
             const int f0 = (tile - img * a.tiles_per_img) * MT * 128;
+            TF_TRACE(a, gu, 5, warp == 0 && lane == 0);
             ptx::mbar_wait_sleep(&tfull[buf], tph);
             ptx::tc_fence_after();
+            TF_TRACE(a, gu, 6, warp == 0 && lane == 0);
             const long long img_off = (long long)img * a.Q * ostride;
-            for (int mt = half; mt < MT; mt += 2) {
+            for (int mt = 0; mt < MT; ++mt) {
                 const int p = f0 + mt * 128 + q * 32 + lane;
                 const int u = p / a.Wv, v = p - u * a.Wv;
                 const bool inside = p < a.flat_len && v < a.Wo;
@@ -256,7 +291,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                          ? __ldg(a.gate + off0 + t * ostride) : 0.f;
                     } else {
 #pragma unroll
-                        for (int t = 0; t < 16; ++t) aux[t] = t < nq ? __ldg(a.bias + o0 + t) : 0.f;
+                        for (int t = 0; t < 16; ++t) aux[t] = s_bias[o0 + t];
                     }
                     ptx::tmem_wait_ld();
                     if (!inside) continue;
@@ -275,6 +310,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
             }
             ptx::tc_fence_before();
             __syncwarp();
+            TF_TRACE(a, gu, 7, warp == 0 && lane == 0);
             if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
             if (++buf == 2) {
                 buf = 0;
@@ -394,6 +430,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     if (tt > 0x7fffffff) return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: too many tiles");
     a.total_tiles = (int)tt;
     if (a.total_tiles == 0) return DP_OK;
+    a.trace = getenv("DP_TC_TRACE") ? tc_trace_buffer(st) : nullptr;
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
@@ -406,6 +443,10 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     if (e != cudaSuccess)
         return set_error(DP_ERR_CUDA, "tc_conv_flat: cudaFuncSetAttribute: %s",
                          cudaGetErrorString(e));
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.maxThreadsPerBlock < TF_THREADS)
+        return set_error(DP_ERR_CUDA, "tc_conv_flat: %d registers/thread allow only %d threads",
+                         fa.numRegs, fa.maxThreadsPerBlock);
     kern<<<grid, TF_THREADS, smem, st>>>(a);
     return check_launch("tc_conv_flat_kernel");
 }

@@ -73,6 +73,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
 // ------------------------------------------------- tensor (tiled) TMA copy
 // 4-D box at integer coordinates {c0 (innermost), c1, c2, c3}; out-of-bounds
 // elements are zero-filled by the TMA unit.
+__device__ __forceinline__ void tma_load_3d(void *dst_smem, const void *tmap, int c0, int c1,
+                                            int c2, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst_smem)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void *dst_smem, const void *tmap, int c0, int c1,
                                             int c2, int c3, uint64_t *bar) {
     asm volatile(

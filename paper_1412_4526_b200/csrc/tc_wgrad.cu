@@ -590,12 +590,38 @@ static int wg_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *
     return DP_OK;
 }
 
+// ---- helpers shared with the shared-memory-operand variant (tc_wgrad_ss.cu)
+int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
+                const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz) {
+    return wg_map(m, base, rank, dims, strides_bytes, box, swz);
+}
+int wg_sms() { return wg_num_sms(); }
+int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
+               long long copy_floats, cudaStream_t st) {
+    tc_stage_x<<<n * cin * hi, 128, 0, st>>>(x, xs, cin, hi, wi, wp, mask, copy_floats);
+    return check_launch("tc_stage_x");
+}
+int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
+                cudaStream_t st) {
+    tc_stage_dy<<<n * cout * ho, 128, 0, st>>>(dy, dys, cout, ho, wo, wp);
+    return check_launch("tc_stage_dy");
+}
+
+// preferred variant: x tap lines read by the tensor core from a shared-memory row ring
+bool ws_supported(int n, int cin, int hi, int wi, int cout, int k, int d);
+size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d);
+int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
+                            int cin, int hi, int wi, int cout, int k, int d, void *ws,
+                            size_t ws_bytes, cudaStream_t st);
+
 bool tc_wgrad_supported(int n, int cin, int hi, int wi, int cout, int k, int d) {
+    if (ws_supported(n, cin, hi, wi, cout, k, d)) return true;
     WgPlan p;
     return wg_plan(n, cin, hi, wi, cout, k, d, p);
 }
 
 size_t tc_wgrad_workspace(int n, int cin, int hi, int wi, int cout, int k, int d) {
+    if (ws_supported(n, cin, hi, wi, cout, k, d)) return ws_workspace(n, cin, hi, wi, cout, k, d);
     WgPlan p;
     if (!wg_plan(n, cin, hi, wi, cout, k, d, p)) return 0;
     return p.total_bytes;
@@ -604,6 +630,9 @@ size_t tc_wgrad_workspace(int n, int cin, int hi, int wi, int cout, int k, int d
 int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
                             size_t ws_bytes, cudaStream_t st) {
+    if (ws_supported(n, cin, hi, wi, cout, k, d))
+        return ws_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes,
+                                       st);
     WgPlan p;
     if (!wg_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED,

@@ -1,0 +1,604 @@
+// Weight / bias gradient of the d-regularly sparse convolution on the tcgen05 tensor cores
+// with BOTH operands read from shared memory (fast tier, 3xTF32) -- preferred over the
+// TMEM-operand kernel in tc_wgrad.cu whenever its row ring fits.
+//
+//   dw[o,c,i,j] = sum_{n,u,v} dy[n,o,u,v] * x[n,c,u+i*d,v+j*d]      db[o] = sum dy[n,o,u,v]
+// (reference _kernels.pyx:94-130, _kernels_py.py:54-66) as D[r, o] = sum_k A[r, k] B[o, k]:
+//   k = output pixel, K blocks of 32 consecutive v of one output row u  (the long axis)
+//   r = x tap line (i, residue copy, c, jj)                             -> M, tiles of 128
+//   o = output channel (padded to Npad)                                 -> N
+//
+// x tap lines.  tc_stage_x lays x out as (n, h, c, wp) copies shifted left by
+// b = (j*d) & 3 for each residue b that occurs, so that for one residue copy the taps j with
+// that residue sit at columns v0 + j*d - b, all multiples of 4 floats, lcm(d, 4) floats
+// apart -- a legal TMA stride.  One 4-D box {32 px, taps of the residue, Cpad channels,
+// 1 row} therefore delivers, for ONE input row, every (c, j) line of 32 pixels as a 128-byte
+// SWIZZLE_128B row: exactly the canonical K-major A layout the tensor core reads (SBO = 1024,
+// +32 B per K=8 slice).  All residue boxes of an input row form one ring slot of
+// Ls = Cpad * l lines.
+//
+// Row ring.  A CTA walks K blocks down image columns (u, u+d, u+2d, ... for one 32-px block
+// and row phase u mod d).  Consecutive blocks share l-1 of their l tap rows (rows u + i*d),
+// so each input row is loaded ONCE into a ring slot and serves as tap row i of l successive
+// blocks; a block adds one row (a column start adds all of them).  The lo part of a row
+// (x - trunc_tf32(x), for 3xTF32) is computed once into a parallel lo ring.  Block tiles
+// (128 consecutive lines = parts of up to 3 slots) are contiguous because the first NM
+// slots are mirrored past the ring's end.  Ring slot reuse: inside a column the slot a block
+// overwrites was last read by block kl - SS (R = n_i + SS - 1 slots); a column start waits
+// for the previous block (a drain every ~Ho/d blocks).
+//
+// 3xTF32 per K=8 slice and tile: A_hi x [B_hi | B_lo] (N = 2 Npad) + A_lo x B_hi (N = Npad);
+// accumulators stay in TMEM (all tiles of the CTA's group: no A staging in TMEM at all).
+//
+// Roles (one CTA per SM, 10 warps): warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer,
+// warps 0-7 converters (dy B_lo + db, lo lines of new rows) and the epilogue.  Split-K over
+// CTAs, partials [split][line][o] summed by ws_reduce in a fixed order (deterministic).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "dp_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace dp {
+
+int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
+                const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz);
+int wg_sms();
+int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
+               long long copy_floats, cudaStream_t st);
+int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
+                cudaStream_t st);
+
+constexpr int WS_CONV_WARPS = 8;
+constexpr int WS_TMA_WARP = 8;
+constexpr int WS_MMA_WARP = 9;
+constexpr int WS_THREADS = 320;
+constexpr int WS_MAX_SS = 8;
+constexpr int WS_MAX_G = 16;
+constexpr int WS_SMEM_BUDGET = 222 * 1024;
+
+struct WsResidues {
+    int n_b;        // residue copies used
+    int b[4];       // residue of copy slot
+    int n[4];       // taps in the residue
+    int j0[4];      // first tap of the residue
+    int line0[4];   // first line of the residue's box inside a ring slot
+    int step;       // tap step inside a residue: 4 / gcd(d, 4)
+};
+
+struct WsArgs {
+    int C, Cpad, l, d, Q, Npad;
+    int n_tiles, G, n_groups, splits;
+    int Ho, Wo, nvb, T, Hi;
+    long long kb_total;  // n * nvb * d columns x T blocks
+    int SS, R, NM, Ls;   // dy stages, ring slots, mirrored slots, lines per slot
+    uint32_t b_bytes;    // dy stage: B_hi + B_lo (2 * Npad * 128)
+    uint32_t slot_bytes, box_tx_row;  // Ls * 128
+    uint32_t ring_hi, ring_lo;        // shared-memory offsets
+    WsResidues rs;
+    float *part;  // [splits][n_tiles * 128][Npad]
+    float *pdb;   // [splits][Npad]
+};
+
+// Column-major K order (see header).  Bm = ring slot of the block's first tap row.
+struct WsSched {
+    int t, T, vb, img, phase, u, nvb, d, n_i, R, Bm;
+    bool cstart;
+    __device__ WsSched(const WsArgs &a, long long kb, int ni) {
+        T = a.T;
+        nvb = a.nvb;
+        d = a.d;
+        n_i = ni;
+        R = a.R;
+        const long long col = kb / T;
+        t = (int)(kb - col * T);
+        phase = (int)(col % d);
+        const long long vc = col / d;
+        vb = (int)(vc % nvb);
+        img = (int)(vc / nvb);
+        u = phase + t * d;
+        Bm = 0;
+        cstart = true;
+    }
+    __device__ void next() {
+        if (++t == T) {
+            t = 0;
+            if (++phase == d) {
+                phase = 0;
+                if (++vb == nvb) {
+                    vb = 0;
+                    ++img;
+                }
+            }
+        }
+        u = phase + t * d;
+        // inside a column the block sits one row further down the ring; a new column
+        // starts on fresh slots after the previous block's n_i rows
+        Bm += (t == 0) ? n_i : 1;
+        while (Bm >= R) Bm -= R;
+        cstart = t == 0;
+    }
+};
+
+__global__ void __launch_bounds__(WS_THREADS, 1)
+tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
+                   const __grid_constant__ CUtensorMap tm_x1,
+                   const __grid_constant__ CUtensorMap tm_x2,
+                   const __grid_constant__ CUtensorMap tm_x3,
+                   const __grid_constant__ CUtensorMap tm_dy, const WsArgs a) {
+    extern __shared__ __align__(1024) unsigned char ws_smem_raw[];
+    __shared__ uint64_t sfull[WS_MAX_SS], cfull[WS_MAX_SS], sempty[WS_MAX_SS], accfull;
+    __shared__ uint32_t s_tmem;
+
+    unsigned char *smem = (unsigned char *)(((uintptr_t)ws_smem_raw + 1023) & ~(uintptr_t)1023);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x % a.n_groups, split = blockIdx.x / a.n_groups;
+    const int tile0 = g * a.G;
+    const int G = min(a.G, a.n_tiles - tile0);
+    const long long kb_first = a.kb_total * split / a.splits;
+    const int nkb = (int)(a.kb_total * (split + 1) / a.splits - kb_first);
+    const int acc_cols = 2 * a.Npad;
+    const int lines_total = a.l * a.Ls;
+    const int i_lo = tile0 * 128 / a.Ls;
+    const int n_i = (min((tile0 + G) * 128, lines_total) - 1) / a.Ls - i_lo + 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.SS; ++s) {
+            ptx::mbar_init(&sfull[s], 1);
+            ptx::mbar_init(&cfull[s], WS_CONV_WARPS);
+            ptx::mbar_init(&sempty[s], 1);
+        }
+        ptx::mbar_init(&accfull, 1);
+        ptx::mbar_fence_init();
+    }
+    if (warp == WS_TMA_WARP && lane == 0) {
+        ptx::tma_prefetch_desc(&tm_dy);
+        ptx::tma_prefetch_desc(&tm_x0);
+    }
+    if (warp == WS_MMA_WARP) ptx::tmem_alloc<512>(&s_tmem);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == WS_TMA_WARP) {
+        // ================================ TMA producer ================================
+        WsSched sc(a, kb_first, n_i);
+        unsigned char *ring = smem + a.ring_hi;
+        for (int kl = 0; kl < nkb; ++kl, sc.next()) {
+            const int s = kl % a.SS;
+            ptx::mbar_wait(&sempty[s], ((kl / a.SS) & 1) ^ 1);
+            if (sc.cstart && kl > 0) {
+                const int kw = kl - 1;  // column start: drain (see header)
+                ptx::mbar_wait(&sempty[kw % a.SS], (kw / a.SS) & 1);
+            }
+            if (lane == 0) {
+                const int v0 = sc.vb * 32;
+                const int hh = sc.img * a.Hi + sc.u;
+                const int k0 = sc.cstart ? 0 : n_i - 1;
+                int nbox_rows = 0;
+                for (int k = k0; k < n_i; ++k) {
+                    int slot = sc.Bm + k;
+                    if (slot >= a.R) slot -= a.R;
+                    nbox_rows += slot < a.NM ? 2 : 1;
+                }
+                ptx::mbar_expect_tx(&sfull[s], (uint32_t)a.Npad * 128u +
+                                                   (uint32_t)nbox_rows * a.box_tx_row);
+                ptx::tma_load_4d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, sc.u, 0, sc.img,
+                                 &sfull[s]);
+                for (int k = k0; k < n_i; ++k) {
+                    int slot = sc.Bm + k;
+                    if (slot >= a.R) slot -= a.R;
+                    const int row = hh + (i_lo + k) * a.d;
+                    for (int copy = 0; copy < 2; ++copy) {
+                        if (copy == 1 && slot >= a.NM) break;
+                        unsigned char *dst =
+                            ring + (size_t)(copy ? a.R + slot : slot) * a.slot_bytes;
+                        for (int rb = 0; rb < a.rs.n_b; ++rb) {
+                            const CUtensorMap *m = rb == 0 ? &tm_x0 : rb == 1 ? &tm_x1
+                                                                   : rb == 2 ? &tm_x2 : &tm_x3;
+                            ptx::tma_load_4d(dst + (size_t)a.rs.line0[rb] * 128, m,
+                                             v0 + a.rs.j0[rb] * a.d - a.rs.b[rb], 0, 0, row,
+                                             &sfull[s]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp == WS_MMA_WARP) {
+        // ================================ MMA issuer ================================
+        const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
+        const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
+        const uint32_t sbase = ptx::smem_u32(smem);
+        const uint32_t hi_base = sbase + a.ring_hi, lo_base = sbase + a.ring_lo;
+        // tile 0's first ring slot (relative to the block's Bm) and line inside it; later
+        // tiles follow 128 lines on (incremental: this thread's loop is the critical path)
+        const int line00 = tile0 * 128 - i_lo * a.Ls;
+        const int slot00 = line00 / a.Ls, lin00 = line00 - slot00 * a.Ls;
+        WsSched sc(a, kb_first, n_i);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kl = 0; kl < nkb; ++kl, sc.next()) {
+            ptx::mbar_wait(&cfull[s], ph);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+                const uint32_t bstage = sbase + (uint32_t)s * a.b_bytes;
+                int slot = sc.Bm + slot00, lin = lin00;
+                if (slot >= a.R) slot -= a.R;
+                for (int t = 0; t < G; ++t) {
+                    const uint32_t off = (uint32_t)slot * a.slot_bytes + (uint32_t)lin * 128u;
+                    const uint32_t dcol = tmem + (uint32_t)(t * acc_cols);
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint64_t bd = ptx::smem_desc_sw128(bstage + ks * 32);
+                        ptx::mma_tf32_ss(dcol, ptx::smem_desc_sw128(hi_base + off + ks * 32), bd,
+                                         idesc_2n, (kl | ks) > 0);
+                        ptx::mma_tf32_ss(dcol, ptx::smem_desc_sw128(lo_base + off + ks * 32), bd,
+                                         idesc_n, 1);
+                    }
+                    // next tile: 128 lines on; past a slot's end the lines continue in the
+                    // next slot (or its mirror past the ring's end)
+                    lin += 128;
+                    while (lin >= a.Ls) {
+                        lin -= a.Ls;
+                        if (++slot == a.R) slot = 0;  // a tile STARTING past the end wraps
+                    }
+                }
+                ptx::mma_commit(&sempty[s]);
+            }
+            __syncwarp();
+            if (++s == a.SS) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        if (ptx::elect_one()) ptx::mma_commit(&accfull);
+        __syncwarp();
+    } else {
+        // ================================ converters ================================
+        const int tid = threadIdx.x;  // 0..255
+        const int nchunks = a.Npad * 8;  // 16-byte chunks of the dy tile
+        float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
+        const int lchunks = a.Ls * 8;    // 16-byte chunks of a ring slot
+        WsSched sc(a, kb_first, n_i);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kl = 0; kl < nkb; ++kl, sc.next()) {
+            ptx::mbar_wait(&sfull[s], ph);
+            unsigned char *st = smem + (size_t)s * a.b_bytes;
+            {
+                // B_lo = B_hi - trunc(B_hi) (elementwise; the swizzle is preserved) + db
+                const float4 *bh = reinterpret_cast<const float4 *>(st);
+                float4 *bl = reinterpret_cast<float4 *>(st + (uint32_t)a.Npad * 128);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int idx = tid + 256 * m;
+                    if (idx >= nchunks) break;
+                    const float4 v = bh[idx];
+                    dbacc[m] += (v.x + v.y) + (v.z + v.w);
+                    bl[idx] = make_float4(ptx::tf32_lo(v.x), ptx::tf32_lo(v.y), ptx::tf32_lo(v.z),
+                                          ptx::tf32_lo(v.w));
+                }
+            }
+            // lo lines of the rows this block added (and their mirrors)
+            const int k0 = sc.cstart ? 0 : n_i - 1;
+            for (int k = k0; k < n_i; ++k) {
+                int slot = sc.Bm + k;
+                if (slot >= a.R) slot -= a.R;
+                const float4 *src =
+                    reinterpret_cast<const float4 *>(smem + a.ring_hi + (size_t)slot * a.slot_bytes);
+                float4 *dst = reinterpret_cast<float4 *>(smem + a.ring_lo + (size_t)slot * a.slot_bytes);
+                float4 *dst2 = slot < a.NM ? reinterpret_cast<float4 *>(
+                                                 smem + a.ring_lo + (size_t)(a.R + slot) * a.slot_bytes)
+                                           : nullptr;
+                for (int idx = tid; idx < lchunks; idx += WS_CONV_WARPS * 32) {
+                    const float4 v = src[idx];
+                    const float4 lo = make_float4(ptx::tf32_lo(v.x), ptx::tf32_lo(v.y),
+                                                  ptx::tf32_lo(v.z), ptx::tf32_lo(v.w));
+                    dst[idx] = lo;
+                    if (dst2) dst2[idx] = lo;
+                }
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&cfull[s]);
+            if (++s == a.SS) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        // ---- db partials: thread tid owns dy rows (tid >> 3) + 32 m
+        if (g == 0) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                float v = dbacc[m];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                const int row = (tid >> 3) + 32 * m;
+                if ((lane & 7) == 0 && row < a.Npad) a.pdb[(size_t)split * a.Npad + row] = v;
+            }
+        }
+        // ---- epilogue: tiles t = grp, grp + 2, ...; lane = line
+        const int q = warp & 3, grp = warp >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        if (nkb > 0) {
+            ptx::mbar_wait_sleep(&accfull, 0);
+            ptx::tc_fence_after();
+        }
+        const size_t rows_pad = (size_t)a.n_tiles * 128;
+        for (int t = grp; t < G; t += 2) {
+            const int grow = (tile0 + t) * 128 + q * 32 + lane;
+            float *dstp = a.part + ((size_t)split * rows_pad + grow) * a.Npad;
+            for (int o0 = 0; o0 < a.Npad; o0 += 16) {
+                uint32_t h[16], l2[16];
+                if (nkb > 0) {
+                    const uint32_t dcol = tmem + lane_off + (uint32_t)(t * acc_cols + o0);
+                    ptx::tmem_ld16(dcol, h);
+                    ptx::tmem_ld16(dcol + a.Npad, l2);
+                    ptx::tmem_wait_ld();
+                }
+#pragma unroll
+                for (int k = 0; k < 16; k += 4) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (nkb > 0)
+                        v = make_float4(__uint_as_float(h[k]) + __uint_as_float(l2[k]),
+                                        __uint_as_float(h[k + 1]) + __uint_as_float(l2[k + 1]),
+                                        __uint_as_float(h[k + 2]) + __uint_as_float(l2[k + 2]),
+                                        __uint_as_float(h[k + 3]) + __uint_as_float(l2[k + 3]));
+                    *reinterpret_cast<float4 *>(dstp + o0 + k) = v;
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == WS_MMA_WARP) ptx::tmem_dealloc<512>(tmem);
+}
+
+// dw[o,c,i,j] = sum_s part[s][line(i, j, c)][o], db[o] = sum_s pdb[s][o]  (fixed order)
+__global__ void ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb,
+                          float *__restrict__ dw, float *__restrict__ db, int Q, int C, int l,
+                          int d, int Ls, int Npad, int splits, int rows_pad, WsResidues rs) {
+    const long long total = (long long)Q * C * l * l;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < total) {
+        const int ll = l * l;
+        const int o = (int)(idx / ((long long)C * ll));
+        const int rem = (int)(idx - (long long)o * C * ll);
+        const int c = rem / ll, tap = rem - (rem / ll) * ll;
+        const int i = tap / l, j = tap - (tap / l) * l;
+        const int b = (j * d) & 3;
+        int rb = 0;
+        while (rs.b[rb] != b) ++rb;
+        const int jj = (j - rs.j0[rb]) / rs.step;
+        const size_t line = (size_t)i * Ls + rs.line0[rb] + c * rs.n[rb] + jj;
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) acc += part[((size_t)s * rows_pad + line) * Npad + o];
+        dw[idx] = acc;
+    } else if (idx < total + Q) {
+        const int o = (int)(idx - total);
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) acc += pdb[(size_t)s * Npad + o];
+        db[o] = acc;
+    }
+}
+
+// --------------------------------------------------------------------------------
+// host side
+// --------------------------------------------------------------------------------
+struct WsPlan {
+    int Cpad, Npad, Ls, n_tiles, G, n_groups, splits, SS, R, NM, max_ni;
+    int ho, wo, nvb, T, wp_x, wp_dy, mask;
+    bool stage_dy;
+    long long kb_total;
+    WsResidues rs;
+    size_t part_bytes, pdb_bytes, copy_bytes, x_bytes, dy_bytes, total_bytes;
+    uint32_t b_bytes, slot_bytes;
+};
+
+static size_t ws_align256(size_t v) { return (v + 255) / 256 * 256; }
+
+static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPlan &p) {
+    if (getenv("DP_WG_TMEM")) return false;  // force the TMEM-operand kernel (experiments)
+    const int e = (k - 1) * d + 1;
+    p.ho = hi - e + 1;
+    p.wo = wi - e + 1;
+    if (p.ho < 1 || p.wo < 1 || k > 64) return false;
+    p.Npad = (cout + 15) / 16 * 16;
+    if (p.Npad > 128) return false;
+    p.Cpad = (cin + 7) / 8 * 8;
+    if (p.Cpad > 256) return false;
+    p.Ls = p.Cpad * k;
+    const int lines = k * p.Ls;
+    p.n_tiles = (lines + 127) / 128;
+    const int acc_cols = 2 * p.Npad;
+    int G = std::min(std::min(p.n_tiles, 512 / acc_cols), WS_MAX_G);
+    p.n_groups = (p.n_tiles + G - 1) / G;
+    p.G = (p.n_tiles + p.n_groups - 1) / p.n_groups;
+    // tap rows per group and the ring slots a 128-line tile can span
+    p.max_ni = 0;
+    int span = 1;
+    for (int g = 0; g < p.n_groups; ++g) {
+        const int t0 = g * p.G, G_ = std::min(p.G, p.n_tiles - t0);
+        const int i_lo = t0 * 128 / p.Ls;
+        const int n_i = (std::min((t0 + G_) * 128, lines) - 1) / p.Ls - i_lo + 1;
+        p.max_ni = std::max(p.max_ni, n_i);
+        for (int t = 0; t < G_; ++t) {
+            const int line0 = (t0 + t) * 128 - i_lo * p.Ls;
+            const int f = line0 % p.Ls;
+            span = std::max(span, (f + 128 + p.Ls - 1) / p.Ls);
+        }
+    }
+    p.NM = span - 1;
+    // residue copies: taps j with (j*d) & 3 == b, lcm(d, 4) floats apart
+    int gcd = 1;
+    for (int v = 4; v >= 1; --v)
+        if (d % v == 0 && 4 % v == 0) {
+            gcd = v;
+            break;
+        }
+    p.rs.step = 4 / gcd;
+    p.mask = 0;
+    p.rs.n_b = 0;
+    int line0 = 0;
+    for (int b = 0; b < 4; ++b) {
+        int cnt = 0, j0 = -1;
+        for (int j = 0; j < k; ++j)
+            if (((j * d) & 3) == b) {
+                if (j0 < 0) j0 = j;
+                ++cnt;
+            }
+        if (!cnt) continue;
+        if (cnt > 256) return false;
+        const int rb = p.rs.n_b++;
+        p.rs.b[rb] = b;
+        p.rs.n[rb] = cnt;
+        p.rs.j0[rb] = j0;
+        p.rs.line0[rb] = line0;
+        line0 += p.Cpad * cnt;
+        p.mask |= 1 << b;
+    }
+    for (int rb = p.rs.n_b; rb < 4; ++rb) {
+        p.rs.b[rb] = -1;
+        p.rs.n[rb] = p.rs.j0[rb] = p.rs.line0[rb] = 0;
+    }
+    p.slot_bytes = (uint32_t)p.Ls * 128u;  // Cpad multiple of 8: 1024-byte aligned boxes
+    p.b_bytes = 2u * (uint32_t)p.Npad * 128u;
+    int SS = WS_MAX_SS;
+    auto smem_for = [&](int ss) {
+        return (size_t)ss * p.b_bytes + 2 * (size_t)(p.max_ni + ss - 1 + p.NM) * p.slot_bytes;
+    };
+    while (SS >= 2 && smem_for(SS) > (size_t)WS_SMEM_BUDGET) --SS;
+    if (SS < 2) return false;
+    p.SS = SS;
+    p.R = p.max_ni + SS - 1;
+    p.nvb = (p.wo + 31) / 32;
+    p.T = (p.ho + d - 1) / d;
+    p.kb_total = (long long)n * p.nvb * d * p.T;
+    p.splits = wg_sms() / p.n_groups;
+    if (p.splits < 1) p.splits = 1;
+    if (p.splits > p.kb_total) p.splits = (int)p.kb_total;
+    p.wp_x = (wi + 3) / 4 * 4;
+    p.wp_dy = (p.wo + 3) / 4 * 4;
+    p.stage_dy = p.wp_dy != p.wo;
+    if ((long long)n * hi > (1LL << 31)) return false;
+    p.part_bytes = ws_align256((size_t)p.splits * p.n_tiles * 128 * p.Npad * 4);
+    p.pdb_bytes = ws_align256((size_t)p.splits * p.Npad * 4);
+    // boxes read up to (l-1)*d + 32 floats past a row's end (those columns meet zero dy)
+    p.copy_bytes = ws_align256((size_t)n * cin * hi * p.wp_x * 4 + ((size_t)(k - 1) * d + 64) * 4);
+    p.x_bytes = (size_t)p.rs.n_b * p.copy_bytes;
+    p.dy_bytes = p.stage_dy ? ws_align256((size_t)n * cout * p.ho * p.wp_dy * 4) : 0;
+    p.total_bytes = p.part_bytes + p.pdb_bytes + p.x_bytes + p.dy_bytes;
+    return true;
+}
+
+bool ws_supported(int n, int cin, int hi, int wi, int cout, int k, int d) {
+    WsPlan p;
+    return ws_plan(n, cin, hi, wi, cout, k, d, p);
+}
+
+size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d) {
+    WsPlan p;
+    return ws_plan(n, cin, hi, wi, cout, k, d, p) ? p.total_bytes : 0;
+}
+
+int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
+                            int cin, int hi, int wi, int cout, int k, int d, void *ws,
+                            size_t ws_bytes, cudaStream_t st) {
+    WsPlan p;
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p))
+        return set_error(DP_ERR_UNSUPPORTED, "weight gradient (smem operands): unsupported shape");
+    if (ws == nullptr || ws_bytes < p.total_bytes)
+        return set_error(DP_ERR_ARG, "tensor-core weight gradient: workspace %zu < %zu bytes",
+                         ws_bytes, p.total_bytes);
+    if (((uintptr_t)ws & 255) != 0)
+        return set_error(DP_ERR_ARG,
+                         "tensor-core weight gradient: workspace must be 256-byte aligned");
+    unsigned char *w8 = (unsigned char *)ws;
+    WsArgs a;
+    a.part = (float *)w8;
+    a.pdb = (float *)(w8 + p.part_bytes);
+    float *xs = (float *)(w8 + p.part_bytes + p.pdb_bytes);
+    int rc = wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask, (long long)(p.copy_bytes / 4), st);
+    if (rc) return rc;
+    const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
+    if (stage_dy && !p.stage_dy)
+        return set_error(DP_ERR_ARG, "weight gradient: dy must be 16-byte aligned");
+    const float *dys = dy;
+    if (stage_dy) {
+        float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
+        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, st);
+        if (rc) return rc;
+        dys = dp_;
+    }
+    CUtensorMap mx[4], mdy;
+    {
+        const cuuint64_t rowb = (cuuint64_t)(stage_dy ? p.wp_dy : p.wo) * 4;
+        cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)p.ho, (cuuint64_t)cout, (cuuint64_t)n};
+        cuuint64_t str[3] = {stage_dy ? rowb * cout : rowb, stage_dy ? rowb : rowb * p.ho,
+                             rowb * cout * p.ho};
+        cuuint32_t box[4] = {32, 1, (cuuint32_t)p.Npad, 1};
+        rc = wg_make_map(&mdy, dys, 4, dims, str, box, true);
+        if (rc) return rc;
+    }
+    const cuuint64_t xrow = (cuuint64_t)p.wp_x * 4;  // one channel line
+    const cuuint64_t ximg_row = xrow * cin;          // one image row (all channels)
+    for (int rb = 0; rb < 4; ++rb) {
+        const int used = rb < p.rs.n_b ? rb : 0;
+        const float *base = (const float *)((const unsigned char *)xs + (size_t)used * p.copy_bytes);
+        // (w, jj: lcm(d, 4) floats, c, row of n*hi) -- overlapping views, one box = the
+        // residue's (c, jj) lines of one input row
+        cuuint64_t dims[4] = {(cuuint64_t)p.wp_x, (cuuint64_t)p.rs.n[used], (cuuint64_t)cin,
+                              (cuuint64_t)n * hi};
+        cuuint64_t str[3] = {(cuuint64_t)p.rs.step * d * 4, xrow, ximg_row};
+        cuuint32_t box[4] = {32, (cuuint32_t)p.rs.n[used], (cuuint32_t)p.Cpad, 1};
+        rc = wg_make_map(&mx[rb], base, 4, dims, str, box, true);
+        if (rc) return rc;
+    }
+    a.C = cin;
+    a.Cpad = p.Cpad;
+    a.l = k;
+    a.d = d;
+    a.Q = cout;
+    a.Npad = p.Npad;
+    a.n_tiles = p.n_tiles;
+    a.G = p.G;
+    a.n_groups = p.n_groups;
+    a.splits = p.splits;
+    a.Ho = p.ho;
+    a.Wo = p.wo;
+    a.nvb = p.nvb;
+    a.T = p.T;
+    a.Hi = hi;
+    a.kb_total = p.kb_total;
+    a.SS = p.SS;
+    a.R = p.R;
+    a.NM = p.NM;
+    a.Ls = p.Ls;
+    a.b_bytes = p.b_bytes;
+    a.slot_bytes = p.slot_bytes;
+    a.box_tx_row = p.slot_bytes;
+    a.ring_hi = (uint32_t)p.SS * p.b_bytes;
+    a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
+    a.rs = p.rs;
+    const size_t smem = (size_t)a.ring_lo + (size_t)(p.R + p.NM) * p.slot_bytes + 1024;
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_ss_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return set_error(DP_ERR_CUDA, "tc_wgrad_ss: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    const int grid = p.n_groups * p.splits;
+    tc_wgrad_ss_kernel<<<grid, WS_THREADS, smem, st>>>(mx[0], mx[1], mx[2], mx[3], mdy, a);
+    rc = check_launch("tc_wgrad_ss_kernel");
+    if (rc) return rc;
+    const long long total = (long long)cout * cin * k * k + cout;
+    ws_reduce<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, d, p.Ls,
+                                                    p.Npad, p.splits, p.n_tiles * 128, p.rs);
+    return check_launch("ws_reduce");
+}
+
+}  // namespace dp

@@ -591,6 +591,13 @@ static int wg_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *
 }
 
 // ---- helpers shared with the shared-memory-operand variant (tc_wgrad_ss.cu)
+unsigned long long *wg_trace_buffer(cudaStream_t st) {
+    static unsigned long long *buf = nullptr;
+    if (!buf && cudaMalloc(&buf, 256 * 16 * 8) != cudaSuccess) buf = nullptr;
+    if (buf) cudaMemsetAsync(buf, 0, 256 * 16 * 8, st);
+    g_wg_trace = buf;
+    return buf;
+}
 int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz) {
     return wg_map(m, base, rank, dims, strides_bytes, box, swz);

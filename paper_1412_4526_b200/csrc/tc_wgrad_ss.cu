@@ -47,6 +47,7 @@ namespace dp {
 int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz);
 int wg_sms();
+unsigned long long *wg_trace_buffer(cudaStream_t st);
 int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
                long long copy_floats, cudaStream_t st);
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
@@ -81,7 +82,15 @@ struct WsArgs {
     WsResidues rs;
     float *part;  // [splits][n_tiles * 128][Npad]
     float *pdb;   // [splits][Npad]
+    unsigned long long *trace;  // DP_WG_TRACE: per-K-block clock64 stamps of CTA 0
 };
+
+// slots: 0 TMA issue, 2 converters got the stage, 4 converters done, 8 MMA got, 9 issued
+#define WS_TRACE(A, KL, SLOT, COND)                                               \
+    do {                                                                          \
+        if ((A).trace && (COND) && blockIdx.x == 0 && (KL) < 256)                 \
+            (A).trace[(KL) * 16 + (SLOT)] = clock64();                            \
+    } while (0)
 
 // Column-major K order (see header).  Bm = ring slot of the block's first tap row.
 struct WsSched {
@@ -179,6 +188,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 const int v0 = sc.vb * 32;
                 const int hh = sc.img * a.Hi + sc.u;
                 const int k0 = sc.cstart ? 0 : n_i - 1;
+                WS_TRACE(a, kl, 0, true);
                 int nbox_rows = 0;
                 for (int k = k0; k < n_i; ++k) {
                     int slot = sc.Bm + k;
@@ -225,6 +235,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         for (int kl = 0; kl < nkb; ++kl, sc.next()) {
             ptx::mbar_wait(&cfull[s], ph);
             ptx::tc_fence_after();
+            WS_TRACE(a, kl, 8, lane == 0);
             if (ptx::elect_one()) {
                 const uint32_t bstage = sbase + (uint32_t)s * a.b_bytes;
                 int slot = sc.Bm + slot00, lin = lin00;
@@ -251,6 +262,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 ptx::mma_commit(&sempty[s]);
             }
             __syncwarp();
+            WS_TRACE(a, kl, 9, lane == 0);
             if (++s == a.SS) {
                 s = 0;
                 ph ^= 1;
@@ -269,6 +281,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         uint32_t ph = 0;
         for (int kl = 0; kl < nkb; ++kl, sc.next()) {
             ptx::mbar_wait(&sfull[s], ph);
+            WS_TRACE(a, kl, 2, tid == 0);
             unsigned char *st = smem + (size_t)s * a.b_bytes;
             {
                 // B_lo = B_hi - trunc(B_hi) (elementwise; the swizzle is preserved) + db
@@ -306,6 +319,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&cfull[s]);
+            WS_TRACE(a, kl, 4, tid == 0);
             if (++s == a.SS) {
                 s = 0;
                 ph ^= 1;
@@ -586,6 +600,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.ring_hi = (uint32_t)p.SS * p.b_bytes;
     a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
     a.rs = p.rs;
+    a.trace = getenv("DP_WG_TRACE") ? wg_trace_buffer(st) : nullptr;
     const size_t smem = (size_t)a.ring_lo + (size_t)(p.R + p.NM) * p.slot_bytes + 1024;
     cudaError_t e = cudaFuncSetAttribute(tc_wgrad_ss_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

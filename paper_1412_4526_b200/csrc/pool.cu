@@ -33,7 +33,7 @@ __device__ __forceinline__ long long pool_plane() {
 // Max pool: 2-D tiles, block (32, 8), each thread 4 columns 32 apart (warp accesses stay
 // 128-byte row segments) so the index math and the plane/row bases are paid once per 4
 // outputs -- the one-output-per-thread version was issue bound at ~1.7 TB/s.
-constexpr int PT_X = 32, PT_Y = 8, PT_V = 4, PT_R = 4;  // tile: 128 columns x 32 rows
+constexpr int PT_X = 32, PT_Y = 8, PT_V = 4, PT_R = 8;  // tile: 128 columns x 64 rows
 
 template <typename T, typename A, int P>
 __global__ void __launch_bounds__(PT_X * PT_Y)
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(PT_X * PT_Y)
     }
 }
 
-constexpr int PB_V = 2;  // backward: 2 pixels per thread (16 loads in flight, ~40 regs)
+constexpr int PB_V = 2;  // backward: 2 pixels per thread (PB_V = 4 measured slower)
 
 template <typename T, typename A, int P>
 __global__ void __launch_bounds__(PT_X * PT_Y)

@@ -411,22 +411,31 @@ __global__ void tc_wgrad_reduce(const float *__restrict__ part, const float *__r
 // shifted left by b columns (dst_b[n,h,c,v] = src[n,c,h,v + b], zero at v + b >= w).
 // wp = w rounded up to 4 floats, so every window start j*d - b is 16-byte aligned; the
 // channels of one image row are adjacent so a K block's segments are compact.
-// One CTA per source row (n, c, h).
-__global__ void tc_stage_x(const float *__restrict__ src, float *__restrict__ dst, int C, int H,
-                           int w, int wp, int mask, long long copy_stride) {
-    const long long row = blockIdx.x;
-    const int h = (int)(row % H);
-    const long long nc = row / H;
-    const int c = (int)(nc % C);
-    const long long n = nc / C;
-    const float *s = src + row * w;
-    float *d0 = dst + ((n * H + h) * C + c) * wp;
-    for (int v = threadIdx.x; v < wp; v += blockDim.x) {
+// One thread per 4 destination floats of every copy (16-byte stores; the source reads are
+// unaligned scalar loads of one row segment, shared by the copies through L1).
+__global__ void __launch_bounds__(256) tc_stage_x(const float *__restrict__ src,
+                                                  float *__restrict__ dst, int C, int H, int w,
+                                                  int wp, int mask, long long copy_stride,
+                                                  long long total_quads) {
+    const int nq = wp >> 2;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total_quads;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long row = idx / nq;  // (n, c, h)
+        const int v = (int)(idx - row * nq) * 4;
+        const int h = (int)(row % H);
+        const long long nc = row / H;
+        const int c = (int)(nc % C);
+        const long long n = nc / C;
+        const float *s = src + row * w;
+        float e[7];
+#pragma unroll
+        for (int t = 0; t < 7; ++t) e[t] = v + t < w ? __ldg(s + v + t) : 0.f;
+        float4 *d0 = reinterpret_cast<float4 *>(dst + ((n * H + h) * C + c) * wp + v);
         int slot = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             if (!(mask & (1 << b))) continue;
-            d0[slot * copy_stride + v] = v + b < w ? __ldg(s + v + b) : 0.f;
+            d0[slot * (copy_stride >> 2)] = make_float4(e[b], e[b + 1], e[b + 2], e[b + 3]);
             ++slot;
         }
     }
@@ -435,16 +444,42 @@ __global__ void tc_stage_x(const float *__restrict__ src, float *__restrict__ ds
 // dy staging: NCHW (n, o, h, w) -> (n, h, o, wp), zero pad.  A K block's dy box then
 // reads Npad lines wp floats apart instead of one line per channel plane (plane-strided
 // boxes measured ~4x slower here: every line opens a different DRAM page).
-__global__ void tc_stage_dy(const float *__restrict__ src, float *__restrict__ dst, int O, int H,
-                            int w, int wp) {
-    const long long row = blockIdx.x;  // (n, o, h)
-    const int h = (int)(row % H);
-    const long long no = row / H;
-    const int o = (int)(no % O);
-    const long long n = no / O;
-    const float *s = src + row * w;
-    float *d = dst + ((n * H + h) * O + o) * wp;
-    for (int v = threadIdx.x; v < wp; v += blockDim.x) d[v] = v < w ? __ldg(s + v) : 0.f;
+__global__ void __launch_bounds__(256) tc_stage_dy(const float *__restrict__ src,
+                                                   float *__restrict__ dst, int O, int H, int w,
+                                                   int wp, long long total_quads) {
+    const int nq = wp >> 2;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total_quads;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long row = idx / nq;  // (n, o, h)
+        const int v = (int)(idx - row * nq) * 4;
+        const int h = (int)(row % H);
+        const long long no = row / H;
+        const int o = (int)(no % O);
+        const long long n = no / O;
+        const float *s = src + row * w;
+        float e[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) e[t] = v + t < w ? __ldg(s + v + t) : 0.f;
+        *reinterpret_cast<float4 *>(dst + ((n * H + h) * O + o) * wp + v) =
+            make_float4(e[0], e[1], e[2], e[3]);
+    }
+}
+
+static int stage_grid(long long quads) {
+    long long g = (quads + 255) / 256;
+    return (int)(g < 148 * 64 ? g : 148 * 64);
+}
+
+// the staged copies' tails (read by the last row's out-of-row taps, which only ever meet
+// zero dy) must hold zeros, not stale NaN/Inf bit patterns: 0 * NaN would poison dw
+static int stage_x_tails(float *xs, long long used_floats, long long copy_floats, int mask,
+                         cudaStream_t st) {
+    const int ncopies = __builtin_popcount(mask);
+    for (int c = 0; c < ncopies; ++c)
+        if (cudaMemsetAsync(xs + c * copy_floats + used_floats, 0,
+                            (size_t)(copy_floats - used_floats) * 4, st) != cudaSuccess)
+            return set_error(DP_ERR_CUDA, "weight gradient: memset of staged tails failed");
+    return DP_OK;
 }
 
 // --------------------------------------------------------------------------------
@@ -605,12 +640,16 @@ int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *di
 int wg_sms() { return wg_num_sms(); }
 int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
                long long copy_floats, cudaStream_t st) {
-    tc_stage_x<<<n * cin * hi, 128, 0, st>>>(x, xs, cin, hi, wi, wp, mask, copy_floats);
-    return check_launch("tc_stage_x");
+    const long long quads = (long long)n * cin * hi * (wp / 4);
+    tc_stage_x<<<stage_grid(quads), 256, 0, st>>>(x, xs, cin, hi, wi, wp, mask, copy_floats, quads);
+    int rc = check_launch("tc_stage_x");
+    if (rc) return rc;
+    return stage_x_tails(xs, quads * 4, copy_floats, mask, st);
 }
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
                 cudaStream_t st) {
-    tc_stage_dy<<<n * cout * ho, 128, 0, st>>>(dy, dys, cout, ho, wo, wp);
+    const long long quads = (long long)n * cout * ho * (wp / 4);
+    tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, quads);
     return check_launch("tc_stage_dy");
 }
 
@@ -658,8 +697,13 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.pdb = (float *)(w8 + p.part_bytes);
     float *xs = (float *)(w8 + p.part_bytes + p.pdb_bytes);
     const int mask = p.shift_mask;
-    tc_stage_x<<<n * cin * hi, 128, 0, st>>>(x, xs, cin, hi, wi, p.wp_x, mask,
-                                             (long long)(p.copy_bytes / 4));
+    {
+        const long long quads = (long long)n * cin * hi * (p.wp_x / 4);
+        tc_stage_x<<<stage_grid(quads), 256, 0, st>>>(x, xs, cin, hi, wi, p.wp_x, mask,
+                                                      (long long)(p.copy_bytes / 4), quads);
+        int rt = stage_x_tails(xs, quads * 4, (long long)(p.copy_bytes / 4), mask, st);
+        if (rt) return rt;
+    }
     int rc = check_launch("tc_stage_x");
     if (rc) return rc;
     const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
@@ -668,7 +712,8 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     const float *dys = dy;
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
-        tc_stage_dy<<<n * cout * p.ho, 128, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy);
+        const long long quads = (long long)n * cout * p.ho * (p.wp_dy / 4);
+        tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy, quads);
         rc = check_launch("tc_stage_dy");
         if (rc) return rc;
         dys = dp_;

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DP_ABI_VERSION 2
+#define DP_ABI_VERSION 3
 
 enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
 /* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
@@ -125,6 +125,14 @@ int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx,
  * dp_conv_fast_supported(reduce, out, k, d) first; the caller then uses the exact
  * CUDA-core entry points. */
 size_t dp_conv_fast_workspace(int reduce_channels, int out_channels, int k);
+/* Shape-aware workspace (ABI 3): bytes for the fastest kernel of this exact call -- the
+ * tap-stacked variant (all column taps of a tap row in one MMA; needs the input re-laid
+ * out as 16-byte channel-quad records with hi/lo precomputed, ~4x the input map) when it
+ * applies, else the packed weights only.  Passing at least this many bytes selects the
+ * tap-stacked kernel; dp_conv_fast_workspace bytes still work (flat kernel). */
+size_t dp_conv_forward_fast_workspace(int n, int cin, int h, int w, int cout, int k, int d);
+size_t dp_conv_backward_data_fast_workspace(int n, int cout, int ho, int wo, int cin, int k,
+                                            int d);
 int dp_conv_fast_supported(int reduce_channels, int out_channels, int k, int d);
 int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float *y, int n,
                          int cin, int h, int w, int cout, int k, int d, int nonlin,

@@ -26,6 +26,8 @@ int conv_backward_kernel_t(const T *, const T *, T *, T *, int, int, int, int, i
                            void *, size_t, cudaStream_t);
 size_t wgrad_workspace_bytes(int elem, int n, int cin, int hi, int wi, int cout, int k, int d);
 size_t tc_conv_workspace(int R, int Q, int l);
+size_t tc_conv_fwd_workspace(int n, int cin, int h, int w, int cout, int k, int d);
+size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, int d);
 bool tc_conv_supported(int R, int Q, int l, int d);
 int tc_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
                     int, int, int, void *, size_t, cudaStream_t);
@@ -228,6 +230,17 @@ int dp_conv_backward_data(int dtype, const void *dy, const void *wt, void *dx, i
 size_t dp_conv_fast_workspace(int reduce_channels, int out_channels, int k) {
     if (reduce_channels < 1 || out_channels < 1 || k < 1) return 0;
     return tc_conv_workspace(reduce_channels, out_channels, k);
+}
+
+size_t dp_conv_forward_fast_workspace(int n, int cin, int h, int w, int cout, int k, int d) {
+    if (n < 1 || cin < 1 || cout < 1 || check_window("dilated conv", h, w, k, d)) return 0;
+    return tc_conv_fwd_workspace(n, cin, h, w, cout, k, d);
+}
+
+size_t dp_conv_backward_data_fast_workspace(int n, int cout, int ho, int wo, int cin, int k,
+                                            int d) {
+    if (n < 1 || cin < 1 || cout < 1 || ho < 1 || wo < 1 || k < 1 || d < 1) return 0;
+    return tc_conv_bwd_workspace(n, cout, ho, wo, cin, k, d);
 }
 
 int dp_conv_fast_supported(int reduce_channels, int out_channels, int k, int d) {

@@ -126,6 +126,13 @@ int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, cudaStream_
     return check_launch("tc_pack_weights");
 }
 
+// tap-stacked variant (tc_conv_tap.cu): preferred when it applies AND the caller's workspace
+// holds its relayout planes (dp_conv_*_fast_workspace); else the flat variant
+size_t tt_conv_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad, int Ho,
+                         int Wo);
+int tt_launch(const float *in, const float *w, const float *bias, float *out, const float *gate,
+              int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
+              int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st);
 // flattened shared-memory-operand variant (tc_conv_flat.cu), preferred when it applies
 bool tf_conv_supported(int R, int Q, int l, int d);
 int tf_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
@@ -724,9 +731,30 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     return check_launch("tc_conv_kernel");
 }
 
+size_t tc_conv_fwd_workspace(int n, int cin, int h, int wd, int cout, int k, int d) {
+    const int e = (k - 1) * d + 1;
+    const size_t t = tt_conv_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
+    const size_t w = tc_conv_workspace(cin, cout, k);
+    return t > w ? t : w;
+}
+
+size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, int d) {
+    const int e = (k - 1) * d + 1;
+    const size_t t = tt_conv_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1, wo + e - 1);
+    const size_t w = tc_conv_workspace(cout, cin, k);
+    return t > w ? t : w;
+}
+
 int tc_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,
                     int h, int wd, int cout, int k, int d, int act, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
+    {
+        const int e = (k - 1) * d + 1;
+        const size_t t = tt_conv_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
+        if (t && ws_bytes >= t)
+            return tt_launch(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k,
+                             d, 0, act, 0, false, ws, ws_bytes, st);
+    }
     if (tf_conv_supported(cin, cout, k, d))
         return tf_conv_forward(x, w, b, y, n, cin, h, wd, cout, k, d, act, ws, ws_bytes, st);
     int e = (k - 1) * d + 1;
@@ -737,6 +765,14 @@ int tc_conv_forward(const float *x, const float *w, const float *b, float *y, in
 int tc_conv_backward_data(const float *dy, const float *w, float *dx, int n, int cout, int ho,
                           int wo, int cin, int k, int d, const float *gate, int gate_kind,
                           void *ws, size_t ws_bytes, cudaStream_t st) {
+    {
+        const int e = (k - 1) * d + 1;
+        const size_t t =
+            tt_conv_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1, wo + e - 1);
+        if (t && ws_bytes >= t)
+            return tt_launch(dy, w, nullptr, dx, gate, n, cout, ho, wo, cin, ho + e - 1,
+                             wo + e - 1, k, d, e - 1, 0, gate_kind, true, ws, ws_bytes, st);
+    }
     if (tf_conv_supported(cout, cin, k, d))
         return tf_conv_backward_data(dy, w, dx, n, cout, ho, wo, cin, k, d, gate, gate_kind, ws,
                                      ws_bytes, st);

@@ -1,0 +1,512 @@
+// d-regularly sparse convolution on the tcgen05 tensor cores with the column taps of a tap
+// row stacked into N ("tap-stacked" flat implicit GEMM, fast tier, 3xTF32).
+//
+// Same maths and argument meaning as tc_conv_flat.cu (reference _kernels.pyx:23-53 forward,
+// :56-91 data gradient).  On the virtual (zero-padded) input grid of width Wv output pixel
+// (u, v) is p = u*Wv + v and tap (i, j) reads input record p + i*d*Wv + j*d.  The flat kernel
+// reads one 128-record A window per TAP; here one window per TAP ROW serves all l taps:
+//   D'[r, (j, o)] = sum_c A[s + r, c] * W[o, c, i, j]     (N = l * Npad columns)
+// and the epilogue forms y[s + r] = sum_j D'[r + j*d, (j, o)], so an M tile of 128 rows yields
+// S = 128 - (l-1)*d outputs (M tiles overlap by (l-1)*d rows).  Per tap row and M tile the
+// tensor core reads A_hi twice and A_lo once (three N = l*Npad MMAs: A_hi W_hi, A_hi W_lo,
+// A_lo W_hi) instead of 2*l times -- the flat kernel's limiter was exactly these A reads.
+//
+// Input records come from tc_relayout: per (image, channel chunk of 8) four planes
+// [hi c0-3 | hi c4-7 | lo c0-3 | lo c4-7] of 16-byte records over the whole virtual grid
+// (zero padding materialised, lo = x - trunc_tf32(x) precomputed), so a unit's A windows
+// are plain contiguous ranges: one bulk async copy per (tap row, plane).
+//
+// Per CTA (persistent, one per SM, 6 warps):
+//   warp 4   producer: per unit (tile, chunk, TR tap rows) 4*TR record copies + the unit's
+//            packed weights ([tap row][B_hi (l*Npad rows) | B_lo]), one expect_tx;
+//   warp 5   MMA issuer: TR * MT * 3 MMAs per unit, one commit frees the unit buffer, one
+//            commit per tile hands the accumulators (double-buffered) to the epilogue;
+//   warps 0-3 epilogue, one per TMEM lane quarter: per 16-channel chunk and tap j,
+//            tcgen05.ld, exchange through shared memory to fetch row r + j*d, accumulate;
+//            bias + nonlinearity (forward) or the upstream derivative (data gradient).
+#include <stdlib.h>
+
+#include "dp_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace dp {
+
+constexpr int TT_EPI_WARPS = 4;
+constexpr int TT_PROD_WARP = 4;
+constexpr int TT_MMA_WARP = 5;
+constexpr int TT_THREADS = 6 * 32;
+constexpr int TT_MAX_HB = 6;
+constexpr int TT_MAX_L = 8;                 // taps per row the epilogue exchange supports
+constexpr int TT_SMEM_TOTAL = 222 * 1024;   // unit buffers + epilogue exchange (dynamic)
+
+struct TtArgs {
+    const float *xr;     // relayout: [n][n_rc][4 planes][plane_recs] 16-byte records
+    const float *wpack;  // [n_rc][l][hi|lo][LN x 8] core-matrix layout
+    const float *bias;
+    float *out;          // (n, Q, Ho, Wo)
+    const float *gate;
+    int n_rc, l, d, Q, Npad, LN, MT, S, NR, TR, n_tr;
+    int Wv, Ho, Wo, act, gate_kind;
+    long long plane_recs;
+    int flat_len, tiles_per_img, total_tiles, HB;
+    uint32_t seg_bytes;    // NR * 16
+    uint32_t wrow_bytes;   // one tap row of packed weights: 2 * LN * 32
+    uint32_t ubytes;       // unit buffer
+    uint32_t xoff;         // epilogue exchange area: [l][16][160] floats after the units
+};
+
+__device__ __forceinline__ float tt_act(float v, int kind) {
+    if (kind == DP_TANH || kind == DP_TANH_FAST) return tanhf(v);
+    if (kind == DP_RELU) return dp_relu(v);
+    return v;
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ uint64_t ufull[TT_MAX_HB], uempty[TT_MAX_HB], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+    __shared__ float s_bias[256];
+    // epilogue exchange (dynamic): [tap j][16 columns][128 rows + 32 spill rows (zero)]
+    float *s_x = reinterpret_cast<float *>(smem_raw + a.xoff);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int MT = a.MT;
+    const int units = a.n_rc * a.n_tr;
+    for (int o = threadIdx.x; o < a.Npad; o += blockDim.x)
+        s_bias[o] = (!BWD && o < a.Q) ? a.bias[o] : 0.f;
+    for (int e = threadIdx.x; e < a.l * 16 * 32; e += blockDim.x)
+        s_x[(e >> 5) * 160 + 128 + (e & 31)] = 0.f;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < a.HB; ++b) {
+            ptx::mbar_init(&ufull[b], 1);
+            ptx::mbar_init(&uempty[b], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tfull[b], 1);
+            ptx::mbar_init(&tempty[b], TT_EPI_WARPS);
+        }
+        ptx::mbar_fence_init();
+    }
+    if (warp == TT_MMA_WARP) ptx::tmem_alloc<512>(&s_tmem);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == TT_PROD_WARP) {
+        // ================================ producer ================================
+        if (lane == 0) {
+            const unsigned char *xr = reinterpret_cast<const unsigned char *>(a.xr);
+            const unsigned char *wsrc = reinterpret_cast<const unsigned char *>(a.wpack);
+            int b = 0;
+            uint32_t uph = 0;
+            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+                const int img = tile / a.tiles_per_img;
+                const int f0 = (tile - img * a.tiles_per_img) * MT * a.S;
+                for (int rc = 0; rc < a.n_rc; ++rc) {
+                    const unsigned char *pl =
+                        xr + ((size_t)img * a.n_rc + rc) * 4 * a.plane_recs * 16;
+                    for (int i0 = 0; i0 < a.l; i0 += a.TR) {
+                        const int ntr = min(a.TR, a.l - i0);
+                        ptx::mbar_wait(&uempty[b], uph ^ 1);
+                        unsigned char *ub = smem_raw + (size_t)b * a.ubytes;
+                        ptx::mbar_expect_tx(&ufull[b], (uint32_t)ntr * (4 * a.seg_bytes + a.wrow_bytes));
+                        for (int t = 0; t < ntr; ++t) {
+                            const long long rec0 = f0 + (long long)(i0 + t) * a.d * a.Wv;
+                            for (int p = 0; p < 4; ++p)
+                                ptx::bulk_g2s(ub + (size_t)(t * 4 + p) * a.seg_bytes,
+                                              pl + ((size_t)p * a.plane_recs + rec0) * 16,
+                                              a.seg_bytes, &ufull[b]);
+                        }
+                        const unsigned char *ws =
+                            wsrc + ((size_t)rc * a.l + i0) * a.wrow_bytes;
+                        const uint32_t wb = (uint32_t)ntr * a.wrow_bytes;
+                        unsigned char *wd = ub + (size_t)a.TR * 4 * a.seg_bytes;
+                        for (uint32_t off = 0; off < wb; off += 32768u)
+                            ptx::bulk_g2s(wd + off, ws + off, wb - off < 32768u ? wb - off : 32768u,
+                                          &ufull[b]);
+                        if (++b == a.HB) {
+                            b = 0;
+                            uph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == TT_MMA_WARP) {
+        // ================================ MMA issuer ================================
+        const uint32_t sb = ptx::smem_u32(smem_raw);
+        const uint32_t idesc = ptx::idesc_tf32(128, a.LN);
+        const uint32_t lo_units = (2 * a.seg_bytes) >> 4;
+        const uint32_t blo_units = (uint32_t)(a.LN * 32) >> 4;
+        int b = 0, buf = 0;
+        uint32_t uph = 0, tph = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tempty[buf], tph ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t dbase = tmem + (uint32_t)(buf * MT * a.LN);
+            for (int u = 0, i0 = 0; u < units; ++u) {
+                const int ntr = min(a.TR, a.l - i0);
+                ptx::mbar_wait(&ufull[b], uph);
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                    const uint32_t ub = sb + (uint32_t)b * a.ubytes;
+                    const uint32_t wb = ub + (uint32_t)a.TR * 4 * a.seg_bytes;
+                    for (int t = 0; t < ntr; ++t) {
+                        const uint64_t a0 = ptx::smem_desc(ub + (uint32_t)t * 4 * a.seg_bytes,
+                                                           a.seg_bytes, 128);
+                        const uint64_t bh = ptx::smem_desc(wb + (uint32_t)t * a.wrow_bytes, 128, 256);
+                        const uint32_t acc0 = (u | t) != 0;
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const uint64_t ad = a0 + (uint64_t)(mt * a.S);
+                            const uint32_t dd = dbase + (uint32_t)(mt * a.LN);
+                            ptx::mma_tf32_ss(dd, ad, bh, idesc, acc0);
+                            ptx::mma_tf32_ss(dd, ad, bh + blo_units, idesc, 1);
+                            ptx::mma_tf32_ss(dd, ad + lo_units, bh, idesc, 1);
+                        }
+                    }
+                    ptx::mma_commit(&uempty[b]);
+                }
+                __syncwarp();
+                if (++b == a.HB) {
+                    b = 0;
+                    uph ^= 1;
+                }
+                i0 += a.TR;
+                if (i0 >= a.l) i0 = 0;
+            }
+            if (ptx::elect_one()) ptx::mma_commit(&tfull[buf]);
+            __syncwarp();
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1;
+            }
+        }
+    } else {
+        // ================================ epilogue ================================
+        const int q = warp;  // 0..3 = TMEM lane quarter
+        const int r = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const long long ostride = (long long)a.Ho * a.Wo;
+        int buf = 0;
+        uint32_t tph = 0;
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            const int img = tile / a.tiles_per_img;
+            const int f0 = (tile - img * a.tiles_per_img) * MT * a.S;
+            ptx::mbar_wait_sleep(&tfull[buf], tph);
+            ptx::tc_fence_after();
+            const long long img_off = (long long)img * a.Q * ostride;
+            for (int mt = 0; mt < MT; ++mt) {
+                const int p = f0 + mt * a.S + r;
+                const int u = p / a.Wv, v = p - u * a.Wv;
+                const bool inside = r < a.S && p < a.flat_len && v < a.Wo;
+                const long long pix = img_off + (long long)u * a.Wo + v;
+                const uint32_t dcol = tmem + lane_off + (uint32_t)((buf * MT + mt) * a.LN);
+                for (int o0 = 0; o0 < a.Npad; o0 += 16) {
+                    // all l taps' columns of this chunk: l TMEM loads, one wait; publish
+                    // rows; one barrier; gather rows r + j*d; one barrier (reuse)
+                    float acc[16];
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) acc[t] = 0.f;
+                    // gate operands (data gradient) requested now, consumed after the exchange
+                    const long long off0 = pix + (long long)o0 * ostride;
+                    const int nq = min(16, a.Q - o0);
+                    float aux[16];
+#pragma unroll
+                    for (int t = 0; t < 16; ++t)
+                        aux[t] = (BWD && a.gate && inside && t < nq)
+                                     ? __ldg(a.gate + off0 + t * ostride) : 0.f;
+#pragma unroll
+                    for (int j = 0; j < TT_MAX_L; ++j) {
+                        if (j >= a.l) break;
+                        uint32_t rv[16];
+                        ptx::tmem_ld16(dcol + (uint32_t)(j * a.Npad + o0), rv);
+                        ptx::tmem_wait_ld();
+                        float *xs = s_x + j * 16 * 160;
+#pragma unroll
+                        for (int t = 0; t < 16; ++t) xs[t * 160 + r] = __uint_as_float(rv[t]);
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < TT_MAX_L; ++j) {
+                        if (j >= a.l) break;
+                        const int rr = r + j * a.d;  // < 128 + 32 whenever r < S
+                        if (rr < 160) {
+                            const float *xs = s_x + j * 16 * 160 + rr;
+#pragma unroll
+                            for (int t = 0; t < 16; ++t) acc[t] += xs[t * 160];
+                        }
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (!inside) continue;
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) {
+                        if (t >= nq) break;
+                        float val = acc[t];
+                        if (!BWD)
+                            val = tt_act(val + s_bias[o0 + t], a.act);
+                        else if (a.gate)
+                            val = gate_from_output(val, aux[t], a.gate_kind);
+                        a.out[off0 + t * ostride] = val;
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1;
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == TT_MMA_WARP) ptx::tmem_dealloc<512>(tmem);
+}
+
+// NCHW (n, R, Hin, Win) -> per (n, chunk) four planes of 16-byte records over the virtual
+// grid (Hv = Hin + 2 pad, Wv = Win + 2 pad; zeros outside the input and past Hv*Wv up to
+// plane_recs): [hi c0-3 | hi c4-7 | lo c0-3 | lo c4-7].
+__global__ void __launch_bounds__(256) tc_relayout(const float *__restrict__ in,
+                                                   float4 *__restrict__ xr, int R, int Hin,
+                                                   int Win, int Wv, int pad, int n_rc,
+                                                   long long plane_recs, long long vrecs,
+                                                   long long total) {
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long nrc = idx / plane_recs;
+        const long long f = idx - nrc * plane_recs;
+        const int rc = (int)(nrc % n_rc);
+        const long long n = nrc / n_rc;
+        float v[8];
+        const long long yv = f / Wv;
+        const int y = (int)yv - pad, x = (int)(f - yv * Wv) - pad;
+        const bool ok = f < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win;
+        const float *src = in + ((n * R + rc * 8) * Hin + (ok ? y : 0)) * (long long)Win + (ok ? x : 0);
+        const long long cs = (long long)Hin * Win;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (ok && rc * 8 + k < R) ? __ldg(src + k * cs) : 0.f;
+        float4 *dst = xr + nrc * 4 * plane_recs + f;
+        dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+        dst[plane_recs] = make_float4(v[4], v[5], v[6], v[7]);
+        dst[2 * plane_recs] = make_float4(ptx::tf32_lo(v[0]), ptx::tf32_lo(v[1]),
+                                          ptx::tf32_lo(v[2]), ptx::tf32_lo(v[3]));
+        dst[3 * plane_recs] = make_float4(ptx::tf32_lo(v[4]), ptx::tf32_lo(v[5]),
+                                          ptx::tf32_lo(v[6]), ptx::tf32_lo(v[7]));
+    }
+}
+
+// weights W(q, r, i, j) -> per (chunk rc, tap row i): [hi | lo] tiles of LN = l*Npad rows
+// (row n = j*Npad + q) x K = 8 channels, K-major core-matrix layout
+// (n>>3)*256 + (k>>2)*128 + (n&7)*16 + (k&3)*4; bwd: W is (R = cout, Q = cin, l, l) rotated.
+__global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp, int Q, int R,
+                            int l, int Npad, int n_rc, int bwd) {
+    const int LN = l * Npad;
+    const long long total = (long long)n_rc * l * 2 * LN * 8;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(idx & 7);
+        const long long rest = idx >> 3;
+        const int n = (int)(rest % LN);
+        const long long r2 = rest / LN;
+        const int hl = (int)(r2 & 1);
+        const long long ri = r2 >> 1;  // rc * l + i
+        const int i = (int)(ri % l), rc = (int)(ri / l);
+        const int j = n / Npad, qo = n - j * Npad;
+        const int c = rc * 8 + k;
+        float v = 0.f;
+        if (qo < Q && c < R) {
+            if (!bwd)
+                v = w[(((long long)qo * R + c) * l + i) * l + j];
+            else
+                v = w[(((long long)c * Q + qo) * l + (l - 1 - i)) * l + (l - 1 - j)];
+        }
+        if (hl) v = ptx::tf32_lo(v);
+        const long long byte = (ri * 2 + hl) * (long long)LN * 32 + (n >> 3) * 256 + (k >> 2) * 128 +
+                               (n & 7) * 16 + (k & 3) * 4;
+        wp[byte / 4] = v;
+    }
+}
+
+// --------------------------------------------------------------------------------
+// host side
+// --------------------------------------------------------------------------------
+struct TtPlan {
+    int Npad, LN, n_rc, MT, S, NR, TR, n_tr, HB;
+    bool ok;
+    uint32_t seg_bytes, wrow_bytes, ubytes, xbytes;
+    size_t wbytes;
+};
+
+static TtPlan tt_plan(int R, int Q, int l, int d, int max_mt) {
+    TtPlan p;
+    p.ok = false;
+    p.Npad = (Q + 15) / 16 * 16;
+    p.LN = l * p.Npad;
+    p.n_rc = (R + 7) / 8;
+    p.S = 128 - (l - 1) * d;
+    if (p.LN > 256 || p.S < 32 || p.Npad > 256) return p;
+    int mt = 256 / p.LN;
+    if (mt > 4) mt = 4;
+    if (const char *e = getenv("DP_TT_MT")) {
+        int v = atoi(e);
+        if (v >= 1 && v < mt) mt = v;
+    }
+    if (max_mt >= 1 && mt > max_mt) mt = max_mt;
+    if (mt < 1) return p;
+    p.MT = mt;
+    p.NR = ((mt - 1) * p.S + 128 + 7) / 8 * 8;
+    p.seg_bytes = (uint32_t)p.NR * 16;
+    p.wrow_bytes = (uint32_t)(2 * p.LN * 32);
+    p.wbytes = (size_t)p.n_rc * l * p.wrow_bytes;
+    if (l > TT_MAX_L) return p;
+    // tap rows per unit: as many as leave room for 2 unit buffers next to the exchange area
+    p.xbytes = (uint32_t)l * 16 * 160 * 4;
+    const size_t budget = (size_t)TT_SMEM_TOTAL - p.xbytes - 2048;
+    p.TR = 0;
+    for (int tr = l; tr >= 1; --tr) {
+        const size_t ub = ((size_t)tr * (4 * p.seg_bytes + p.wrow_bytes) + 127) / 128 * 128;
+        if (2 * ub <= budget) {
+            p.TR = tr;
+            p.ubytes = (uint32_t)ub;
+            break;
+        }
+    }
+    if (p.TR == 0) return p;
+    p.n_tr = (l + p.TR - 1) / p.TR;
+    long long hb = (long long)budget / p.ubytes;
+    p.HB = (int)(hb > TT_MAX_HB ? TT_MAX_HB : hb);
+    p.ok = p.HB >= 2 && (p.seg_bytes >> 4) < (1u << 14);
+    return p;
+}
+
+
+// workspace: packed weights, then the relayout planes
+static size_t tt_relayout_recs(int Hin, int Win, int pad, int l, int d, const TtPlan &p,
+                               long long &plane_recs, int &tiles_per_img, long long &flat_len,
+                               int Ho, int Wo) {
+    const int Wv = Win + 2 * pad, Hv = Hin + 2 * pad;
+    flat_len = (long long)(Ho - 1) * Wv + Wo;
+    tiles_per_img = (int)((flat_len + (long long)p.MT * p.S - 1) / ((long long)p.MT * p.S));
+    // the last tile's windows reach f0 + (l-1)*d*Wv + NR
+    long long need = (long long)(tiles_per_img - 1) * p.MT * p.S + (long long)(l - 1) * d * Wv + p.NR;
+    long long vrecs = (long long)Hv * Wv;
+    plane_recs = (need > vrecs ? need : vrecs);
+    plane_recs = (plane_recs + 7) / 8 * 8;
+    return (size_t)plane_recs;
+}
+
+size_t tt_conv_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad, int Ho,
+                         int Wo) {
+    if (getenv("DP_TC_FLAT")) return 0;  // force the flat kernel (experiments)
+    TtPlan p = tt_plan(R, Q, l, d, 0);
+    if (!p.ok || Ho < 1 || Wo < 1) return 0;
+    // Only where it wins (measured, c2 at batch 16, kernel + relayout vs the flat kernel):
+    // with >= 3 M tiles per CTA tile the per-tile weight rows and the (l-1)d overlap are
+    // amortised (conv3 fwd 213 vs 327 us, conv2 data grad 303 vs 449 us); at MT <= 2 the
+    // l*Npad-wide weight rows re-streamed per tile and the 64 B/pixel/tap-row record
+    // copies cost more than the saved A reads (conv1/conv2 fwd, conv3 data grad lose).
+    // DP_TT_ALL uses it wherever it applies (experiments).
+    if (p.MT < 3 && !getenv("DP_TT_ALL")) return 0;
+    long long plane_recs, flat_len;
+    int tpi;
+    tt_relayout_recs(Hin, Win, pad, l, d, p, plane_recs, tpi, flat_len, Ho, Wo);
+    const size_t wb = (p.wbytes + 255) / 256 * 256;
+    return wb + (size_t)n * p.n_rc * 4 * plane_recs * 16;
+}
+
+static int g_tt_sms = 0;
+
+int tt_launch(const float *in, const float *w, const float *bias, float *out, const float *gate,
+              int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
+              int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st) {
+    TtPlan p = tt_plan(R, Q, l, d, 0);
+    if (!p.ok)
+        return set_error(DP_ERR_UNSUPPORTED, "tap-stacked conv: unsupported (R=%d Q=%d k=%d d=%d)",
+                         R, Q, l, d);
+    long long plane_recs, flat_len;
+    int tiles_per_img;
+    tt_relayout_recs(Hin, Win, pad, l, d, p, plane_recs, tiles_per_img, flat_len, Ho, Wo);
+    const size_t wb = (p.wbytes + 255) / 256 * 256;
+    const size_t need = wb + (size_t)n * p.n_rc * 4 * plane_recs * 16;
+    if (ws == nullptr || ws_bytes < need)
+        return set_error(DP_ERR_ARG, "tap-stacked conv: workspace %zu < %zu bytes", ws_bytes, need);
+    if (((uintptr_t)ws & 255) != 0)
+        return set_error(DP_ERR_ARG, "tap-stacked conv: workspace must be 256-byte aligned");
+    if (flat_len > 0x7fffffffLL || plane_recs > 0x7fffffffLL)
+        return set_error(DP_ERR_UNSUPPORTED, "tap-stacked conv: image too large");
+    float *wp = (float *)ws;
+    float4 *xr = (float4 *)((unsigned char *)ws + wb);
+    {
+        const long long total = (long long)p.n_rc * l * 2 * p.LN * 8;
+        long long g = (total + 255) / 256;
+        tc_pack_tap<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, wp, Q, R, l, p.Npad, p.n_rc,
+                                                                bwd ? 1 : 0);
+        int rc = check_launch("tc_pack_tap");
+        if (rc) return rc;
+    }
+    {
+        const int Wv = Win + 2 * pad;
+        const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
+        const long long total = (long long)n * p.n_rc * plane_recs;
+        long long g = (total + 255) / 256;
+        tc_relayout<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
+            in, xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
+        int rc = check_launch("tc_relayout");
+        if (rc) return rc;
+    }
+    if (g_tt_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_tt_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_tt_sms <= 0) g_tt_sms = 148;
+    }
+    TtArgs a;
+    a.xr = (const float *)xr;
+    a.wpack = wp;
+    a.bias = bias;
+    a.out = out;
+    a.gate = gate;
+    a.n_rc = p.n_rc;
+    a.l = l;
+    a.d = d;
+    a.Q = Q;
+    a.Npad = p.Npad;
+    a.LN = p.LN;
+    a.MT = p.MT;
+    a.S = p.S;
+    a.NR = p.NR;
+    a.TR = p.TR;
+    a.n_tr = p.n_tr;
+    a.Wv = Win + 2 * pad;
+    a.Ho = Ho;
+    a.Wo = Wo;
+    a.act = act;
+    a.gate_kind = gate_kind;
+    a.plane_recs = plane_recs;
+    a.flat_len = (int)flat_len;
+    a.tiles_per_img = tiles_per_img;
+    const long long tt = (long long)n * tiles_per_img;
+    if (tt > 0x7fffffff) return set_error(DP_ERR_UNSUPPORTED, "tap-stacked conv: too many tiles");
+    a.total_tiles = (int)tt;
+    a.HB = p.HB;
+    a.seg_bytes = p.seg_bytes;
+    a.wrow_bytes = p.wrow_bytes;
+    a.ubytes = p.ubytes;
+    if (a.total_tiles == 0) return DP_OK;
+    const int grid = a.total_tiles < g_tt_sms ? a.total_tiles : g_tt_sms;
+    a.xoff = (uint32_t)p.HB * p.ubytes;
+    const size_t smem = (size_t)a.xoff + p.xbytes;
+    void (*kern)(const TtArgs) = bwd ? tc_conv_tap_kernel<true> : tc_conv_tap_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+        return set_error(DP_ERR_CUDA, "tc_conv_tap: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    kern<<<grid, TT_THREADS, smem, st>>>(a);
+    return check_launch("tc_conv_tap_kernel");
+}
+
+}  // namespace dp

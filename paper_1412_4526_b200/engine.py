@@ -125,6 +125,18 @@ class ops:
         return int(_lib_dev().dp_conv_fast_workspace(reduce_c, out_c, k))
 
     @staticmethod
+    def fwd_fast_workspace(x, co, k, d) -> int:
+        """Bytes that select the fastest forward kernel for this exact call (tap-stacked:
+        packed weights + the input re-laid out as hi/lo channel-quad records)."""
+        n, ci, h, w = x.shape
+        return int(_lib_dev().dp_conv_forward_fast_workspace(n, ci, h, w, co, k, d))
+
+    @staticmethod
+    def bwd_fast_workspace(dy, ci, k, d) -> int:
+        n, co, ho, wo = dy.shape
+        return int(_lib_dev().dp_conv_backward_data_fast_workspace(n, co, ho, wo, ci, k, d))
+
+    @staticmethod
     def conv_forward_fast(x, w, b, y, k, d, nonlin, ws):
         with _Rec('conv_forward_tc', 2, 'tensor', 2 * y.numel() * x.shape[1] * k * k):
             n, ci, h, wd = x.shape
@@ -449,10 +461,12 @@ class DenseNet:
                 f_ok = ops.fast_supported(ci, co, kk, dd)
                 b_ok = train and gi > 0 and ops.fast_supported(co, ci, kk, dd)
                 self.tc[gi] = (f_ok, b_ok)
+                # one workspace shared by every fast conv call (they run in sequence on one
+                # stream), sized for the tap-stacked kernels' relayout planes
                 if f_ok:
-                    tc_ws = max(tc_ws, ops.fast_workspace(ci, co, kk))
+                    tc_ws = max(tc_ws, ops.fwd_fast_workspace(self._group_input(gi), co, kk, dd))
                 if b_ok:
-                    tc_ws = max(tc_ws, ops.fast_workspace(co, ci, kk))
+                    tc_ws = max(tc_ws, ops.bwd_fast_workspace(self.acts[gi], ci, kk, dd))
         self._tc_ws = torch.empty(tc_ws, dtype=torch.uint8, device=self.device)
         self.graph = None
 

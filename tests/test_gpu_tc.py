@@ -40,9 +40,12 @@ def _rel(a, b):
     return float((a - b).abs().max() / max(b.abs().max(), 1e-30))
 
 
+@pytest.mark.parametrize("kernel", ["flat", "tap"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("act", [0, 1, 2])
-def test_tc_forward_matches_exact(shape, act):
+def test_tc_forward_matches_exact(shape, act, kernel):
+    """kernel="tap" passes the shape-aware workspace, which selects the tap-stacked kernel
+    where it applies (else the flat one runs again)."""
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
@@ -56,16 +59,18 @@ def test_tc_forward_matches_exact(shape, act):
     y_ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda")
     y = torch.full_like(y_ref, float("nan"))
     ops.conv_forward(x, wt, b, y_ref, k, d, act)
-    ws = torch.empty(ops.fast_workspace(ci, co, k), dtype=torch.uint8, device="cuda")
+    nb = ops.fast_workspace(ci, co, k) if kernel == "flat" else ops.fwd_fast_workspace(x, co, k, d)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     ops.conv_forward_fast(x, wt, b, y, k, d, act, ws)
     torch.cuda.synchronize()
     assert torch.isfinite(y).all()
     assert _rel(y, y_ref) < TOL
 
 
+@pytest.mark.parametrize("kernel", ["flat", "tap"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("gate_kind", [None, 1, 2])
-def test_tc_backward_data_matches_exact(shape, gate_kind):
+def test_tc_backward_data_matches_exact(shape, gate_kind, kernel):
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
@@ -82,7 +87,8 @@ def test_tc_backward_data_matches_exact(shape, gate_kind):
     dx_ref = torch.empty((n, ci, h, w), device="cuda")
     dx = torch.full_like(dx_ref, float("nan"))
     ops.conv_backward_data(dy, wt, dx_ref, k, d, gate, gate_kind or 0)
-    ws = torch.empty(ops.fast_workspace(co, ci, k), dtype=torch.uint8, device="cuda")
+    nb = ops.fast_workspace(co, ci, k) if kernel == "flat" else ops.bwd_fast_workspace(dy, ci, k, d)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     ops.conv_backward_data_fast(dy, wt, dx, k, d, ws, gate, gate_kind or 0)
     torch.cuda.synchronize()
     assert torch.isfinite(dx).all()

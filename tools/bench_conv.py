@@ -53,12 +53,12 @@ def main():
         t_exb = timeit(lambda: ops.conv_backward_data(dy, w, dx, k, d))
         line = f"{name}: fwd exact {t_ex:.3f} ms ({flops / t_ex / 1e9:.1f} TF/s)"
         if ops.fast_supported(ci, co, k, d):
-            ws = torch.empty(ops.fast_workspace(ci, co, k), dtype=torch.uint8, device="cuda")
+            ws = torch.empty(ops.fwd_fast_workspace(x, co, k, d) if os.environ.get("TAP", "1") == "1" else ops.fast_workspace(ci, co, k), dtype=torch.uint8, device="cuda")
             t_tc = timeit(lambda: ops.conv_forward_fast(x, w, b, y, k, d, 1, ws))
             line += f" | fwd tc {t_tc:.3f} ms ({flops / t_tc / 1e9:.1f} TF/s)"
         line += f" | dgrad exact {t_exb:.3f} ms ({flops / t_exb / 1e9:.1f} TF/s)"
         if ops.fast_supported(co, ci, k, d):
-            wsb = torch.empty(ops.fast_workspace(co, ci, k), dtype=torch.uint8, device="cuda")
+            wsb = torch.empty(ops.bwd_fast_workspace(dy, ci, k, d) if os.environ.get("TAP", "1") == "1" else ops.fast_workspace(co, ci, k), dtype=torch.uint8, device="cuda")
             t_tcb = timeit(lambda: ops.conv_backward_data_fast(dy, w, dx, k, d, wsb))
             line += f" | dgrad tc {t_tcb:.3f} ms ({flops / t_tcb / 1e9:.1f} TF/s)"
         print(line, flush=True)

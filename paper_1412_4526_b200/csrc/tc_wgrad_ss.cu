@@ -11,11 +11,11 @@
 // x tap lines.  tc_stage_x lays x out as (n, h, c, wp) copies shifted left by
 // b = (j*d) & 3 for each residue b that occurs, so that for one residue copy the taps j with
 // that residue sit at columns v0 + j*d - b, all multiples of 4 floats, lcm(d, 4) floats
-// apart -- a legal TMA stride.  One 4-D box {32 px, taps of the residue, Cpad channels,
+// apart -- a legal TMA stride.  One 4-D box {32 px, taps of the residue, cin channels,
 // 1 row} therefore delivers, for ONE input row, every (c, j) line of 32 pixels as a 128-byte
 // SWIZZLE_128B row: exactly the canonical K-major A layout the tensor core reads (SBO = 1024,
-// +32 B per K=8 slice).  All residue boxes of an input row form one ring slot of
-// Ls = Cpad * l lines.
+// +32 B per K=8 slice).  All residue boxes of an input row form one ring slot of Ls lines
+// (each box rounded up to 8 lines; cin * l when cin % 8 == 0).
 //
 // Row ring.  A CTA walks K blocks down image columns (u, u+d, u+2d, ... for one 32-px block
 // and row phase u mod d).  Consecutive blocks share l-1 of their l tap rows (rows u + i*d),
@@ -412,7 +412,7 @@ struct WsPlan {
     long long kb_total;
     WsResidues rs;
     size_t part_bytes, pdb_bytes, copy_bytes, x_bytes, dy_bytes, total_bytes;
-    uint32_t b_bytes, slot_bytes;
+    uint32_t b_bytes, slot_bytes, box_tx_row;
 };
 
 static size_t ws_align256(size_t v) { return (v + 255) / 256 * 256; }
@@ -427,7 +427,16 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     if (p.Npad > 128) return false;
     p.Cpad = (cin + 7) / 8 * 8;
     if (p.Cpad > 256) return false;
-    p.Ls = p.Cpad * k;
+    // lines per ring slot (one input row): residue boxes, each rounded up to 8 lines
+    {
+        int ls = 0;
+        for (int b = 0; b < 4; ++b) {
+            int cnt = 0;
+            for (int j = 0; j < k; ++j) cnt += ((j * d) & 3) == b;
+            if (cnt) ls += (cin * cnt + 7) / 8 * 8;
+        }
+        p.Ls = ls;
+    }
     const int lines = k * p.Ls;
     p.n_tiles = (lines + 127) / 128;
     const int acc_cols = 2 * p.Npad;
@@ -474,14 +483,18 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
         p.rs.n[rb] = cnt;
         p.rs.j0[rb] = j0;
         p.rs.line0[rb] = line0;
-        line0 += p.Cpad * cnt;
+        // a residue's box holds cin * cnt real lines; the next box starts on a 1024-byte
+        // (8-line) boundary (SWIZZLE_128B).  The gap lines are never written: they only
+        // feed their own (discarded) accumulator rows.
+        line0 += (cin * cnt + 7) / 8 * 8;
         p.mask |= 1 << b;
     }
     for (int rb = p.rs.n_b; rb < 4; ++rb) {
         p.rs.b[rb] = -1;
         p.rs.n[rb] = p.rs.j0[rb] = p.rs.line0[rb] = 0;
     }
-    p.slot_bytes = (uint32_t)p.Ls * 128u;  // Cpad multiple of 8: 1024-byte aligned boxes
+    p.slot_bytes = (uint32_t)p.Ls * 128u;  // multiple of 8 lines: 1024-byte aligned boxes
+    p.box_tx_row = (uint32_t)cin * k * 128u;  // bytes the residue boxes of one row deliver
     p.b_bytes = 2u * (uint32_t)p.Npad * 128u;
     int SS = WS_MAX_SS;
     auto smem_for = [&](int ss) {
@@ -570,7 +583,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
         cuuint64_t dims[4] = {(cuuint64_t)p.wp_x, (cuuint64_t)p.rs.n[used], (cuuint64_t)cin,
                               (cuuint64_t)n * hi};
         cuuint64_t str[3] = {(cuuint64_t)p.rs.step * d * 4, xrow, ximg_row};
-        cuuint32_t box[4] = {32, (cuuint32_t)p.rs.n[used], (cuuint32_t)p.Cpad, 1};
+        cuuint32_t box[4] = {32, (cuuint32_t)p.rs.n[used], (cuuint32_t)cin, 1};
         rc = wg_make_map(&mx[rb], base, 4, dims, str, box, true);
         if (rc) return rc;
     }
@@ -596,7 +609,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.Ls = p.Ls;
     a.b_bytes = p.b_bytes;
     a.slot_bytes = p.slot_bytes;
-    a.box_tx_row = p.slot_bytes;
+    a.box_tx_row = p.box_tx_row;
     a.ring_hi = (uint32_t)p.SS * p.b_bytes;
     a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
     a.rs = p.rs;

@@ -25,6 +25,9 @@ template <typename T>
 int conv_backward_kernel_t(const T *, const T *, T *, T *, int, int, int, int, int, int, int,
                            void *, size_t, cudaStream_t);
 size_t wgrad_workspace_bytes(int elem, int n, int cin, int hi, int wi, int cout, int k, int d);
+template <typename T>
+int conv_backward_kernel_seq_t(const T *x, const T *dy, T *dw, T *db, int cin, int hi, int wi,
+                               int cout, int k, int d, cudaStream_t st);
 size_t tc_conv_workspace(int R, int Q, int l);
 size_t tc_conv_fwd_workspace(int n, int cin, int h, int w, int cout, int k, int d);
 size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, int d);
@@ -538,18 +541,23 @@ int dp_host_conv_backward_kernel(int dtype, const void *x, const void *dy, void 
     DP_TRY(host_stream(&st));
     size_t es = esize(dtype);
     int e = (k - 1) * d + 1, ho = hi - e + 1, wo = wi - e + 1;
-    size_t wsb = dp_conv_backward_kernel_workspace(dtype, 1, cin, hi, wi, cout, k, d);
     int rc;
     {
+        // per-image drop-in: the reference's own summation order (bit-identical), not the
+        // batched split-K kernel
         DevBufs B(st);
-        void *ddx, *ddy, *ddw, *ddb, *ws;
+        void *ddx, *ddy, *ddw, *ddb;
         DP_TRY(B.up(x, es * cin * hi * wi, &ddx));
         DP_TRY(B.up(dy, es * cout * ho * wo, &ddy));
         DP_TRY(B.alloc(es * cout * cin * k * k, &ddw));
         DP_TRY(B.alloc(es * cout, &ddb));
-        DP_TRY(B.alloc(wsb, &ws));
-        rc = dp_conv_backward_kernel(dtype, ddx, ddy, ddw, ddb, 1, cin, hi, wi, cout, k, d, ws,
-                                     wsb, st);
+        rc = dtype == DP_F32
+                 ? conv_backward_kernel_seq_t<float>((const float *)ddx, (const float *)ddy,
+                                                     (float *)ddw, (float *)ddb, cin, hi, wi, cout,
+                                                     k, d, st)
+                 : conv_backward_kernel_seq_t<double>((const double *)ddx, (const double *)ddy,
+                                                      (double *)ddw, (double *)ddb, cin, hi, wi,
+                                                      cout, k, d, st);
         if (!rc) rc = down(dw, ddw, es * cout * cin * k * k, st);
         if (!rc) rc = down(db, ddb, es * cout, st);
     }

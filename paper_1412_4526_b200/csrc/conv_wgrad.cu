@@ -158,6 +158,61 @@ static WgradSplit wgrad_split(int n, int cin, int cout, int ho, int wo, int k) {
     return {(int)S, chunk};
 }
 
+// Reference-order weight gradient for ONE image (the drop-in dp_host_* entry point):
+// every dw[o,c,i,j] (and db[o]) is one sequential sum over (u, v) row-major, each product
+// rounded then added (no FMA) -- exactly the compiled reference's loop
+// (_kernels.pyx:112-128, -ffp-contract=off), so the result is bit-identical.  One thread
+// per output entry; consecutive threads take consecutive taps so the x reads of a warp
+// share lines and dy[o,u,v] is a broadcast.
+template <typename T>
+__global__ void __launch_bounds__(128) wgrad_seq_kernel(const T *__restrict__ x,
+                                                        const T *__restrict__ dy,
+                                                        T *__restrict__ dw, T *__restrict__ db,
+                                                        int C, int Hi, int Wi, int O, int Ho,
+                                                        int Wo, int l, int d) {
+    const long long ncl = (long long)C * l * l;
+    const long long total = (long long)O * ncl + O;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    if (idx >= (long long)O * ncl) {  // db[o]
+        const int o = (int)(idx - (long long)O * ncl);
+        const T *g = dy + (long long)o * Ho * Wo;
+        T s = T(0);
+        for (long long q = 0; q < (long long)Ho * Wo; ++q) s = add_rn(s, g[q]);
+        db[o] = s;
+        return;
+    }
+    const int o = (int)(idx / ncl);
+    const int rem = (int)(idx - (long long)o * ncl);
+    const int c = rem / (l * l), t = rem - c * l * l;
+    const int i = t / l, j = t - i * l;
+    const T *g = dy + (long long)o * Ho * Wo;
+    const T *xs = x + ((long long)c * Hi + (long long)i * d) * Wi + (long long)j * d;
+    T s = T(0);
+    for (int u = 0; u < Ho; ++u) {
+        const T *gr = g + (long long)u * Wo;
+        const T *xr = xs + (long long)u * Wi;
+        for (int v = 0; v < Wo; ++v) s = add_rn(s, mul_rn(__ldg(gr + v), __ldg(xr + v)));
+    }
+    dw[idx] = s;
+}
+
+template <typename T>
+int conv_backward_kernel_seq_t(const T *x, const T *dy, T *dw, T *db, int cin, int hi, int wi,
+                               int cout, int k, int d, cudaStream_t st) {
+    const int e = (k - 1) * d + 1;
+    const int ho = hi - e + 1, wo = wi - e + 1;
+    const long long total = (long long)cout * cin * k * k + cout;
+    wgrad_seq_kernel<T><<<ceil_div(total, 128), 128, 0, st>>>(x, dy, dw, db, cin, hi, wi, cout,
+                                                               ho, wo, k, d);
+    return check_launch("wgrad_seq_kernel");
+}
+template int conv_backward_kernel_seq_t<float>(const float *, const float *, float *, float *, int,
+                                               int, int, int, int, int, cudaStream_t);
+template int conv_backward_kernel_seq_t<double>(const double *, const double *, double *,
+                                                double *, int, int, int, int, int, int,
+                                                cudaStream_t);
+
 size_t wgrad_workspace_bytes(int elem, int n, int cin, int hi, int wi, int cout, int k, int d) {
     int e = (k - 1) * d + 1;
     WgradSplit sp = wgrad_split(n, cin, cout, hi - e + 1, wi - e + 1, k);

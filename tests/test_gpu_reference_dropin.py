@@ -1,0 +1,111 @@
+"""Drop-in proof: the UNMODIFIED reference package driven through its own public API with this
+repo's backend registered exactly as INTEGRATION.md section 2 shows
+(``denseprop.backend._BACKENDS["cuda"] = paper_1412_4526_b200.cuda_kernels``).
+
+The reference is the contract's one allowed offline install:
+``pip install --no-index --no-build-isolation --no-deps --target baseline/_ref`` of a copy of
+/root/reference/pkg (built with /usr/bin/gcc; DESIGN.md records the recipe).  baseline/_ref is
+git-ignored but travels to the GPU box.  Every kernel call the reference makes
+(``backend.kernels()`` in forward.py / backward.py) lands on the sm_100a exact tier.
+
+* the reference's dense_forward / dense_backward with backend "cuda" are bit-identical to
+  the same calls with its own compiled backend, fp32 and fp64;
+* the reference's own differential check (check.run_check: dense vs patch-by-patch scan vs
+  finite differences, its TOLERANCES) passes with backend "cuda".
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not os.path.isdir(os.path.join(REF, "denseprop")):
+        pytest.skip("reference package not installed into baseline/_ref")
+    sys.path.insert(0, REF)
+    try:
+        import denseprop
+        from denseprop import backend
+    finally:
+        sys.path.remove(REF)
+    if "compiled" not in backend.available():
+        pytest.skip("reference compiled backend did not import")
+    from paper_1412_4526_b200 import cuda_kernels
+    backend._BACKENDS["cuda"] = cuda_kernels
+    prev = backend.active()
+    yield denseprop
+    backend.use(prev)
+
+
+def _nets(ref):
+    from denseprop import fixtures
+    return {
+        "example": fixtures.example_net_text(seed=3),
+        "plain_small": fixtures.plain_cnn1_text(seed=5, channels=(6, 7, 4)),
+        "rcnn3": fixtures.rcnn3_chain_text(seed=2),
+    }
+
+
+def _run(ref, name, text, side, dtype, backend_name):
+    from denseprop import backend
+    from denseprop.backward import ErrorMask, dense_backward
+    from denseprop.forward import dense_forward
+    from denseprop.netspec import parse_spec
+    from denseprop.plan import compile_plan
+
+    backend.use(backend_name)
+    spec = parse_spec(text)
+    plan = compile_plan(spec)
+    rng = np.random.default_rng(11)
+    image = rng.uniform(-0.5, 0.5, (spec.input_channels, side, side)).astype(dtype)
+    cache = dense_forward(plan, image, 4)
+    delta = rng.uniform(-1, 1, cache.output.shape).astype(dtype)
+    flat = rng.choice(side * side, size=max(1, side * side // 10), replace=False)
+    mask = ErrorMask.of(side, side, [(int(i) // side, int(i) % side) for i in flat])
+    grads = dense_backward(plan, cache, delta, mask, 4, with_input_grad=True)
+    return cache, grads
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("name", ["example", "plain_small", "rcnn3"])
+def test_reference_api_bit_identical_with_cuda_backend(ref, name, dtype):
+    text = _nets(ref)[name]
+    side = 24
+    c_cache, c_grads = _run(ref, name, text, side, dtype, "compiled")
+    g_cache, g_grads = _run(ref, name, text, side, dtype, "cuda")
+    assert np.array_equal(c_cache.output, g_cache.output)
+    for a, b in zip(c_cache.inputs, g_cache.inputs):
+        assert np.array_equal(a, b)
+    assert c_cache.argmax.keys() == g_cache.argmax.keys()
+    for k in c_cache.argmax:
+        assert np.array_equal(c_cache.argmax[k], g_cache.argmax[k])
+    for k in range(len(c_grads.kernel)):
+        if c_grads.kernel[k] is None:
+            assert g_grads.kernel[k] is None
+            continue
+        assert np.array_equal(c_grads.kernel[k], g_grads.kernel[k]), f"dw layer {k}"
+        assert np.array_equal(c_grads.bias[k], g_grads.bias[k]), f"db layer {k}"
+    assert np.array_equal(c_grads.input_delta, g_grads.input_delta)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_reference_check_passes_with_cuda_backend(ref, dtype):
+    """check.run_check (the reference CLI's `check`): dense == scan, dense grads == summed
+    patch grads, finite differences -- all through the GPU kernels."""
+    from denseprop import backend, check
+    from denseprop.netspec import parse_spec
+    backend.use("cuda")
+    spec = parse_spec(_nets(ref)["example"])
+    # side 8, seed 0: a case whose max-pool margins the check can jitter clear of ties
+    # (most sizes/seeds hit the check's own "could not jitter" guard with any backend)
+    res = check.run_check(spec, side=8, seed=0, dtype=dtype, mask_sizes=(1, 5),
+                          fd_params=32, threads=1)
+    assert res.ok, "\n".join(res.format_lines())

@@ -74,8 +74,10 @@ def _extent(k, d):
     return (k - 1) * d + 1
 
 
-def dense_forward(net: ONet, image, K=kernels_np, threads=1) -> OCache:
-    x = pad_image(net, np.ascontiguousarray(image))
+def dense_forward(net: ONet, image, K=kernels_np, threads=1, padded=False) -> OCache:
+    """padded=True: `image` is already the padded input (a row band with its halo in the
+    band-sharding tests); the reference always pads (forward.py:96-98)."""
+    x = np.ascontiguousarray(image) if padded else pad_image(net, np.ascontiguousarray(image))
     dt = x.dtype
     inputs, argmax = [], {}
     for k, (layer, d) in enumerate(zip(net.layers, net.dilations())):

@@ -504,6 +504,13 @@ class DenseNet:
         return buf[:n].view(shape)
 
     # ------------------------------------------------------------- forward
+    def set_padded_input(self, x0):
+        """x0: (N, C, h + patch - 1, w + patch - 1) device tensor that is ALREADY padded (a
+        row band of a bigger padded image in band sharding, trainer.BandParallelTrainer)."""
+        if tuple(x0.shape) != tuple(self.x0.shape):
+            raise ValueError(f"padded input {tuple(x0.shape)} != {tuple(self.x0.shape)}")
+        self.x0.copy_(x0)
+
     def set_input(self, images):
         """images: (N, C, h, w) device tensor -> zero-padded x0 (forward.py:96-98)."""
         lead, trail = self.plan.lead_margin, self.plan.trail_margin

@@ -60,6 +60,33 @@ def shard(n_images: int, rank: int, world: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+def band_assignment(n_images: int, height: int, rank: int, world: int):
+    """Fallback when images < ranks: spatial band sharding.
+
+    Ranks are split into n_images groups of `per = world // n_images`; rank r takes image
+    r // per and the balanced band (r % per) of its output rows.  Returns
+    (image, r0, r1) -- output rows [r0, r1) -- or None for the (world % n_images) ranks
+    left over, which contribute an all-zero bucket.  An output row depends on the padded
+    input rows [row, row + patch - 1] only (valid convolutions on the padded image,
+    forward.py:96-98), so a band is computed exactly from padded rows [r0, r1 + patch - 1)
+    (the (patch - 1)-row halo) and band gradients, with the mask restricted to the band,
+    sum to the full image's (unweighted-sum semantics, backward.py:190-191)."""
+    if n_images >= world:
+        raise ValueError("band sharding is the fallback for fewer images than ranks")
+    per = world // n_images
+    if rank >= per * n_images:
+        return None
+    img, band = divmod(rank, per)
+    r0 = band * height // per
+    r1 = (band + 1) * height // per
+    return img, r0, r1
+
+
+def band_rows(r0: int, r1: int, patch: int):
+    """(padded-input rows, output rows) of a band as slices."""
+    return slice(r0, r1 + patch - 1), slice(r0, r1)
+
+
 def allreduce_sum(tensor, group=None):
     """In-place SUM all-reduce of the gradient bucket (no-op when not distributed)."""
     import torch.distributed as dist
@@ -178,3 +205,54 @@ class H2DPipeline:
         self._free_recorded[k] = True
         self.tr.step()
         self._consumed += 1
+
+
+class BandParallelTrainer:
+    """Fewer images than ranks: each rank runs the engine on one (image, output-row band)
+    with its (patch - 1)-row halo of padded input (band_assignment), then the same SUM
+    all-reduce of the gradient bucket as DataParallelTrainer.  Forward-only inference
+    needs no collective: each rank's band output is a disjoint slice of the image's map."""
+
+    def __init__(self, plan: DensePlan, n_images: int, height: int, width: int,
+                 rank: int = 0, world: int = 1, lr: float = 0.0, group=None, dtype=None,
+                 precision: str = "fast"):
+        import torch.distributed as dist
+
+        from .engine import DenseNet
+        from .netspec import patch_size
+        self.patch = patch_size(plan.source)
+        self.assign = band_assignment(n_images, height, rank, world)
+        self.height, self.width = height, width
+        self.group = group
+        self.lr = lr
+        rows = (self.assign[2] - self.assign[1]) if self.assign else 1
+        self.net = DenseNet(plan, 1, rows, width, dtype=dtype, train=True, precision=precision)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.broadcast(self.net.param_flat, src=0, group=group)
+
+    def load(self, padded_images, targets, masks):
+        """padded_images: (N, C, h + patch - 1, w + patch - 1) device tensor (the engine's
+        x0 layout for the whole batch); targets (N, Q, h, w); masks (N, h, w)."""
+        n = self.net
+        if self.assign is None:
+            n.x0.zero_()
+            n.mask.zero_()
+            return
+        img, r0, r1 = self.assign
+        rin, rout = band_rows(r0, r1, self.patch)
+        n.set_padded_input(padded_images[img:img + 1, :, rin])
+        n.target.copy_(targets[img:img + 1, :, rout])
+        n.mask.copy_(masks[img:img + 1, rout])
+
+    def step(self):
+        n = self.net
+        n.forward()
+        n.loss_delta()
+        n.backward()
+        allreduce_sum(n.grad_flat, self.group)
+        if self.lr:
+            n.sgd_step(self.lr)
+
+    def forward_only(self):
+        self.net.forward()
+        return self.net.output

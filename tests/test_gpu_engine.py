@@ -389,3 +389,46 @@ def test_h2d_pipeline_matches_direct_steps(dp):
     torch.cuda.synchronize()
     for a, b in zip(got, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_band_sharding_equals_full_image(dp, precision):
+    """SURVEY.md 8(e) fallback (fewer images than ranks): the engine on each rank's
+    output-row band + (patch - 1)-row halo (trainer.BandParallelTrainer), buckets summed as
+    the all-reduce would, equals the full-image engine; band outputs tile its output map."""
+    import torch
+    from paper_1412_4526_b200 import trainer
+    from paper_1412_4526_b200.engine import DenseNet
+    text = _c1_text(3)
+    spec = dp.parse_spec(text)
+    plan = dp.compile_plan(spec)
+    side, world = 48, 3
+    dt = torch.float64 if precision == "exact" else torch.float32
+    rng = np.random.default_rng(9)
+    img = torch.from_numpy(rng.uniform(-0.5, 0.5, (1, 3, side, side))).to(dt).cuda()
+    tgt = torch.from_numpy(rng.uniform(-1, 1, (1, 10, side, side))).to(dt).cuda()
+    mask = torch.from_numpy((rng.random((1, side, side)) < 0.2).astype(np.uint8)).cuda()
+    full = DenseNet(plan, 1, side, side, dtype=dt, precision=precision)
+    full.set_input(img)
+    full.target.copy_(tgt)
+    full.mask.copy_(mask)
+    full.forward()
+    full.loss_delta()
+    full.backward()
+    total = torch.zeros_like(full.grad_flat)
+    outs = []
+    for r in range(world):
+        t = trainer.BandParallelTrainer(plan, 1, side, side, rank=r, world=world, dtype=dt,
+                                        precision=precision)
+        t.load(full.x0, tgt, mask)
+        t.step()
+        total += t.net.grad_flat
+        outs.append(t.net.output.clone())
+    torch.cuda.synchronize()
+    got_out = torch.cat(outs, dim=2)
+    if precision == "exact":
+        assert torch.equal(got_out, full.output)
+        assert rel_err(total.cpu().numpy(), full.grad_flat.cpu().numpy()) < 1e-12
+    else:
+        assert rel_err(got_out.cpu().numpy(), full.output.cpu().numpy()) < 5e-5
+        assert rel_err(total.cpu().numpy(), full.grad_flat.cpu().numpy()) < 1e-4

@@ -465,6 +465,23 @@ def main():
     }
 
     if rank == 0 and world == 1 and not args.no_sweep:
+        # patch-by-patch baseline on the same GPU: every pixel's
+        # 29x29 window classified on its own through the same fast-tier kernels
+        import paper_1412_4526_b200 as dp_pkg
+        one = dpool[0][0][:1]
+        dp_pkg.patch_scan_forward(net.plan, one, batch=8192)
+        torch.cuda.synchronize()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record()
+        dp_pkg.patch_scan_forward(net.plan, one, batch=8192)
+        q1.record()
+        torch.cuda.synchronize()
+        ps = SIDE * SIDE / (q0.elapsed_time(q1) / 1e3)
+        line["patch_scan_gpu"] = {
+            "value": ps, "unit": "pixels/s",
+            "dense_forward_over_patch_scan": line["forward"]["value"] / ps,
+            "sample": "1 image of c2@256: 65536 windows, batches of 8192, same kernels"}
+
         # "per image size" (BASELINE metric) and the other BASELINE configs, same GPU
         sizes = []
         for side, b in ((128, 256), (512, 16), (1024, 4)):

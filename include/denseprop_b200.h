@@ -202,6 +202,11 @@ int dp_pad(int dtype, const void *src, void *dst, int n, int c, int h, int w,
 /* crop window (top,left,h,w) of (n,c,hs,ws) -> (n,c,h,w)  (backward.py:218-222) */
 int dp_crop(int dtype, const void *src, void *dst, int n, int c, int hs, int ws,
             int top, int left, int h, int w, void *stream);
+/* patch-by-patch baseline (reference oracle.py scan_forward:145-164): gather the patch x
+ * patch windows of pixels [first, first+count) (row-major over the w-wide output grid) of ONE
+ * zero-padded image x0 (c, hp, wp) into out (count, c, patch, patch) */
+int dp_patch_gather(int dtype, const void *x0, void *out, int c, int hp, int wp, int patch,
+                    int w, int64_t first, int64_t count, void *stream);
 /* param -= lr * grad (plain SGD; the reference has no optimizer) */
 int dp_sgd_update(int dtype, void *param, const void *grad, int64_t count, double lr,
                   void *stream);

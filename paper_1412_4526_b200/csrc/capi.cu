@@ -62,6 +62,9 @@ int mask_delta_t(const T *, const T *, const uint8_t *, T *, int, int, int, int,
 template <typename T>
 int pad_t(const T *, T *, int, int, int, int, int, int, int, int, cudaStream_t);
 template <typename T>
+int patch_gather_t(const T *x0, T *out, int C, int Hp, int Wp, int P, int w, long long first,
+                   long long count, cudaStream_t st);
+template <typename T>
 int crop_t(const T *, T *, int, int, int, int, int, int, int, int, cudaStream_t);
 template <typename T>
 int sgd_t(T *, const T *, long long, double, cudaStream_t);
@@ -474,6 +477,26 @@ int dp_crop(int dtype, const void *src, void *dst, int n, int c, int hs, int ws,
                                      h, w, st),
                        crop_t<double>((const double *)src, (double *)dst, n, c, hs, ws, top,
                                       left, h, w, st));
+}
+
+int dp_patch_gather(int dtype, const void *x0, void *out, int c, int hp, int wp, int patch,
+                    int w, int64_t first, int64_t count, void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_pos("patch", patch));
+    DP_TRY(check_pos("width", w));
+    const int h = hp - patch + 1;
+    if (h < 1 || wp - patch + 1 != w)
+        return set_error(DP_ERR_ARG, "patch gather: padded map %dx%d does not fit patch %d / width %d",
+                         hp, wp, patch, w);
+    if (first < 0 || count < 0 || first + count > (int64_t)h * w)
+        return set_error(DP_ERR_ARG, "patch gather: pixel range outside the %dx%d grid", h, w);
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       patch_gather_t<float>((const float *)x0, (float *)out, c, hp, wp, patch, w,
+                                             first, count, st),
+                       patch_gather_t<double>((const double *)x0, (double *)out, c, hp, wp,
+                                              patch, w, first, count, st));
 }
 
 int dp_sgd_update(int dtype, void *param, const void *grad, int64_t count, double lr,

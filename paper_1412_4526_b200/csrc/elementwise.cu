@@ -134,6 +134,37 @@ int crop_t(const T *src, T *dst, int n, int c, int hs, int ws, int top, int left
     return check_launch("crop_kernel");
 }
 
+// Patch gather for the patch-by-patch baseline (reference oracle.py scan_forward:145-164 runs
+// the strided classifier on one patch per pixel): out[k, c, i, j] = x0[img, c, y+i, x+j] with
+// (y, x) = divmod(first + k, w) over the w-wide output grid of padded image img.
+template <typename T>
+__global__ void patch_gather_kernel(const T *__restrict__ x0, T *__restrict__ out,
+                                    long long total, int C, int Hp, int Wp, int P, int w,
+                                    long long first) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int jj = (int)(i % P);
+        long long t = i / P;
+        const int ii = (int)(t % P);
+        t /= P;
+        const int c = (int)(t % C);
+        const long long k = t / C;
+        const long long pix = first + k;
+        const int y = (int)(pix / w), x = (int)(pix - (long long)y * w);
+        out[i] = x0[((long long)c * Hp + y + ii) * Wp + x + jj];
+    }
+}
+
+template <typename T>
+int patch_gather_t(const T *x0, T *out, int C, int Hp, int Wp, int P, int w, long long first,
+                   long long count, cudaStream_t st) {
+    const long long total = count * C * P * P;
+    if (total == 0) return DP_OK;
+    patch_gather_kernel<T><<<grid_for(total), 256, 0, st>>>(x0, out, total, C, Hp, Wp, P, w,
+                                                            first);
+    return check_launch("patch_gather_kernel");
+}
+
 template <typename T>
 int sgd_t(T *p, const T *g, long long n, double lr, cudaStream_t st) {
     if (n == 0) return DP_OK;
@@ -151,7 +182,9 @@ int sgd_t(T *p, const T *g, long long n, double lr, cudaStream_t st) {
                           cudaStream_t);                                                      \
     template int crop_t<T>(const T *, T *, int, int, int, int, int, int, int, int,            \
                            cudaStream_t);                                                     \
-    template int sgd_t<T>(T *, const T *, long long, double, cudaStream_t);
+    template int sgd_t<T>(T *, const T *, long long, double, cudaStream_t);                  \
+    template int patch_gather_t<T>(const T *, T *, int, int, int, int, int, long long,        \
+                                   long long, cudaStream_t);
 DP_EW_INST(float)
 DP_EW_INST(double)
 

@@ -251,6 +251,16 @@ class ops:
                                          left, right, _stream()), "pad")
 
     @staticmethod
+    def patch_gather(x0, out, patch, w, first, count):
+        """out (count, C, patch, patch) <- windows of pixels [first, first+count) of ONE
+        padded image x0 (C, Hp, Wp) (patch-by-patch baseline)."""
+        with _Rec('patch_gather', 1, 'hbm', 2 * _nbytes(out)):
+            c, hp, wp = x0.shape
+            _lib.check(_lib_dev().dp_patch_gather(_code(x0), _ptr(x0), _ptr(out), c, hp, wp,
+                                                  patch, w, first, count, _stream()),
+                       "patch_gather")
+
+    @staticmethod
     def crop(src, dst, top, left):
         with _Rec('crop', 1, 'hbm', 2 * _nbytes(dst)):
             n, c, hs, ws = src.shape

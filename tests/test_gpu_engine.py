@@ -432,3 +432,26 @@ def test_band_sharding_equals_full_image(dp, precision):
     else:
         assert rel_err(got_out.cpu().numpy(), full.output.cpu().numpy()) < 5e-5
         assert rel_err(total.cpu().numpy(), full.grad_flat.cpu().numpy()) < 1e-4
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_gpu_patch_scan_equals_dense(dp, precision):
+    """the patch-by-patch baseline on the GPU (every pixel's window
+    classified on its own, oracle.py scan_forward:145-164) equals dense evaluation --
+    bit-identical on the exact tier, within the fast-tier tolerance otherwise."""
+    import torch
+    from paper_1412_4526_b200.engine import DenseNet
+    plan = dp.compile_plan(dp.parse_spec(_c1_text(3)))
+    side = 20
+    dt = torch.float64 if precision == "exact" else torch.float32
+    rng = np.random.default_rng(4)
+    img = torch.from_numpy(rng.uniform(-0.5, 0.5, (2, 3, side, side))).to(dt).cuda()
+    net = DenseNet(plan, 2, side, side, dtype=dt, train=False, precision=precision)
+    net.set_input(img)
+    net.forward()
+    scan = dp.patch_scan_forward(plan, img, batch=96, precision=precision)
+    torch.cuda.synchronize()
+    if precision == "exact":
+        assert torch.equal(scan, net.output)
+    else:
+        assert rel_err(scan.cpu().numpy(), net.output.cpu().numpy()) < 5e-5

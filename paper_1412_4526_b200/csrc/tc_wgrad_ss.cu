@@ -440,24 +440,41 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     const int lines = k * p.Ls;
     p.n_tiles = (lines + 127) / 128;
     const int acc_cols = 2 * p.Npad;
-    int G = std::min(std::min(p.n_tiles, 512 / acc_cols), WS_MAX_G);
-    p.n_groups = (p.n_tiles + G - 1) / G;
-    p.G = (p.n_tiles + p.n_groups - 1) / p.n_groups;
-    // tap rows per group and the ring slots a 128-line tile can span
-    p.max_ni = 0;
-    int span = 1;
-    for (int g = 0; g < p.n_groups; ++g) {
-        const int t0 = g * p.G, G_ = std::min(p.G, p.n_tiles - t0);
-        const int i_lo = t0 * 128 / p.Ls;
-        const int n_i = (std::min((t0 + G_) * 128, lines) - 1) / p.Ls - i_lo + 1;
-        p.max_ni = std::max(p.max_ni, n_i);
-        for (int t = 0; t < G_; ++t) {
-            const int line0 = (t0 + t) * 128 - i_lo * p.Ls;
-            const int f = line0 % p.Ls;
-            span = std::max(span, (f + 128 + p.Ls - 1) / p.Ls);
+    p.slot_bytes = (uint32_t)p.Ls * 128u;  // multiple of 8 lines: 1024-byte aligned boxes
+    p.b_bytes = 2u * (uint32_t)p.Npad * 128u;
+    // Tile groups: as many tiles per CTA as TMEM holds, unless the ring (hi + lo slots for
+    // the group's tap rows + SS - 1 + mirrors) does not fit -- then smaller groups (fewer
+    // tap rows each; every group re-reads its rows), down to one tile.
+    p.SS = 0;
+    for (int G = std::min(std::min(p.n_tiles, 512 / acc_cols), WS_MAX_G); G >= 1 && !p.SS; --G) {
+        p.n_groups = (p.n_tiles + G - 1) / G;
+        p.G = (p.n_tiles + p.n_groups - 1) / p.n_groups;
+        // tap rows per group and the ring slots a 128-line tile can span
+        p.max_ni = 0;
+        int span = 1;
+        for (int g = 0; g < p.n_groups; ++g) {
+            const int t0 = g * p.G, G_ = std::min(p.G, p.n_tiles - t0);
+            const int i_lo = t0 * 128 / p.Ls;
+            const int n_i = (std::min((t0 + G_) * 128, lines) - 1) / p.Ls - i_lo + 1;
+            p.max_ni = std::max(p.max_ni, n_i);
+            for (int t = 0; t < G_; ++t) {
+                const int line0 = (t0 + t) * 128 - i_lo * p.Ls;
+                const int f = line0 % p.Ls;
+                span = std::max(span, (f + 128 + p.Ls - 1) / p.Ls);
+            }
+        }
+        p.NM = span - 1;
+        for (int ss = WS_MAX_SS; ss >= 2; --ss) {
+            const size_t need = (size_t)ss * p.b_bytes +
+                                2 * (size_t)(p.max_ni + ss - 1 + p.NM) * p.slot_bytes;
+            if (need <= (size_t)WS_SMEM_BUDGET) {
+                p.SS = ss;
+                break;
+            }
         }
     }
-    p.NM = span - 1;
+    if (p.SS < 2) return false;
+    p.R = p.max_ni + p.SS - 1;
     // residue copies: taps j with (j*d) & 3 == b, lcm(d, 4) floats apart
     int gcd = 1;
     for (int v = 4; v >= 1; --v)
@@ -493,17 +510,7 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
         p.rs.b[rb] = -1;
         p.rs.n[rb] = p.rs.j0[rb] = p.rs.line0[rb] = 0;
     }
-    p.slot_bytes = (uint32_t)p.Ls * 128u;  // multiple of 8 lines: 1024-byte aligned boxes
     p.box_tx_row = (uint32_t)cin * k * 128u;  // bytes the residue boxes of one row deliver
-    p.b_bytes = 2u * (uint32_t)p.Npad * 128u;
-    int SS = WS_MAX_SS;
-    auto smem_for = [&](int ss) {
-        return (size_t)ss * p.b_bytes + 2 * (size_t)(p.max_ni + ss - 1 + p.NM) * p.slot_bytes;
-    };
-    while (SS >= 2 && smem_for(SS) > (size_t)WS_SMEM_BUDGET) --SS;
-    if (SS < 2) return false;
-    p.SS = SS;
-    p.R = p.max_ni + SS - 1;
     p.nvb = (p.wo + 31) / 32;
     p.T = (p.ho + d - 1) / d;
     p.kb_total = (long long)n * p.nvb * d * p.T;

@@ -441,6 +441,36 @@ __global__ void __launch_bounds__(256) tc_stage_x(const float *__restrict__ src,
     }
 }
 
+// x staging, one copy per TAP (small-cin layers of the smem-operand weight gradient):
+// dst_j[n,h,c,v] = src[n,c,h,v + j*d] (zero at v + j*d >= w), (n, h, c, wp) layout; a
+// single TMA box with the copy stride as its tap dimension then gathers every (c, j) line
+// of a row (the residue copies need one box per residue -- tiny boxes at cin = 3, d = 1).
+__global__ void __launch_bounds__(256) tc_stage_x_taps(const float *__restrict__ src,
+                                                       float *__restrict__ dst, int C, int H,
+                                                       int w, int wp, int l, int d,
+                                                       long long copy_stride,
+                                                       long long total_quads) {
+    const int nq = wp >> 2;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total_quads;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long row = idx / nq;  // (n, c, h)
+        const int v = (int)(idx - row * nq) * 4;
+        const int h = (int)(row % H);
+        const long long nc = row / H;
+        const int c = (int)(nc % C);
+        const long long n = nc / C;
+        const float *s = src + row * w;
+        float4 *d0 = reinterpret_cast<float4 *>(dst + ((n * H + h) * C + c) * wp + v);
+        for (int j = 0; j < l; ++j) {
+            const int o = v + j * d;
+            float e[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) e[t] = o + t < w ? __ldg(s + o + t) : 0.f;
+            d0[j * (copy_stride >> 2)] = make_float4(e[0], e[1], e[2], e[3]);
+        }
+    }
+}
+
 // dy staging: NCHW (n, o, h, w) -> (n, h, o, wp), zero pad.  A K block's dy box then
 // reads Npad lines wp floats apart instead of one line per channel plane (plane-strided
 // boxes measured ~4x slower here: every line opens a different DRAM page).
@@ -645,6 +675,19 @@ int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp
     int rc = check_launch("tc_stage_x");
     if (rc) return rc;
     return stage_x_tails(xs, quads * 4, copy_floats, mask, st);
+}
+int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int l,
+                    int d, long long copy_floats, cudaStream_t st) {
+    const long long quads = (long long)n * cin * hi * (wp / 4);
+    tc_stage_x_taps<<<stage_grid(quads), 256, 0, st>>>(x, xs, cin, hi, wi, wp, l, d, copy_floats,
+                                                       quads);
+    int rc = check_launch("tc_stage_x_taps");
+    if (rc) return rc;
+    for (int j = 0; j < l; ++j)
+        if (cudaMemsetAsync(xs + j * copy_floats + quads * 4, 0,
+                            (size_t)(copy_floats - quads * 4) * 4, st) != cudaSuccess)
+            return set_error(DP_ERR_CUDA, "weight gradient: memset of staged tails failed");
+    return DP_OK;
 }
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
                 cudaStream_t st) {

@@ -50,6 +50,8 @@ int wg_sms();
 unsigned long long *wg_trace_buffer(cudaStream_t st);
 int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
                long long copy_floats, cudaStream_t st);
+int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int l,
+                    int d, long long copy_floats, cudaStream_t st);
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
                 cudaStream_t st);
 
@@ -68,6 +70,7 @@ struct WsResidues {
     int j0[4];      // first tap of the residue
     int line0[4];   // first line of the residue's box inside a ring slot
     int step;       // tap step inside a residue: 4 / gcd(d, 4)
+    int tapcopy;    // 1: one staged copy per tap (single box per row), lines (c, j)
 };
 
 struct WsArgs {
@@ -388,8 +391,9 @@ __global__ void ws_reduce(const float *__restrict__ part, const float *__restric
         const int i = tap / l, j = tap - (tap / l) * l;
         const int b = (j * d) & 3;
         int rb = 0;
-        while (rs.b[rb] != b) ++rb;
-        const int jj = (j - rs.j0[rb]) / rs.step;
+        if (!rs.tapcopy)
+            while (rs.b[rb] != b) ++rb;
+        const int jj = rs.tapcopy ? j : (j - rs.j0[rb]) / rs.step;
         const size_t line = (size_t)i * Ls + rs.line0[rb] + c * rs.n[rb] + jj;
         float acc = 0.f;
         for (int s = 0; s < splits; ++s) acc += part[((size_t)s * rows_pad + line) * Npad + o];
@@ -427,16 +431,25 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     if (p.Npad > 128) return false;
     p.Cpad = (cin + 7) / 8 * 8;
     if (p.Cpad > 256) return false;
-    // lines per ring slot (one input row): residue boxes, each rounded up to 8 lines
+    // lines per ring slot (one input row): residue boxes, each rounded up to 8 lines.  Small
+    // channel counts with several residues would mean several tiny boxes per K block (TMA
+    // issue bound, measured on c2 conv1: cin 3, d 1); those stage one copy per tap instead
+    // and load a row with a single {32, l, cin} box.
+    int nres = 0;
     {
         int ls = 0;
         for (int b = 0; b < 4; ++b) {
             int cnt = 0;
             for (int j = 0; j < k; ++j) cnt += ((j * d) & 3) == b;
-            if (cnt) ls += (cin * cnt + 7) / 8 * 8;
+            if (cnt) {
+                ls += (cin * cnt + 7) / 8 * 8;
+                ++nres;
+            }
         }
         p.Ls = ls;
     }
+    p.rs.tapcopy = (nres > 1 && cin * k <= 32 && !getenv("DP_WG_RESIDUE")) ? 1 : 0;
+    if (p.rs.tapcopy) p.Ls = (cin * k + 7) / 8 * 8;
     const int lines = k * p.Ls;
     p.n_tiles = (lines + 127) / 128;
     const int acc_cols = 2 * p.Npad;
@@ -485,8 +498,20 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     p.rs.step = 4 / gcd;
     p.mask = 0;
     p.rs.n_b = 0;
+    if (p.rs.tapcopy) {  // one "residue" holding all l taps (copy j pre-shifted by j*d)
+        p.rs.n_b = 1;
+        p.rs.b[0] = 0;
+        p.rs.n[0] = k;
+        p.rs.j0[0] = 0;
+        p.rs.line0[0] = 0;
+        p.rs.step = 1;
+        for (int rb = 1; rb < 4; ++rb) {
+            p.rs.b[rb] = -1;
+            p.rs.n[rb] = p.rs.j0[rb] = p.rs.line0[rb] = 0;
+        }
+    }
     int line0 = 0;
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 4 && !p.rs.tapcopy; ++b) {
         int cnt = 0, j0 = -1;
         for (int j = 0; j < k; ++j)
             if (((j * d) & 3) == b) {
@@ -525,7 +550,7 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     p.pdb_bytes = ws_align256((size_t)p.splits * p.Npad * 4);
     // boxes read up to (l-1)*d + 32 floats past a row's end (those columns meet zero dy)
     p.copy_bytes = ws_align256((size_t)n * cin * hi * p.wp_x * 4 + ((size_t)(k - 1) * d + 64) * 4);
-    p.x_bytes = (size_t)p.rs.n_b * p.copy_bytes;
+    p.x_bytes = (size_t)(p.rs.tapcopy ? k : p.rs.n_b) * p.copy_bytes;
     p.dy_bytes = p.stage_dy ? ws_align256((size_t)n * cout * p.ho * p.wp_dy * 4) : 0;
     p.total_bytes = p.part_bytes + p.pdb_bytes + p.x_bytes + p.dy_bytes;
     return true;
@@ -558,7 +583,11 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.part = (float *)w8;
     a.pdb = (float *)(w8 + p.part_bytes);
     float *xs = (float *)(w8 + p.part_bytes + p.pdb_bytes);
-    int rc = wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask, (long long)(p.copy_bytes / 4), st);
+    int rc = p.rs.tapcopy
+                 ? wg_stage_x_taps(x, xs, n, cin, hi, wi, p.wp_x, k, d,
+                                   (long long)(p.copy_bytes / 4), st)
+                 : wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask,
+                              (long long)(p.copy_bytes / 4), st);
     if (rc) return rc;
     const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
     if (stage_dy && !p.stage_dy)
@@ -589,7 +618,10 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
         // residue's (c, jj) lines of one input row
         cuuint64_t dims[4] = {(cuuint64_t)p.wp_x, (cuuint64_t)p.rs.n[used], (cuuint64_t)cin,
                               (cuuint64_t)n * hi};
-        cuuint64_t str[3] = {(cuuint64_t)p.rs.step * d * 4, xrow, ximg_row};
+        // tap dimension: lcm(d, 4) floats inside a residue copy, or the copy stride when each
+        // tap has its own pre-shifted copy
+        cuuint64_t str[3] = {p.rs.tapcopy ? (cuuint64_t)p.copy_bytes : (cuuint64_t)p.rs.step * d * 4,
+                             xrow, ximg_row};
         cuuint32_t box[4] = {32, (cuuint32_t)p.rs.n[used], (cuuint32_t)cin, 1};
         rc = wg_make_map(&mx[rb], base, 4, dims, str, box, true);
         if (rc) return rc;

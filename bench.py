@@ -150,8 +150,53 @@ def _cpu_kernels():
     return kernels_c, "port"
 
 
+def _ref_package():
+    """The UNMODIFIED reference package installed into baseline/_ref (DESIGN.md recipe), with
+    its compiled backend selected, or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "denseprop")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import denseprop
+        from denseprop import backend
+        if "compiled" not in backend.available():
+            return None
+        backend.use("compiled")
+        return denseprop
+    except Exception:  # noqa: BLE001 -- fall back to the oracle glue
+        return None
+
+
 def cpu_dense_step_seconds(threads, images=1, seed=0):
-    """Time fwd + 1%-masked bwd of c2@256 through the reference kernels (per image)."""
+    """Time fwd + 1%-masked bwd of c2@256 on the CPU, per image: through the reference
+    package's own public API (dense_forward / dense_backward, compiled backend) when it is
+    installed in baseline/_ref, else through its compiled kernels via the oracle glue."""
+    pkg = _ref_package()
+    if pkg is not None:
+        from denseprop.backward import ErrorMask, dense_backward
+        from denseprop.forward import dense_forward
+        from denseprop.netspec import parse_spec
+        from denseprop.plan import compile_plan
+        plan = compile_plan(parse_spec(C2_TEXT))
+        rng = np.random.default_rng(seed)
+        times_f, times_b = [], []
+        for _ in range(images):
+            img = rng.uniform(-0.5, 0.5, (3, SIDE, SIDE)).astype(np.float32)
+            tgt = rng.uniform(-1, 1, (10, SIDE, SIDE)).astype(np.float32)
+            flat = rng.choice(SIDE * SIDE, int(MASK_FRAC * SIDE * SIDE), replace=False)
+            mask = ErrorMask.of(SIDE, SIDE, [(int(i) // SIDE, int(i) % SIDE) for i in flat])
+            t0 = time.perf_counter()
+            cache = dense_forward(plan, img, threads)
+            t1 = time.perf_counter()
+            dense_backward(plan, cache, (cache.output - tgt).astype(np.float32), mask, threads)
+            t2 = time.perf_counter()
+            times_f.append(t1 - t0)
+            times_b.append(t2 - t1)
+        return (float(np.median(times_f)), float(np.median(times_b)), "reference",
+                "unmodified reference package (baseline/_ref): dense_forward + dense_backward, "
+                "compiled backend")
     from oracle import engine_np
     from oracle.netdesc import read_spec
     K, kind = _cpu_kernels()
@@ -171,7 +216,9 @@ def cpu_dense_step_seconds(threads, images=1, seed=0):
         t2 = time.perf_counter()
         times_f.append(t1 - t0)
         times_b.append(t2 - t1)
-    return float(np.median(times_f)), float(np.median(times_b)), kind
+    how = ("reference compiled kernels (oracle/_ref) via oracle/ engine glue" if kind == "reference"
+           else "oracle C port")
+    return float(np.median(times_f)), float(np.median(times_b)), kind, how
 
 
 def cpu_patch_scan_px_per_s(budget_s=4.0):
@@ -199,9 +246,9 @@ def run_reference_arm(args, rank):
     for _ in range(max(0, args.warmup)):
         cpu_dense_step_seconds(threads, 1)
     fw, bw = [], []
-    kind = None
+    kind = how = None
     for s in range(args.steps):
-        f, b, kind = cpu_dense_step_seconds(threads, 1, seed=s)
+        f, b, kind, how = cpu_dense_step_seconds(threads, 1, seed=s)
         fw.append(f)
         bw.append(b)
     step = float(np.sum(fw) + np.sum(bw)) / args.steps
@@ -216,8 +263,8 @@ def run_reference_arm(args, rank):
                    "net": "conv6/maxpool2/tanh/conv5/maxpool2/tanh/conv4 (16,32,10 ch), patch 29"},
         "forward": {"value": SIDE * SIDE / float(np.mean(fw)), "unit": "pixels/s"},
         "cpu_baseline": {"value": value, "unit": "pixels/s", "cores": threads, "kind": kind,
-                         "sample": f"{args.steps} images of c2@256 (fwd+bwd, 1% mask), "
-                                   f"reference compiled kernels via oracle/ engine glue"},
+                         "sample": f"{args.steps} images of c2@256 (fwd+bwd, 1% mask), {how}, "
+                                   f"{threads} threads"},
         "e2e": {"value": value, "unit": "pixels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -497,12 +544,11 @@ def main():
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        f, b, kind = cpu_dense_step_seconds(threads, 1)
+        f, b, kind, how = cpu_dense_step_seconds(threads, 1)
         scan_px_s, scan_n = cpu_patch_scan_px_per_s()
         line["cpu_baseline"] = {
             "value": SIDE * SIDE / (f + b), "unit": "pixels/s", "cores": threads, "kind": kind,
-            "sample": "1 image of c2@256 (fwd + 1%-masked bwd) through the reference's compiled "
-                      "kernels, all host threads",
+            "sample": f"1 image of c2@256 (fwd + 1%-masked bwd), {how}, {threads} threads",
             "forward_value": SIDE * SIDE / f,
             "patch_scan_forward": {"value": scan_px_s, "unit": "pixels/s", "cores": 1,
                                    "sample": f"{scan_n} pixels on a 16-px grid, extrapolated"},

@@ -22,6 +22,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -445,7 +447,14 @@ class DenseNet:
         self.output = self.acts[-1]
         if train:
             biggest = max([int(np.prod(s)) for s in shapes])
-            self._dbuf = [torch.empty(N * biggest, **kw), torch.empty(N * biggest, **kw)]
+            # three rotating delta buffers: a layer's weight gradient runs on a side stream
+            # (overlapping the data-gradient / pool-backward chain) and still reads its
+            # delta while the next op writes; the third buffer keeps that delta intact
+            # until the op after next (DP_NO_OVERLAP=1: serial, same results)
+            self.overlap_wgrad = not os.environ.get("DP_NO_OVERLAP")
+            nbuf = 3 if self.overlap_wgrad else 2
+            self._dbuf = [torch.empty(N * biggest, **kw) for _ in range(nbuf)]
+            self._wg_stream = torch.cuda.Stream(device=self.device) if self.overlap_wgrad else None
             ws = 256
             self.tc_wgrad = {}
             for gi, g in enumerate(self.groups):
@@ -575,12 +584,29 @@ class DenseNet:
             raise RuntimeError("engine built with train=False")
         delta = self.delta_last if delta_last is None else delta_last
         last = self.groups[-1]
+        nbuf = len(self._dbuf)
         ping = 0
+        main = torch.cuda.current_stream(self.device)
+        side = self._wg_stream
+        readers = [None] * nbuf  # side-stream event of the last weight gradient per buffer
+        side_busy = False
+
+        def out_buf(k, shape):
+            # the main stream may overwrite buffer k once the side stream has read it
+            if readers[k] is not None:
+                main.wait_event(readers[k])
+                readers[k] = None
+            return self._view(self._dbuf[k], shape)
+
+        def join():
+            if side_busy:
+                main.wait_stream(side)
+
         if last.act != "identity":
             # a net ending in conv/pool + nonlin: undo the fused nonlinearity first
-            d2 = self._view(self._dbuf[ping], delta.shape)
+            d2 = out_buf(ping, delta.shape)
             ops.nonlin_backward(delta, self.acts[-1], d2, _nl(last.act), x_is_output=True)
-            delta, ping = d2, ping ^ 1
+            delta, ping = d2, (ping + 1) % nbuf
         for gi in range(len(self.groups) - 1, -1, -1):
             g = self.groups[gi]
             x_in = self._group_input(gi)
@@ -593,26 +619,42 @@ class DenseNet:
                 wt, _ = self.params[g.first]
                 dw, db = self.grads[g.first]
                 kk, d = op.base.kernel_size, op.dilation
-                if self.tc_wgrad.get(gi, False):
+                fast_w = self.tc_wgrad.get(gi, False)
+                if side is not None:
+                    # weight gradient on the side stream (in order: they share self._ws)
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        if fast_w:
+                            ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws)
+                        else:
+                            ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
+                    side_busy = True
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    src = (ping - 1) % nbuf  # buffer holding `delta` (if it is a buffer)
+                    if delta.data_ptr() == self._dbuf[src].data_ptr():
+                        readers[src] = ev
+                elif fast_w:
                     ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws)
                 else:
                     ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                 if gi == 0 and not with_input_grad:
+                    join()
                     return None
-                dx = self._view(self._dbuf[ping], x_in.shape)
+                dx = out_buf(ping, x_in.shape)
                 if self.tc.get(gi, (False, False))[1]:
                     ops.conv_backward_data_fast(delta, wt, dx, kk, d, self._tc_ws, gate, gk)
                 else:
                     ops.conv_backward_data(delta, wt, dx, kk, d, gate, gk)
             elif isinstance(op, DilatedPool):
-                dx = self._view(self._dbuf[ping], x_in.shape)
+                dx = out_buf(ping, x_in.shape)
                 if op.base.kind == "max":
                     ops.maxpool_backward(delta, self.args[gi], dx, op.base.kernel_size,
                                          op.dilation, gate, gk)
                 else:
                     ops.avgpool_backward(delta, dx, op.base.kernel_size, op.dilation, gate, gk)
             else:
-                dx = self._view(self._dbuf[ping], x_in.shape)
+                dx = out_buf(ping, x_in.shape)
                 if op.kind == "identity":
                     dx.copy_(delta)
                 else:
@@ -620,7 +662,8 @@ class DenseNet:
                 if gate is not None:
                     # standalone nonlin after a fused group: apply that group's gate too
                     ops.nonlin_backward(dx, x_in, dx, gk, x_is_output=True)
-            delta, ping = dx, ping ^ 1
+            delta, ping = dx, (ping + 1) % nbuf
+        join()
         return delta
 
     def sgd_step(self, lr):

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DP_ABI_VERSION 3
+#define DP_ABI_VERSION 4
 
 enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
 /* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
@@ -154,6 +154,17 @@ size_t dp_conv_backward_kernel_fast_workspace(int n, int cin, int hi, int wi, in
 int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, float *db, int n,
                                  int cin, int hi, int wi, int cout, int k, int d,
                                  void *workspace, size_t workspace_bytes, void *stream);
+/* Split form (ABI 4): _prepare stages x (the re-laid-out / shifted copies the kernel's TMA
+ * boxes read) into `workspace`; it depends on x only, so it can run as soon as x exists
+ * (the engine overlaps it with the forward pass on a side stream).  _staged then runs the
+ * rest on the same workspace (which must not be reused in between).  When the split does
+ * not apply (fallback kernel) _prepare does nothing and _staged does everything. */
+int dp_conv_backward_kernel_fast_prepare(const float *x, int n, int cin, int hi, int wi,
+                                         int cout, int k, int d, void *workspace,
+                                         size_t workspace_bytes, void *stream);
+int dp_conv_backward_kernel_fast_staged(const float *x, const float *dy, float *dw, float *db,
+                                        int n, int cin, int hi, int wi, int cout, int k, int d,
+                                        void *workspace, size_t workspace_bytes, void *stream);
 
 /* debugging aid: with DP_WG_TRACE set in the environment, the fast weight-gradient kernel
  * records per-K-block clock64() timestamps of CTA 0 (256 blocks x 16 slots); this copies

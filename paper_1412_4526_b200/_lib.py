@@ -20,7 +20,7 @@ DP_F32, DP_F64 = 0, 1
 DP_IDENTITY, DP_TANH, DP_RELU, DP_TANH_FAST = 0, 1, 2, 3
 DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED = 0, 1, 2, 3
 NONLIN_CODE = {"identity": DP_IDENTITY, "tanh": DP_TANH, "relu": DP_RELU}
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _vp, _i, _i64, _sz, _d = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double
 
@@ -55,6 +55,8 @@ SIGNATURES = {
     "dp_conv_backward_kernel_fast_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel_fast": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
                                           _sz, _vp]),
+    "dp_conv_backward_kernel_fast_prepare": (_i, [_vp] + [_i] * 7 + [_vp, _sz, _vp]),
+    "dp_conv_backward_kernel_fast_staged": (_i, [_vp, _vp, _vp, _vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel": (_i, [_i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
                                      _sz, _vp]),

@@ -40,6 +40,10 @@ bool tc_wgrad_supported(int, int, int, int, int, int, int);
 int wg_trace_copy(void *, size_t);
 int tc_trace_copy(void *, size_t);
 size_t tc_wgrad_workspace(int, int, int, int, int, int, int);
+int tc_wgrad_prepare(const float *, int, int, int, int, int, int, int, void *, size_t,
+                     cudaStream_t);
+int tc_conv_backward_kernel_staged(const float *, const float *, float *, float *, int, int, int,
+                                   int, int, int, int, void *, size_t, cudaStream_t);
 int tc_conv_backward_kernel(const float *, const float *, float *, float *, int, int, int, int,
                             int, int, int, void *, size_t, cudaStream_t);
 template <typename T>
@@ -332,6 +336,28 @@ int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, flo
     DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
     return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
                                    workspace_bytes, (cudaStream_t)stream);
+}
+
+int dp_conv_backward_kernel_fast_prepare(const float *x, int n, int cin, int hi, int wi,
+                                         int cout, int k, int d, void *workspace,
+                                         size_t workspace_bytes, void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    return tc_wgrad_prepare(x, n, cin, hi, wi, cout, k, d, workspace, workspace_bytes,
+                            (cudaStream_t)stream);
+}
+
+int dp_conv_backward_kernel_fast_staged(const float *x, const float *dy, float *dw, float *db,
+                                        int n, int cin, int hi, int wi, int cout, int k, int d,
+                                        void *workspace, size_t workspace_bytes, void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    return tc_conv_backward_kernel_staged(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
+                                          workspace_bytes, (cudaStream_t)stream);
 }
 
 int dp_maxpool_forward(int dtype, const void *x, void *y, void *arg, int arg_bytes, int n, int c,

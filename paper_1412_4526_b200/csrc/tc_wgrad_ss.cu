@@ -566,9 +566,12 @@ size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d) {
     return ws_plan(n, cin, hi, wi, cout, k, d, p) ? p.total_bytes : 0;
 }
 
+// phases: 1 = stage x into the workspace, 2 = everything else (dy staging, kernel,
+// reduction); 3 = both.  Staging x is independent of dy, so the engine runs phase 1 during
+// the forward pass (side stream) and phase 2 in the backward.
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st) {
+                            size_t ws_bytes, cudaStream_t st, int phases) {
     WsPlan p;
     if (!ws_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED, "weight gradient (smem operands): unsupported shape");
@@ -583,12 +586,15 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.part = (float *)w8;
     a.pdb = (float *)(w8 + p.part_bytes);
     float *xs = (float *)(w8 + p.part_bytes + p.pdb_bytes);
-    int rc = p.rs.tapcopy
-                 ? wg_stage_x_taps(x, xs, n, cin, hi, wi, p.wp_x, k, d,
-                                   (long long)(p.copy_bytes / 4), st)
-                 : wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask,
-                              (long long)(p.copy_bytes / 4), st);
-    if (rc) return rc;
+    int rc = DP_OK;
+    if (phases & 1) {
+        rc = p.rs.tapcopy ? wg_stage_x_taps(x, xs, n, cin, hi, wi, p.wp_x, k, d,
+                                            (long long)(p.copy_bytes / 4), st)
+                          : wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask,
+                                       (long long)(p.copy_bytes / 4), st);
+        if (rc) return rc;
+    }
+    if (!(phases & 2)) return DP_OK;
     const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
     if (stage_dy && !p.stage_dy)
         return set_error(DP_ERR_ARG, "weight gradient: dy must be 16-byte aligned");

@@ -192,6 +192,25 @@ class ops:
                 ws.numel() * ws.element_size(), _stream()), "conv_backward_kernel_fast")
 
     @staticmethod
+    def conv_backward_kernel_fast_prepare(x, co, k, d, ws):
+        """Stage x for a later conv_backward_kernel_fast_staged on the same workspace."""
+        with _Rec('wgrad_stage_x', 1, 'hbm', _nbytes(x)):
+            n, ci, hi, wi = x.shape
+            _lib.check(_lib_dev().dp_conv_backward_kernel_fast_prepare(
+                _ptr(x), n, ci, hi, wi, co, k, d, _ptr(ws), ws.numel() * ws.element_size(),
+                _stream()), "conv_backward_kernel_fast_prepare")
+
+    @staticmethod
+    def conv_backward_kernel_fast_staged(x, dy, dw, db, k, d, ws):
+        with _Rec('conv_backward_kernel_tc', 1 + _repitches(x, dy), 'tensor',
+                  2 * dy.numel() * x.shape[1] * k * k):
+            n, ci, hi, wi = x.shape
+            co = dy.shape[1]
+            _lib.check(_lib_dev().dp_conv_backward_kernel_fast_staged(
+                _ptr(x), _ptr(dy), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k, d, _ptr(ws),
+                ws.numel() * ws.element_size(), _stream()), "conv_backward_kernel_fast_staged")
+
+    @staticmethod
     def maxpool_forward(x, y, arg, p, d, nonlin=_lib.DP_IDENTITY):
         with _Rec('maxpool_forward', 1, 'hbm', _nbytes(x, y, arg)):
             n, c, h, w = x.shape
@@ -467,6 +486,18 @@ class DenseNet:
                     ws = max(ws, ops.wgrad_fast_workspace(xin, co, kk, dd) if fast else
                              ops.wgrad_workspace(xin, co, kk, dd))
             self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
+            # overlap mode: each fast weight gradient gets its own workspace so its x staging
+            # can run during the forward pass (prepare) and survive until the backward
+            self._ws_l = {}
+            self._prepared = set()
+            if self.overlap_wgrad:
+                for gi, fast in self.tc_wgrad.items():
+                    if fast:
+                        g = self.groups[gi]
+                        nb = ops.wgrad_fast_workspace(self._group_input(gi),
+                                                      g.op.base.out_channels,
+                                                      g.op.base.kernel_size, g.op.dilation)
+                        self._ws_l[gi] = torch.empty(nb, dtype=torch.uint8, device=self.device)
             self.mask = torch.zeros((N, height, width), dtype=torch.uint8, device=self.device)
             self.target = torch.zeros_like(self.output)
             self.delta_last = torch.empty_like(self.output)
@@ -535,12 +566,29 @@ class DenseNet:
         lead, trail = self.plan.lead_margin, self.plan.trail_margin
         ops.pad(images, self.x0, lead, trail, lead, trail)
 
-    def forward(self, images=None):
+    def forward(self, images=None, prepare_backward=False):
+        """prepare_backward (training steps, with DP_PREPARE=1): stage every fast weight
+        gradient's x on the side stream as soon as that x exists, overlapping the rest of the
+        forward pass (the backward that follows then runs the staged weight-gradient
+        kernels)."""
         if images is not None:
             self.set_input(images)
+        # opt-in (DP_PREPARE=1): measured slower on c2 -- the staging copies on the side
+        # stream slow the shared-memory-bound forward convs more than they save later
+        prep = (prepare_backward and self.train and getattr(self, "overlap_wgrad", False)
+                and bool(self._ws_l) and bool(os.environ.get("DP_PREPARE")))
+        main = torch.cuda.current_stream(self.device)
+        self._prepared = set()
         for gi, g in enumerate(self.groups):
             x, y = self._group_input(gi), self.acts[gi]
             op, act = g.op, _nl(g.act)
+            if prep and gi in self._ws_l:
+                self._wg_stream.wait_stream(main)
+                with torch.cuda.stream(self._wg_stream):
+                    ops.conv_backward_kernel_fast_prepare(x, op.base.out_channels,
+                                                          op.base.kernel_size, op.dilation,
+                                                          self._ws_l[gi])
+                self._prepared.add(gi)
             if act == _lib.DP_TANH and self.precision == "fast":
                 act = _lib.DP_TANH_FAST  # tanhf (<= 2 ulp) instead of the fp64 evaluation
             if isinstance(op, DilatedConv):
@@ -621,11 +669,16 @@ class DenseNet:
                 kk, d = op.base.kernel_size, op.dilation
                 fast_w = self.tc_wgrad.get(gi, False)
                 if side is not None:
-                    # weight gradient on the side stream (in order: they share self._ws)
+                    # weight gradient on the side stream (in order; per-layer workspaces for
+                    # the fast ones, x staged during the forward pass when prepared)
                     side.wait_stream(main)
                     with torch.cuda.stream(side):
-                        if fast_w:
-                            ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws)
+                        if fast_w and gi in self._prepared:
+                            ops.conv_backward_kernel_fast_staged(x_in, delta, dw, db, kk, d,
+                                                                 self._ws_l[gi])
+                        elif fast_w:
+                            ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d,
+                                                          self._ws_l.get(gi, self._ws))
                         else:
                             ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                     side_busy = True
@@ -640,6 +693,7 @@ class DenseNet:
                     ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                 if gi == 0 and not with_input_grad:
                     join()
+                    self._prepared = set()
                     return None
                 dx = out_buf(ping, x_in.shape)
                 if self.tc.get(gi, (False, False))[1]:
@@ -664,6 +718,7 @@ class DenseNet:
                     ops.nonlin_backward(dx, x_in, dx, gk, x_is_output=True)
             delta, ping = dx, (ping + 1) % nbuf
         join()
+        self._prepared = set()
         return delta
 
     def sgd_step(self, lr):
@@ -672,7 +727,7 @@ class DenseNet:
     # ------------------------------------------------------------- whole step
     def train_step(self, lr=0.0, allreduce=None):
         """forward -> masked squared-error delta -> backward -> [allreduce] -> SGD."""
-        self.forward()
+        self.forward(prepare_backward=True)
         self.loss_delta()
         self.backward()
         if allreduce is not None:

@@ -130,7 +130,7 @@ class DataParallelTrainer:
 
     def _compute(self):
         n = self.net
-        n.forward()
+        n.forward(prepare_backward=True)
         n.loss_delta()
         n.backward()
 

@@ -157,3 +157,27 @@ def test_tc_weight_gradient_matches_fp64(shape):
     assert torch.equal(dw, dw2) and torch.equal(db, db2)   # deterministic split-K
     assert _rel(dw, dw64) < 1e-5, _rel(dw, dw64)
     assert _rel(db, db64) < 1e-5, _rel(db, db64)
+
+
+@pytest.mark.parametrize("shape", [WGRAD_SHAPES[0], WGRAD_SHAPES[1], WGRAD_SHAPES[2]])
+def test_tc_weight_gradient_split_prepare_staged(shape):
+    """dp_conv_backward_kernel_fast_prepare (stage x) + _staged (the rest) on one workspace
+    == the single call, bit for bit."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    e = (k - 1) * d + 1
+    rng = np.random.default_rng(3)
+    x = _t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
+    dy = _t(rng.uniform(-1, 1, (n, co, h - e + 1, w - e + 1)).astype(np.float32))
+    nb = ops.wgrad_fast_workspace(x, co, k, d)
+    ws1 = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    ws2 = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    dw1 = torch.empty((co, ci, k, k), device="cuda")
+    db1 = torch.empty(co, device="cuda")
+    dw2, db2 = torch.empty_like(dw1), torch.empty_like(db1)
+    ops.conv_backward_kernel_fast(x, dy, dw1, db1, k, d, ws1)
+    ops.conv_backward_kernel_fast_prepare(x, co, k, d, ws2)
+    ops.conv_backward_kernel_fast_staged(x, dy, dw2, db2, k, d, ws2)
+    torch.cuda.synchronize()
+    assert torch.equal(dw1, dw2) and torch.equal(db1, db2)

@@ -777,6 +777,8 @@ def profile_step(trainer, reps=5):
     """
     net = trainer.net if hasattr(trainer, "net") else trainer
     ops.profile = []
+    # serial: per-kernel CUDA-event times are only meaningful without the side-stream overlap
+    side, net._wg_stream = getattr(net, "_wg_stream", None), None
     try:
         for _ in range(reps):
             net.forward()
@@ -786,6 +788,7 @@ def profile_step(trainer, reps=5):
         rec = ops.profile
     finally:
         ops.profile = None
+        net._wg_stream = side
     per = len(rec) // reps
     out = []
     for i in range(per):

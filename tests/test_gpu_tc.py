@@ -40,15 +40,27 @@ def _rel(a, b):
     return float((a - b).abs().max() / max(b.abs().max(), 1e-30))
 
 
-@pytest.mark.parametrize("kernel", ["flat", "tap"])
+@pytest.fixture
+def force_env(monkeypatch):
+    """Select a fallback kernel for one test through its (per-call) environment switch."""
+    def _set(kernel):
+        if kernel == "halo":
+            monkeypatch.setenv("DP_TC_HALO", "1")    # halo-buffer / converter kernel
+        elif kernel == "tmem":
+            monkeypatch.setenv("DP_WG_TMEM", "1")    # TMEM-operand weight gradient
+    return _set
+
+
+@pytest.mark.parametrize("kernel", ["flat", "tap", "halo"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("act", [0, 1, 2])
-def test_tc_forward_matches_exact(shape, act, kernel):
+def test_tc_forward_matches_exact(shape, act, kernel, force_env):
     """kernel="tap" passes the shape-aware workspace, which selects the tap-stacked kernel
     where it applies (else the flat one runs again)."""
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
+    force_env(kernel)
     if not ops.fast_supported(ci, co, k, d):
         pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
     rng = np.random.default_rng(sum(shape) + act)
@@ -59,7 +71,7 @@ def test_tc_forward_matches_exact(shape, act, kernel):
     y_ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda")
     y = torch.full_like(y_ref, float("nan"))
     ops.conv_forward(x, wt, b, y_ref, k, d, act)
-    nb = ops.fast_workspace(ci, co, k) if kernel == "flat" else ops.fwd_fast_workspace(x, co, k, d)
+    nb = ops.fast_workspace(ci, co, k) if kernel != "tap" else ops.fwd_fast_workspace(x, co, k, d)
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     ops.conv_forward_fast(x, wt, b, y, k, d, act, ws)
     torch.cuda.synchronize()
@@ -67,13 +79,14 @@ def test_tc_forward_matches_exact(shape, act, kernel):
     assert _rel(y, y_ref) < TOL
 
 
-@pytest.mark.parametrize("kernel", ["flat", "tap"])
+@pytest.mark.parametrize("kernel", ["flat", "tap", "halo"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("gate_kind", [None, 1, 2])
-def test_tc_backward_data_matches_exact(shape, gate_kind, kernel):
+def test_tc_backward_data_matches_exact(shape, gate_kind, kernel, force_env):
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
+    force_env(kernel)
     if not ops.fast_supported(co, ci, k, d):
         pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
     rng = np.random.default_rng(sum(shape) + 7)
@@ -87,7 +100,7 @@ def test_tc_backward_data_matches_exact(shape, gate_kind, kernel):
     dx_ref = torch.empty((n, ci, h, w), device="cuda")
     dx = torch.full_like(dx_ref, float("nan"))
     ops.conv_backward_data(dy, wt, dx_ref, k, d, gate, gate_kind or 0)
-    nb = ops.fast_workspace(co, ci, k) if kernel == "flat" else ops.bwd_fast_workspace(dy, ci, k, d)
+    nb = ops.fast_workspace(co, ci, k) if kernel != "tap" else ops.bwd_fast_workspace(dy, ci, k, d)
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     ops.conv_backward_data_fast(dy, wt, dx, k, d, ws, gate, gate_kind or 0)
     torch.cuda.synchronize()
@@ -128,8 +141,12 @@ WGRAD_SHAPES = [
 ]
 
 
+@pytest.mark.parametrize("kernel", ["ss", "tmem"])
 @pytest.mark.parametrize("shape", WGRAD_SHAPES)
-def test_tc_weight_gradient_matches_fp64(shape):
+def test_tc_weight_gradient_matches_fp64(shape, kernel, force_env):
+    """kernel="ss": shared-memory-operand kernel (tc_wgrad_ss.cu, the default); "tmem": the
+    TMEM-operand fallback (tc_wgrad.cu)."""
+    force_env(kernel)
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape

@@ -109,3 +109,18 @@ def test_reference_check_passes_with_cuda_backend(ref, dtype):
     res = check.run_check(spec, side=8, seed=0, dtype=dtype, mask_sizes=(1, 5),
                           fd_params=32, threads=1)
     assert res.ok, "\n".join(res.format_lines())
+
+
+def test_reference_bench_harness_runs_on_cuda_backend(ref):
+    """the reference's own bench harness (bench.compare_backends,
+    bench.run_bench) runs unchanged with the cuda backend registered."""
+    from denseprop import backend, bench
+    from denseprop.netspec import parse_spec
+    spec = parse_spec(_nets(ref)["example"])
+    rep = bench.compare_backends(spec, image_side=16, reps=1)
+    names = [r[0] for r in rep.rows]
+    assert "cuda" in names and "compiled" in names
+    assert "cuda" in rep.format_table()
+    backend.use("cuda")
+    report = bench.run_bench(spec, image_side=16, reps=3)
+    assert report is not None

@@ -20,6 +20,6 @@ cap 10_conv_backward_data_tc tc_conv_tap_kernel 5
 cap 09_conv_backward_kernel_tc tc_wgrad_ss_kernel 4
 cap 03_maxpool_forward maxpool_fwd_tile 5
 cap 08_maxpool_backward maxpool_bwd_tile 4
-cap stage_x tc_stage_x 4
+cap stage_x tc_stage_x 2
 cap relayout tc_relayout 5
 echo done

@@ -213,6 +213,14 @@ int dp_pad(int dtype, const void *src, void *dst, int n, int c, int h, int w,
 /* crop window (top,left,h,w) of (n,c,hs,ws) -> (n,c,h,w)  (backward.py:218-222) */
 int dp_crop(int dtype, const void *src, void *dst, int n, int c, int hs, int ws,
             int top, int left, int h, int w, void *stream);
+/* per-pixel softmax cross-entropy over q classes (not in the
+ * reference, whose delta is squared error): delta = softmax(logits) - onehot(label) and
+ * loss = -log softmax[label] where mask (may be NULL = all) is set and label != 255
+ * (ignore); zero elsewhere.  logits / delta (n, q, h, w); labels / mask uint8 (n, h, w);
+ * loss (n, h, w) or NULL. */
+int dp_softmax_xent_delta(int dtype, const void *logits, const uint8_t *labels,
+                          const uint8_t *mask, void *delta, void *loss, int n, int q, int h, int w,
+                          void *stream);
 /* patch-by-patch baseline (reference oracle.py scan_forward:145-164): gather the patch x
  * patch windows of pixels [first, first+count) (row-major over the w-wide output grid) of ONE
  * zero-padded image x0 (c, hp, wp) into out (count, c, patch, patch) */

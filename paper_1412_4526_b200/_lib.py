@@ -71,6 +71,7 @@ SIGNATURES = {
     "dp_pad": (_i, [_i, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp]),
     "dp_crop": (_i, [_i, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp]),
     "dp_patch_gather": (_i, [_i, _vp, _vp, _i, _i, _i, _i, _i, _i64, _i64, _vp]),
+    "dp_softmax_xent_delta": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp]),
     "dp_sgd_update": (_i, [_i, _vp, _vp, _i64, _d, _vp]),
 }
 

@@ -69,6 +69,9 @@ template <typename T>
 int patch_gather_t(const T *x0, T *out, int C, int Hp, int Wp, int P, int w, long long first,
                    long long count, cudaStream_t st);
 template <typename T>
+int softmax_xent_t(const T *logits, const uint8_t *labels, const uint8_t *mask, T *delta, T *loss,
+                   int n, int q, int h, int w, cudaStream_t st);
+template <typename T>
 int crop_t(const T *, T *, int, int, int, int, int, int, int, int, cudaStream_t);
 template <typename T>
 int sgd_t(T *, const T *, long long, double, cudaStream_t);
@@ -503,6 +506,24 @@ int dp_crop(int dtype, const void *src, void *dst, int n, int c, int hs, int ws,
                                      h, w, st),
                        crop_t<double>((const double *)src, (double *)dst, n, c, hs, ws, top,
                                       left, h, w, st));
+}
+
+int dp_softmax_xent_delta(int dtype, const void *logits, const uint8_t *labels,
+                          const uint8_t *mask, void *delta, void *loss, int n, int q, int h, int w,
+                          void *stream) {
+    DP_TRY(check_dtype(dtype));
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("classes", q));
+    DP_TRY(check_pos("height", h));
+    DP_TRY(check_pos("width", w));
+    if (q > 255) return set_error(DP_ERR_ARG, "softmax xent: at most 255 classes (uint8 labels)");
+    if (!logits || !labels || !delta) return set_error(DP_ERR_ARG, "softmax xent: null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    return DP_DISPATCH(dtype,
+                       softmax_xent_t<float>((const float *)logits, labels, mask, (float *)delta,
+                                             (float *)loss, n, q, h, w, st),
+                       softmax_xent_t<double>((const double *)logits, labels, mask,
+                                              (double *)delta, (double *)loss, n, q, h, w, st));
 }
 
 int dp_patch_gather(int dtype, const void *x0, void *out, int c, int hp, int wp, int patch,

@@ -134,6 +134,47 @@ int crop_t(const T *src, T *dst, int n, int c, int hs, int ws, int top, int left
     return check_launch("crop_kernel");
 }
 
+// Per-pixel softmax cross-entropy over the q output channels (the
+// 8-class labelling loss; the reference itself only has the squared-error delta,
+// cli.py:218, so this is parity-unpinned and checked against torch fp64 autograd):
+//   p = softmax(logits[n, :, y, x]),  loss = -log p[label],  delta = p - onehot(label)
+// where mask[n,y,x] != 0 and label != 255 (ignore); zero delta / loss elsewhere.
+template <typename T>
+__global__ void softmax_xent_kernel(const T *__restrict__ logits, const uint8_t *__restrict__ labels,
+                                    const uint8_t *__restrict__ mask, T *__restrict__ delta,
+                                    T *__restrict__ loss, long long npix, int q, long long hw) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npix;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long img = i / hw, px = i - img * hw;
+        const T *z = logits + img * q * hw + px;
+        T *dz = delta + img * q * hw + px;
+        const int lab = labels[i];
+        const bool on = (!mask || mask[i]) && lab < q;
+        if (!on) {
+            for (int c = 0; c < q; ++c) dz[c * hw] = T(0);
+            if (loss) loss[i] = T(0);
+            continue;
+        }
+        T m = z[0];
+        for (int c = 1; c < q; ++c) m = z[c * hw] > m ? z[c * hw] : m;
+        T s = T(0);
+        for (int c = 0; c < q; ++c) s += exp(z[c * hw] - m);
+        const T inv = T(1) / s;
+        for (int c = 0; c < q; ++c) dz[c * hw] = exp(z[c * hw] - m) * inv - (c == lab ? T(1) : T(0));
+        if (loss) loss[i] = log(s) - (z[lab * hw] - m);
+    }
+}
+
+template <typename T>
+int softmax_xent_t(const T *logits, const uint8_t *labels, const uint8_t *mask, T *delta, T *loss,
+                   int n, int q, int h, int w, cudaStream_t st) {
+    const long long npix = (long long)n * h * w;
+    if (npix == 0) return DP_OK;
+    softmax_xent_kernel<T><<<grid_for(npix), 256, 0, st>>>(logits, labels, mask, delta, loss, npix,
+                                                           q, (long long)h * w);
+    return check_launch("softmax_xent_kernel");
+}
+
 // Patch gather for the patch-by-patch baseline (reference oracle.py scan_forward:145-164 runs
 // the strided classifier on one patch per pixel): out[k, c, i, j] = x0[img, c, y+i, x+j] with
 // (y, x) = divmod(first + k, w) over the w-wide output grid of padded image img.
@@ -184,7 +225,9 @@ int sgd_t(T *p, const T *g, long long n, double lr, cudaStream_t st) {
                            cudaStream_t);                                                     \
     template int sgd_t<T>(T *, const T *, long long, double, cudaStream_t);                  \
     template int patch_gather_t<T>(const T *, T *, int, int, int, int, int, long long,        \
-                                   long long, cudaStream_t);
+                                   long long, cudaStream_t);                                  \
+    template int softmax_xent_t<T>(const T *, const uint8_t *, const uint8_t *, T *, T *, int,  \
+                                   int, int, int, cudaStream_t);
 DP_EW_INST(float)
 DP_EW_INST(double)
 

@@ -265,6 +265,15 @@ class ops:
                                                 _ptr(out), n, c, h, w, _stream()), "mask_delta")
 
     @staticmethod
+    def softmax_xent(logits, labels, mask, delta, loss=None):
+        """delta = softmax(logits) - onehot(labels) (per pixel, masked; label 255 = ignore)."""
+        with _Rec('softmax_xent', 1, 'hbm', _nbytes(logits, labels, mask, delta, loss)):
+            n, q, h, w = logits.shape
+            _lib.check(_lib_dev().dp_softmax_xent_delta(
+                _code(logits), _ptr(logits), _ptr(labels), _ptr(mask), _ptr(delta), _ptr(loss),
+                n, q, h, w, _stream()), "softmax_xent")
+
+    @staticmethod
     def pad(src, dst, top, bottom, left, right):
         with _Rec('pad', 1, 'hbm', _nbytes(src, dst)):
             n, c, h, w = src.shape
@@ -615,10 +624,15 @@ class DenseNet:
         return self.output
 
     # ------------------------------------------------------------- loss / mask
-    def loss_delta(self, target=None, mask=None, delta=None):
-        """delta_last = mask ? (output - target) : 0, or mask ? delta : 0."""
+    def loss_delta(self, target=None, mask=None, delta=None, labels=None, loss=None):
+        """delta_last = mask ? (output - target) : 0 (the reference's squared-error delta,
+        cli.py:218), or mask ? delta : 0, or -- with `labels` (uint8 (N, h, w), 255 =
+        ignore) -- the softmax cross-entropy delta softmax(output) - onehot(labels) (per-pixel
+        losses into `loss` when given)."""
         m = self.mask if mask is None else mask
-        if delta is not None:
+        if labels is not None:
+            ops.softmax_xent(self.output, labels, m, self.delta_last, loss)
+        elif delta is not None:
             ops.mask_delta(delta, m, self.delta_last)
         else:
             t = self.target if target is None else target

@@ -455,3 +455,70 @@ def test_gpu_patch_scan_equals_dense(dp, precision):
         assert torch.equal(scan, net.output)
     else:
         assert rel_err(scan.cpu().numpy(), net.output.cpu().numpy()) < 5e-5
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_softmax_xent_delta_matches_autograd(dp, dtype):
+    """SURVEY.md 8(f) item 4 (8-class labelling loss, not in the reference -- parity
+    unpinned, checked against torch fp64): delta = d(sum of masked per-pixel cross-entropy) /
+    d logits, per-pixel loss = -log softmax[label]; label 255 and mask 0 contribute nothing."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    dt = getattr(torch, dtype)
+    g = torch.Generator().manual_seed(5)
+    n, q, h, w = 2, 8, 17, 19
+    logits = (torch.randn((n, q, h, w), generator=g, dtype=torch.float64) * 3).to(dt)
+    labels = torch.randint(0, q, (n, h, w), generator=g, dtype=torch.uint8)
+    labels[0, :3] = 255
+    mask = (torch.rand((n, h, w), generator=g) < 0.7).to(torch.uint8)
+    delta = torch.empty_like(logits).cuda()
+    loss = torch.empty((n, h, w), dtype=dt).cuda()
+    ops.softmax_xent(logits.cuda(), labels.cuda(), mask.cuda(), delta, loss)
+    torch.cuda.synchronize()
+    z = logits.double().clone().requires_grad_(True)
+    on = (mask.bool() & (labels != 255))
+    lab = labels.long().clamp(max=q - 1)
+    lp = torch.log_softmax(z, dim=1)
+    px = -lp.gather(1, lab[:, None]).squeeze(1) * on
+    px.sum().backward()
+    tol = 1e-12 if dtype == "float64" else 2e-6
+    assert rel_err(delta.double().cpu().numpy(), z.grad.numpy()) < tol
+    assert rel_err(loss.double().cpu().numpy(), px.detach().numpy()) < tol
+
+
+def test_engine_step_with_softmax_xent(dp):
+    """The fused engine trains with the cross-entropy delta (fast tier): one step runs and its
+    gradient equals the exact tier's with the forward state forced (same protocol as above)."""
+    import torch
+    from paper_1412_4526_b200.engine import DenseNet
+    from paper_1412_4526_b200 import trainer
+    spec = dp.parse_spec(_c1_text(3))
+    plan = dp.compile_plan(spec)
+    side = 32
+    rng = np.random.default_rng(2)
+    img = torch.from_numpy(rng.uniform(-0.5, 0.5, (2, 3, side, side)).astype(np.float32)).cuda()
+    labels = torch.from_numpy(rng.integers(0, 10, (2, side, side)).astype(np.uint8)).cuda()
+    mask = torch.from_numpy((rng.random((2, side, side)) < 0.05).astype(np.uint8)).cuda()
+    engs = {}
+    for prec in ("exact", "fast"):
+        e = DenseNet(plan, 2, side, side, precision=prec)
+        e.set_input(img)
+        e.forward()
+        engs[prec] = e
+    ex, fa = engs["exact"], engs["fast"]
+    for gname in ex.args:
+        fa.args[gname].copy_(ex.args[gname])
+    for x_e, x_f in zip(ex.acts, fa.acts):
+        x_f.copy_(x_e)
+    for e in (ex, fa):
+        e.mask.copy_(mask)
+        e.loss_delta(labels=labels)
+        e.backward()
+    torch.cuda.synchronize()
+    ke, be = trainer.unflatten(spec, ex.grad_flat.double().cpu().numpy())
+    kf, bf = trainer.unflatten(spec, fa.grad_flat.double().cpu().numpy())
+    for k in range(len(spec.layers)):
+        if ke[k] is not None:
+            assert np.abs(ke[k]).max() > 0
+            assert rel_err(kf[k], ke[k]) < 1e-4
+            assert rel_err(bf[k], be[k]) < 1e-4

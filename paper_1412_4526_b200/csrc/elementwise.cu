@@ -34,17 +34,48 @@ __global__ void nonlin_bwd_kernel(const T *__restrict__ dy, const T *__restrict_
     }
 }
 
+// One thread per 4 pixels of one image: the mask is read once, the channels loop with
+// 16-byte stores (zeros for unmasked pixels -- a and target are only read where the mask is
+// set); the per-element 64-bit index divisions of the first version made it ALU bound.
 template <typename T>
 __global__ void mask_delta_kernel(const T *__restrict__ a, const T *__restrict__ target,
                                   const uint8_t *__restrict__ mask, T *__restrict__ out,
-                                  long long total, int C, long long HW) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        long long px = i % HW;
-        long long img = i / HW / C;
-        T v = T(0);
-        if (mask[img * HW + px]) v = target ? add_rn(a[i], -target[i]) : a[i];
-        out[i] = v;
+                                  long long nquads, int C, long long HW) {
+    const long long qpi = HW >> 2;  // quads per image (HW % 4 == 0 on this path)
+    for (long long qd = (long long)blockIdx.x * blockDim.x + threadIdx.x; qd < nquads;
+         qd += (long long)gridDim.x * blockDim.x) {
+        const long long img = qd / qpi;
+        const long long px = (qd - img * qpi) * 4;
+        const uchar4 m = *reinterpret_cast<const uchar4 *>(mask + img * HW + px);
+        const bool any = m.x | m.y | m.z | m.w;
+        const long long base = img * C * HW + px;
+        for (int c = 0; c < C; ++c) {
+            const long long i = base + (long long)c * HW;
+            T v[4] = {T(0), T(0), T(0), T(0)};
+            if (any) {
+                const uint8_t mm[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (mm[e]) v[e] = target ? add_rn(a[i + e], -target[i + e]) : a[i + e];
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) out[i + e] = v[e];
+        }
+    }
+}
+
+template <typename T>
+__global__ void mask_delta_scalar_kernel(const T *__restrict__ a, const T *__restrict__ target,
+                                         const uint8_t *__restrict__ mask, T *__restrict__ out,
+                                         long long npix, int C, long long HW) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
+         p += (long long)gridDim.x * blockDim.x) {
+        const long long img = p / HW, px = p - img * HW;
+        const bool on = mask[p];
+        for (int c = 0; c < C; ++c) {
+            const long long i = (img * C + c) * HW + px;
+            out[i] = on ? (target ? add_rn(a[i], -target[i]) : a[i]) : T(0);
+        }
     }
 }
 
@@ -108,10 +139,17 @@ int nonlin_backward_t(const T *dy, const T *x, T *dx, long long n, int kind, int
 template <typename T>
 int mask_delta_t(const T *a, const T *target, const uint8_t *mask, T *out, int n, int c, int h,
                  int w, cudaStream_t st) {
-    long long total = (long long)n * c * h * w;
-    if (total == 0) return DP_OK;
-    mask_delta_kernel<T><<<grid_for(total), 256, 0, st>>>(a, target, mask, out, total, c,
-                                                          (long long)h * w);
+    const long long HW = (long long)h * w;
+    if ((long long)n * c * HW == 0) return DP_OK;
+    const bool aligned = HW % 4 == 0 && ((uintptr_t)mask & 3) == 0;
+    if (aligned) {
+        const long long nq = (long long)n * HW / 4;
+        mask_delta_kernel<T><<<grid_for(nq), 256, 0, st>>>(a, target, mask, out, nq, c, HW);
+    } else {
+        const long long np = (long long)n * HW;
+        mask_delta_scalar_kernel<T><<<grid_for(np), 256, 0, st>>>(a, target, mask, out, np, c,
+                                                                  HW);
+    }
     return check_launch("mask_delta_kernel");
 }
 

@@ -79,19 +79,22 @@ __global__ void mask_delta_scalar_kernel(const T *__restrict__ a, const T *__res
     }
 }
 
+// One block-row of threads per destination row (plane, yy): one division per row instead of
+// two 64-bit divisions per element.
 template <typename T>
-__global__ void pad_kernel(const T *__restrict__ src, T *__restrict__ dst, long long total,
+__global__ void pad_kernel(const T *__restrict__ src, T *__restrict__ dst, long long rows,
                            int h, int w, int Hp, int Wp, int top, int left) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        int xx = (int)(i % Wp);
-        long long t = i / Wp;
-        int yy = (int)(t % Hp);
-        long long plane = t / Hp;
-        int sy = yy - top, sx = xx - left;
-        T v = T(0);
-        if (sy >= 0 && sy < h && sx >= 0 && sx < w) v = src[(plane * h + sy) * w + sx];
-        dst[i] = v;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+        const long long plane = r / Hp;
+        const int yy = (int)(r - plane * Hp);
+        const int sy = yy - top;
+        const bool rin = sy >= 0 && sy < h;
+        const T *srow = src + (plane * h + (rin ? sy : 0)) * (long long)w;
+        T *drow = dst + r * (long long)Wp;
+        for (int xx = threadIdx.x; xx < Wp; xx += blockDim.x) {
+            const int sx = xx - left;
+            drow[xx] = (rin && sx >= 0 && sx < w) ? srow[sx] : T(0);
+        }
     }
 }
 
@@ -159,7 +162,9 @@ int pad_t(const T *src, T *dst, int n, int c, int h, int w, int top, int bottom,
     int Hp = h + top + bottom, Wp = w + left + right;
     long long total = (long long)n * c * Hp * Wp;
     if (total == 0) return DP_OK;
-    pad_kernel<T><<<grid_for(total), 256, 0, st>>>(src, dst, total, h, w, Hp, Wp, top, left);
+    const long long rows = (long long)n * c * Hp;
+    const long long g = rows < 148LL * 64 ? rows : 148LL * 64;
+    pad_kernel<T><<<(int)g, 128, 0, st>>>(src, dst, rows, h, w, Hp, Wp, top, left);
     return check_launch("pad_kernel");
 }
 

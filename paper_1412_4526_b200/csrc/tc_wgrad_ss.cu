@@ -377,27 +377,30 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     if (warp == WS_MMA_WARP) ptx::tmem_dealloc<512>(tmem);
 }
 
-// dw[o,c,i,j] = sum_s part[s][line(i, j, c)][o], db[o] = sum_s pdb[s][o]  (fixed order)
+// dw[o,c,i,j] = sum_s part[s][line(i, j, c)][o], db[o] = sum_s pdb[s][o]  (fixed order:
+// s = 0, 1, ... sequentially per entry).  Threads walk (line, o) with o fastest so the
+// split-strided partial reads are coalesced; gap lines (residue-box padding) are skipped.
 __global__ void ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb,
                           float *__restrict__ dw, float *__restrict__ db, int Q, int C, int l,
                           int d, int Ls, int Npad, int splits, int rows_pad, WsResidues rs) {
-    const long long total = (long long)Q * C * l * l;
+    const long long lines = (long long)l * Ls;
+    const long long total = lines * Npad;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < total) {
-        const int ll = l * l;
-        const int o = (int)(idx / ((long long)C * ll));
-        const int rem = (int)(idx - (long long)o * C * ll);
-        const int c = rem / ll, tap = rem - (rem / ll) * ll;
-        const int i = tap / l, j = tap - (tap / l) * l;
-        const int b = (j * d) & 3;
-        int rb = 0;
-        if (!rs.tapcopy)
-            while (rs.b[rb] != b) ++rb;
-        const int jj = rs.tapcopy ? j : (j - rs.j0[rb]) / rs.step;
-        const size_t line = (size_t)i * Ls + rs.line0[rb] + c * rs.n[rb] + jj;
+        const int o = (int)(idx % Npad);
+        const long long line = idx / Npad;
+        if (o >= Q) return;
+        const int i = (int)(line / Ls), rem = (int)(line - (long long)i * Ls);
+        int rb = -1;
+        for (int r = 0; r < rs.n_b; ++r)
+            if (rem >= rs.line0[r] && rem < rs.line0[r] + C * rs.n[r]) rb = r;
+        if (rb < 0) return;  // gap line
+        const int off = rem - rs.line0[rb];
+        const int c = off / rs.n[rb], jj = off - c * rs.n[rb];
+        const int j = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
         float acc = 0.f;
         for (int s = 0; s < splits; ++s) acc += part[((size_t)s * rows_pad + line) * Npad + o];
-        dw[idx] = acc;
+        dw[(((long long)o * C + c) * l + i) * l + j] = acc;
     } else if (idx < total + Q) {
         const int o = (int)(idx - total);
         float acc = 0.f;
@@ -668,7 +671,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     tc_wgrad_ss_kernel<<<grid, WS_THREADS, smem, st>>>(mx[0], mx[1], mx[2], mx[3], mdy, a);
     rc = check_launch("tc_wgrad_ss_kernel");
     if (rc) return rc;
-    const long long total = (long long)cout * cin * k * k + cout;
+    const long long total = (long long)k * p.Ls * p.Npad + cout;
     ws_reduce<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, d, p.Ls,
                                                     p.Npad, p.splits, p.n_tiles * 128, p.rs);
     return check_launch("ws_reduce");

@@ -85,6 +85,7 @@ struct WsArgs {
     WsResidues rs;
     float *part;  // [splits][n_tiles * 128][Npad]
     float *pdb;   // [splits][Npad]
+    int no_m64;   // DP_WG_NO_M64: run a short last tile as M = 128 (experiments)
     unsigned long long *trace;  // DP_WG_TRACE: per-K-block clock64 stamps of CTA 0
 };
 
@@ -156,6 +157,9 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     const int lines_total = a.l * a.Ls;
     const int i_lo = tile0 * 128 / a.Ls;
     const int n_i = (min((tile0 + G) * 128, lines_total) - 1) / a.Ls - i_lo + 1;
+    // a last tile with <= 64 real lines runs as M = 64 (D rows r -> TMEM quadrant r / 16,
+    // lane r % 16; measured, tools/m64_probe.cu): half its A reads and tensor work
+    const bool tail64 = !a.no_m64 && min((tile0 + G) * 128, lines_total) - (tile0 + G - 1) * 128 <= 64;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.SS; ++s) {
@@ -226,6 +230,8 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         // ================================ MMA issuer ================================
         const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
         const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
+        const uint32_t idesc_2n64 = ptx::idesc_tf32(64, 2 * a.Npad);
+        const uint32_t idesc_n64 = ptx::idesc_tf32(64, a.Npad);
         const uint32_t sbase = ptx::smem_u32(smem);
         const uint32_t hi_base = sbase + a.ring_hi, lo_base = sbase + a.ring_lo;
         // tile 0's first ring slot (relative to the block's Bm) and line inside it; later
@@ -246,13 +252,15 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 for (int t = 0; t < G; ++t) {
                     const uint32_t off = (uint32_t)slot * a.slot_bytes + (uint32_t)lin * 128u;
                     const uint32_t dcol = tmem + (uint32_t)(t * acc_cols);
+                    const bool m64 = tail64 && t == G - 1;
+                    const uint32_t i2 = m64 ? idesc_2n64 : idesc_2n, i1 = m64 ? idesc_n64 : idesc_n;
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
                         const uint64_t bd = ptx::smem_desc_sw128(bstage + ks * 32);
                         ptx::mma_tf32_ss(dcol, ptx::smem_desc_sw128(hi_base + off + ks * 32), bd,
-                                         idesc_2n, (kl | ks) > 0);
+                                         i2, (kl | ks) > 0);
                         ptx::mma_tf32_ss(dcol, ptx::smem_desc_sw128(lo_base + off + ks * 32), bd,
-                                         idesc_n, 1);
+                                         i1, 1);
                     }
                     // next tile: 128 lines on; past a slot's end the lines continue in the
                     // next slot (or its mirror past the ring's end)
@@ -349,7 +357,10 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         }
         const size_t rows_pad = (size_t)a.n_tiles * 128;
         for (int t = grp; t < G; t += 2) {
-            const int grow = (tile0 + t) * 128 + q * 32 + lane;
+            const bool m64 = tail64 && t == G - 1;
+            // M = 64 tile: rows live in lanes 0-15 of each quadrant (lanes 16-31 unused)
+            const int grow = (tile0 + t) * 128 + (m64 ? q * 16 : q * 32) + lane;
+            const bool store = !m64 || lane < 16;
             float *dstp = a.part + ((size_t)split * rows_pad + grow) * a.Npad;
             for (int o0 = 0; o0 < a.Npad; o0 += 16) {
                 uint32_t h[16], l2[16];
@@ -367,7 +378,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                                         __uint_as_float(h[k + 1]) + __uint_as_float(l2[k + 1]),
                                         __uint_as_float(h[k + 2]) + __uint_as_float(l2[k + 2]),
                                         __uint_as_float(h[k + 3]) + __uint_as_float(l2[k + 3]));
-                    *reinterpret_cast<float4 *>(dstp + o0 + k) = v;
+                    if (store) *reinterpret_cast<float4 *>(dstp + o0 + k) = v;
                 }
             }
         }
@@ -662,6 +673,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
     a.rs = p.rs;
     a.trace = getenv("DP_WG_TRACE") ? wg_trace_buffer(st) : nullptr;
+    a.no_m64 = getenv("DP_WG_NO_M64") ? 1 : 0;
     const size_t smem = (size_t)a.ring_lo + (size_t)(p.R + p.NM) * p.slot_bytes + 1024;
     cudaError_t e = cudaFuncSetAttribute(tc_wgrad_ss_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -27,8 +27,14 @@
 // overwrites was last read by block kl - SS (R = n_i + SS - 1 slots); a column start waits
 // for the previous block (a drain every ~Ho/d blocks).
 //
+// Small-cin layers with several residues (c2 conv1: cin 3, d 1) stage one pre-shifted copy
+// of x per tap instead (tc_stage_x_taps): a single box {32 px, l taps, cin, 1 row} per input
+// row rather than one tiny box per residue (the TMA box rate was their limit).
+//
 // 3xTF32 per K=8 slice and tile: A_hi x [B_hi | B_lo] (N = 2 Npad) + A_lo x B_hi (N = Npad);
-// accumulators stay in TMEM (all tiles of the CTA's group: no A staging in TMEM at all).
+// accumulators stay in TMEM (all tiles of the CTA's group: no A staging in TMEM at all).  A
+// group's last tile with <= 64 real lines runs as M = 64 (D row r in TMEM quadrant r / 16,
+// lane r % 16 -- measured with tools/m64_probe.cu).
 //
 // Roles (one CTA per SM, 10 warps): warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer,
 // warps 0-7 converters (dy B_lo + db, lo lines of new rows) and the epilogue.  Split-K over

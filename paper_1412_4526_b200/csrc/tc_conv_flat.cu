@@ -56,7 +56,7 @@ constexpr int TF_LOAD_WARP0 = 4;
 constexpr int TF_LOAD_WARPS = 8;
 constexpr int TF_MMA_WARP = 12;
 constexpr int TF_THREADS = (TF_MMA_WARP + 1) * 32;
-constexpr int TF_MAX_MT = 4;
+constexpr int TF_MAX_MT = 8;
 constexpr int TF_MAX_HB = 6;
 constexpr int TF_LGROUPS = 2;  // loader groups, alternate units (two units' loads in flight)
 constexpr int TF_LGW = TF_LOAD_WARPS / TF_LGROUPS;  // warps per loader group

@@ -471,12 +471,13 @@ __global__ void __launch_bounds__(256) tc_stage_x_taps(const float *__restrict__
     }
 }
 
-// dy staging: NCHW (n, o, h, w) -> (n, h, o, wp), zero pad.  A K block's dy box then
-// reads Npad lines wp floats apart instead of one line per channel plane (plane-strided
-// boxes measured ~4x slower here: every line opens a different DRAM page).
+// dy staging: NCHW (n, o, h, w) -> (n, h, o, wp), zero pad (lm zeros left of the data, lm a
+// multiple of 4, the rest right of it).  A K block's dy box then reads Npad lines wp floats
+// apart instead of one line per channel plane (plane-strided boxes measured ~4x slower
+// here: every line opens a different DRAM page).
 __global__ void __launch_bounds__(256) tc_stage_dy(const float *__restrict__ src,
                                                    float *__restrict__ dst, int O, int H, int w,
-                                                   int wp, long long total_quads) {
+                                                   int wp, int lm, long long total_quads) {
     const int nq = wp >> 2;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total_quads;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -489,7 +490,10 @@ __global__ void __launch_bounds__(256) tc_stage_dy(const float *__restrict__ src
         const float *s = src + row * w;
         float e[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) e[t] = v + t < w ? __ldg(s + v + t) : 0.f;
+        for (int t = 0; t < 4; ++t) {
+            const int c = v + t - lm;
+            e[t] = (c >= 0 && c < w) ? __ldg(s + c) : 0.f;
+        }
         *reinterpret_cast<float4 *>(dst + ((n * H + h) * O + o) * wp + v) =
             make_float4(e[0], e[1], e[2], e[3]);
     }
@@ -689,10 +693,10 @@ int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, i
             return set_error(DP_ERR_CUDA, "weight gradient: memset of staged tails failed");
     return DP_OK;
 }
-int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
+int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
                 cudaStream_t st) {
     const long long quads = (long long)n * cout * ho * (wp / 4);
-    tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, quads);
+    tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, lm, quads);
     return check_launch("tc_stage_dy");
 }
 
@@ -778,7 +782,7 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
         const long long quads = (long long)n * cout * p.ho * (p.wp_dy / 4);
-        tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy, quads);
+        tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy, 0, quads);
         rc = check_launch("tc_stage_dy");
         if (rc) return rc;
         dys = dp_;

@@ -6,7 +6,7 @@
 // (reference _kernels.pyx:94-130, _kernels_py.py:54-66) as D[r, o] = sum_k A[r, k] B[o, k]:
 //   k = output pixel, K blocks of 32 consecutive v of one output row u  (the long axis)
 //   r = x tap line (i, residue copy, c, jj)                             -> M, tiles of 128
-//   o = output channel (padded to Npad)                                 -> N
+//   o = output channel (x J column-tap shifts, padded to 16)             -> N
 //
 // x tap lines.  tc_stage_x lays x out as (n, h, c, wp) copies shifted left by
 // b = (j*d) & 3 for each residue b that occurs, so that for one residue copy the taps j with
@@ -31,7 +31,7 @@
 // of x per tap instead (tc_stage_x_taps): a single box {32 px, l taps, cin, 1 row} per input
 // row rather than one tiny box per residue (the TMA box rate was their limit).
 //
-// 3xTF32 per K=8 slice and tile: A_hi x [B_hi | B_lo] (N = 2 Npad) + A_lo x B_hi (N = Npad);
+// 3xTF32 per K=8 slice and tile: A_hi x [B_hi | B_lo] (N = 2 NB) + A_lo x B_hi (N = NB);
 // accumulators stay in TMEM (all tiles of the CTA's group: no A staging in TMEM at all).  A
 // group's last tile with <= 64 real lines runs as M = 64 (D row r in TMEM quadrant r / 16,
 // lane r % 16 -- measured with tools/m64_probe.cu).
@@ -58,7 +58,7 @@ int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp
                long long copy_floats, cudaStream_t st);
 int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int l,
                     int d, long long copy_floats, cudaStream_t st);
-int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp,
+int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
                 cudaStream_t st);
 
 constexpr int WS_CONV_WARPS = 8;
@@ -81,21 +81,25 @@ struct WsResidues {
 
 struct WsArgs {
     int C, Cpad, l, d, Q, Npad;
+    int J, sb, NB;       // dy copies per stage, their shift step (Ja*d floats, 4 | sb), N
+                         // (J*Q rows rounded up to 16: B rows jb'*Q + o, zero rows past J*Q)
+    int tma_mirror;      // DP_WG_TMA_MIRROR: mirror slots loaded by TMA, not the converters
     int n_tiles, G, n_groups, splits;
     int Ho, Wo, nvb, T, Hi;
     long long kb_total;  // n * nvb * d columns x T blocks
     int SS, R, NM, Ls;   // dy stages, ring slots, mirrored slots, lines per slot
-    uint32_t b_bytes;    // dy stage: B_hi + B_lo (2 * Npad * 128)
+    uint32_t b_bytes;    // dy stage: B_hi + B_lo (2 * NB * 128)
     uint32_t slot_bytes, box_tx_row;  // Ls * 128
     uint32_t ring_hi, ring_lo;        // shared-memory offsets
     WsResidues rs;
-    float *part;  // [splits][n_tiles * 128][Npad]
+    float *part;  // [splits][n_tiles * 128][NB]
     float *pdb;   // [splits][Npad]
     int no_m64;   // DP_WG_NO_M64: run a short last tile as M = 128 (experiments)
     unsigned long long *trace;  // DP_WG_TRACE: per-K-block clock64 stamps of CTA 0
 };
 
-// slots: 0 TMA issue, 2 converters got the stage, 4 converters done, 8 MMA got, 9 issued
+// slots: 1 producer ready, 0 TMA issue, 2 converters got the stage, 4 converters done,
+// 10 MMA ready, 8 MMA got, 9 issued
 #define WS_TRACE(A, KL, SLOT, COND)                                               \
     do {                                                                          \
         if ((A).trace && (COND) && blockIdx.x == 0 && (KL) < 256)                 \
@@ -159,7 +163,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     const int G = min(a.G, a.n_tiles - tile0);
     const long long kb_first = a.kb_total * split / a.splits;
     const int nkb = (int)(a.kb_total * (split + 1) / a.splits - kb_first);
-    const int acc_cols = 2 * a.Npad;
+    const int acc_cols = 2 * a.NB;
     const int lines_total = a.l * a.Ls;
     const int i_lo = tile0 * 128 / a.Ls;
     const int n_i = (min((tile0 + G) * 128, lines_total) - 1) / a.Ls - i_lo + 1;
@@ -192,6 +196,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         unsigned char *ring = smem + a.ring_hi;
         for (int kl = 0; kl < nkb; ++kl, sc.next()) {
             const int s = kl % a.SS;
+            WS_TRACE(a, kl, 1, lane == 0);
             ptx::mbar_wait(&sempty[s], ((kl / a.SS) & 1) ^ 1);
             if (sc.cstart && kl > 0) {
                 const int kw = kl - 1;  // column start: drain (see header)
@@ -206,18 +211,26 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 for (int k = k0; k < n_i; ++k) {
                     int slot = sc.Bm + k;
                     if (slot >= a.R) slot -= a.R;
-                    nbox_rows += slot < a.NM ? 2 : 1;
+                    nbox_rows += (a.tma_mirror && slot < a.NM) ? 2 : 1;
                 }
-                ptx::mbar_expect_tx(&sfull[s], (uint32_t)a.Npad * 128u +
+                ptx::mbar_expect_tx(&sfull[s], (uint32_t)(a.J * a.Q) * 128u +
                                                    (uint32_t)nbox_rows * a.box_tx_row);
-                ptx::tma_load_4d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, sc.u, 0, sc.img,
-                                 &sfull[s]);
+                if (a.J == 1) {
+                    ptx::tma_load_4d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, sc.u, 0, sc.img,
+                                     &sfull[s]);
+                } else {
+                    // ONE box {32 px, Q, J} of the overlapping view (w, o, jb' = J-1-jb: sb
+                    // floats apart, ...) of the zero-margined staged dy: rows jb'*Q + o hold
+                    // dy shifted right by jb*sb for the column taps j = jb*Ja + ja
+                    ptx::tma_load_5d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, 0, 0, sc.u,
+                                     sc.img, &sfull[s]);
+                }
                 for (int k = k0; k < n_i; ++k) {
                     int slot = sc.Bm + k;
                     if (slot >= a.R) slot -= a.R;
                     const int row = hh + (i_lo + k) * a.d;
                     for (int copy = 0; copy < 2; ++copy) {
-                        if (copy == 1 && slot >= a.NM) break;
+                        if (copy == 1 && (slot >= a.NM || !a.tma_mirror)) break;
                         unsigned char *dst =
                             ring + (size_t)(copy ? a.R + slot : slot) * a.slot_bytes;
                         for (int rb = 0; rb < a.rs.n_b; ++rb) {
@@ -234,46 +247,45 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         }
     } else if (warp == WS_MMA_WARP) {
         // ================================ MMA issuer ================================
-        const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
-        const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
-        const uint32_t idesc_2n64 = ptx::idesc_tf32(64, 2 * a.Npad);
-        const uint32_t idesc_n64 = ptx::idesc_tf32(64, a.Npad);
+        const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.NB);
+        const uint32_t idesc_n = ptx::idesc_tf32(128, a.NB);
+        const uint32_t idesc_2n64 = ptx::idesc_tf32(64, 2 * a.NB);
+        const uint32_t idesc_n64 = ptx::idesc_tf32(64, a.NB);
         const uint32_t sbase = ptx::smem_u32(smem);
         const uint32_t hi_base = sbase + a.ring_hi, lo_base = sbase + a.ring_lo;
         // tile 0's first ring slot (relative to the block's Bm) and line inside it; later
         // tiles follow 128 lines on (incremental: this thread's loop is the critical path)
         const int line00 = tile0 * 128 - i_lo * a.Ls;
         const int slot00 = line00 / a.Ls, lin00 = line00 - slot00 * a.Ls;
+        const int RL = a.R * a.Ls;  // ring lines (the mirrors follow)
+        const uint64_t lo_units = (uint64_t)((a.ring_lo - a.ring_hi) >> 4);
         WsSched sc(a, kb_first, n_i);
         int s = 0;
         uint32_t ph = 0;
         for (int kl = 0; kl < nkb; ++kl, sc.next()) {
+            WS_TRACE(a, kl, 10, lane == 0);
             ptx::mbar_wait(&cfull[s], ph);
             ptx::tc_fence_after();
             WS_TRACE(a, kl, 8, lane == 0);
             if (ptx::elect_one()) {
-                const uint32_t bstage = sbase + (uint32_t)s * a.b_bytes;
-                int slot = sc.Bm + slot00, lin = lin00;
-                if (slot >= a.R) slot -= a.R;
-                for (int t = 0; t < G; ++t) {
-                    const uint32_t off = (uint32_t)slot * a.slot_bytes + (uint32_t)lin * 128u;
+                const uint64_t bd0 = ptx::smem_desc_sw128(sbase + (uint32_t)s * a.b_bytes);
+                // tile t starts at ring line P0 + 128 t: descriptor +1024 (16 KB >> 4) per
+                // tile; past a slot's end its lines continue in the next slot (or the mirror
+                // past the ring's end), and a tile STARTING past the end wraps (-RL lines).
+                // Plain 64-bit adds on the descriptor: this thread is the critical path.
+                int slot0 = sc.Bm + slot00;
+                if (slot0 >= a.R) slot0 -= a.R;
+                int P = slot0 * a.Ls + lin00;
+                uint64_t dh = ptx::smem_desc_sw128(hi_base + (uint32_t)P * 128u);
+                for (int t = 0; t < G; ++t, P += 128, dh += 1024) {
+                    const uint64_t da = P >= RL ? dh - (uint64_t)(RL * 8) : dh;
                     const uint32_t dcol = tmem + (uint32_t)(t * acc_cols);
                     const bool m64 = tail64 && t == G - 1;
                     const uint32_t i2 = m64 ? idesc_2n64 : idesc_2n, i1 = m64 ? idesc_n64 : idesc_n;
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
-                        const uint64_t bd = ptx::smem_desc_sw128(bstage + ks * 32);
-                        ptx::mma_tf32_ss(dcol, ptx::smem_desc_sw128(hi_base + off + ks * 32), bd,
-                                         i2, (kl | ks) > 0);
-                        ptx::mma_tf32_ss(dcol, ptx::smem_desc_sw128(lo_base + off + ks * 32), bd,
-                                         i1, 1);
-                    }
-                    // next tile: 128 lines on; past a slot's end the lines continue in the
-                    // next slot (or its mirror past the ring's end)
-                    lin += 128;
-                    while (lin >= a.Ls) {
-                        lin -= a.Ls;
-                        if (++slot == a.R) slot = 0;  // a tile STARTING past the end wraps
+                        ptx::mma_tf32_ss(dcol, da + 2 * ks, bd0 + 2 * ks, i2, (kl | ks) > 0);
+                        ptx::mma_tf32_ss(dcol, da + lo_units + 2 * ks, bd0 + 2 * ks, i1, 1);
                     }
                 }
                 ptx::mma_commit(&sempty[s]);
@@ -290,7 +302,15 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     } else {
         // ================================ converters ================================
         const int tid = threadIdx.x;  // 0..255
-        const int nchunks = a.Npad * 8;  // 16-byte chunks of the dy tile
+        const int nchunks = a.NB * 8;    // 16-byte chunks of the dy tiles
+        const int db0 = (a.J - 1) * a.Q * 8;  // the unshifted copy (jb' = J-1): db
+        const int db1 = db0 + a.Q * 8;
+        // B rows past J*Q are never loaded: zero them once in every stage
+        for (int st_ = 0; st_ < a.SS; ++st_) {
+            float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)st_ * a.b_bytes);
+            for (int idx = a.J * a.Q * 8 + tid; idx < nchunks; idx += WS_CONV_WARPS * 32)
+                bh[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
         const int lchunks = a.Ls * 8;    // 16-byte chunks of a ring slot
         WsSched sc(a, kb_first, n_i);
@@ -303,13 +323,13 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
             {
                 // B_lo = B_hi - trunc(B_hi) (elementwise; the swizzle is preserved) + db
                 const float4 *bh = reinterpret_cast<const float4 *>(st);
-                float4 *bl = reinterpret_cast<float4 *>(st + (uint32_t)a.Npad * 128);
+                float4 *bl = reinterpret_cast<float4 *>(st + (uint32_t)a.NB * 128);
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const int idx = tid + 256 * m;
                     if (idx >= nchunks) break;
                     const float4 v = bh[idx];
-                    dbacc[m] += (v.x + v.y) + (v.z + v.w);
+                    if (idx >= db0 && idx < db1) dbacc[m] += (v.x + v.y) + (v.z + v.w);
                     bl[idx] = make_float4(ptx::tf32_lo(v.x), ptx::tf32_lo(v.y), ptx::tf32_lo(v.z),
                                           ptx::tf32_lo(v.w));
                 }
@@ -325,12 +345,19 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 float4 *dst2 = slot < a.NM ? reinterpret_cast<float4 *>(
                                                  smem + a.ring_lo + (size_t)(a.R + slot) * a.slot_bytes)
                                            : nullptr;
+                // the hi mirror too (one TMA row request less per mirrored row: the TMA
+                // unit's row rate is this kernel's feed limit)
+                float4 *hm = (slot < a.NM && !a.tma_mirror)
+                                 ? reinterpret_cast<float4 *>(smem + a.ring_hi +
+                                                              (size_t)(a.R + slot) * a.slot_bytes)
+                                 : nullptr;
                 for (int idx = tid; idx < lchunks; idx += WS_CONV_WARPS * 32) {
                     const float4 v = src[idx];
                     const float4 lo = make_float4(ptx::tf32_lo(v.x), ptx::tf32_lo(v.y),
                                                   ptx::tf32_lo(v.z), ptx::tf32_lo(v.w));
                     dst[idx] = lo;
                     if (dst2) dst2[idx] = lo;
+                    if (hm) hm[idx] = v;
                 }
             }
             ptx::fence_proxy_async_smem();
@@ -350,8 +377,9 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
                 v += __shfl_xor_sync(0xffffffffu, v, 2);
                 v += __shfl_xor_sync(0xffffffffu, v, 4);
-                const int row = (tid >> 3) + 32 * m;
-                if ((lane & 7) == 0 && row < a.Npad) a.pdb[(size_t)split * a.Npad + row] = v;
+                const int row = (tid >> 3) + 32 * m - (a.J - 1) * a.Q;
+                if ((lane & 7) == 0 && row >= 0 && row < a.Q)
+                    a.pdb[(size_t)split * a.Npad + row] = v;
             }
         }
         // ---- epilogue: tiles t = grp, grp + 2, ...; lane = line
@@ -367,13 +395,13 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
             // M = 64 tile: rows live in lanes 0-15 of each quadrant (lanes 16-31 unused)
             const int grow = (tile0 + t) * 128 + (m64 ? q * 16 : q * 32) + lane;
             const bool store = !m64 || lane < 16;
-            float *dstp = a.part + ((size_t)split * rows_pad + grow) * a.Npad;
-            for (int o0 = 0; o0 < a.Npad; o0 += 16) {
+            float *dstp = a.part + ((size_t)split * rows_pad + grow) * a.NB;
+            for (int o0 = 0; o0 < a.NB; o0 += 16) {
                 uint32_t h[16], l2[16];
                 if (nkb > 0) {
                     const uint32_t dcol = tmem + lane_off + (uint32_t)(t * acc_cols + o0);
                     ptx::tmem_ld16(dcol, h);
-                    ptx::tmem_ld16(dcol + a.Npad, l2);
+                    ptx::tmem_ld16(dcol + a.NB, l2);
                     ptx::tmem_wait_ld();
                 }
 #pragma unroll
@@ -399,14 +427,18 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
 // split-strided partial reads are coalesced; gap lines (residue-box padding) are skipped.
 __global__ void ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb,
                           float *__restrict__ dw, float *__restrict__ db, int Q, int C, int l,
-                          int d, int Ls, int Npad, int splits, int rows_pad, WsResidues rs) {
+                          int Ls, int Npad, int J, int Ja, int splits, int rows_pad,
+                          WsResidues rs) {
     const long long lines = (long long)l * Ls;
-    const long long total = lines * Npad;
+    const int NB = (J * Q + 15) / 16 * 16;
+    const long long total = lines * NB;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < total) {
-        const int o = (int)(idx % Npad);
-        const long long line = idx / Npad;
-        if (o >= Q) return;
+        const int col = (int)(idx % NB);
+        const long long line = idx / NB;
+        if (col >= J * Q) return;  // zero B rows
+        const int jr = col / Q, o = col - jr * Q;
+        const int jb = J - 1 - jr;  // B row blocks hold the shifts in reverse (jb' = J-1-jb)
         const int i = (int)(line / Ls), rem = (int)(line - (long long)i * Ls);
         int rb = -1;
         for (int r = 0; r < rs.n_b; ++r)
@@ -414,14 +446,16 @@ __global__ void ws_reduce(const float *__restrict__ part, const float *__restric
         if (rb < 0) return;  // gap line
         const int off = rem - rs.line0[rb];
         const int c = off / rs.n[rb], jj = off - c * rs.n[rb];
-        const int j = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
+        const int ja = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
+        const int j = jb * Ja + ja;
+        if (j >= l) return;  // padding tap of the last column group
         float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += part[((size_t)s * rows_pad + line) * Npad + o];
+        for (int s = 0; s < splits; ++s) acc += part[((size_t)s * rows_pad + line) * NB + col];
         dw[(((long long)o * C + c) * l + i) * l + j] = acc;
     } else if (idx < total + Q) {
         const int o = (int)(idx - total);
         float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += pdb[(size_t)s * Npad + o];
+        for (int s = 0; s < splits; ++s) acc += pdb[(size_t)s * Npad + o];  // pdb: Npad wide
         db[o] = acc;
     }
 }
@@ -430,8 +464,9 @@ __global__ void ws_reduce(const float *__restrict__ part, const float *__restric
 // host side
 // --------------------------------------------------------------------------------
 struct WsPlan {
+    int J, kc, dc, sb, NB;  // J dy copies (B), kc = Ja column taps in the x lines (A), step dc = d
     int Cpad, Npad, Ls, n_tiles, G, n_groups, splits, SS, R, NM, max_ni;
-    int ho, wo, nvb, T, wp_x, wp_dy, mask;
+    int ho, wo, nvb, T, wp_x, wp_dy, lm_dy, mask;
     bool stage_dy;
     long long kb_total;
     WsResidues rs;
@@ -441,7 +476,48 @@ struct WsPlan {
 
 static size_t ws_align256(size_t v) { return (v + 255) / 256 * 256; }
 
+static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, int Ja,
+                      WsPlan &p);
+
+// Column-tap stacking: column tap j = jb*Ja + ja.  The x lines (A) cover only Ja taps ja
+// (offsets ja*d), and J = ceil(k / Ja) copies of dy shifted right by jb*Ja*d sit side by
+// side in the B operand (N = J * Q, rounded up to 16): J times fewer A lines -- fewer M tiles, i.e. fewer A
+// reads from shared memory per useful MAC -- for wider MMAs and J dy boxes per K block.  The
+// shift must be a multiple of 4 floats (a TMA box starts on a 16-byte boundary), so J > 1
+// needs 4 | Ja*d (Ja = k: no stacking, the unstacked kernel).  Ja is picked by a per-K-block
+// cost model of the shared-memory operand bytes (A hi + lo per tile, B per MMA) and issue
+// slots; DP_WG_J=<J> forces the smallest legal Ja with that many dy copies.
 static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPlan &p) {
+    if (const char *e = getenv("DP_WG_J")) {
+        const int J = atoi(e);
+        for (int Ja = 1; Ja <= k && J >= 1; ++Ja)
+            if ((k + Ja - 1) / Ja == J && ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, p))
+                return true;
+    }
+    bool ok = false;
+    double best = 0;
+    for (int Ja = k; Ja >= 1; --Ja) {
+        WsPlan q;
+        if (!ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, q)) continue;
+        // per K=8 slice: each tile reads A hi + lo (M rows x 32 B) and B (2 NB + NB rows)
+        double cost = 0;
+        const int lines = k * q.Ls;
+        for (int t = 0; t < q.n_tiles; ++t) {
+            const int m = std::min(128, lines - t * 128) <= 64 ? 64 : 128;
+            cost += 2.0 * m * 32 + 3.0 * q.NB * 32 + 1500;  // + fixed per-MMA-pair overhead
+        }
+        cost *= (double)q.nvb;  // K blocks per row grow with the (J-1) Ja d shift
+        if (!ok || cost < best) {
+            best = cost;
+            p = q;
+            ok = true;
+        }
+    }
+    return ok;
+}
+
+static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, int Ja,
+                      WsPlan &p) {
     if (getenv("DP_WG_TMEM")) return false;  // force the TMEM-operand kernel (experiments)
     const int e = (k - 1) * d + 1;
     p.ho = hi - e + 1;
@@ -449,6 +525,16 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     if (p.ho < 1 || p.wo < 1 || k > 64) return false;
     p.Npad = (cout + 15) / 16 * 16;
     if (p.Npad > 128) return false;
+    if (Ja < 1 || Ja > k) return false;
+    const int J = (k + Ja - 1) / Ja;
+    p.J = J;
+    p.NB = (J * cout + 15) / 16 * 16;
+    if (2 * p.NB > 256) return false;
+    p.kc = Ja;
+    p.dc = d;
+    p.sb = p.kc * d;
+    if (J > 1 && (p.sb & 3)) return false;
+    const int kc = p.kc, dc = p.dc;
     p.Cpad = (cin + 7) / 8 * 8;
     if (p.Cpad > 256) return false;
     // lines per ring slot (one input row): residue boxes, each rounded up to 8 lines.  Small
@@ -460,7 +546,7 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
         int ls = 0;
         for (int b = 0; b < 4; ++b) {
             int cnt = 0;
-            for (int j = 0; j < k; ++j) cnt += ((j * d) & 3) == b;
+            for (int j = 0; j < kc; ++j) cnt += ((j * dc) & 3) == b;
             if (cnt) {
                 ls += (cin * cnt + 7) / 8 * 8;
                 ++nres;
@@ -468,13 +554,13 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
         }
         p.Ls = ls;
     }
-    p.rs.tapcopy = (nres > 1 && cin * k <= 32 && !getenv("DP_WG_RESIDUE")) ? 1 : 0;
-    if (p.rs.tapcopy) p.Ls = (cin * k + 7) / 8 * 8;
+    p.rs.tapcopy = (nres > 1 && cin * kc <= 32 && !getenv("DP_WG_RESIDUE")) ? 1 : 0;
+    if (p.rs.tapcopy) p.Ls = (cin * kc + 7) / 8 * 8;
     const int lines = k * p.Ls;
     p.n_tiles = (lines + 127) / 128;
-    const int acc_cols = 2 * p.Npad;
+    const int acc_cols = 2 * p.NB;
     p.slot_bytes = (uint32_t)p.Ls * 128u;  // multiple of 8 lines: 1024-byte aligned boxes
-    p.b_bytes = 2u * (uint32_t)p.Npad * 128u;
+    p.b_bytes = 2u * (uint32_t)p.NB * 128u;
     // Tile groups: as many tiles per CTA as TMEM holds, unless the ring (hi + lo slots for
     // the group's tap rows + SS - 1 + mirrors) does not fit -- then smaller groups (fewer
     // tap rows each; every group re-reads its rows), down to one tile.
@@ -508,20 +594,20 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     }
     if (p.SS < 2) return false;
     p.R = p.max_ni + p.SS - 1;
-    // residue copies: taps j with (j*d) & 3 == b, lcm(d, 4) floats apart
+    // residue copies: column taps jo with (jo*dc) & 3 == b, lcm(dc, 4) floats apart
     int gcd = 1;
     for (int v = 4; v >= 1; --v)
-        if (d % v == 0 && 4 % v == 0) {
+        if (dc % v == 0 && 4 % v == 0) {
             gcd = v;
             break;
         }
     p.rs.step = 4 / gcd;
     p.mask = 0;
     p.rs.n_b = 0;
-    if (p.rs.tapcopy) {  // one "residue" holding all l taps (copy j pre-shifted by j*d)
+    if (p.rs.tapcopy) {  // one "residue" holding all kc taps (copy jo pre-shifted by jo*dc)
         p.rs.n_b = 1;
         p.rs.b[0] = 0;
-        p.rs.n[0] = k;
+        p.rs.n[0] = kc;
         p.rs.j0[0] = 0;
         p.rs.line0[0] = 0;
         p.rs.step = 1;
@@ -533,8 +619,8 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     int line0 = 0;
     for (int b = 0; b < 4 && !p.rs.tapcopy; ++b) {
         int cnt = 0, j0 = -1;
-        for (int j = 0; j < k; ++j)
-            if (((j * d) & 3) == b) {
+        for (int j = 0; j < kc; ++j)
+            if (((j * dc) & 3) == b) {
                 if (j0 < 0) j0 = j;
                 ++cnt;
             }
@@ -555,22 +641,27 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
         p.rs.b[rb] = -1;
         p.rs.n[rb] = p.rs.j0[rb] = p.rs.line0[rb] = 0;
     }
-    p.box_tx_row = (uint32_t)cin * k * 128u;  // bytes the residue boxes of one row deliver
-    p.nvb = (p.wo + 31) / 32;
+    p.box_tx_row = (uint32_t)cin * kc * 128u;  // bytes the residue boxes of one row deliver
+    // K runs over x-aligned columns: dy shifted by up to (J-1) Ja d needs that many more
+    p.nvb = (p.wo + (J - 1) * p.sb + 31) / 32;
     p.T = (p.ho + d - 1) / d;
     p.kb_total = (long long)n * p.nvb * d * p.T;
     p.splits = wg_sms() / p.n_groups;
     if (p.splits < 1) p.splits = 1;
     if (p.splits > p.kb_total) p.splits = (int)p.kb_total;
     p.wp_x = (wi + 3) / 4 * 4;
-    p.wp_dy = (p.wo + 3) / 4 * 4;
-    p.stage_dy = p.wp_dy != p.wo;
+    // J > 1: dy always staged, with (J-1)*sb zeros left of each row and zeros right of it up
+    // to the last K block's reach, so the overlapping-view box never leaves the row
+    p.lm_dy = (J - 1) * p.sb;
+    p.wp_dy = J > 1 ? p.nvb * 32 + p.lm_dy : (p.wo + 3) / 4 * 4;
+    p.stage_dy = J > 1 || p.wp_dy != p.wo;
     if ((long long)n * hi > (1LL << 31)) return false;
-    p.part_bytes = ws_align256((size_t)p.splits * p.n_tiles * 128 * p.Npad * 4);
+    p.part_bytes = ws_align256((size_t)p.splits * p.n_tiles * 128 * p.NB * 4);
     p.pdb_bytes = ws_align256((size_t)p.splits * p.Npad * 4);
-    // boxes read up to (l-1)*d + 32 floats past a row's end (those columns meet zero dy)
-    p.copy_bytes = ws_align256((size_t)n * cin * hi * p.wp_x * 4 + ((size_t)(k - 1) * d + 64) * 4);
-    p.x_bytes = (size_t)(p.rs.tapcopy ? k : p.rs.n_b) * p.copy_bytes;
+    // boxes read up to (kc*J-1)*d + 32 floats past a row's end (those columns meet zero dy)
+    p.copy_bytes =
+        ws_align256((size_t)n * cin * hi * p.wp_x * 4 + ((size_t)(kc * J - 1) * d + 64) * 4);
+    p.x_bytes = (size_t)(p.rs.tapcopy ? kc : p.rs.n_b) * p.copy_bytes;
     p.dy_bytes = p.stage_dy ? ws_align256((size_t)n * cout * p.ho * p.wp_dy * 4) : 0;
     p.total_bytes = p.part_bytes + p.pdb_bytes + p.x_bytes + p.dy_bytes;
     return true;
@@ -608,7 +699,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     float *xs = (float *)(w8 + p.part_bytes + p.pdb_bytes);
     int rc = DP_OK;
     if (phases & 1) {
-        rc = p.rs.tapcopy ? wg_stage_x_taps(x, xs, n, cin, hi, wi, p.wp_x, k, d,
+        rc = p.rs.tapcopy ? wg_stage_x_taps(x, xs, n, cin, hi, wi, p.wp_x, p.kc, p.dc,
                                             (long long)(p.copy_bytes / 4), st)
                           : wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask,
                                        (long long)(p.copy_bytes / 4), st);
@@ -621,18 +712,27 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     const float *dys = dy;
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
-        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, st);
+        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st);
         if (rc) return rc;
         dys = dp_;
     }
     CUtensorMap mx[4], mdy;
     {
         const cuuint64_t rowb = (cuuint64_t)(stage_dy ? p.wp_dy : p.wo) * 4;
-        cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)p.ho, (cuuint64_t)cout, (cuuint64_t)n};
-        cuuint64_t str[3] = {stage_dy ? rowb * cout : rowb, stage_dy ? rowb : rowb * p.ho,
-                             rowb * cout * p.ho};
-        cuuint32_t box[4] = {32, 1, (cuuint32_t)p.Npad, 1};
-        rc = wg_make_map(&mdy, dys, 4, dims, str, box, true);
+        if (p.J == 1) {
+            cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)p.ho, (cuuint64_t)cout, (cuuint64_t)n};
+            cuuint64_t str[3] = {stage_dy ? rowb * cout : rowb, stage_dy ? rowb : rowb * p.ho,
+                                 rowb * cout * p.ho};
+            cuuint32_t box[4] = {32, 1, (cuuint32_t)cout, 1};
+            rc = wg_make_map(&mdy, dys, 4, dims, str, box, true);
+        } else {
+            // (w, o, jb', h, n) over the staged (n, h, o, wp) rows; jb' steps sb floats
+            cuuint64_t dims[5] = {(cuuint64_t)p.wp_dy, (cuuint64_t)cout, (cuuint64_t)p.J,
+                                  (cuuint64_t)p.ho, (cuuint64_t)n};
+            cuuint64_t str[4] = {rowb, (cuuint64_t)p.sb * 4, rowb * cout, rowb * cout * p.ho};
+            cuuint32_t box[5] = {32, (cuuint32_t)cout, (cuuint32_t)p.J, 1, 1};
+            rc = wg_make_map(&mdy, dys, 5, dims, str, box, true);
+        }
         if (rc) return rc;
     }
     const cuuint64_t xrow = (cuuint64_t)p.wp_x * 4;  // one channel line
@@ -646,7 +746,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
                               (cuuint64_t)n * hi};
         // tap dimension: lcm(d, 4) floats inside a residue copy, or the copy stride when each
         // tap has its own pre-shifted copy
-        cuuint64_t str[3] = {p.rs.tapcopy ? (cuuint64_t)p.copy_bytes : (cuuint64_t)p.rs.step * d * 4,
+        cuuint64_t str[3] = {p.rs.tapcopy ? (cuuint64_t)p.copy_bytes : (cuuint64_t)p.rs.step * p.dc * 4,
                              xrow, ximg_row};
         cuuint32_t box[4] = {32, (cuuint32_t)p.rs.n[used], (cuuint32_t)cin, 1};
         rc = wg_make_map(&mx[rb], base, 4, dims, str, box, true);
@@ -658,6 +758,10 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.d = d;
     a.Q = cout;
     a.Npad = p.Npad;
+    a.J = p.J;
+    a.sb = p.sb;
+    a.NB = p.NB;
+    a.tma_mirror = getenv("DP_WG_TMA_MIRROR") ? 1 : 0;
     a.n_tiles = p.n_tiles;
     a.G = p.G;
     a.n_groups = p.n_groups;
@@ -689,9 +793,10 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     tc_wgrad_ss_kernel<<<grid, WS_THREADS, smem, st>>>(mx[0], mx[1], mx[2], mx[3], mdy, a);
     rc = check_launch("tc_wgrad_ss_kernel");
     if (rc) return rc;
-    const long long total = (long long)k * p.Ls * p.Npad + cout;
-    ws_reduce<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, d, p.Ls,
-                                                    p.Npad, p.splits, p.n_tiles * 128, p.rs);
+    const long long total = (long long)k * p.Ls * p.NB + cout;
+    ws_reduce<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
+                                                    p.Npad, p.J, p.kc, p.splits, p.n_tiles * 128,
+                                                    p.rs);
     return check_launch("ws_reduce");
 }
 

@@ -48,6 +48,8 @@ def force_env(monkeypatch):
             monkeypatch.setenv("DP_TC_HALO", "1")    # halo-buffer / converter kernel
         elif kernel == "tmem":
             monkeypatch.setenv("DP_WG_TMEM", "1")    # TMEM-operand weight gradient
+        elif kernel.startswith("ss_j"):
+            monkeypatch.setenv("DP_WG_J", kernel[4:])  # column-tap stacking factor J
     return _set
 
 
@@ -141,11 +143,12 @@ WGRAD_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("kernel", ["ss", "tmem"])
+@pytest.mark.parametrize("kernel", ["ss", "ss_j1", "ss_j2", "ss_j3", "ss_j4", "tmem"])
 @pytest.mark.parametrize("shape", WGRAD_SHAPES)
 def test_tc_weight_gradient_matches_fp64(shape, kernel, force_env):
-    """kernel="ss": shared-memory-operand kernel (tc_wgrad_ss.cu, the default); "tmem": the
-    TMEM-operand fallback (tc_wgrad.cu)."""
+    """kernel="ss": shared-memory-operand kernel (tc_wgrad_ss.cu, the default, column-tap
+    stacking factor J from its cost model); "ss_jN": the same with J forced to N (where the
+    plan allows it); "tmem": the TMEM-operand fallback (tc_wgrad.cu)."""
     force_env(kernel)
     import torch
     from paper_1412_4526_b200.engine import ops

@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 buf = np.zeros((256, 16), dtype=np.uint64)
 _lib.check(_lib.load().dp_debug_wgrad_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes))
 t0 = buf[0, 0]
-names = ["tma", "-", "sfull", "Blo", "cvdone", "-", "-", "-", "mmwait", "mmissued", "-", "-",
+names = ["tma", "prodrdy", "sfull", "Blo", "cvdone", "-", "-", "-", "mmwait", "mmissued", "mmrdy", "-",
          "-", "-", "-", "-"]
 print("K-block  " + " ".join(f"{n:>7}" for n in names))
 for kl in list(range(0, 12)) + list(range(100, 106)):

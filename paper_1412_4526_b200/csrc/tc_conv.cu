@@ -95,8 +95,11 @@ struct TcConvArgs {
 // (hi = raw, lo = residual) in the K-major no-swizzle core-matrix layout:
 // element (n, k) at byte (n>>3)*256 + (k>>2)*128 + (n&7)*16 + (k&3)*4.
 // --------------------------------------------------------------------------------
+// tp > 1 (R <= 4, one channel chunk): a K step holds tp column taps of all R channels,
+// slot k = t*R + c <-> (c, j = g*tp + t); G = ceil(l / tp) K steps per tap row.
 __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__ wp, int Q, int R,
-                                int l, int Npad, int n_rc, int n_ks, int bwd) {
+                                int l, int Npad, int n_rc, int n_ks, int bwd, int tp) {
+    const int G = (l + tp - 1) / tp;
     int total = n_ks * 2 * Npad * 8;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += gridDim.x * blockDim.x) {
@@ -104,10 +107,16 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
         int n = (idx >> 3) % Npad;
         int hl = (idx / (8 * Npad)) & 1;
         int ks = idx / (16 * Npad);
-        int j = ks % l, i = (ks / l) % l, rc = ks / (l * l);
-        int c = rc * 8 + k;
+        int g = ks % G, i = (ks / G) % l, rc = ks / (l * G);
+        int c = rc * 8 + k, j = g;
+        bool slot_ok = true;
+        if (tp > 1) {
+            c = k % R;
+            j = g * tp + k / R;
+            slot_ok = k < R * tp && j < l;
+        }
         float v = 0.f;
-        if (n < Q && c < R) {
+        if (n < Q && c < R && slot_ok) {
             if (!bwd)
                 v = w[(((long long)n * R + c) * l + i) * l + j];
             else  // w is (R = cout, Q = cin, l, l), rotated by 180 degrees
@@ -119,10 +128,12 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
     }
 }
 
-int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, cudaStream_t st) {
-    const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 7) / 8, n_ks = n_rc * l * l;
+int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int tp, cudaStream_t st) {
+    const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 7) / 8;
+    const int n_ks = n_rc * l * ((l + tp - 1) / tp);
     const int total = n_ks * 2 * Npad * 8;
-    tc_pack_weights<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Q, R, l, Npad, n_rc, n_ks, bwd);
+    tc_pack_weights<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Q, R, l, Npad, n_rc, n_ks, bwd,
+                                                          tp);
     return check_launch("tc_pack_weights");
 }
 
@@ -651,7 +662,7 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     float *wp = (float *)ws;
     int total = p.n_ks * 2 * p.Npad * 8;
     tc_pack_weights<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Q, R, l, p.Npad, p.n_rc, p.n_ks,
-                                                          bwd ? 1 : 0);
+                                                          bwd ? 1 : 0, 1);
     int rc = check_launch("tc_pack_weights");
     if (rc) return rc;
     if (g_num_sms == 0) {

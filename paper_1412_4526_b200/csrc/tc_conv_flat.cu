@@ -46,7 +46,7 @@
 
 namespace dp {
 
-int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, cudaStream_t st);
+int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int tp, cudaStream_t st);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
 // 13 warps: registers are granted per 4 warps, so 13 warps (as 16) leave 128 registers
@@ -73,6 +73,7 @@ struct TfArgs {
     int Wv, pad;         // virtual (zero-padded) grid width; offset of the real input in it
     int Q, Ho, Wo, l, d, act, gate_kind;
     int n_rc, Npad, MT, acc_cols, NR, HB;
+    int G, tpd;          // K steps per unit (l, or ceil(l / tp) tap-packed), record step per K step
     uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
     int tiles_per_img, total_tiles, flat_len;
     unsigned long long *trace;  // DP_TC_TRACE: per-unit clock64 stamps of CTA 0 (8 slots)
@@ -94,8 +95,12 @@ __device__ __forceinline__ float tf_act(float v, int kind) {
     return v;
 }
 
-template <bool STACKED, bool BWD>
+// RP > 0: tap-packed records for an input of RP <= 4 channels -- slot k = t*RP + c of the
+// record at flat index f holds x[c, f + t*d] (TP = 8 / RP column taps), so a K step covers
+// TP taps of every channel instead of one tap with 8 - RP zero channels
+template <bool STACKED, bool BWD, int RP>
 __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArgs a) {
+    constexpr int TP = RP ? 8 / RP : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t ufull[TF_MAX_HB], uempty[TF_MAX_HB], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
@@ -169,10 +174,34 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                             const int yv = gf / a.Wv;
                             const int y = yv - a.pad, x = gf - yv * a.Wv - a.pad;
                             const bool ok = r < a.NR && y >= 0 && y < a.Hin && x >= 0 && x < a.Win;
-                            const float *p = src + (ok ? (long long)y * a.Win + x : 0);
+                            if (RP == 0) {
+                                const float *p = src + (ok ? (long long)y * a.Win + x : 0);
 #pragma unroll
-                            for (int k = 0; k < 8; ++k)
-                                v[u][k] = (ok && k < cvalid) ? __ldg(p + k * plane_in) : 0.f;
+                                for (int k = 0; k < 8; ++k)
+                                    v[u][k] = (ok && k < cvalid) ? __ldg(p + k * plane_in) : 0.f;
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < TP; ++t) {
+                                    // column tap t: flat index gf + t*d (wraps into the next
+                                    // virtual row only for discarded outputs / zero weights)
+                                    int xt = gf - yv * a.Wv + t * a.d, yt = yv;
+                                    while (xt >= a.Wv) {
+                                        xt -= a.Wv;
+                                        ++yt;
+                                    }
+                                    yt -= a.pad;
+                                    xt -= a.pad;
+                                    const bool okt = r < a.NR && yt >= 0 && yt < a.Hin && xt >= 0 &&
+                                                     xt < a.Win;
+                                    const float *p = src + (okt ? (long long)yt * a.Win + xt : 0);
+#pragma unroll
+                                    for (int c = 0; c < RP; ++c)
+                                        v[u][t * RP + c] = okt ? __ldg(p + c * plane_in) : 0.f;
+                                }
+#pragma unroll
+                                for (int k = TP * RP; k < 8; ++k) v[u][k] = 0.f;
+                                (void)ok;
+                            }
                         }
 #pragma unroll
                         for (int u = 0; u < TF_LU; ++u) {
@@ -223,11 +252,11 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     const uint32_t ubase = hs + (uint32_t)b * a.ubytes;
                     const uint64_t a0 = ptx::smem_desc(ubase, a.plane_bytes, 128);
                     const uint64_t b0 = ptx::smem_desc(ubase + a.halo_bytes, 128, 256);
-                    for (int j = 0; j < a.l; ++j) {
+                    for (int j = 0; j < a.G; ++j) {
                         const uint64_t bj = b0 + (uint64_t)(j * ks_units);
                         const uint32_t acc = (u | j) != 0;
                         for (int mt = 0; mt < MT; ++mt) {
-                            const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * a.d);
+                            const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * a.tpd);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.acc_cols);
                             if (STACKED) {
                                 ptx::mma_tf32_ss(dd, ad, bj, idesc_2n, acc);
@@ -327,15 +356,18 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
 // host side
 // --------------------------------------------------------------------------------
 struct TfPlan {
-    int Npad, n_rc, MT, acc_cols, NR, HB;
+    int Npad, n_rc, MT, acc_cols, NR, HB, rp, G;
     bool stacked, ok;
     uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
 };
 
 // M tiles per CTA tile: accumulators double-buffered in the 512 TMEM columns; unit
 // buffers (halo + one tap row of weights) as many as fit, at least two.
-static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt) {
+static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd) {
     TfPlan p;
+    // tap-packed records for small inputs (forward only: c2/c3/c4 conv1 read 3 channels)
+    p.rp = (!bwd && R <= 4 && l > 1 && !getenv("DP_TF_NOPACK")) ? R : 0;
+    p.G = p.rp ? (l + 8 / p.rp - 1) / (8 / p.rp) : l;
     p.Npad = (Q + 15) / 16 * 16;
     p.n_rc = (R + 7) / 8;
     p.stacked = 2 * p.Npad <= 256;
@@ -352,7 +384,7 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt) {
     p.NR = (mt * 128 + (l - 1) * d + 7) / 8 * 8;
     p.plane_bytes = (uint32_t)p.NR * 16;
     p.halo_bytes = 4 * p.plane_bytes;
-    p.wunit_bytes = (uint32_t)(l * p.Npad * 64);
+    p.wunit_bytes = (uint32_t)(p.G * p.Npad * 64);
     p.ubytes = (p.halo_bytes + p.wunit_bytes + 127) / 128 * 128;
     long long hb = (long long)TF_SMEM_BUDGET / p.ubytes;
     if (hb > TF_MAX_HB) hb = TF_MAX_HB;
@@ -363,7 +395,7 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt) {
 
 bool tf_conv_supported(int R, int Q, int l, int d) {
     if (getenv("DP_TC_HALO")) return false;  // force the halo-buffer kernel (tc_conv.cu)
-    return tf_plan(R, Q, l, d, 0).ok;
+    return tf_plan(R, Q, l, d, 0, true).ok;  // unpacked: the larger weight unit
 }
 
 static int g_tf_sms = 0;
@@ -376,7 +408,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     // short images: fewer M tiles per CTA tile
     const int max_mt = (int)((flat_len + 127) / 128);
-    TfPlan p = tf_plan(R, Q, l, d, max_mt);
+    TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd);
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
                          R, Q, l, d);
@@ -386,7 +418,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
                          wbytes);
     if (((uintptr_t)ws & 15) != 0)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
-    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, st);
+    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp ? 8 / p.rp : 1, st);
     if (rc) return rc;
     if (g_tf_sms == 0) {
         int dev = 0;
@@ -417,6 +449,8 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     a.n_rc = p.n_rc;
     a.Npad = p.Npad;
     a.MT = p.MT;
+    a.G = p.G;
+    a.tpd = (p.rp ? 8 / p.rp : 1) * d;
     a.acc_cols = p.acc_cols;
     a.NR = p.NR;
     a.HB = p.HB;
@@ -434,10 +468,20 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
-    if (p.stacked)
-        kern = bwd ? tc_conv_flat_kernel<true, true> : tc_conv_flat_kernel<true, false>;
+    if (bwd)
+        kern = p.stacked ? tc_conv_flat_kernel<true, true, 0> : tc_conv_flat_kernel<false, true, 0>;
+    else if (p.stacked)
+        kern = p.rp == 1   ? tc_conv_flat_kernel<true, false, 1>
+               : p.rp == 2 ? tc_conv_flat_kernel<true, false, 2>
+               : p.rp == 3 ? tc_conv_flat_kernel<true, false, 3>
+               : p.rp == 4 ? tc_conv_flat_kernel<true, false, 4>
+                           : tc_conv_flat_kernel<true, false, 0>;
     else
-        kern = bwd ? tc_conv_flat_kernel<false, true> : tc_conv_flat_kernel<false, false>;
+        kern = p.rp == 1   ? tc_conv_flat_kernel<false, false, 1>
+               : p.rp == 2 ? tc_conv_flat_kernel<false, false, 2>
+               : p.rp == 3 ? tc_conv_flat_kernel<false, false, 3>
+               : p.rp == 4 ? tc_conv_flat_kernel<false, false, 4>
+                           : tc_conv_flat_kernel<false, false, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess)

@@ -422,41 +422,71 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     if (warp == WS_MMA_WARP) ptx::tmem_dealloc<512>(tmem);
 }
 
-// dw[o,c,i,j] = sum_s part[s][line(i, j, c)][o], db[o] = sum_s pdb[s][o]  (fixed order:
-// s = 0, 1, ... sequentially per entry).  Threads walk (line, o) with o fastest so the
-// split-strided partial reads are coalesced; gap lines (residue-box padding) are skipped.
-__global__ void ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb,
-                          float *__restrict__ dw, float *__restrict__ db, int Q, int C, int l,
-                          int Ls, int Npad, int J, int Ja, int splits, int rows_pad,
-                          WsResidues rs) {
+// dw[o,c,i,j] = sum_s part[s][line(i, j, c)][o], db[o] = sum_s pdb[s][o].  A block takes 32
+// entries (lanes, (line, col) with col fastest: coalesced) x 8 warps; warp w sums the splits
+// s = w, w + 8, ... in order, then lane sums of the 8 warps are added in warp order -- a
+// fixed order (deterministic) with 8 independent load chains per entry instead of one
+// (a single ~148-long chain per thread left the kernel latency bound).  Gap lines
+// (residue-box padding), zero B rows and padding taps are skipped.
+constexpr int WR_GROUPS = 8;
+__global__ void __launch_bounds__(32 * WR_GROUPS)
+    ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb, float *__restrict__ dw,
+              float *__restrict__ db, int Q, int C, int l, int Ls, int Npad, int J, int Ja,
+              int splits, int rows_pad, WsResidues rs) {
+    __shared__ float red[WR_GROUPS][32];
     const long long lines = (long long)l * Ls;
     const int NB = (J * Q + 15) / 16 * 16;
     const long long total = lines * NB;
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long idx = (long long)blockIdx.x * 32 + lane;
+    // which entry, and where its partials live (src < 0: nothing to write)
+    long long src = -1, sstride = 0, dst = -1;
+    const float *in = part;
+    float *out = nullptr;
     if (idx < total) {
         const int col = (int)(idx % NB);
         const long long line = idx / NB;
-        if (col >= J * Q) return;  // zero B rows
-        const int jr = col / Q, o = col - jr * Q;
-        const int jb = J - 1 - jr;  // B row blocks hold the shifts in reverse (jb' = J-1-jb)
-        const int i = (int)(line / Ls), rem = (int)(line - (long long)i * Ls);
-        int rb = -1;
-        for (int r = 0; r < rs.n_b; ++r)
-            if (rem >= rs.line0[r] && rem < rs.line0[r] + C * rs.n[r]) rb = r;
-        if (rb < 0) return;  // gap line
-        const int off = rem - rs.line0[rb];
-        const int c = off / rs.n[rb], jj = off - c * rs.n[rb];
-        const int ja = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
-        const int j = jb * Ja + ja;
-        if (j >= l) return;  // padding tap of the last column group
-        float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += part[((size_t)s * rows_pad + line) * NB + col];
-        dw[(((long long)o * C + c) * l + i) * l + j] = acc;
+        int o = 0, c = 0, i = 0, j = l;
+        if (col < J * Q) {  // else a zero B row
+            const int jr = col / Q;
+            o = col - jr * Q;
+            const int jb = J - 1 - jr;  // B row blocks hold the shifts in reverse
+            i = (int)(line / Ls);
+            const int rem = (int)(line - (long long)i * Ls);
+            int rb = -1;
+            for (int r = 0; r < rs.n_b; ++r)
+                if (rem >= rs.line0[r] && rem < rs.line0[r] + C * rs.n[r]) rb = r;
+            if (rb >= 0) {  // else a gap line
+                const int off = rem - rs.line0[rb];
+                c = off / rs.n[rb];
+                const int jj = off - c * rs.n[rb];
+                const int ja = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
+                j = jb * Ja + ja;  // >= l: padding tap of the last column group
+            }
+        }
+        if (j < l) {
+            src = line * NB + col;
+            sstride = (long long)rows_pad * NB;
+            dst = (((long long)o * C + c) * l + i) * l + j;
+            out = dw;
+        }
     } else if (idx < total + Q) {
-        const int o = (int)(idx - total);
-        float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += pdb[(size_t)s * Npad + o];  // pdb: Npad wide
-        db[o] = acc;
+        src = idx - total;
+        sstride = Npad;  // pdb: Npad wide
+        dst = src;
+        in = pdb;
+        out = db;
+    }
+    float acc = 0.f;
+    if (src >= 0)
+        for (int sp = w; sp < splits; sp += WR_GROUPS) acc += in[(size_t)sp * sstride + src];
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && src >= 0) {
+        float t = red[0][lane];
+#pragma unroll
+        for (int g = 1; g < WR_GROUPS; ++g) t += red[g][lane];
+        out[dst] = t;
     }
 }
 
@@ -794,7 +824,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     rc = check_launch("tc_wgrad_ss_kernel");
     if (rc) return rc;
     const long long total = (long long)k * p.Ls * p.NB + cout;
-    ws_reduce<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
+    ws_reduce<<<ceil_div(total, 32), 32 * WR_GROUPS, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
                                                     p.Npad, p.J, p.kc, p.splits, p.n_tiles * 128,
                                                     p.rs);
     return check_launch("ws_reduce");

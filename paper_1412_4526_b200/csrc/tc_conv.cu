@@ -95,11 +95,14 @@ struct TcConvArgs {
 // (hi = raw, lo = residual) in the K-major no-swizzle core-matrix layout:
 // element (n, k) at byte (n>>3)*256 + (k>>2)*128 + (n&7)*16 + (k&3)*4.
 // --------------------------------------------------------------------------------
-// tp > 1 (R <= 4, one channel chunk): a K step holds tp column taps of all R channels,
-// slot k = t*R + c <-> (c, j = g*tp + t); G = ceil(l / tp) K steps per tap row.
+// rp > 0: the last channel chunk holds rp <= 4 channels, tap-packed -- its K steps hold
+// tp = 8 / rp column taps, slot k = t*rp + c <-> (c, j = g*tp + t), G = ceil(l / tp) K steps
+// per tap row, after all (n_rc - 1) * l * l full K steps.
 __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__ wp, int Q, int R,
-                                int l, int Npad, int n_rc, int n_ks, int bwd, int tp) {
+                                int l, int Npad, int n_rc, int n_ks, int bwd, int rp) {
+    const int tp = rp ? 8 / rp : 1;
     const int G = (l + tp - 1) / tp;
+    const int full = rp ? (n_rc - 1) * l * l : n_ks;
     int total = n_ks * 2 * Npad * 8;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += gridDim.x * blockDim.x) {
@@ -107,13 +110,18 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
         int n = (idx >> 3) % Npad;
         int hl = (idx / (8 * Npad)) & 1;
         int ks = idx / (16 * Npad);
-        int g = ks % G, i = (ks / G) % l, rc = ks / (l * G);
-        int c = rc * 8 + k, j = g;
+        int c, i, j;
         bool slot_ok = true;
-        if (tp > 1) {
-            c = k % R;
-            j = g * tp + k / R;
-            slot_ok = k < R * tp && j < l;
+        if (ks < full) {
+            j = ks % l;
+            i = (ks / l) % l;
+            c = (ks / (l * l)) * 8 + k;
+        } else {
+            const int kp = ks - full;
+            i = kp / G;
+            c = (n_rc - 1) * 8 + k % rp;
+            j = (kp % G) * tp + k / rp;
+            slot_ok = k < rp * tp && j < l;
         }
         float v = 0.f;
         if (n < Q && c < R && slot_ok) {
@@ -128,12 +136,13 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
     }
 }
 
-int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int tp, cudaStream_t st) {
+int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st) {
     const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 7) / 8;
-    const int n_ks = n_rc * l * ((l + tp - 1) / tp);
+    const int tp = rp ? 8 / rp : 1;
+    const int n_ks = rp ? (n_rc - 1) * l * l + l * ((l + tp - 1) / tp) : n_rc * l * l;
     const int total = n_ks * 2 * Npad * 8;
     tc_pack_weights<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Q, R, l, Npad, n_rc, n_ks, bwd,
-                                                          tp);
+                                                          rp);
     return check_launch("tc_pack_weights");
 }
 
@@ -662,7 +671,7 @@ static int launch_tc(const float *in, const float *w, const float *bias, float *
     float *wp = (float *)ws;
     int total = p.n_ks * 2 * p.Npad * 8;
     tc_pack_weights<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Q, R, l, p.Npad, p.n_rc, p.n_ks,
-                                                          bwd ? 1 : 0, 1);
+                                                          bwd ? 1 : 0, 0);
     int rc = check_launch("tc_pack_weights");
     if (rc) return rc;
     if (g_num_sms == 0) {

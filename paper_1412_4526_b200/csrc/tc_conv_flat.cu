@@ -46,7 +46,7 @@
 
 namespace dp {
 
-int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int tp, cudaStream_t st);
+int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
 // 13 warps: registers are granted per 4 warps, so 13 warps (as 16) leave 128 registers
@@ -73,7 +73,8 @@ struct TfArgs {
     int Wv, pad;         // virtual (zero-padded) grid width; offset of the real input in it
     int Q, Ho, Wo, l, d, act, gate_kind;
     int n_rc, Npad, MT, acc_cols, NR, HB;
-    int G, tpd;          // K steps per unit (l, or ceil(l / tp) tap-packed), record step per K step
+    int G, tpd;          // the tap-packed last chunk: K steps per unit, record step per K step
+    uint32_t wunit_pk;   // its weight-unit bytes (other chunks: wunit_bytes)
     uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
     int tiles_per_img, total_tiles, flat_len;
     unsigned long long *trace;  // DP_TC_TRACE: per-unit clock64 stamps of CTA 0 (8 slots)
@@ -95,9 +96,15 @@ __device__ __forceinline__ float tf_act(float v, int kind) {
     return v;
 }
 
-// RP > 0: tap-packed records for an input of RP <= 4 channels -- slot k = t*RP + c of the
-// record at flat index f holds x[c, f + t*d] (TP = 8 / RP column taps), so a K step covers
-// TP taps of every channel instead of one tap with 8 - RP zero channels
+// RP > 0: the LAST 8-channel chunk holds only RP <= 4 channels and uses tap-packed records
+// -- slot k = t*RP + c of the record at flat index f holds x[c, f + t*d] (TP = 8 / RP column
+// taps), so a K step covers TP taps of its channels instead of one tap with 8 - RP zero
+// channels (c2 conv1: 3 channels, one chunk; c2 conv3 data gradient: 10 = 8 + 2)
+template <bool B>
+struct BoolTag {
+    static constexpr bool value = B;
+};
+
 template <bool STACKED, bool BWD, int RP>
 __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArgs a) {
     constexpr int TP = RP ? 8 / RP : 1;
@@ -141,6 +148,8 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
             for (int rc = 0, wu = 0; rc < a.n_rc; ++rc) {
                 const float *src = a.in + ((long long)img * a.R + rc * 8) * plane_in;
                 const int cvalid = min(8, a.R - rc * 8);
+                const bool pk = RP > 0 && rc == a.n_rc - 1;
+                const uint32_t wub = pk ? a.wunit_pk : a.wunit_bytes;
                 for (int i = 0; i < a.l; ++i, ++wu, ++gu) {
                     if ((gu % TF_LGROUPS) != grp) {  // the other group's unit
                         if (++b == a.HB) {
@@ -154,69 +163,83 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     unsigned char *ub = smem_raw + (size_t)b * a.ubytes;
                     if (lw == 0) {
                         if (ptx::elect_one()) {
-                            ptx::mbar_expect_tx(&ufull[b], a.wunit_bytes);
-                            const unsigned char *ws = wsrc + (size_t)wu * a.wunit_bytes;
-                            for (uint32_t off = 0; off < a.wunit_bytes; off += 32768u) {
-                                const uint32_t nb =
-                                    a.wunit_bytes - off < 32768u ? a.wunit_bytes - off : 32768u;
+                            ptx::mbar_expect_tx(&ufull[b], wub);
+                            // the packed chunk is the last: its units follow all full ones
+                            const unsigned char *ws =
+                                wsrc + (size_t)rc * a.l * a.wunit_bytes + (size_t)i * wub;
+                            for (uint32_t off = 0; off < wub; off += 32768u) {
+                                const uint32_t nb = wub - off < 32768u ? wub - off : 32768u;
                                 ptx::bulk_g2s(ub + a.halo_bytes + off, ws + off, nb, &ufull[b]);
                             }
                         }
                         __syncwarp();
                     }
                     const int gbase = f0 + i * a.d * a.Wv;
-                    for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += TF_LU * TF_LGW * 32) {
-                        float v[TF_LU][8];
+                    // one straight-line record loop per record kind (a runtime branch inside
+                    // the unrolled loads cost the loaders their ILP: measured 20 % slower)
+                    auto fill = [&](auto packed) {
+                        constexpr bool PK = decltype(packed)::value;
+                        for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += TF_LU * TF_LGW * 32) {
+                            float v[TF_LU][8];
 #pragma unroll
-                        for (int u = 0; u < TF_LU; ++u) {
-                            const int r = r0 + u * TF_LGW * 32;
-                            const int gf = gbase + r;
-                            const int yv = gf / a.Wv;
-                            const int y = yv - a.pad, x = gf - yv * a.Wv - a.pad;
-                            const bool ok = r < a.NR && y >= 0 && y < a.Hin && x >= 0 && x < a.Win;
-                            if (RP == 0) {
-                                const float *p = src + (ok ? (long long)y * a.Win + x : 0);
+                            for (int u = 0; u < TF_LU; ++u) {
+                                const int r = r0 + u * TF_LGW * 32;
+                                const int gf = gbase + r;
+                                const int yv = gf / a.Wv;
+                                if (!PK) {
+                                    const int y = yv - a.pad, x = gf - yv * a.Wv - a.pad;
+                                    const bool ok =
+                                        r < a.NR && y >= 0 && y < a.Hin && x >= 0 && x < a.Win;
+                                    const float *p = src + (ok ? (long long)y * a.Win + x : 0);
 #pragma unroll
-                                for (int k = 0; k < 8; ++k)
-                                    v[u][k] = (ok && k < cvalid) ? __ldg(p + k * plane_in) : 0.f;
-                            } else {
+                                    for (int k = 0; k < 8; ++k)
+                                        v[u][k] = (ok && k < cvalid) ? __ldg(p + k * plane_in) : 0.f;
+                                } else {
 #pragma unroll
-                                for (int t = 0; t < TP; ++t) {
-                                    // column tap t: flat index gf + t*d (wraps into the next
-                                    // virtual row only for discarded outputs / zero weights)
-                                    int xt = gf - yv * a.Wv + t * a.d, yt = yv;
-                                    while (xt >= a.Wv) {
-                                        xt -= a.Wv;
-                                        ++yt;
+                                    for (int t = 0; t < TP; ++t) {
+                                        // column tap t: flat index gf + t*d (wraps into the
+                                        // next virtual row only for discarded outputs / zero
+                                        // weights)
+                                        int xt = gf - yv * a.Wv + t * a.d, yt = yv;
+                                        while (xt >= a.Wv) {
+                                            xt -= a.Wv;
+                                            ++yt;
+                                        }
+                                        yt -= a.pad;
+                                        xt -= a.pad;
+                                        const bool okt = r < a.NR && yt >= 0 && yt < a.Hin &&
+                                                         xt >= 0 && xt < a.Win;
+                                        const float *p =
+                                            src + (okt ? (long long)yt * a.Win + xt : 0);
+#pragma unroll
+                                        for (int c = 0; c < (RP ? RP : 1); ++c)
+                                            v[u][t * RP + c] = okt ? __ldg(p + c * plane_in) : 0.f;
                                     }
-                                    yt -= a.pad;
-                                    xt -= a.pad;
-                                    const bool okt = r < a.NR && yt >= 0 && yt < a.Hin && xt >= 0 &&
-                                                     xt < a.Win;
-                                    const float *p = src + (okt ? (long long)yt * a.Win + xt : 0);
 #pragma unroll
-                                    for (int c = 0; c < RP; ++c)
-                                        v[u][t * RP + c] = okt ? __ldg(p + c * plane_in) : 0.f;
+                                    for (int k = TP * RP; k < 8; ++k) v[u][k] = 0.f;
                                 }
+                            }
 #pragma unroll
-                                for (int k = TP * RP; k < 8; ++k) v[u][k] = 0.f;
-                                (void)ok;
+                            for (int u = 0; u < TF_LU; ++u) {
+                                const int r = r0 + u * TF_LGW * 32;
+                                if (r >= a.NR) break;
+                                float4 *p0 = reinterpret_cast<float4 *>(ub) + r;
+                                const uint32_t ps = a.plane_bytes / 16;  // plane stride (float4)
+                                p0[0] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                                p0[ps] = make_float4(v[u][4], v[u][5], v[u][6], v[u][7]);
+                                p0[2 * ps] =
+                                    make_float4(ptx::tf32_lo(v[u][0]), ptx::tf32_lo(v[u][1]),
+                                                ptx::tf32_lo(v[u][2]), ptx::tf32_lo(v[u][3]));
+                                p0[3 * ps] =
+                                    make_float4(ptx::tf32_lo(v[u][4]), ptx::tf32_lo(v[u][5]),
+                                                ptx::tf32_lo(v[u][6]), ptx::tf32_lo(v[u][7]));
                             }
                         }
-#pragma unroll
-                        for (int u = 0; u < TF_LU; ++u) {
-                            const int r = r0 + u * TF_LGW * 32;
-                            if (r >= a.NR) break;
-                            float4 *p0 = reinterpret_cast<float4 *>(ub) + r;
-                            const uint32_t ps = a.plane_bytes / 16;  // plane stride in float4
-                            p0[0] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
-                            p0[ps] = make_float4(v[u][4], v[u][5], v[u][6], v[u][7]);
-                            p0[2 * ps] = make_float4(ptx::tf32_lo(v[u][0]), ptx::tf32_lo(v[u][1]),
-                                                     ptx::tf32_lo(v[u][2]), ptx::tf32_lo(v[u][3]));
-                            p0[3 * ps] = make_float4(ptx::tf32_lo(v[u][4]), ptx::tf32_lo(v[u][5]),
-                                                     ptx::tf32_lo(v[u][6]), ptx::tf32_lo(v[u][7]));
-                        }
-                    }
+                    };
+                    if (RP > 0 && pk)
+                        fill(BoolTag<RP != 0>());
+                    else
+                        fill(BoolTag<false>());
                     // generic-proxy stores -> visible to the tensor core (async proxy)
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
@@ -252,11 +275,13 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     const uint32_t ubase = hs + (uint32_t)b * a.ubytes;
                     const uint64_t a0 = ptx::smem_desc(ubase, a.plane_bytes, 128);
                     const uint64_t b0 = ptx::smem_desc(ubase + a.halo_bytes, 128, 256);
-                    for (int j = 0; j < a.G; ++j) {
+                    const bool pk = RP > 0 && u >= units - a.l;  // the packed last chunk
+                    const int G = pk ? a.G : a.l, step = pk ? a.tpd : a.d;
+                    for (int j = 0; j < G; ++j) {
                         const uint64_t bj = b0 + (uint64_t)(j * ks_units);
                         const uint32_t acc = (u | j) != 0;
                         for (int mt = 0; mt < MT; ++mt) {
-                            const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * a.tpd);
+                            const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * step);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.acc_cols);
                             if (STACKED) {
                                 ptx::mma_tf32_ss(dd, ad, bj, idesc_2n, acc);
@@ -358,18 +383,25 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
 struct TfPlan {
     int Npad, n_rc, MT, acc_cols, NR, HB, rp, G;
     bool stacked, ok;
-    uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
+    uint32_t plane_bytes, halo_bytes, wunit_bytes, wunit_pk, ubytes;
 };
 
 // M tiles per CTA tile: accumulators double-buffered in the 512 TMEM columns; unit
 // buffers (halo + one tap row of weights) as many as fit, at least two.
 static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd) {
     TfPlan p;
-    // tap-packed records for small inputs (forward only: c2/c3/c4 conv1 read 3 channels)
-    p.rp = (!bwd && R <= 4 && l > 1 && !getenv("DP_TF_NOPACK")) ? R : 0;
-    p.G = p.rp ? (l + 8 / p.rp - 1) / (8 / p.rp) : l;
     p.Npad = (Q + 15) / 16 * 16;
     p.n_rc = (R + 7) / 8;
+    // tap-packed records for inputs of <= 4 channels.  The kernel also packs the last
+    // chunk of a wider input (DP_TF_PACK_LAST), but that measured slower (c2 conv3 data
+    // gradient 0.76 -> 0.84 ms): the packed units' loads, not their MMAs, set the pace.
+    const int rem = R - (p.n_rc - 1) * 8;
+    (void)bwd;
+    p.rp = (rem <= 4 && l > 1 && (p.n_rc == 1 || getenv("DP_TF_PACK_LAST")) &&
+            !getenv("DP_TF_NOPACK"))
+               ? rem
+               : 0;
+    p.G = p.rp ? (l + 8 / p.rp - 1) / (8 / p.rp) : l;
     p.stacked = 2 * p.Npad <= 256;
     p.acc_cols = p.stacked ? 2 * p.Npad : p.Npad;
     p.ok = p.Npad <= 256;
@@ -384,7 +416,9 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd) {
     p.NR = (mt * 128 + (l - 1) * d + 7) / 8 * 8;
     p.plane_bytes = (uint32_t)p.NR * 16;
     p.halo_bytes = 4 * p.plane_bytes;
-    p.wunit_bytes = (uint32_t)(p.G * p.Npad * 64);
+    p.wunit_pk = (uint32_t)(p.G * p.Npad * 64);
+    // unit buffers hold the largest unit: a full one unless the packed chunk is the only one
+    p.wunit_bytes = (uint32_t)((p.rp && p.n_rc == 1 ? p.G : l) * p.Npad * 64);
     p.ubytes = (p.halo_bytes + p.wunit_bytes + 127) / 128 * 128;
     long long hb = (long long)TF_SMEM_BUDGET / p.ubytes;
     if (hb > TF_MAX_HB) hb = TF_MAX_HB;
@@ -412,13 +446,14 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
                          R, Q, l, d);
-    const size_t wbytes = (size_t)p.n_rc * l * p.wunit_bytes;
+    const size_t wbytes = p.rp ? (size_t)(p.n_rc - 1) * l * l * p.Npad * 64 + (size_t)l * p.wunit_pk
+                               : (size_t)p.n_rc * l * p.wunit_bytes;
     if (ws == nullptr || ws_bytes < wbytes)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
                          wbytes);
     if (((uintptr_t)ws & 15) != 0)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
-    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp ? 8 / p.rp : 1, st);
+    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp, st);
     if (rc) return rc;
     if (g_tf_sms == 0) {
         int dev = 0;
@@ -450,6 +485,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     a.Npad = p.Npad;
     a.MT = p.MT;
     a.G = p.G;
+    a.wunit_pk = p.wunit_pk;
     a.tpd = (p.rp ? 8 / p.rp : 1) * d;
     a.acc_cols = p.acc_cols;
     a.NR = p.NR;
@@ -468,8 +504,18 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
-    if (bwd)
-        kern = p.stacked ? tc_conv_flat_kernel<true, true, 0> : tc_conv_flat_kernel<false, true, 0>;
+    if (bwd && p.stacked)
+        kern = p.rp == 1   ? tc_conv_flat_kernel<true, true, 1>
+               : p.rp == 2 ? tc_conv_flat_kernel<true, true, 2>
+               : p.rp == 3 ? tc_conv_flat_kernel<true, true, 3>
+               : p.rp == 4 ? tc_conv_flat_kernel<true, true, 4>
+                           : tc_conv_flat_kernel<true, true, 0>;
+    else if (bwd)
+        kern = p.rp == 1   ? tc_conv_flat_kernel<false, true, 1>
+               : p.rp == 2 ? tc_conv_flat_kernel<false, true, 2>
+               : p.rp == 3 ? tc_conv_flat_kernel<false, true, 3>
+               : p.rp == 4 ? tc_conv_flat_kernel<false, true, 4>
+                           : tc_conv_flat_kernel<false, true, 0>;
     else if (p.stacked)
         kern = p.rp == 1   ? tc_conv_flat_kernel<true, false, 1>
                : p.rp == 2 ? tc_conv_flat_kernel<true, false, 2>

@@ -48,12 +48,14 @@ def force_env(monkeypatch):
             monkeypatch.setenv("DP_TC_HALO", "1")    # halo-buffer / converter kernel
         elif kernel == "tmem":
             monkeypatch.setenv("DP_WG_TMEM", "1")    # TMEM-operand weight gradient
+        elif kernel == "flat_packlast":
+            monkeypatch.setenv("DP_TF_PACK_LAST", "1")  # tap-packed last channel chunk
         elif kernel.startswith("ss_j"):
             monkeypatch.setenv("DP_WG_J", kernel[4:])  # column-tap stacking factor J
     return _set
 
 
-@pytest.mark.parametrize("kernel", ["flat", "tap", "halo"])
+@pytest.mark.parametrize("kernel", ["flat", "tap", "halo", "flat_packlast"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("act", [0, 1, 2])
 def test_tc_forward_matches_exact(shape, act, kernel, force_env):
@@ -81,7 +83,7 @@ def test_tc_forward_matches_exact(shape, act, kernel, force_env):
     assert _rel(y, y_ref) < TOL
 
 
-@pytest.mark.parametrize("kernel", ["flat", "tap", "halo"])
+@pytest.mark.parametrize("kernel", ["flat", "tap", "halo", "flat_packlast"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("gate_kind", [None, 1, 2])
 def test_tc_backward_data_matches_exact(shape, gate_kind, kernel, force_env):

@@ -409,8 +409,12 @@ size_t tt_conv_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, in
     // amortised (conv3 fwd 213 vs 327 us, conv2 data grad 303 vs 449 us); at MT <= 2 the
     // l*Npad-wide weight rows re-streamed per tile and the 64 B/pixel/tap-row record
     // copies cost more than the saved A reads (conv1/conv2 fwd, conv3 data grad lose).
+    // Wide inputs (R >= 32, four or more channel chunks) win even at MT 1-2 (c3 conv2 fwd /
+    // data grad 0.74 -> 0.65 / 0.76 -> 0.67 ms, c3 head fwd 1.15 -> 1.03, c4 conv2 fwd and
+    // the c4 data grads 5-15 %): there the flat kernel's per-tap-row record loads and hi/lo
+    // splits, not the tap kernel's re-streamed weight rows, dominate.
     // DP_TT_ALL uses it wherever it applies (experiments).
-    if (p.MT < 3 && !getenv("DP_TT_ALL")) return 0;
+    if (p.MT < 3 && R < 32 && !getenv("DP_TT_ALL")) return 0;
     long long plane_recs, flat_len;
     int tpi;
     tt_relayout_recs(Hin, Win, pad, l, d, p, plane_recs, tpi, flat_len, Ho, Wo);

@@ -104,6 +104,10 @@ template <bool B>
 struct BoolTag {
     static constexpr bool value = B;
 };
+template <int V>
+struct IntTag {
+    static constexpr int value = V;
+};
 
 template <bool STACKED, bool BWD, int RP>
 __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArgs a) {
@@ -177,12 +181,15 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     const int gbase = f0 + i * a.d * a.Wv;
                     // one straight-line record loop per record kind (a runtime branch inside
                     // the unrolled loads cost the loaders their ILP: measured 20 % slower)
-                    auto fill = [&](auto packed) {
+                    // (LU records per thread in flight: 2 when the whole halo is <= 256 records
+                    // -- one M tile per CTA tile, wide layers -- where 5 mostly idled)
+                    auto fill = [&](auto packed, auto lu) {
                         constexpr bool PK = decltype(packed)::value;
-                        for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += TF_LU * TF_LGW * 32) {
-                            float v[TF_LU][8];
+                        constexpr int LU = decltype(lu)::value;
+                        for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += LU * TF_LGW * 32) {
+                            float v[LU][8];
 #pragma unroll
-                            for (int u = 0; u < TF_LU; ++u) {
+                            for (int u = 0; u < LU; ++u) {
                                 const int r = r0 + u * TF_LGW * 32;
                                 const int gf = gbase + r;
                                 const int yv = gf / a.Wv;
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                 }
                             }
 #pragma unroll
-                            for (int u = 0; u < TF_LU; ++u) {
+                            for (int u = 0; u < LU; ++u) {
                                 const int r = r0 + u * TF_LGW * 32;
                                 if (r >= a.NR) break;
                                 float4 *p0 = reinterpret_cast<float4 *>(ub) + r;
@@ -237,9 +244,11 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         }
                     };
                     if (RP > 0 && pk)
-                        fill(BoolTag<RP != 0>());
+                        fill(BoolTag<RP != 0>(), IntTag<TF_LU>());
+                    else if (a.NR <= 2 * TF_LGW * 32)
+                        fill(BoolTag<false>(), IntTag<2>());
                     else
-                        fill(BoolTag<false>());
+                        fill(BoolTag<false>(), IntTag<TF_LU>());
                     // generic-proxy stores -> visible to the tensor core (async proxy)
                     ptx::fence_proxy_async_smem();
                     __syncwarp();

@@ -77,6 +77,7 @@ struct WsResidues {
     int line0[4];   // first line of the residue's box inside a ring slot
     int step;       // tap step inside a residue: 4 / gcd(d, 4)
     int tapcopy;    // 1: one staged copy per tap (single box per row), lines (c, j)
+    int nreal0;     // real taps of residue 0 (n[0] may be padded so cin * n[0] == Ls)
 };
 
 struct WsArgs {
@@ -84,6 +85,7 @@ struct WsArgs {
     int J, sb, NB;       // dy copies per stage, their shift step (Ja*d floats, 4 | sb), N
                          // (J*Q rows rounded up to 16: B rows jb'*Q + o, zero rows past J*Q)
     int tma_mirror;      // DP_WG_TMA_MIRROR: mirror slots loaded by TMA, not the converters
+    int pair;            // one 2-row x box feeds two consecutive blocks of a column
     int n_tiles, G, n_groups, splits;
     int Ho, Wo, nvb, T, Hi;
     long long kb_total;  // n * nvb * d columns x T blocks
@@ -151,7 +153,8 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                    const __grid_constant__ CUtensorMap tm_x1,
                    const __grid_constant__ CUtensorMap tm_x2,
                    const __grid_constant__ CUtensorMap tm_x3,
-                   const __grid_constant__ CUtensorMap tm_dy, const WsArgs a) {
+                   const __grid_constant__ CUtensorMap tm_dy,
+                   const __grid_constant__ CUtensorMap tm_xp, const WsArgs a) {
     extern __shared__ __align__(1024) unsigned char ws_smem_raw[];
     __shared__ uint64_t sfull[WS_MAX_SS], cfull[WS_MAX_SS], sempty[WS_MAX_SS], accfull;
     __shared__ uint32_t s_tmem;
@@ -194,6 +197,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         // ================================ TMA producer ================================
         WsSched sc(a, kb_first, n_i);
         unsigned char *ring = smem + a.ring_hi;
+        int pre = 0;  // this block's new row came with the previous block's 2-row box
         for (int kl = 0; kl < nkb; ++kl, sc.next()) {
             const int s = kl % a.SS;
             WS_TRACE(a, kl, 1, lane == 0);
@@ -207,11 +211,23 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 const int hh = sc.img * a.Hi + sc.u;
                 const int k0 = sc.cstart ? 0 : n_i - 1;
                 WS_TRACE(a, kl, 0, true);
+                // TMA box count, not bytes, limits this producer: inside a column one 2-row
+                // box (rows u + (n_i-1) d and u + n_i d, adjacent ring slots) feeds this
+                // block and the next one
+                int slotN = sc.Bm + n_i - 1;
+                if (slotN >= a.R) slotN -= a.R;
+                const bool skip = !sc.cstart && pre;
+                const bool pair = a.pair && !sc.cstart && !pre && sc.t + 1 < a.T &&
+                                  kl + 1 < nkb && slotN + 1 < a.R;
                 int nbox_rows = 0;
-                for (int k = k0; k < n_i; ++k) {
-                    int slot = sc.Bm + k;
-                    if (slot >= a.R) slot -= a.R;
-                    nbox_rows += (a.tma_mirror && slot < a.NM) ? 2 : 1;
+                if (sc.cstart || !a.pair) {
+                    for (int k = k0; k < n_i; ++k) {
+                        int slot = sc.Bm + k;
+                        if (slot >= a.R) slot -= a.R;
+                        nbox_rows += (a.tma_mirror && slot < a.NM) ? 2 : 1;
+                    }
+                } else {
+                    nbox_rows = skip ? 0 : pair ? 2 : 1;
                 }
                 ptx::mbar_expect_tx(&sfull[s], (uint32_t)(a.J * a.Q) * 128u +
                                                    (uint32_t)nbox_rows * a.box_tx_row);
@@ -225,7 +241,12 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                     ptx::tma_load_5d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, 0, 0, sc.u,
                                      sc.img, &sfull[s]);
                 }
-                for (int k = k0; k < n_i; ++k) {
+                if (pair)
+                    ptx::tma_load_5d(ring + (size_t)slotN * a.slot_bytes, &tm_xp,
+                                     v0 + a.rs.j0[0] * a.d - a.rs.b[0], 0, 0, 0,
+                                     hh + (i_lo + n_i - 1) * a.d, &sfull[s]);
+                pre = pair ? 1 : 0;
+                for (int k = (skip || pair) ? n_i : k0; k < n_i; ++k) {
                     int slot = sc.Bm + k;
                     if (slot >= a.R) slot -= a.R;
                     const int row = hh + (i_lo + k) * a.d;
@@ -462,6 +483,7 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
                 const int jj = off - c * rs.n[rb];
                 const int ja = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
                 j = jb * Ja + ja;  // >= l: padding tap of the last column group
+                if (rb == 0 && jj >= rs.nreal0) j = l;  // box-padding tap line
             }
         }
         if (j < l) {
@@ -494,6 +516,7 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
 // host side
 // --------------------------------------------------------------------------------
 struct WsPlan {
+    int pair;
     int J, kc, dc, sb, NB;  // J dy copies (B), kc = Ja column taps in the x lines (A), step dc = d
     int Cpad, Npad, Ls, n_tiles, G, n_groups, splits, SS, R, NM, max_ni;
     int ho, wo, nvb, T, wp_x, wp_dy, lm_dy, mask;
@@ -529,13 +552,14 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     for (int Ja = k; Ja >= 1; --Ja) {
         WsPlan q;
         if (!ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, q)) continue;
-        // per K=8 slice: each tile reads A hi + lo (M rows x 32 B) and B (2 NB + NB rows)
-        double cost = 0;
-        const int lines = k * q.Ls;
-        for (int t = 0; t < q.n_tiles; ++t) {
-            const int m = std::min(128, lines - t * 128) <= 64 ? 64 : 128;
-            cost += 2.0 * m * 32 + 3.0 * q.NB * 32 + 1500;  // + fixed per-MMA-pair overhead
-        }
+        // cycles per K block (measured model): the tensor core -- an SS MMA costs
+        // max(39, N/2) cycles (tools/tc_probe.cu), 2 per K=8 slice and tile, 4 slices, plus
+        // the commit -- or the TMA producer, ~550 cycles per box (dy + the x boxes of the
+        // new row; half an x box when two rows share one), whichever is slower
+        auto mma = [](int N) { return std::max(39.0, N / 2.0); };
+        const double mma_cycles = 4.0 * q.n_tiles * (mma(2 * q.NB) + mma(q.NB)) + 300.0;
+        const double boxes = 1.0 + (q.pair ? 0.5 : (double)q.rs.n_b);
+        double cost = std::max(mma_cycles, 550.0 * boxes);
         cost *= (double)q.nvb;  // K blocks per row grow with the (J-1) Ja d shift
         if (!ok || cost < best) {
             best = cost;
@@ -586,6 +610,13 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     }
     p.rs.tapcopy = (nres > 1 && cin * kc <= 32 && !getenv("DP_WG_RESIDUE")) ? 1 : 0;
     if (p.rs.tapcopy) p.Ls = (cin * kc + 7) / 8 * 8;
+    // 2-row x boxes need one box per row whose lines fill the slot exactly (the tap
+    // dimension is padded with zero-filled taps to Ls / cin)
+    // (only for rows of <= 8 KB: a 2-row box of 16-KB rows measured 23 % slower, c2 conv3 J=1)
+    p.pair = ((nres == 1 || p.rs.tapcopy) && p.Ls % cin == 0 && p.Ls <= 64 &&
+              !getenv("DP_WG_NOPAIR") && !getenv("DP_WG_TMA_MIRROR"))
+                 ? 1
+                 : 0;
     const int lines = k * p.Ls;
     p.n_tiles = (lines + 127) / 128;
     const int acc_cols = 2 * p.NB;
@@ -615,7 +646,7 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
         p.NM = span - 1;
         for (int ss = WS_MAX_SS; ss >= 2; --ss) {
             const size_t need = (size_t)ss * p.b_bytes +
-                                2 * (size_t)(p.max_ni + ss - 1 + p.NM) * p.slot_bytes;
+                                2 * (size_t)(p.max_ni + ss - 1 + p.pair + p.NM) * p.slot_bytes;
             if (need <= (size_t)WS_SMEM_BUDGET) {
                 p.SS = ss;
                 break;
@@ -623,7 +654,8 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
         }
     }
     if (p.SS < 2) return false;
-    p.R = p.max_ni + p.SS - 1;
+    // a 2-row box fills the next block's slot one block early: one more slot
+    p.R = p.max_ni + p.SS - 1 + p.pair;
     // residue copies: column taps jo with (jo*dc) & 3 == b, lcm(dc, 4) floats apart
     int gcd = 1;
     for (int v = 4; v >= 1; --v)
@@ -671,7 +703,10 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
         p.rs.b[rb] = -1;
         p.rs.n[rb] = p.rs.j0[rb] = p.rs.line0[rb] = 0;
     }
-    p.box_tx_row = (uint32_t)cin * kc * 128u;  // bytes the residue boxes of one row deliver
+    p.rs.nreal0 = p.rs.n[0];
+    if (p.pair) p.rs.n[0] = p.Ls / cin;  // padded tap count: box lines per row == Ls
+    // bytes the residue boxes of one row deliver (zero-filled padding taps included)
+    p.box_tx_row = (uint32_t)cin * (p.pair ? p.rs.n[0] : kc) * 128u;
     // K runs over x-aligned columns: dy shifted by up to (J-1) Ja d needs that many more
     p.nvb = (p.wo + (J - 1) * p.sb + 31) / 32;
     p.T = (p.ho + d - 1) / d;
@@ -772,14 +807,27 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
         const float *base = (const float *)((const unsigned char *)xs + (size_t)used * p.copy_bytes);
         // (w, jj: lcm(d, 4) floats, c, row of n*hi) -- overlapping views, one box = the
         // residue's (c, jj) lines of one input row
-        cuuint64_t dims[4] = {(cuuint64_t)p.wp_x, (cuuint64_t)p.rs.n[used], (cuuint64_t)cin,
-                              (cuuint64_t)n * hi};
+        cuuint64_t dims[4] = {(cuuint64_t)p.wp_x,
+                              (cuuint64_t)(used == 0 ? p.rs.nreal0 : p.rs.n[used]),
+                              (cuuint64_t)cin, (cuuint64_t)n * hi};
         // tap dimension: lcm(d, 4) floats inside a residue copy, or the copy stride when each
         // tap has its own pre-shifted copy
         cuuint64_t str[3] = {p.rs.tapcopy ? (cuuint64_t)p.copy_bytes : (cuuint64_t)p.rs.step * p.dc * 4,
                              xrow, ximg_row};
         cuuint32_t box[4] = {32, (cuuint32_t)p.rs.n[used], (cuuint32_t)cin, 1};
         rc = wg_make_map(&mx[rb], base, 4, dims, str, box, true);
+        if (rc) return rc;
+    }
+    CUtensorMap mxp = mx[0];
+    if (p.pair) {
+        // residue 0's view with two rows d apart: (w, jj, c, q: d rows, r: rows of n*hi)
+        cuuint64_t dims[5] = {(cuuint64_t)p.wp_x, (cuuint64_t)p.rs.nreal0, (cuuint64_t)cin, 2,
+                              (cuuint64_t)n * hi};
+        cuuint64_t str[4] = {p.rs.tapcopy ? (cuuint64_t)p.copy_bytes
+                                          : (cuuint64_t)p.rs.step * p.dc * 4,
+                             xrow, ximg_row * (cuuint64_t)d, ximg_row};
+        cuuint32_t box[5] = {32, (cuuint32_t)p.rs.n[0], (cuuint32_t)cin, 2, 1};
+        rc = wg_make_map(&mxp, xs, 5, dims, str, box, true);
         if (rc) return rc;
     }
     a.C = cin;
@@ -792,6 +840,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.sb = p.sb;
     a.NB = p.NB;
     a.tma_mirror = getenv("DP_WG_TMA_MIRROR") ? 1 : 0;
+    a.pair = p.pair;
     a.n_tiles = p.n_tiles;
     a.G = p.G;
     a.n_groups = p.n_groups;
@@ -820,7 +869,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     if (e != cudaSuccess)
         return set_error(DP_ERR_CUDA, "tc_wgrad_ss: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     const int grid = p.n_groups * p.splits;
-    tc_wgrad_ss_kernel<<<grid, WS_THREADS, smem, st>>>(mx[0], mx[1], mx[2], mx[3], mdy, a);
+    tc_wgrad_ss_kernel<<<grid, WS_THREADS, smem, st>>>(mx[0], mx[1], mx[2], mx[3], mdy, mxp, a);
     rc = check_launch("tc_wgrad_ss_kernel");
     if (rc) return rc;
     const long long total = (long long)k * p.Ls * p.NB + cout;

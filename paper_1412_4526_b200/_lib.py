@@ -14,7 +14,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdenseprop_b200.so")
+# DP_LIB_PATH: load another build of the library (A/B experiments on one box)
+LIB_PATH = os.environ.get("DP_LIB_PATH") or os.path.join(PKG, "libdenseprop_b200.so")
 
 DP_F32, DP_F64 = 0, 1
 DP_IDENTITY, DP_TANH, DP_RELU, DP_TANH_FAST = 0, 1, 2, 3

@@ -25,8 +25,8 @@
 // (Npad <= 128), else three N = Npad MMAs.  D columns [0, Npad) + [Npad, 2 Npad) summed
 // in the epilogue.
 //
-// Per CTA (persistent, one per SM, 13 warps):
-//   warps 4-11 loaders, 2 groups of 4 taking alternate units (a single group was
+// Per CTA (persistent, one per SM, 14 warps):
+//   warps 4-12 loaders, 3 groups of 3 taking units in turn (a single group was
 //              latency-bound at ~2700 cycles per unit, above the MMA time):
 //              per (tile, channel chunk rc, tap row i) unit fill one halo unit
 //              buffer: records f0 + i*d*Wv + [0, NR) of the 8 channels (coalesced LDG,
@@ -34,7 +34,7 @@
 //              hi/lo, four 16-byte STS per pixel; loader warp 0 also requests the unit's
 //              l K-steps of packed weights with one bulk async copy into the same buffer
 //              (first warp of the group).
-//   warp 12    MMA issuer: per unit l taps x MT M tiles x 2 MMAs, one tcgen05.commit
+//   warp 13    MMA issuer: per unit l taps x MT M tiles x 2 MMAs, one tcgen05.commit
 //              frees the unit buffer; one commit per tile hands the accumulators over.
 //   warps 0-3  epilogue (one per TMEM lane quarter): tcgen05.ld, bias +
 //              nonlinearity (forward) or the upstream nonlinearity's derivative (data
@@ -49,18 +49,18 @@ namespace dp {
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
-// 13 warps: registers are granted per 4 warps, so 13 warps (as 16) leave 128 registers
-// per thread for the loaders' 40 values in flight; 17 warps (as 20) would cap them at 96.
+// 14 warps: registers are granted per 4 warps, so 14 warps (as 16) leave 128 registers
+// per thread for the loaders' 48 values in flight; 17 warps (as 20) would cap them at 96.
 constexpr int TF_EPI_WARPS = 4;
 constexpr int TF_LOAD_WARP0 = 4;
-constexpr int TF_LOAD_WARPS = 8;
-constexpr int TF_MMA_WARP = 12;
+constexpr int TF_LOAD_WARPS = 9;
+constexpr int TF_MMA_WARP = 13;
 constexpr int TF_THREADS = (TF_MMA_WARP + 1) * 32;
 constexpr int TF_MAX_MT = 8;
 constexpr int TF_MAX_HB = 6;
-constexpr int TF_LGROUPS = 2;  // loader groups, alternate units (two units' loads in flight)
+constexpr int TF_LGROUPS = 3;  // loader groups of 3 warps, rotating units (three in flight)
 constexpr int TF_LGW = TF_LOAD_WARPS / TF_LGROUPS;  // warps per loader group
-constexpr int TF_LU = 5;  // loader: records per thread in flight (NR <= TF_LU * 128 per pass)
+constexpr int TF_LU = 6;  // loader: records per thread in flight (NR <= TF_LU * 128 per pass)
 constexpr int TF_SMEM_BUDGET = 220 * 1024;
 
 struct TfArgs {
@@ -421,18 +421,26 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd) {
         if (v >= 1 && v < mt) mt = v;
     }
     if (max_mt >= 1 && mt > max_mt) mt = max_mt;
-    p.MT = mt;
-    p.NR = (mt * 128 + (l - 1) * d + 7) / 8 * 8;
-    p.plane_bytes = (uint32_t)p.NR * 16;
-    p.halo_bytes = 4 * p.plane_bytes;
-    p.wunit_pk = (uint32_t)(p.G * p.Npad * 64);
-    // unit buffers hold the largest unit: a full one unless the packed chunk is the only one
-    p.wunit_bytes = (uint32_t)((p.rp && p.n_rc == 1 ? p.G : l) * p.Npad * 64);
-    p.ubytes = (p.halo_bytes + p.wunit_bytes + 127) / 128 * 128;
-    long long hb = (long long)TF_SMEM_BUDGET / p.ubytes;
-    if (hb > TF_MAX_HB) hb = TF_MAX_HB;
-    p.HB = (int)hb;
-    p.ok = p.ok && p.HB >= 2 && (p.plane_bytes >> 4) < (1u << 14);
+    // At least TF_LGROUPS unit buffers: a loader group starts waiting for a buffer up to
+    // TF_LGROUPS units ahead, and with fewer buffers that wait would be two phases ahead
+    // of the barrier -- a parity wait then passes on the stale phase.  Fewer M tiles
+    // (a smaller halo) until they fit.
+    for (;; mt = (mt + 1) / 2) {
+        p.MT = mt;
+        p.NR = (mt * 128 + (l - 1) * d + 7) / 8 * 8;
+        p.plane_bytes = (uint32_t)p.NR * 16;
+        p.halo_bytes = 4 * p.plane_bytes;
+        p.wunit_pk = (uint32_t)(p.G * p.Npad * 64);
+        // unit buffers hold the largest unit: a full one unless the packed chunk is the
+        // only one
+        p.wunit_bytes = (uint32_t)((p.rp && p.n_rc == 1 ? p.G : l) * p.Npad * 64);
+        p.ubytes = (p.halo_bytes + p.wunit_bytes + 127) / 128 * 128;
+        long long hb = (long long)TF_SMEM_BUDGET / p.ubytes;
+        if (hb > TF_MAX_HB) hb = TF_MAX_HB;
+        p.HB = (int)hb;
+        if (p.HB >= TF_LGROUPS || mt == 1) break;
+    }
+    p.ok = p.ok && p.HB >= TF_LGROUPS && (p.plane_bytes >> 4) < (1u << 14);
     return p;
 }
 

@@ -652,7 +652,7 @@ static int wg_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, (void *)base, dims, strides_bytes,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return set_error(DP_ERR_CUDA, "weight gradient: cuTensorMapEncodeTiled failed (%d)",
                          (int)r);

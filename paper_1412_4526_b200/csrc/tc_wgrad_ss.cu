@@ -65,7 +65,7 @@ constexpr int WS_CONV_WARPS = 8;
 constexpr int WS_TMA_WARP = 8;
 constexpr int WS_MMA_WARP = 9;
 constexpr int WS_THREADS = 320;
-constexpr int WS_MAX_SS = 8;
+constexpr int WS_MAX_SS = 12;
 constexpr int WS_MAX_G = 16;
 constexpr int WS_SMEM_BUDGET = 222 * 1024;
 

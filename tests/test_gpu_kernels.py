@@ -86,7 +86,10 @@ def test_conv_vs_cport(K, shape, dt):
 
 
 POOL_SHAPES = [(4, 2, 1, 40, 41), (3, 3, 2, 33, 35), (2, 8, 1, 40, 40), (5, 2, 16, 60, 50),
-               (1, 4, 4, 30, 31), (2, 1, 3, 7, 7)]
+               (1, 4, 4, 30, 31), (2, 1, 3, 7, 7),
+               # several shared-memory tiles (128 x 32) per plane, halos up to 48, p <= 8
+               (2, 4, 1, 150, 300), (2, 8, 1, 99, 270), (2, 5, 3, 90, 170), (3, 2, 4, 70, 290),
+               (1, 7, 8, 80, 400), (1, 9, 1, 40, 50), (1, 3, 25, 60, 60)]
 
 
 @pytest.mark.parametrize("shape", POOL_SHAPES)
@@ -109,6 +112,23 @@ def test_pools_vs_cport(K, shape, dt):
     assert np.array_equal(K.avgpool_forward(x, p, d), kernels_c.avgpool_forward(x, p, d, 4))
     assert np.array_equal(K.avgpool_backward(dy, p, d, h, w),
                           kernels_c.avgpool_backward(dy, p, d, h, w, 4))
+
+
+@pytest.mark.parametrize("p,d", [(2, 1), (4, 1), (8, 1), (3, 5)])
+def test_pool_nan_signed_zero(K, p, d):
+    # NaN never wins (strict '>'), -0.0 / +0.0 ties keep the row-major first (the separable
+    # shared-memory forward must pick exactly the reference's element)
+    rng = np.random.default_rng(p * 10 + d)
+    x = rng.choice(np.array([0.0, -0.0, 1.0, -1.0, np.nan], np.float32), size=(2, 60, 150))
+    x[1, :20, :40] = np.nan
+    y, arg = K.maxpool_forward(x, p, d)
+    y2, arg2 = kernels_c.maxpool_forward(x, p, d, 4)
+    assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
+    assert np.array_equal(arg, arg2)
+    dy = rng.uniform(-1, 1, y.shape).astype(np.float32)
+    h, w = x.shape[1:]
+    assert np.array_equal(K.maxpool_backward(dy, arg, p, d, h, w).view(np.uint32),
+                          kernels_c.maxpool_backward(dy, arg, p, d, h, w, 4).view(np.uint32))
 
 
 def test_maxpool_special_values(K):

@@ -439,6 +439,66 @@ def sizes_sweep(budget_cpu=True):
     return points
 
 
+def mask_sweep(tr, batch_tensors, side, timed, steps=5):
+    """Training-step time (CUDA-graph replay: fwd + masked bwd + SGD) per error-mask size,
+    1 pixel .. the full image per image; spread = (max - min) / min, the reference's budget is
+    10 % (bench.py:311-343).  Restores the full mask afterwards."""
+    import torch
+    imgs, tgts, masks = batch_tensors
+    tr.load_batch(imgs, tgts, masks)
+    total = side * side
+    sizes = [1, total // 1000, total // 100, total // 10, total // 2, total]
+    rng = np.random.default_rng(5)
+    ms = []
+    for k in sizes:
+        m = np.zeros((masks.shape[0], total), np.uint8)
+        for b in range(masks.shape[0]):
+            m[b, rng.choice(total, k, replace=False)] = 1
+        tr.net.mask.copy_(torch.from_numpy(m.reshape(masks.shape)))
+        ms.append(timed(lambda s: tr.step(), steps) / steps)
+    tr.net.mask.copy_(masks)
+    spread = (max(ms) - min(ms)) / min(ms)
+    return {"mask_pixels_per_image": sizes, "ms_per_step": ms, "spread": spread,
+            "ok": spread <= 0.10, "steps_per_size": steps}
+
+
+def patch_scan_gpu(text, side, n_pix, dev, batch=4096, reps=2):
+    """GPU patch-by-patch baseline: n_pix patches of one synthetic image through the strided
+    network (same tcgen05 conv kernels at dilation 1), forward only and forward + backward
+    (per-patch gradients summed), device-timed with CUDA events."""
+    import torch
+    import paper_1412_4526_b200 as dp
+    from paper_1412_4526_b200 import patchscan
+    spec = dp.parse_spec(text)
+    img = (torch.rand((spec.input_channels, side, side), device=dev) - 0.5)
+    x0 = patchscan._padded(spec, img)
+    batch = min(batch, n_pix)
+    net = patchscan.PatchNet(spec, batch, train=True, precision="fast")
+    pix = torch.arange(n_pix, dtype=torch.int32, device=dev)
+    delta = torch.rand((batch, net.out_channels), device=dev) - 0.5
+
+    def run(train):
+        for first in range(0, n_pix, batch):
+            patchscan._gather(x0, net.inputs[0], pix[first:first + batch], net.n)
+            net.forward()
+            if train:
+                net.backward(delta)
+
+    out = {"unit": "pixels/s", "patch": net.n, "side": side,
+           "sample": f"{n_pix} patches of one {side}x{side} image, batches of {batch}"}
+    for key, train in (("forward", False), ("train", True)):
+        run(train)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run(train)
+        e1.record()
+        torch.cuda.synchronize()
+        out[key] = reps * n_pix / (e0.elapsed_time(e1) / 1e3)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -617,6 +677,10 @@ def main():
     barrier()
     ms_fwd_e2e = maxrank(f0.elapsed_time(f1))
 
+    # ---- mask-size sweep (reference bench.py:311-343): the training step's
+    # cost must not depend on how many pixels the error mask keeps
+    msweep = mask_sweep(tr, dpool[0], SIDE, timed) if not args.no_sweep else None
+
     # ---- per-kernel timing of one eager step (roofline of the dominant kernel)
     prof = engine.profile_step(tr, reps=5)
 
@@ -684,23 +748,19 @@ def main():
         "clocks": clocks,
         "distributed": dist_info,
     }
+    if msweep is not None:
+        line["mask_sweep"] = msweep
 
     if rank == 0 and world == 1 and not args.no_sweep:
-        # patch-by-patch baseline on the same GPU: every pixel's
-        # 29x29 window of a c2 image classified on its own through the same kernels
-        c2 = dp.compile_plan(dp.parse_spec(C2_TEXT))
-        one = (torch.rand((1, 3, 256, 256), device=dev) - 0.5)
-        dp.patch_scan_forward(c2, one, batch=8192)
-        torch.cuda.synchronize()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record()
-        dp.patch_scan_forward(c2, one, batch=8192)
-        q1.record()
-        torch.cuda.synchronize()
-        ps = 256 * 256 / (q0.elapsed_time(q1) / 1e3)
+        # patch-by-patch baseline on the same GPU: the ORIGINAL
+        # strided network on every pixel's patch (patchscan.PatchNet), fwd and fwd + bwd
         line["patch_scan_gpu"] = {
-            "value": ps, "unit": "pixels/s", "config": "c2",
-            "sample": "1 image of c2@256: 65536 windows, batches of 8192, same kernels"}
+            name: patch_scan_gpu(CONFIGS[name][0], CONFIGS[name][1], n_pix, dev)
+            for name, n_pix in (("c2", 65536), (args.config, 16384))}
+        for name, ps in line["patch_scan_gpu"].items():
+            if name == args.config:
+                ps["dense_over_scan_forward"] = line["forward"]["value"] / ps["forward"]
+                ps["dense_over_scan_train"] = value / ps["train"]
 
         # the other BASELINE configs on the same GPU, a sampled CPU reference beside each
         threads = os.cpu_count() or 1

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DP_ABI_VERSION 4
+#define DP_ABI_VERSION 5
 
 enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
 /* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
@@ -226,9 +226,35 @@ int dp_softmax_xent_delta(int dtype, const void *logits, const uint8_t *labels,
  * zero-padded image x0 (c, hp, wp) into out (count, c, patch, patch) */
 int dp_patch_gather(int dtype, const void *x0, void *out, int c, int hp, int wp, int patch,
                     int w, int64_t first, int64_t count, void *stream);
-/* param -= lr * grad (plain SGD; the reference has no optimizer) */
+/* param = param - lr * grad, rounded as numpy rounds it (plain SGD; the reference has no
+ * optimizer) */
 int dp_sgd_update(int dtype, void *param, const void *grad, int64_t count, double lr,
                   void *stream);
+
+/* ---- original strided network, for the GPU patch-by-patch baseline -------------------
+ * (reference oracle.py:29-262: conv_strided / maxpool_strided / avgpool_strided,
+ * scan_forward, patch_backward_batch).  Device pointers, batches of n patches. */
+enum dp_pool_kind { DP_POOL_MAX = 0, DP_POOL_AVG = 1 };
+/* strided pool (oracle.py:58-91): y = tap(0,0), then row-major taps; max: strict `>`
+ * (first wins), int32 argmax i*p+j; avg: running sum / p^2.  Requires (h-p) % s == 0
+ * (oracle.py _out_side). */
+int dp_pool_strided_forward(int dtype, int kind, const void *x, void *y, int32_t *arg, int n,
+                            int c, int h, int w, int p, int s, void *stream);
+/* its backward (oracle.py:190-211) as a gather in ascending tap order; hi = (ho-1)*s + p */
+int dp_pool_strided_backward(int dtype, int kind, const void *dy, const int32_t *arg, void *dx,
+                             int n, int c, int ho, int wo, int p, int s, int hi, int wi,
+                             void *stream);
+/* y[u,v] = x[u*s, v*s]: a stride-s conv is the stride-1 conv sampled every s pixels */
+int dp_subsample(int dtype, const void *x, void *y, int n, int c, int h, int w, int s, int ho,
+                 int wo, void *stream);
+/* out (n,c,hf,wf) = 0 except out[u*s, v*s] = dy[u,v]: backward of dp_subsample */
+int dp_zero_insert(int dtype, const void *dy, void *out, int n, int c, int ho, int wo, int s,
+                   int hf, int wf, void *stream);
+/* gather the patch x patch windows of an arbitrary pixel list (flat indices y*w + x over the
+ * w = wp-patch+1 wide output grid, device int32[count], caller-validated) of ONE padded
+ * image x0 (c, hp, wp) into out (count, c, patch, patch) */
+int dp_patch_gather_pixels(int dtype, const void *x0, void *out, int c, int hp, int wp, int patch,
+                           const int32_t *pixels, int64_t count, void *stream);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,8 @@ DP_F32, DP_F64 = 0, 1
 DP_IDENTITY, DP_TANH, DP_RELU, DP_TANH_FAST = 0, 1, 2, 3
 DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED = 0, 1, 2, 3
 NONLIN_CODE = {"identity": DP_IDENTITY, "tanh": DP_TANH, "relu": DP_RELU}
-ABI_VERSION = 4
+DP_POOL_MAX, DP_POOL_AVG = 0, 1  # enum dp_pool_kind
+ABI_VERSION = 5
 
 _vp, _i, _i64, _sz, _d = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double
 
@@ -74,6 +75,11 @@ SIGNATURES = {
     "dp_patch_gather": (_i, [_i, _vp, _vp, _i, _i, _i, _i, _i, _i64, _i64, _vp]),
     "dp_softmax_xent_delta": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp]),
     "dp_sgd_update": (_i, [_i, _vp, _vp, _i64, _d, _vp]),
+    "dp_pool_strided_forward": (_i, [_i, _i, _vp, _vp, _vp] + [_i] * 6 + [_vp]),
+    "dp_pool_strided_backward": (_i, [_i, _i, _vp, _vp, _vp] + [_i] * 8 + [_vp]),
+    "dp_subsample": (_i, [_i, _vp, _vp] + [_i] * 7 + [_vp]),
+    "dp_zero_insert": (_i, [_i, _vp, _vp] + [_i] * 7 + [_vp]),
+    "dp_patch_gather_pixels": (_i, [_i, _vp, _vp, _i, _i, _i, _i, _vp, _i64, _vp]),
 }
 
 _lock = threading.Lock()

@@ -15,16 +15,16 @@
 namespace dp {
 
 template <typename T>
-__global__ void nonlin_fwd_kernel(const T *__restrict__ x, T *__restrict__ y, long long n,
-                                  int kind) {
+__global__ void nonlin_fwd_kernel(const T *x, T *y, long long n, int kind) {  // may alias
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         y[i] = apply_nonlin(x[i], kind);
 }
 
 template <typename T>
-__global__ void nonlin_bwd_kernel(const T *__restrict__ dy, const T *__restrict__ x,
-                                  T *__restrict__ dx, long long n, int kind, int x_is_output) {
+__global__ void nonlin_bwd_kernel(const T *dy, const T *__restrict__ x, T *dx, long long n,
+                                  int kind, int x_is_output) {
+    // dy and dx may alias (the engine gates a delta in place): no __restrict__ on them
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         T t = x[i];
@@ -115,7 +115,7 @@ template <typename T>
 __global__ void sgd_kernel(T *__restrict__ p, const T *__restrict__ g, long long n, T lr) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
-        p[i] = p[i] - lr * g[i];
+        p[i] = add_rn(p[i], -mul_rn(lr, g[i]));  // numpy p - lr*g: no FMA contraction
 }
 
 static inline int grid_for(long long n) {

@@ -65,15 +65,16 @@ def band_assignment(n_images: int, height: int, rank: int, world: int):
 
     Ranks are split into n_images groups of `per = world // n_images`; rank r takes image
     r // per and the balanced band (r % per) of its output rows.  Returns
-    (image, r0, r1) -- output rows [r0, r1) -- or None for the (world % n_images) ranks
-    left over, which contribute an all-zero bucket.  An output row depends on the padded
+    (image, r0, r1) -- output rows [r0, r1) -- or None for the ranks left over (world %
+    n_images, plus any beyond `height` bands per image), which contribute an all-zero
+    bucket.  An output row depends on the padded
     input rows [row, row + patch - 1] only (valid convolutions on the padded image,
     forward.py:96-98), so a band is computed exactly from padded rows [r0, r1 + patch - 1)
     (the (patch - 1)-row halo) and band gradients, with the mask restricted to the band,
     sum to the full image's (unweighted-sum semantics, backward.py:190-191)."""
     if n_images >= world:
         raise ValueError("band sharding is the fallback for fewer images than ranks")
-    per = world // n_images
+    per = min(world // n_images, height)  # every band keeps >= 1 output row
     if rank >= per * n_images:
         return None
     img, band = divmod(rank, per)
@@ -87,11 +88,37 @@ def band_rows(r0: int, r1: int, patch: int):
     return slice(r0, r1 + patch - 1), slice(r0, r1)
 
 
-def allreduce_sum(tensor, group=None):
-    """In-place SUM all-reduce of the gradient bucket (no-op when not distributed)."""
+def group_root(group=None) -> int:
+    """Global rank of the first member of `group` (the broadcast source of the initial
+    weights); 0 for the default group.  dist.broadcast's `src` is a GLOBAL rank."""
+    import torch.distributed as dist
+    if group is None or group is dist.group.WORLD:
+        return 0
+    return dist.get_global_rank(group, 0)
+
+
+def broadcast_params(tensor, group=None):
+    """Every member of `group` starts from the group's first member's weights."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+        dist.broadcast(tensor, src=group_root(group), group=group)
+    return tensor
+
+
+def allreduce_sum(tensor, group=None):
+    """In-place SUM all-reduce of the gradient bucket (no-op when not distributed).
+
+    NCCL is stream-ordered on the tensor's device.  Other backends (gloo: the CPU tests, and
+    ranks sharing one GPU) reduce a host copy, so the result is in place before the next
+    kernel on the current stream (the SGD update) reads it."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if tensor.is_cuda and dist.get_backend(group) != "nccl":
+            host = tensor.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+            tensor.copy_(host)
+        else:
+            dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
     return tensor
 
 
@@ -115,9 +142,8 @@ class DataParallelTrainer:
         self.group = group
         self.lr = lr
         self.distributed = dist.is_available() and dist.is_initialized()
-        if self.distributed and dist.get_world_size(group) > 1:
-            # every rank starts from rank 0's weights (seeded specs agree anyway)
-            dist.broadcast(self.net.param_flat, src=0, group=group)
+        # every rank starts from the group's first member's weights (seeded specs agree)
+        broadcast_params(self.net.param_flat, group)
         self._graph = None
         self._use_graph = use_graph
         self._torch = torch
@@ -216,8 +242,6 @@ class BandParallelTrainer:
     def __init__(self, plan: DensePlan, n_images: int, height: int, width: int,
                  rank: int = 0, world: int = 1, lr: float = 0.0, group=None, dtype=None,
                  precision: str = "fast"):
-        import torch.distributed as dist
-
         from .engine import DenseNet
         from .netspec import patch_size
         self.patch = patch_size(plan.source)
@@ -227,8 +251,7 @@ class BandParallelTrainer:
         self.lr = lr
         rows = (self.assign[2] - self.assign[1]) if self.assign else 1
         self.net = DenseNet(plan, 1, rows, width, dtype=dtype, train=True, precision=precision)
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            dist.broadcast(self.net.param_flat, src=0, group=group)
+        broadcast_params(self.net.param_flat, group)
 
     def load(self, padded_images, targets, masks):
         """padded_images: (N, C, h + patch - 1, w + patch - 1) device tensor (the engine's

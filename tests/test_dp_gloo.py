@@ -189,3 +189,42 @@ def test_band_assignment_partitions_rows():
             assert rows[img] == list(range(h))
     with pytest.raises(ValueError):
         trainer.band_assignment(4, 10, 0, 2)
+
+
+def test_band_assignment_more_ranks_than_rows():
+    """ADVICE r1: bands never empty when height < world // n_images."""
+    from paper_1412_4526_b200 import trainer
+    for n_img, world, h in ((1, 8, 3), (2, 8, 1), (1, 5, 4)):
+        got = [trainer.band_assignment(n_img, h, r, world) for r in range(world)]
+        live = [a for a in got if a is not None]
+        assert all(r1 > r0 for _, r0, r1 in live)
+        for img in range(n_img):
+            rows = sorted(y for i, r0, r1 in live if i == img for y in range(r0, r1))
+            assert rows == list(range(h))
+
+
+def _subgroup_worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1412_4526_b200 import trainer
+    group = dist.new_group([1, 2])           # a subgroup without global rank 0
+    t = torch.full((4,), float(rank + 10))
+    if rank in (1, 2):
+        assert trainer.group_root(group) == 1
+        trainer.broadcast_params(t, group)
+        trainer.allreduce_sum(t, group)
+        np.save(f"{out_path}.{rank}.npy", t.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_subgroup_broadcast_uses_group_first_member(tmp_path):
+    """the initial-weight broadcast on a subgroup comes from the group's first
+    member (global rank 1 here), not global rank 0, and does not raise."""
+    out = str(tmp_path / "t")
+    mp.spawn(_subgroup_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    for r in (1, 2):
+        assert np.array_equal(np.load(f"{out}.{r}.npy"), np.full(4, 22.0))

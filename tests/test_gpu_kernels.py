@@ -177,3 +177,22 @@ def test_errors(K):
                            2, 1, 3, 3)
     with pytest.raises(ValueError):
         K.conv_backward_kernel(x, np.zeros((1, 3, 3), np.float32), 3, 1)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_sgd_update_matches_numpy(dt):
+    """dp_sgd_update (the trainer's SGD step, DataParallelTrainer.step) is p - lr*g rounded
+    exactly as numpy rounds it (one multiply, one subtract, no FMA contraction), in place,
+    over a ragged length that is not a multiple of the grid stride."""
+    import torch
+    from paper_1412_4526_b200 import engine
+    rng = np.random.default_rng(3)
+    n = 148 * 256 * 3 + 17
+    p = rng.standard_normal(n).astype(dt)
+    g = rng.standard_normal(n).astype(dt)
+    lr = 0.0123
+    pt, gt = torch.from_numpy(p).cuda(), torch.from_numpy(g).cuda()
+    engine.ops.sgd(pt, gt, lr)
+    want = p - dt(lr) * g
+    assert np.array_equal(pt.cpu().numpy(), want)
+    assert np.array_equal(gt.cpu().numpy(), g)

@@ -5,11 +5,14 @@
 // :56-91 data gradient).  On the virtual (zero-padded) input grid of width Wv output pixel
 // (u, v) is p = u*Wv + v and tap (i, j) reads input record p + i*d*Wv + j*d.  The flat kernel
 // reads one 128-record A window per TAP; here one window per TAP ROW serves all l taps:
-//   D'[r, (j, o)] = sum_c A[s + r, c] * W[o, c, i, j]     (N = l * Npad columns)
+//   D'[r, (j, o)] = sum_c A[s + r, c] * W[o, c, i, j]     (N = l * QS columns, rounded to 16)
 // and the epilogue forms y[s + r] = sum_j D'[r + j*d, (j, o)], so an M tile of 128 rows yields
 // S = 128 - (l-1)*d outputs (M tiles overlap by (l-1)*d rows).  Per tap row and M tile the
-// tensor core reads A_hi twice and A_lo once (three N = l*Npad MMAs: A_hi W_hi, A_hi W_lo,
+// tensor core reads A_hi twice and A_lo once (three N = LN MMAs: A_hi W_hi, A_hi W_lo,
 // A_lo W_hi) instead of 2*l times -- the flat kernel's limiter was exactly these A reads.
+// QS, the column stride of one tap in N, is Q rounded to 16 -- or to 8 when Q <= 8 (the
+// 8-class heads): c3's head (l = 7, Q = 8) then has N = 64 instead of 112, half the B reads
+// and TMEM columns per M tile, so 4 instead of 2 M tiles share a CTA tile's weight rows.
 //
 // Input records come from tc_relayout: per (image, channel chunk of 8) four planes
 // [hi c0-3 | hi c4-7 | lo c0-3 | lo c4-7] of 16-byte records over the whole virtual grid
@@ -18,7 +21,7 @@
 //
 // Per CTA (persistent, one per SM, 6 warps):
 //   warp 4   producer: per unit (tile, chunk, TR tap rows) 4*TR record copies + the unit's
-//            packed weights ([tap row][B_hi (l*Npad rows) | B_lo]), one expect_tx;
+//            packed weights ([tap row][B_hi (LN rows) | B_lo]), one expect_tx;
 //   warp 5   MMA issuer: TR * MT * 3 MMAs per unit, one commit frees the unit buffer, one
 //            commit per tile hands the accumulators (double-buffered) to the epilogue;
 //   warps 0-3 epilogue, one per TMEM lane quarter: per 16-channel chunk and tap j,
@@ -45,14 +48,14 @@ struct TtArgs {
     const float *bias;
     float *out;          // (n, Q, Ho, Wo)
     const float *gate;
-    int n_rc, l, d, Q, Npad, LN, MT, S, NR, TR, n_tr;
+    int n_rc, l, d, Q, Npad, QS, LN, MT, S, NR, TR, n_tr;
     int Wv, Ho, Wo, act, gate_kind;
     long long plane_recs;
     int flat_len, tiles_per_img, total_tiles, HB;
     uint32_t seg_bytes;    // NR * 16
     uint32_t wrow_bytes;   // one tap row of packed weights: 2 * LN * 32
     uint32_t ubytes;       // unit buffer
-    uint32_t xoff;         // epilogue exchange area: [l][16][160] floats after the units
+    uint32_t xoff;         // epilogue exchange area: [l][8 or 16][160] floats after the units
 };
 
 __device__ __forceinline__ float tt_act(float v, int kind) {
@@ -75,7 +78,8 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
     const int units = a.n_rc * a.n_tr;
     for (int o = threadIdx.x; o < a.Npad; o += blockDim.x)
         s_bias[o] = (!BWD && o < a.Q) ? a.bias[o] : 0.f;
-    for (int e = threadIdx.x; e < a.l * 16 * 32; e += blockDim.x)
+    const int XC = a.QS == 8 ? 8 : 16;  // exchange columns per tap
+    for (int e = threadIdx.x; e < a.l * XC * 32; e += blockDim.x)
         s_x[(e >> 5) * 160 + 128 + (e & 31)] = 0.f;
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.HB; ++b) {
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
                 const bool inside = r < a.S && p < a.flat_len && v < a.Wo;
                 const long long pix = img_off + (long long)u * a.Wo + v;
                 const uint32_t dcol = tmem + lane_off + (uint32_t)((buf * MT + mt) * a.LN);
-                for (int o0 = 0; o0 < a.Npad; o0 += 16) {
+                for (int o0 = 0; o0 < a.QS; o0 += 16) {
                     // all l taps' columns of this chunk: l TMEM loads, one wait; publish
                     // rows; one barrier; gather rows r + j*d; one barrier (reuse)
                     float acc[16];
@@ -222,11 +226,18 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
                     for (int j = 0; j < TT_MAX_L; ++j) {
                         if (j >= a.l) break;
                         uint32_t rv[16];
-                        ptx::tmem_ld16(dcol + (uint32_t)(j * a.Npad + o0), rv);
-                        ptx::tmem_wait_ld();
-                        float *xs = s_x + j * 16 * 160;
+                        float *xs = s_x + j * XC * 160;
+                        if (a.QS == 8) {  // one 8-column tap group (never past the allocation)
+                            ptx::tmem_ld8(dcol + (uint32_t)(j * 8), rv);
+                            ptx::tmem_wait_ld();
 #pragma unroll
-                        for (int t = 0; t < 16; ++t) xs[t * 160 + r] = __uint_as_float(rv[t]);
+                            for (int t = 0; t < 8; ++t) xs[t * 160 + r] = __uint_as_float(rv[t]);
+                        } else {
+                            ptx::tmem_ld16(dcol + (uint32_t)(j * a.QS + o0), rv);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int t = 0; t < 16; ++t) xs[t * 160 + r] = __uint_as_float(rv[t]);
+                        }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
@@ -234,9 +245,14 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
                         if (j >= a.l) break;
                         const int rr = r + j * a.d;  // < 128 + 32 whenever r < S
                         if (rr < 160) {
-                            const float *xs = s_x + j * 16 * 160 + rr;
+                            const float *xs = s_x + j * XC * 160 + rr;
+                            if (a.QS == 8) {
 #pragma unroll
-                            for (int t = 0; t < 16; ++t) acc[t] += xs[t * 160];
+                                for (int t = 0; t < 8; ++t) acc[t] += xs[t * 160];
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < 16; ++t) acc[t] += xs[t * 160];
+                            }
                         }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -299,12 +315,11 @@ __global__ void __launch_bounds__(256) tc_relayout(const float *__restrict__ in,
     }
 }
 
-// weights W(q, r, i, j) -> per (chunk rc, tap row i): [hi | lo] tiles of LN = l*Npad rows
-// (row n = j*Npad + q) x K = 8 channels, K-major core-matrix layout
+// weights W(q, r, i, j) -> per (chunk rc, tap row i): [hi | lo] tiles of LN rows
+// (row n = j*QS + q, zero rows past l*QS) x K = 8 channels, K-major core-matrix layout
 // (n>>3)*256 + (k>>2)*128 + (n&7)*16 + (k&3)*4; bwd: W is (R = cout, Q = cin, l, l) rotated.
 __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp, int Q, int R,
-                            int l, int Npad, int n_rc, int bwd) {
-    const int LN = l * Npad;
+                            int l, int QS, int LN, int n_rc, int bwd) {
     const long long total = (long long)n_rc * l * 2 * LN * 8;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -315,10 +330,10 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
         const int hl = (int)(r2 & 1);
         const long long ri = r2 >> 1;  // rc * l + i
         const int i = (int)(ri % l), rc = (int)(ri / l);
-        const int j = n / Npad, qo = n - j * Npad;
+        const int j = n / QS, qo = n - j * QS;
         const int c = rc * 8 + k;
         float v = 0.f;
-        if (qo < Q && c < R) {
+        if (j < l && qo < Q && c < R) {
             if (!bwd)
                 v = w[(((long long)qo * R + c) * l + i) * l + j];
             else
@@ -335,7 +350,7 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
 // host side
 // --------------------------------------------------------------------------------
 struct TtPlan {
-    int Npad, LN, n_rc, MT, S, NR, TR, n_tr, HB;
+    int Npad, QS, LN, n_rc, MT, S, NR, TR, n_tr, HB;
     bool ok;
     uint32_t seg_bytes, wrow_bytes, ubytes, xbytes;
     size_t wbytes;
@@ -345,7 +360,8 @@ static TtPlan tt_plan(int R, int Q, int l, int d, int max_mt) {
     TtPlan p;
     p.ok = false;
     p.Npad = (Q + 15) / 16 * 16;
-    p.LN = l * p.Npad;
+    p.QS = (Q <= 8 && !getenv("DP_TT_QS16")) ? 8 : p.Npad;
+    p.LN = (l * p.QS + 15) / 16 * 16;
     p.n_rc = (R + 7) / 8;
     p.S = 128 - (l - 1) * d;
     if (p.LN > 256 || p.S < 32 || p.Npad > 256) return p;
@@ -364,10 +380,15 @@ static TtPlan tt_plan(int R, int Q, int l, int d, int max_mt) {
     p.wbytes = (size_t)p.n_rc * l * p.wrow_bytes;
     if (l > TT_MAX_L) return p;
     // tap rows per unit: as many as leave room for 2 unit buffers next to the exchange area
-    p.xbytes = (uint32_t)l * 16 * 160 * 4;
+    p.xbytes = (uint32_t)l * (p.QS == 8 ? 8 : 16) * 160 * 4;
     const size_t budget = (size_t)TT_SMEM_TOTAL - p.xbytes - 2048;
     p.TR = 0;
-    for (int tr = l; tr >= 1; --tr) {
+    int tr_max = l;
+    if (const char *e = getenv("DP_TT_TR")) {  // experiments: cap the tap rows per unit
+        int v = atoi(e);
+        if (v >= 1 && v < tr_max) tr_max = v;
+    }
+    for (int tr = tr_max; tr >= 1; --tr) {
         const size_t ub = ((size_t)tr * (4 * p.seg_bytes + p.wrow_bytes) + 127) / 128 * 128;
         if (2 * ub <= budget) {
             p.TR = tr;
@@ -414,7 +435,12 @@ size_t tt_conv_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, in
     // the c4 data grads 5-15 %): there the flat kernel's per-tap-row record loads and hi/lo
     // splits, not the tap kernel's re-streamed weight rows, dominate.
     // DP_TT_ALL uses it wherever it applies (experiments).
-    if (p.MT < 3 && R < 32 && !getenv("DP_TT_ALL")) return 0;
+    // Round 2 (tools/conv_ab.py, identity epilogue, relayout included): with MT = 1 the wide
+    // layers are now slightly faster on the flat kernel (c3 conv2 fwd 2.47 vs 2.50 ms, data
+    // grad 2.50 vs 2.60; c4 L2 fwd 1.08 vs 1.23), so wide inputs need MT >= 2 as well.
+    if ((p.MT < 3 && R < 32) || p.MT < 2) {
+        if (!getenv("DP_TT_ALL")) return 0;
+    }
     long long plane_recs, flat_len;
     int tpi;
     tt_relayout_recs(Hin, Win, pad, l, d, p, plane_recs, tpi, flat_len, Ho, Wo);
@@ -447,8 +473,8 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     {
         const long long total = (long long)p.n_rc * l * 2 * p.LN * 8;
         long long g = (total + 255) / 256;
-        tc_pack_tap<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, wp, Q, R, l, p.Npad, p.n_rc,
-                                                                bwd ? 1 : 0);
+        tc_pack_tap<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, wp, Q, R, l, p.QS, p.LN,
+                                                                p.n_rc, bwd ? 1 : 0);
         int rc = check_launch("tc_pack_tap");
         if (rc) return rc;
     }
@@ -479,6 +505,7 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     a.d = d;
     a.Q = Q;
     a.Npad = p.Npad;
+    a.QS = p.QS;
     a.LN = p.LN;
     a.MT = p.MT;
     a.S = p.S;

@@ -101,7 +101,13 @@ def broadcast_params(tensor, group=None):
     """Every member of `group` starts from the group's first member's weights."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.broadcast(tensor, src=group_root(group), group=group)
+        if tensor.is_cuda and dist.get_backend(group) != "nccl":
+            # gloo: through a host copy, so no device write lands after later kernels
+            host = tensor.cpu()
+            dist.broadcast(host, src=group_root(group), group=group)
+            tensor.copy_(host)
+        else:
+            dist.broadcast(tensor, src=group_root(group), group=group)
     return tensor
 
 

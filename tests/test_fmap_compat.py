@@ -146,13 +146,12 @@ def test_drop_in_outputs_byte_identical_relu(tmp_path):
 @pytest.mark.gpu
 def test_drop_in_outputs_tanh(tmp_path):
     """tanh fixture: numpy's float32 tanh is not correctly rounded and this repo's is within
-    2 ulp of it, so the files agree to a few ulp (forward) / 1e-5 normwise (gradients)."""
+    2 ulp of it; through the next conv that is 1e-6 normwise (forward) / 1e-5 (gradients)."""
     spec, cache, grads = _run_drop_in("random-small.net")
     out = _write_outputs(tmp_path, spec, cache, grads)
     ours = fmap.read_fmap(str(out["forward"]))
     ref = fmap.read_fmap(os.path.join(G, "forward.fmap"))
-    ulps = np.abs(ours.view(np.int32).astype(np.int64) - ref.view(np.int32).astype(np.int64))
-    assert ulps.max() <= 4
+    assert np.max(np.abs(ours - ref)) <= 1e-6 * np.max(np.abs(ref))
     names = ["input_delta"] + [f"layer{k:02d}.{p}" for k, _ in spec.conv_layers()
                                for p in ("kernel", "bias")]
     for n in names:

@@ -1,8 +1,9 @@
 """Fast tier: tcgen05 3xTF32 conv (forward and data gradient) vs the exact tier (GPU).
 
-The exact CUDA-core kernels are bit-identical to the reference (test_gpu_kernels.py),
-so they are the yardstick here; the north-star tolerance for fp32 is 1e-4 normwise
-relative, and 3xTF32 should land near 1e-7.
+The exact CUDA-core kernels are bit-identical to the reference (test_gpu_kernels.py); run in
+fp64 they are the yardstick here (the fp32 exact tier carries its own rounding: on the c3 head
+at its real widths, K = 2450, fast-vs-fp32-exact differences reach 1.5e-4 after tanh).
+Bound: the north-star 1e-4 normwise relative.
 """
 
 import numpy as np
@@ -10,8 +11,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-# normwise; differences are fp32 reassociation of 1e2-1e3-term sums (~2e-6 seen)
-TOL = 5e-5
+# normwise vs fp64 (north-star bound)
+TOL = 1e-4
 
 SHAPES = [
     # n, cin, cout, k, d, h, w
@@ -26,6 +27,9 @@ SHAPES = [
     (1, 16, 8, 3, 32, 80, 90),      # d=32: tap-row / tap-column halo layout
     (1, 8, 16, 7, 8, 60, 66),       # 7x7 FC-style head, d=8
     (4, 3, 16, 6, 1, 20, 23),       # tiny images: one M tile, several images per CTA
+    (1, 50, 8, 7, 8, 96, 90),       # c3 head at its real widths (tap stride QS = 8, N = 64)
+    (2, 16, 6, 4, 4, 50, 52),       # Q < 8, even l: QS = 8, N = 32 (8-column TMEM loads)
+    (1, 24, 8, 2, 3, 40, 41),       # Q = 8, l = 2: N = 16
 ]
 
 
@@ -72,9 +76,9 @@ def test_tc_forward_matches_exact(shape, act, kernel, force_env):
     wt = _t(rng.uniform(-0.5, 0.5, (co, ci, k, k)).astype(np.float32))
     b = _t(rng.uniform(-0.5, 0.5, co).astype(np.float32))
     e = (k - 1) * d + 1
-    y_ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda")
-    y = torch.full_like(y_ref, float("nan"))
-    ops.conv_forward(x, wt, b, y_ref, k, d, act)
+    y_ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda", dtype=torch.float64)
+    y = torch.full(y_ref.shape, float("nan"), device="cuda")
+    ops.conv_forward(x.double(), wt.double(), b.double(), y_ref, k, d, act)
     nb = ops.fast_workspace(ci, co, k) if kernel != "tap" else ops.fwd_fast_workspace(x, co, k, d)
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     ops.conv_forward_fast(x, wt, b, y, k, d, act, ws)
@@ -101,9 +105,10 @@ def test_tc_backward_data_matches_exact(shape, gate_kind, kernel, force_env):
     gate = None
     if gate_kind is not None:
         gate = _t(np.tanh(rng.normal(size=(n, ci, h, w))).astype(np.float32))
-    dx_ref = torch.empty((n, ci, h, w), device="cuda")
-    dx = torch.full_like(dx_ref, float("nan"))
-    ops.conv_backward_data(dy, wt, dx_ref, k, d, gate, gate_kind or 0)
+    dx_ref = torch.empty((n, ci, h, w), device="cuda", dtype=torch.float64)
+    dx = torch.full(dx_ref.shape, float("nan"), device="cuda")
+    ops.conv_backward_data(dy.double(), wt.double(), dx_ref, k, d,
+                           None if gate is None else gate.double(), gate_kind or 0)
     nb = ops.fast_workspace(co, ci, k) if kernel != "tap" else ops.bwd_fast_workspace(dy, ci, k, d)
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     ops.conv_backward_data_fast(dy, wt, dx, k, d, ws, gate, gate_kind or 0)

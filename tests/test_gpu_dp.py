@@ -99,4 +99,5 @@ def test_two_rank_trainer_step_equals_single_process(tmp_path):
     want = net.grad_flat.double().cpu().numpy()
     scale = np.max(np.abs(want))
     assert np.max(np.abs(g0 - want)) <= 1e-5 * scale
-    assert np.max(np.abs(p0 - (p_init - LR * g0))) <= 1e-6 * max(1.0, np.max(np.abs(p_init)))
+    # fp32 rounding of the updated parameters (|p| reaches ~1e2 here: summed gradients ~1e5)
+    assert np.max(np.abs(p0 - (p_init - LR * g0))) <= 1e-6 * max(1.0, np.max(np.abs(p0)))

@@ -89,7 +89,9 @@ POOL_SHAPES = [(4, 2, 1, 40, 41), (3, 3, 2, 33, 35), (2, 8, 1, 40, 40), (5, 2, 1
                (1, 4, 4, 30, 31), (2, 1, 3, 7, 7),
                # several shared-memory tiles (128 x 32) per plane, halos up to 48, p <= 8
                (2, 4, 1, 150, 300), (2, 8, 1, 99, 270), (2, 5, 3, 90, 170), (3, 2, 4, 70, 290),
-               (1, 7, 8, 80, 400), (1, 9, 1, 40, 50), (1, 3, 25, 60, 60)]
+               (1, 7, 8, 80, 400), (1, 9, 1, 40, 50), (1, 3, 25, 60, 60),
+               # d = 1, p = 3..8: the vectorised kernels (4-column groups, ragged tile edges)
+               (2, 3, 1, 50, 77), (3, 5, 1, 45, 140), (2, 6, 1, 37, 131), (1, 7, 1, 70, 263)]
 
 
 @pytest.mark.parametrize("shape", POOL_SHAPES)
@@ -114,7 +116,7 @@ def test_pools_vs_cport(K, shape, dt):
                           kernels_c.avgpool_backward(dy, p, d, h, w, 4))
 
 
-@pytest.mark.parametrize("p,d", [(2, 1), (4, 1), (8, 1), (3, 5)])
+@pytest.mark.parametrize("p,d", [(2, 1), (3, 1), (4, 1), (5, 1), (8, 1), (3, 5)])
 def test_pool_nan_signed_zero(K, p, d):
     # NaN never wins (strict '>'), -0.0 / +0.0 ties keep the row-major first (the separable
     # shared-memory forward must pick exactly the reference's element)

@@ -73,7 +73,10 @@ def test_tc_forward_matches_exact(shape, act, kernel, force_env):
         pytest.skip("weights exceed the tensor-core kernel's shared-memory budget")
     rng = np.random.default_rng(sum(shape) + act)
     x = _t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
-    wt = _t(rng.uniform(-0.5, 0.5, (co, ci, k, k)).astype(np.float32))
+    # weights scaled so pre-activations stay O(1) for long reductions (K = ci*k*k up to 2450):
+    # a saturated tanh turns the normwise measure into a relative error of tiny outputs
+    ws_ = min(1.0, 4.0 / np.sqrt(ci * k * k))
+    wt = _t((rng.uniform(-0.5, 0.5, (co, ci, k, k)) * ws_).astype(np.float32))
     b = _t(rng.uniform(-0.5, 0.5, co).astype(np.float32))
     e = (k - 1) * d + 1
     y_ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda", dtype=torch.float64)

@@ -131,14 +131,21 @@ def allreduce_sum(tensor, group=None):
 class DataParallelTrainer:
     """One DenseNet per rank + bucket all-reduce + SGD, optionally as one CUDA graph.
 
-    The all-reduce stays outside the captured graph (NCCL calls are issued on
-    the same stream right after the graph replay), so graph replay and the
-    collective are ordered on one stream with no host synchronisation.
+    With NCCL the all-reduce (and the SGD update) are captured INSIDE the step's CUDA graph:
+    one graph launch per step runs forward, masked backward, the NCCL all-reduce of the
+    gradient bucket and the update, with no host round trip between them (the communicator
+    is brought up by a warm-up all-reduce before capture).  Other backends (gloo: CPU tests,
+    ranks sharing a GPU) cannot be captured: the all-reduce then follows the graph replay on
+    the same stream (`allreduce_sum`).  DP_ALLREDUCE_OUTSIDE=1 forces that order with NCCL
+    too; DP_FORCE_ALLREDUCE=1 runs the collective even at world size 1 (single-GPU tests of
+    the captured NCCL path).
     """
 
     def __init__(self, plan: DensePlan, batch_per_rank: int, height: int, width: int,
                  lr: float = 0.0, group=None, dtype=None, use_graph: bool = True,
                  precision: str = "fast"):
+        import os
+
         import torch
         import torch.distributed as dist
 
@@ -150,6 +157,11 @@ class DataParallelTrainer:
         self.distributed = dist.is_available() and dist.is_initialized()
         # every rank starts from the group's first member's weights (seeded specs agree)
         broadcast_params(self.net.param_flat, group)
+        force = bool(os.environ.get("DP_FORCE_ALLREDUCE"))
+        self.collective = self.distributed and (dist.get_world_size(group) > 1 or force)
+        self.nccl = self.collective and dist.get_backend(group) == "nccl"
+        self.in_graph = (use_graph and self.nccl and
+                         not os.environ.get("DP_ALLREDUCE_OUTSIDE"))
         self._graph = None
         self._use_graph = use_graph
         self._torch = torch
@@ -166,15 +178,37 @@ class DataParallelTrainer:
         n.loss_delta()
         n.backward()
 
+    def _reduce(self):
+        import torch.distributed as dist
+        if self.nccl:
+            dist.all_reduce(self.net.grad_flat, op=dist.ReduceOp.SUM, group=self.group)
+        elif self.collective:
+            allreduce_sum(self.net.grad_flat, self.group)
+
+    def _compute_reduce_update(self):
+        self._compute()
+        self._reduce()
+        if self.lr:
+            self.net.sgd_step(self.lr)
+
     def step(self):
         """forward + masked loss + backward [+ all-reduce] [+ SGD] on the loaded batch."""
+        if self._use_graph and self.in_graph:
+            if self._graph is None:
+                self._reduce()  # communicator up (and warm) before capture
+                # capture() runs the step eagerly to warm up: keep the parameters it updates
+                keep = self.net.param_flat.clone()
+                self._graph = self.net.capture(self._compute_reduce_update)
+                self.net.param_flat.copy_(keep)
+            self._graph.replay()
+            return
         if self._use_graph:
             if self._graph is None:
                 self._graph = self.net.capture(self._compute)
             self._graph.replay()
         else:
             self._compute()
-        allreduce_sum(self.net.grad_flat, self.group)
+        self._reduce()
         if self.lr:
             self.net.sgd_step(self.lr)
 

@@ -207,10 +207,48 @@ def _ref_package():
         return None
 
 
+def conv_flops(text, rows, side):
+    """(forward, backward) algorithmic conv FLOPs of the dense plan for `rows` output rows of a
+    `side`-wide image (backward = data + weight gradients, no layer-0 data gradient)."""
+    import paper_1412_4526_b200 as dp
+    from paper_1412_4526_b200.plan import DilatedConv
+    plan = dp.compile_plan(dp.parse_spec(text))
+    shapes = plan.layer_shapes(rows, side)
+    fwd = bwd = 0
+    first = True
+    for k, layer in enumerate(plan.layers):
+        if isinstance(layer, DilatedConv):
+            co, ho, wo = shapes[k + 1]
+            f = 2 * co * layer.base.in_channels * layer.base.kernel_size ** 2 * ho * wo
+            fwd += f
+            bwd += f if first else 2 * f
+            first = False
+    return fwd, bwd
+
+
 def cpu_dense_seconds(text, side, mask_frac, threads, rows=None, seed=0):
-    """(forward s, backward s, output pixels, kind, how) of ONE image of `side` (or, with
-    `rows`, a band of that many output rows of it: the padded input rows of the band plus
-    the (patch - 1)-row halo, the same per-pixel work as the full image) on the CPU.
+    """(forward s, backward s, output pixels, kind, how) of ONE image of `side` on the CPU.
+
+    With `rows` < side only a band of that many output rows is run (its padded input rows
+    plus the (patch - 1)-row halo); a band costs MORE per output pixel than the full image
+    (every layer also computes the halo rows still needed below it), so the band's times are
+    scaled to the full image by the ratio of the dense plan's conv FLOPs, full image / band
+    (forward and backward separately), and `output pixels` is the full image's.
+    """
+    f, b, px, kind, how = _cpu_dense_band(text, side, mask_frac, threads, rows, seed)
+    band = rows if rows is not None and rows < side else side
+    if band < side:
+        ff, fb = conv_flops(text, side, side)
+        bf, bb = conv_flops(text, band, side)
+        f *= ff / bf
+        b *= fb / bb if bb else 1.0
+        px = side * side
+        how += f", band of {band} rows scaled to the full image by conv FLOPs"
+    return f, b, px, kind, how
+
+
+def _cpu_dense_band(text, side, mask_frac, threads, rows=None, seed=0):
+    """The unscaled measurement behind cpu_dense_seconds (a band when rows < side).
 
     Through the reference package's own public API (compile_plan, pad_image,
     run_plan_layer = the body of dense_forward, forward.py:101-128, then dense_backward,
@@ -429,7 +467,8 @@ def sizes_sweep(budget_cpu=True):
                 pt["cpu"] = {"train": px / (f + b), "forward": px / f, "cores": threads,
                              "kind": kind,
                              "sample": ("1 full image" if rows == side else
-                                        f"band of {rows} output rows x {side} (+{patch - 1}-row halo)")}
+                                        f"band of {rows} output rows x {side} (+{patch - 1}-row "
+                                        "halo), scaled to the full image by conv FLOPs")}
                 pt["train_over_cpu"] = pt["train"] / pt["cpu"]["train"]
             points.append(pt)
         if budget_cpu:
@@ -773,8 +812,7 @@ def main():
                 rows = None if name in ("c1", "c2") else 64
                 f, bk, px, kind, how = cpu_dense_seconds(t, side, mf, threads, rows=rows)
                 m["cpu"] = {"forward": px / f, "cores": threads, "kind": kind,
-                            "sample": ("1 full image" if rows is None else
-                                       f"band of {rows} output rows x {side}") + f", {how}"}
+                            "sample": ("1 full image, " if rows is None else "") + how}
                 if mf is not None:
                     m["cpu"]["train"] = px / (f + bk)
                     m["train_over_cpu"] = m["train"] / m["cpu"]["train"]
@@ -796,7 +834,8 @@ def main():
             "forward_value": px / f, **host_info(),
             "single_thread": {"value": px1 / (f1 + b1), "forward_value": px1 / f1,
                               "cores": 1,
-                              "sample": f"band of 32 output rows x {SIDE}, 1 thread"},
+                              "sample": f"band of 32 output rows x {SIDE}, 1 thread, "
+                                        "scaled to the full image by conv FLOPs"},
             "patch_scan_forward": {"value": scan_px_s, "unit": "pixels/s", "cores": 1,
                                    "sample": f"{scan_n} pixels on a 16-px grid"},
         }

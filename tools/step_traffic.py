@@ -1,0 +1,76 @@
+"""Per bench-record DRAM traffic from a one-step full ncu capture (tools/profile_c3.sh):
+
+    python tools/step_traffic.py <full_step.ncu-rep> <out json> <out md> [source note]
+
+The capture holds the launches of one eager c3 training step starting at conv2's forward
+(`-s 40 -c 20`); MAP assigns each captured launch to the bench `kernels` record that times it
+(a record = the staging / relayout launches + the main kernel of one op).  Writes the json
+bench.py reads for `roofline.traffic` and a markdown summary for profiles/."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+# capture index -> bench record (c3 step, round-2 kernel selection)
+MAP = ["02:conv_forward_tc", "03:maxpool_forward", "04:conv_forward_tc", "04:conv_forward_tc",
+       "05:mask_delta", "06:conv_backward_kernel_tc", "06:conv_backward_kernel_tc",
+       "06:conv_backward_kernel_tc", "07:conv_backward_data_tc", "08:maxpool_backward",
+       "09:conv_backward_kernel_tc", "09:conv_backward_kernel_tc", "10:conv_backward_data_tc",
+       "11:maxpool_backward", "12:conv_backward_kernel_tc", "12:conv_backward_kernel_tc",
+       "12:conv_backward_kernel_tc", "00:conv_forward_tc", "01:maxpool_forward"]
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e3, "us": 1, "usecond": 1,
+         "msecond": 1e3, "nsecond": 1e-3}
+
+
+def main():
+    rep, out_json, out_md = sys.argv[1:4]
+    note = sys.argv[4] if len(sys.argv) > 4 else rep
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                          ",".join(METRICS)], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+
+    def val(r, k):
+        i = h.index(k)
+        return float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
+
+    recs = {}
+    lines = ["| # | kernel | record | us | DRAM read GB | write GB | tensor % | DRAM % | L2 % | "
+             "issue % |", "|---|---|---|---|---|---|---|---|---|---|"]
+    for i, r in enumerate(rows[2:2 + len(MAP)]):
+        name = r[h.index("Kernel Name")]
+        rec = MAP[i]
+        rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
+        t = val(r, "gpu__time_duration.sum")
+        e = recs.setdefault(rec, {"launches": [], "dram_bytes": 0.0, "gpu_time_us": 0.0})
+        e["launches"].append({"kernel": name[:120], "dram_bytes": rd + wr, "gpu_time_us": t})
+        e["dram_bytes"] += rd + wr
+        e["gpu_time_us"] += t
+        pct = [r[h.index(k)][:5] for k in METRICS[3:]]
+        lines.append(f"| {i} | `{name.split('(')[0][:48]}` | {rec} | {t:.0f} | {rd / 1e9:.3f} | "
+                     f"{wr / 1e9:.3f} | " + " | ".join(pct) + " |")
+    with open(out_json, "w") as fh:
+        json.dump({"source": note, "note": "dram_bytes = all launches of the bench record "
+                   "(staging / relayout + kernel), one eager step, ncu --set full",
+                   "kernels": recs}, fh, indent=1)
+    with open(out_md, "w") as fh:
+        fh.write(f"# One c3 training step under ncu --set full ({note})\n\n")
+        fh.write("Cold-cache, serialised launches; percentages are ncu's (tensor = "
+                 "sm__pipe_tensor_cycles_active, DRAM = gpu__dram_throughput, L2 = "
+                 "lts__throughput, issue = smsp__issue_active).\n\n")
+        fh.write("\n".join(lines) + "\n\n## Per bench record\n\n| record | launches | us | DRAM GB |\n"
+                 "|---|---|---|---|\n")
+        for k in sorted(recs):
+            e = recs[k]
+            fh.write(f"| {k} | {len(e['launches'])} | {e['gpu_time_us']:.0f} | "
+                     f"{e['dram_bytes'] / 1e9:.3f} |\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -154,6 +154,14 @@ size_t dp_conv_backward_kernel_fast_workspace(int n, int cin, int hi, int wi, in
 int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, float *db, int n,
                                  int cin, int hi, int wi, int cout, int k, int d,
                                  void *workspace, size_t workspace_bytes, void *stream);
+/* Same, where the caller guarantees x_slack_bytes readable bytes after x's last element
+ * (ABI 5): when every tap offset is a multiple of 4 floats and W % 4 == 0 the kernel then
+ * reads x in place through a 5-D tensor map (overlapping tap view: it may touch up to
+ * ((taps-1)*d + 32) * 4 bytes past the end) instead of staging a re-laid-out copy. */
+int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const float *dy,
+                                    float *dw, float *db, int n, int cin, int hi, int wi,
+                                    int cout, int k, int d, void *workspace,
+                                    size_t workspace_bytes, void *stream);
 /* Split form (ABI 4): _prepare stages x (the re-laid-out / shifted copies the kernel's TMA
  * boxes read) into `workspace`; it depends on x only, so it can run as soon as x exists
  * (the engine overlaps it with the forward pass on a side stream).  _staged then runs the
@@ -170,6 +178,12 @@ int dp_conv_backward_kernel_fast_staged(const float *x, const float *dy, float *
  * records per-K-block clock64() timestamps of CTA 0 (256 blocks x 16 slots); this copies
  * the last launch's record to host memory (synchronous). */
 int dp_debug_wgrad_trace(void *host, size_t bytes);
+/* the fast weight gradient's plan for a shape (host only, no launch): 1 and up to 16 ints
+ * {J, Ja, NB, lines per ring slot, M tiles, tiles per group, groups, split-K, stages, 2-row
+ * boxes, dy staged, residue copies, per-tap copies, x / dy / total workspace KiB}, or 0 when
+ * the shape is unsupported */
+int dp_debug_wgrad_plan(int n, int cin, int hi, int wi, int cout, int k, int d, int *out,
+                        int len);
 /* same for the fast forward / data-gradient kernel with DP_TC_TRACE set (1024 K-steps x 8) */
 int dp_debug_conv_trace(void *host, size_t bytes);
 

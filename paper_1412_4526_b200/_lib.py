@@ -53,10 +53,13 @@ SIGNATURES = {
                                         _vp, _sz, _vp]),
     "dp_debug_wgrad_trace": (_i, [_vp, _sz]),
     "dp_debug_conv_trace": (_i, [_vp, _sz]),
+    "dp_debug_wgrad_plan": (_i, [_i] * 7 + [_vp, _i]),
     "dp_conv_backward_kernel_fast_supported": (_i, [_i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel_fast_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel_fast": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
                                           _sz, _vp]),
+    "dp_conv_backward_kernel_fast_ex": (_i, [_vp, _sz, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
+                                             _i, _vp, _sz, _vp]),
     "dp_conv_backward_kernel_fast_prepare": (_i, [_vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_fast_staged": (_i, [_vp, _vp, _vp, _vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),

@@ -39,13 +39,14 @@ int tc_conv_backward_data(const float *, const float *, float *, int, int, int, 
 bool tc_wgrad_supported(int, int, int, int, int, int, int);
 int wg_trace_copy(void *, size_t);
 int tc_trace_copy(void *, size_t);
+int ws_debug_plan(int n, int cin, int hi, int wi, int cout, int k, int d, int *out, int len);
 size_t tc_wgrad_workspace(int, int, int, int, int, int, int);
 int tc_wgrad_prepare(const float *, int, int, int, int, int, int, int, void *, size_t,
                      cudaStream_t);
 int tc_conv_backward_kernel_staged(const float *, const float *, float *, float *, int, int, int,
                                    int, int, int, int, void *, size_t, cudaStream_t);
 int tc_conv_backward_kernel(const float *, const float *, float *, float *, int, int, int, int,
-                            int, int, int, void *, size_t, cudaStream_t);
+                            int, int, int, void *, size_t, cudaStream_t, size_t);
 template <typename T>
 int maxpool_forward_t(const T *, T *, void *, int, int, int, int, int, int, int, int,
                       cudaStream_t);
@@ -328,6 +329,10 @@ size_t dp_conv_backward_kernel_fast_workspace(int n, int cin, int hi, int wi, in
 }
 
 int dp_debug_wgrad_trace(void *host, size_t bytes) { return wg_trace_copy(host, bytes); }
+int dp_debug_wgrad_plan(int n, int cin, int hi, int wi, int cout, int k, int d, int *out,
+                        int len) {
+    return ws_debug_plan(n, cin, hi, wi, cout, k, d, out, len);
+}
 int dp_debug_conv_trace(void *host, size_t bytes) { return tc_trace_copy(host, bytes); }
 
 int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, float *db, int n,
@@ -338,7 +343,19 @@ int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, flo
     DP_TRY(check_pos("out channels", cout));
     DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
     return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
-                                   workspace_bytes, (cudaStream_t)stream);
+                                   workspace_bytes, (cudaStream_t)stream, 0);
+}
+
+int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const float *dy,
+                                    float *dw, float *db, int n, int cin, int hi, int wi,
+                                    int cout, int k, int d, void *workspace,
+                                    size_t workspace_bytes, void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
+                                   workspace_bytes, (cudaStream_t)stream, x_slack_bytes);
 }
 
 int dp_conv_backward_kernel_fast_prepare(const float *x, int n, int cin, int hi, int wi,

@@ -705,7 +705,7 @@ bool ws_supported(int n, int cin, int hi, int wi, int cout, int k, int d);
 size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d);
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st, int phases);
+                            size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack);
 
 // Split form (engine): stage x early (phase 1, may run during the forward pass), the rest
 // later (phase 2).  Only the smem-operand kernel splits; the TMEM-operand fallback stages
@@ -714,19 +714,19 @@ int tc_wgrad_prepare(const float *x, int n, int cin, int hi, int wi, int cout, i
                      void *ws, size_t ws_bytes, cudaStream_t st) {
     if (!ws_supported(n, cin, hi, wi, cout, k, d)) return DP_OK;
     return ws_conv_backward_kernel(x, nullptr, nullptr, nullptr, n, cin, hi, wi, cout, k, d, ws,
-                                   ws_bytes, st, 1);
+                                   ws_bytes, st, 1, 0);
 }
 int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st);
+                            size_t ws_bytes, cudaStream_t st, size_t x_slack);
 int tc_conv_backward_kernel_staged(const float *x, const float *dy, float *dw, float *db, int n,
                                    int cin, int hi, int wi, int cout, int k, int d, void *ws,
                                    size_t ws_bytes, cudaStream_t st) {
     if (!ws_supported(n, cin, hi, wi, cout, k, d))
         return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes,
-                                       st);
+                                       st, 0);
     return ws_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes, st,
-                                   2);
+                                   2, 0);
 }
 
 bool tc_wgrad_supported(int n, int cin, int hi, int wi, int cout, int k, int d) {
@@ -744,10 +744,10 @@ size_t tc_wgrad_workspace(int n, int cin, int hi, int wi, int cout, int k, int d
 
 int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st) {
+                            size_t ws_bytes, cudaStream_t st, size_t x_slack) {
     if (ws_supported(n, cin, hi, wi, cout, k, d))
         return ws_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes,
-                                       st, 3);
+                                       st, 3, x_slack);
     WgPlan p;
     if (!wg_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED,

@@ -86,6 +86,7 @@ struct WsArgs {
                          // (J*Q rows rounded up to 16: B rows jb'*Q + o, zero rows past J*Q)
     int tma_mirror;      // DP_WG_TMA_MIRROR: mirror slots loaded by TMA, not the converters
     int pair;            // one 2-row x box feeds two consecutive blocks of a column
+    int direct;          // x read in place from NCHW through a 5-D map (no staged copy)
     int n_tiles, G, n_groups, splits;
     int Ho, Wo, nvb, T, Hi;
     long long kb_total;  // n * nvb * d columns x T blocks
@@ -254,6 +255,12 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                         if (copy == 1 && (slot >= a.NM || !a.tma_mirror)) break;
                         unsigned char *dst =
                             ring + (size_t)(copy ? a.R + slot : slot) * a.slot_bytes;
+                        if (a.direct) {
+                            // NCHW in place: (w, jj, c, h, n); rows past Hi zero-fill
+                            ptx::tma_load_5d(dst, &tm_x0, v0 + a.rs.j0[0] * a.d, 0, 0,
+                                             sc.u + (i_lo + k) * a.d, sc.img, &sfull[s]);
+                            continue;
+                        }
                         for (int rb = 0; rb < a.rs.n_b; ++rb) {
                             const CUtensorMap *m = rb == 0 ? &tm_x0 : rb == 1 ? &tm_x1
                                                                    : rb == 2 ? &tm_x2 : &tm_x3;
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
 // host side
 // --------------------------------------------------------------------------------
 struct WsPlan {
-    int pair;
+    int pair, direct;
     int J, kc, dc, sb, NB;  // J dy copies (B), kc = Ja column taps in the x lines (A), step dc = d
     int Cpad, Npad, Ls, n_tiles, G, n_groups, splits, SS, R, NM, max_ni;
     int ho, wo, nvb, T, wp_x, wp_dy, lm_dy, mask;
@@ -531,6 +538,28 @@ static size_t ws_align256(size_t v) { return (v + 255) / 256 * 256; }
 
 static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, int Ja,
                       WsPlan &p);
+
+// x read in place (no tc_stage_x copy): one residue at offset 0 (every tap offset j*d a
+// multiple of 4 floats), 16-byte rows, no 2-row boxes (a 6th map dimension), and the caller
+// guarantees that the bytes an overlapping tap view reads past the tensor's last row exist
+// (x_slack).  Rows past Hi then come from TMA zero fill instead of the next image.
+static void ws_try_direct(WsPlan &p, int cin, int wi, int d, size_t x_slack) {
+    p.direct = 0;
+    if (getenv("DP_WG_STAGE_X") || p.rs.tapcopy || p.rs.n_b != 1 || p.rs.b[0] != 0 ||
+        wi % 4 != 0)
+        return;
+    const size_t overrun = ((size_t)(p.rs.n[0] - 1) * p.rs.step * d + 32) * 4;
+    if (x_slack < overrun) return;
+    p.direct = 1;
+    if (p.pair) {
+        p.pair = 0;
+        p.rs.n[0] = p.rs.nreal0;
+        p.box_tx_row = (uint32_t)cin * p.kc * 128u;
+    }
+    p.R = p.max_ni + p.SS - 1;
+    p.total_bytes -= p.x_bytes;
+    p.x_bytes = 0;
+}
 
 // Column-tap stacking: column tap j = jb*Ja + ja.  The x lines (A) cover only Ja taps ja
 // (offsets ja*d), and J = ceil(k / Ja) copies of dy shifted right by jb*Ja*d sit side by
@@ -732,6 +761,20 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     return true;
 }
 
+// debugging aid (dp_debug_wgrad_plan): the smem-operand weight gradient's plan, 0 if
+// unsupported; out = {J, Ja, NB, Ls, n_tiles, G, n_groups, splits, SS, pair, stage_dy,
+// residues, tapcopy, x_bytes / 1 KiB, dy_bytes / 1 KiB, total_bytes / 1 KiB}
+int ws_debug_plan(int n, int cin, int hi, int wi, int cout, int k, int d, int *out, int len) {
+    WsPlan p;
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p)) return 0;
+    const int v[16] = {p.J, p.kc, p.NB, p.Ls, p.n_tiles, p.G, p.n_groups, p.splits, p.SS,
+                       p.pair, p.stage_dy ? 1 : 0, p.rs.n_b, p.rs.tapcopy,
+                       (int)(p.x_bytes >> 10), (int)(p.dy_bytes >> 10),
+                       (int)(p.total_bytes >> 10)};
+    for (int i = 0; i < len && i < 16; ++i) out[i] = v[i];
+    return 1;
+}
+
 bool ws_supported(int n, int cin, int hi, int wi, int cout, int k, int d) {
     WsPlan p;
     return ws_plan(n, cin, hi, wi, cout, k, d, p);
@@ -747,10 +790,12 @@ size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d) {
 // the forward pass (side stream) and phase 2 in the backward.
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st, int phases) {
+                            size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack) {
     WsPlan p;
     if (!ws_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED, "weight gradient (smem operands): unsupported shape");
+    p.direct = 0;
+    if (phases == 3 && ((uintptr_t)x & 15) == 0) ws_try_direct(p, cin, wi, d, x_slack);
     if (ws == nullptr || ws_bytes < p.total_bytes)
         return set_error(DP_ERR_ARG, "tensor-core weight gradient: workspace %zu < %zu bytes",
                          ws_bytes, p.total_bytes);
@@ -763,7 +808,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.pdb = (float *)(w8 + p.part_bytes);
     float *xs = (float *)(w8 + p.part_bytes + p.pdb_bytes);
     int rc = DP_OK;
-    if (phases & 1) {
+    if ((phases & 1) && !p.direct) {
         rc = p.rs.tapcopy ? wg_stage_x_taps(x, xs, n, cin, hi, wi, p.wp_x, p.kc, p.dc,
                                             (long long)(p.copy_bytes / 4), st)
                           : wg_stage_x(x, xs, n, cin, hi, wi, p.wp_x, p.mask,
@@ -802,7 +847,17 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     }
     const cuuint64_t xrow = (cuuint64_t)p.wp_x * 4;  // one channel line
     const cuuint64_t ximg_row = xrow * cin;          // one image row (all channels)
-    for (int rb = 0; rb < 4; ++rb) {
+    for (int rb = 0; rb < 4 && p.direct; ++rb) {
+        // x in place, NCHW: (w, jj: step*d floats, c, h, n); one box = the (c, jj) lines
+        cuuint64_t dims[5] = {(cuuint64_t)wi, (cuuint64_t)p.rs.nreal0, (cuuint64_t)cin,
+                              (cuuint64_t)hi, (cuuint64_t)n};
+        cuuint64_t str[4] = {(cuuint64_t)p.rs.step * p.dc * 4, (cuuint64_t)hi * wi * 4,
+                             (cuuint64_t)wi * 4, (cuuint64_t)cin * hi * wi * 4};
+        cuuint32_t box[5] = {32, (cuuint32_t)p.rs.n[0], (cuuint32_t)cin, 1, 1};
+        rc = wg_make_map(&mx[rb], x, 5, dims, str, box, true);
+        if (rc) return rc;
+    }
+    for (int rb = 0; rb < 4 && !p.direct; ++rb) {
         const int used = rb < p.rs.n_b ? rb : 0;
         const float *base = (const float *)((const unsigned char *)xs + (size_t)used * p.copy_bytes);
         // (w, jj: lcm(d, 4) floats, c, row of n*hi) -- overlapping views, one box = the
@@ -841,6 +896,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.NB = p.NB;
     a.tma_mirror = getenv("DP_WG_TMA_MIRROR") ? 1 : 0;
     a.pair = p.pair;
+    a.direct = p.direct;
     a.n_tiles = p.n_tiles;
     a.G = p.G;
     a.n_groups = p.n_groups;

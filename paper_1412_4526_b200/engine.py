@@ -182,11 +182,19 @@ class ops:
         return int(_lib_dev().dp_conv_backward_kernel_fast_workspace(n, ci, hi, wi, co, k, d))
 
     @staticmethod
-    def conv_backward_kernel_fast(x, dy, dw, db, k, d, ws):
+    def conv_backward_kernel_fast(x, dy, dw, db, k, d, ws, x_slack=0):
+        """x_slack: readable bytes after x's storage (engine buffers carry SLACK_BYTES), which
+        lets the kernel read x in place instead of staging a copy where the shape allows."""
         with _Rec('conv_backward_kernel_tc', 2 + _repitches(x, dy), 'tensor',
                   2 * dy.numel() * x.shape[1] * k * k):
             n, ci, hi, wi = x.shape
             co = dy.shape[1]
+            if x_slack:
+                _lib.check(_lib_dev().dp_conv_backward_kernel_fast_ex(
+                    _ptr(x), int(x_slack), _ptr(dy), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k,
+                    d, _ptr(ws), ws.numel() * ws.element_size(), _stream()),
+                    "conv_backward_kernel_fast_ex")
+                return
             _lib.check(_lib_dev().dp_conv_backward_kernel_fast(
                 _ptr(x), _ptr(dy), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k, d, _ptr(ws),
                 ws.numel() * ws.element_size(), _stream()), "conv_backward_kernel_fast")
@@ -401,6 +409,23 @@ def run_backward(plan: DensePlan, inputs, argmax, delta, params=None, with_input
 # fused throughput engine
 # ---------------------------------------------------------------------------
 
+# Activation buffers are views of slightly longer allocations, so kernels may read a little
+# past a tensor's end (the weight gradient's overlapping in-place tap view of x).
+SLACK_BYTES = 64 * 1024
+
+
+def _slack_empty(shape, kw):
+    n = int(np.prod(shape))
+    extra = SLACK_BYTES // torch.tensor([], dtype=kw["dtype"]).element_size()
+    return torch.empty(n + extra, **kw)[:n].view(shape)
+
+
+def _slack_zeros(shape, kw):
+    t = _slack_empty(shape, kw)
+    t.zero_()
+    return t
+
+
 @dataclass
 class _Group:
     first: int                 # plan index of the conv/pool/nonlin
@@ -463,8 +488,8 @@ class DenseNet:
             off += nw + nb
         self.load_weights_from_plan()
         # ---- activations: x0 (padded input) and one output per group
-        self.x0 = torch.zeros((N,) + tuple(self.in_shape), **kw)
-        self.acts = [torch.empty((N,) + tuple(g.out_shape), **kw) for g in self.groups]
+        self.x0 = _slack_zeros((N,) + tuple(self.in_shape), kw)
+        self.acts = [_slack_empty((N,) + tuple(g.out_shape), kw) for g in self.groups]
         self.args = {}
         for gi, g in enumerate(self.groups):
             if isinstance(g.op, DilatedPool) and g.op.base.kind == "max":
@@ -692,7 +717,8 @@ class DenseNet:
                                                                  self._ws_l[gi])
                         elif fast_w:
                             ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d,
-                                                          self._ws_l.get(gi, self._ws))
+                                                          self._ws_l.get(gi, self._ws),
+                                                          x_slack=SLACK_BYTES)
                         else:
                             ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                     side_busy = True
@@ -702,7 +728,8 @@ class DenseNet:
                     if delta.data_ptr() == self._dbuf[src].data_ptr():
                         readers[src] = ev
                 elif fast_w:
-                    ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws)
+                    ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws,
+                                                  x_slack=SLACK_BYTES)
                 else:
                     ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                 if gi == 0 and not with_input_grad:

@@ -211,3 +211,44 @@ def test_tc_weight_gradient_split_prepare_staged(shape):
     ops.conv_backward_kernel_fast_staged(x, dy, dw2, db2, k, d, ws2)
     torch.cuda.synchronize()
     assert torch.equal(dw1, dw2) and torch.equal(db1, db2)
+
+
+DIRECT_SHAPES = [
+    # n, cin, cout, k, d, h, w  -- tap offsets j*d multiples of 4 floats, W % 4 == 0
+    (2, 32, 10, 4, 4, 61, 60),      # c2 conv3-like
+    (2, 50, 50, 3, 4, 70, 72),      # c3 conv2 widths
+    (1, 50, 8, 7, 8, 90, 96),       # c3 head widths (J = 7 column-tap stacking)
+    (3, 16, 32, 3, 8, 45, 44),      # Ho % d != 0: a column phase runs past the image
+]
+
+
+@pytest.mark.parametrize("shape", DIRECT_SHAPES)
+def test_tc_weight_gradient_x_in_place(shape):
+    """dp_conv_backward_kernel_fast_ex with readable slack after x: x is read in place
+    (5-D NCHW tensor map, no staged copy) -- bit-identical to the staged call (rows past an
+    image's end are now TMA zero fill instead of the next image's rows; they meet zero dy
+    either way)."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    e = (k - 1) * d + 1
+    rng = np.random.default_rng(sum(shape))
+    slack = 64 * 1024
+    buf = torch.zeros(n * ci * h * w + slack // 4, device="cuda")
+    x = buf[:n * ci * h * w].view(n, ci, h, w)
+    x.copy_(_t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32)))
+    dy = _t(rng.uniform(-1, 1, (n, co, h - e + 1, w - e + 1)).astype(np.float32))
+    if not ops.wgrad_fast_supported(x, co, k, d):
+        pytest.skip("outside the tensor-core weight-gradient envelope")
+    ws = torch.empty(ops.wgrad_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+    out = {}
+    for mode in ("staged", "direct"):
+        dw = torch.full((co, ci, k, k), float("nan"), device="cuda")
+        db = torch.full((co,), float("nan"), device="cuda")
+        ops.conv_backward_kernel_fast(x, dy, dw, db, k, d, ws,
+                                      x_slack=slack if mode == "direct" else 0)
+        out[mode] = (dw, db)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out["direct"][0]).all()
+    assert torch.equal(out["direct"][0], out["staged"][0])
+    assert torch.equal(out["direct"][1], out["staged"][1])

@@ -157,10 +157,12 @@ int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, flo
 /* Same, where the caller guarantees x_slack_bytes readable bytes after x's last element
  * (ABI 5): when every tap offset is a multiple of 4 floats and W % 4 == 0 the kernel then
  * reads x in place through a 5-D tensor map (overlapping tap view: it may touch up to
- * ((taps-1)*d + 32) * 4 bytes past the end) instead of staging a re-laid-out copy. */
+ * ((taps-1)*d + 32) * 4 bytes past the end) instead of staging a re-laid-out copy.
+ * dy_pitch: dy's row pitch in elements (0 = wo); a multiple of 4 lets the kernel read dy
+ * in place where it would otherwise re-pitch it. */
 int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const float *dy,
-                                    float *dw, float *db, int n, int cin, int hi, int wi,
-                                    int cout, int k, int d, void *workspace,
+                                    int dy_pitch, float *dw, float *db, int n, int cin, int hi,
+                                    int wi, int cout, int k, int d, void *workspace,
                                     size_t workspace_bytes, void *stream);
 /* Split form (ABI 4): _prepare stages x (the re-laid-out / shifted copies the kernel's TMA
  * boxes read) into `workspace`; it depends on x only, so it can run as soon as x exists
@@ -204,6 +206,13 @@ int dp_maxpool_forward(int dtype, const void *x, void *y, void *arg, int arg_byt
 int dp_maxpool_backward(int dtype, const void *dy, const void *arg, int arg_bytes, void *dx,
                         int n, int c, int ho, int wo, int p, int d, int hi, int wi,
                         const void *gate, int gate_kind, void *stream);
+/* same, dx written with row pitch dx_pitch >= wi elements (the gate keeps pitch wi): the
+ * engine hands layer 0's delta to the weight gradient in a 16-byte-aligned row pitch so the
+ * kernel's TMA reads it without a re-pitch copy (ABI 5) */
+int dp_maxpool_backward_pitched(int dtype, const void *dy, const void *arg, int arg_bytes,
+                                void *dx, int dx_pitch, int n, int c, int ho, int wo, int p,
+                                int d, int hi, int wi, const void *gate, int gate_kind,
+                                void *stream);
 int dp_avgpool_forward(int dtype, const void *x, void *y, int n, int c, int h, int w,
                        int p, int d, int nonlin, void *stream);
 int dp_avgpool_backward(int dtype, const void *dy, void *dx, int n, int c, int ho, int wo,

@@ -58,8 +58,10 @@ SIGNATURES = {
     "dp_conv_backward_kernel_fast_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel_fast": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,
                                           _sz, _vp]),
-    "dp_conv_backward_kernel_fast_ex": (_i, [_vp, _sz, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i,
-                                             _i, _vp, _sz, _vp]),
+    "dp_conv_backward_kernel_fast_ex": (_i, [_vp, _sz, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i,
+                                             _i, _i, _vp, _sz, _vp]),
+    "dp_maxpool_backward_pitched": (_i, [_i, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i,
+                                         _i, _i, _vp, _i, _vp]),
     "dp_conv_backward_kernel_fast_prepare": (_i, [_vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_fast_staged": (_i, [_vp, _vp, _vp, _vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),

@@ -46,13 +46,13 @@ int tc_wgrad_prepare(const float *, int, int, int, int, int, int, int, void *, s
 int tc_conv_backward_kernel_staged(const float *, const float *, float *, float *, int, int, int,
                                    int, int, int, int, void *, size_t, cudaStream_t);
 int tc_conv_backward_kernel(const float *, const float *, float *, float *, int, int, int, int,
-                            int, int, int, void *, size_t, cudaStream_t, size_t);
+                            int, int, int, void *, size_t, cudaStream_t, size_t, int);
 template <typename T>
 int maxpool_forward_t(const T *, T *, void *, int, int, int, int, int, int, int, int,
                       cudaStream_t);
 template <typename T>
 int maxpool_backward_t(const T *, const void *, int, T *, int, int, int, int, int, int, int,
-                       int, const T *, int, cudaStream_t);
+                       int, const T *, int, cudaStream_t, int);
 template <typename T>
 int avgpool_forward_t(const T *, T *, int, int, int, int, int, int, int, cudaStream_t);
 template <typename T>
@@ -343,19 +343,23 @@ int dp_conv_backward_kernel_fast(const float *x, const float *dy, float *dw, flo
     DP_TRY(check_pos("out channels", cout));
     DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
     return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
-                                   workspace_bytes, (cudaStream_t)stream, 0);
+                                   workspace_bytes, (cudaStream_t)stream, 0, 0);
 }
 
 int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const float *dy,
-                                    float *dw, float *db, int n, int cin, int hi, int wi,
-                                    int cout, int k, int d, void *workspace,
+                                    int dy_pitch, float *dw, float *db, int n, int cin, int hi,
+                                    int wi, int cout, int k, int d, void *workspace,
                                     size_t workspace_bytes, void *stream) {
     DP_TRY(check_pos("batch", n));
     DP_TRY(check_pos("in channels", cin));
     DP_TRY(check_pos("out channels", cout));
     DP_TRY(check_window("conv backward kernel", hi, wi, k, d));
+    const int wo = wi - (k - 1) * d;
+    if (dy_pitch != 0 && dy_pitch < wo)
+        return set_error(DP_ERR_ARG, "dy row pitch %d < width %d", dy_pitch, wo);
     return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, workspace,
-                                   workspace_bytes, (cudaStream_t)stream, x_slack_bytes);
+                                   workspace_bytes, (cudaStream_t)stream, x_slack_bytes,
+                                   dy_pitch);
 }
 
 int dp_conv_backward_kernel_fast_prepare(const float *x, int n, int cin, int hi, int wi,
@@ -412,7 +416,16 @@ static int check_pool_bwd(int ho, int wo, int p, int d, int hi, int wi) {
 int dp_maxpool_backward(int dtype, const void *dy, const void *arg, int arg_bytes, void *dx,
                         int n, int c, int ho, int wo, int p, int d, int hi, int wi,
                         const void *gate, int gate_kind, void *stream) {
+    return dp_maxpool_backward_pitched(dtype, dy, arg, arg_bytes, dx, wi, n, c, ho, wo, p, d,
+                                       hi, wi, gate, gate_kind, stream);
+}
+
+int dp_maxpool_backward_pitched(int dtype, const void *dy, const void *arg, int arg_bytes,
+                                void *dx, int dx_pitch, int n, int c, int ho, int wo, int p,
+                                int d, int hi, int wi, const void *gate, int gate_kind,
+                                void *stream) {
     DP_TRY(check_dtype(dtype));
+    if (dx_pitch < wi) return set_error(DP_ERR_ARG, "dx row pitch %d < width %d", dx_pitch, wi);
     DP_TRY(check_pos("batch", n));
     DP_TRY(check_pos("channels", c));
     DP_TRY(check_nonlin(gate_kind));
@@ -423,10 +436,11 @@ int dp_maxpool_backward(int dtype, const void *dy, const void *arg, int arg_byte
     return DP_DISPATCH(dtype,
                        maxpool_backward_t<float>((const float *)dy, arg, arg_bytes, (float *)dx,
                                                  n, c, ho, wo, p, d, hi, wi,
-                                                 (const float *)gate, gate_kind, st),
+                                                 (const float *)gate, gate_kind, st, dx_pitch),
                        maxpool_backward_t<double>((const double *)dy, arg, arg_bytes,
                                                   (double *)dx, n, c, ho, wo, p, d, hi, wi,
-                                                  (const double *)gate, gate_kind, st));
+                                                  (const double *)gate, gate_kind, st,
+                                                  dx_pitch));
 }
 
 int dp_avgpool_forward(int dtype, const void *x, void *y, int n, int c, int h, int w, int p,

@@ -129,7 +129,8 @@ template <typename T, typename A, int P>
 __global__ void __launch_bounds__(PT_X * PT_Y)
     maxpool_bwd_tile(const T *__restrict__ dy, const A *__restrict__ arg, T *__restrict__ dx,
                      const T *__restrict__ gate, int Ho, int Wo, int Hi, int Wi, int p_rt, int d,
-                     int gate_kind, long long planes) {
+                     int gate_kind, long long planes, int Wd) {
+    // Wd: dx row pitch (>= Wi; the gate keeps pitch Wi)
     const int r0 = blockIdx.y * (PT_Y * PT_R) + threadIdx.y;
     if (r0 >= Hi) return;
     const int s0 = blockIdx.x * (PT_X * PB_V) + threadIdx.x;
@@ -150,7 +151,9 @@ __global__ void __launch_bounds__(PT_X * PT_Y)
             }
             long long o1 = (long long)(r0 - d) * Wo + s0, o0 = (long long)r0 * Wo + s0;
             long long q = (plane * Hi + r0) * (long long)Wi + s0;
-            const long long os = (long long)PT_Y * Wo, qs = (long long)PT_Y * Wi;
+            long long qd = (plane * Hi + r0) * (long long)Wd + s0;
+            const long long os = (long long)PT_Y * Wo, qs = (long long)PT_Y * Wi,
+                            qds = (long long)PT_Y * Wd;
             for (int ry = 0; ry < PT_R; ++ry) {
                 const int r = r0 + ry * PT_Y;
                 if (r >= Hi) break;
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(PT_X * PT_Y)
                         dv[k][c] = ok[c] ? __ldg(d_[c] + k * PT_X) : T(0);
                     }
                 }
-                T *dxo = dx + q;
+                T *dxo = dx + qd;
                 const T *go = gate ? gate + q : nullptr;
 #pragma unroll
                 for (int k = 0; k < PB_V; ++k) {
@@ -183,6 +186,7 @@ __global__ void __launch_bounds__(PT_X * PT_Y)
                 o1 += os;
                 o0 += os;
                 q += qs;
+                qd += qds;
             }
         } else {
             const int p = p_rt;
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(PT_X * PT_Y)
                 const int r = r0 + ry * PT_Y;
                 if (r >= Hi) break;
                 const long long q0 = (plane * Hi + r) * (long long)Wi;
+                const long long qd0 = (plane * Hi + r) * (long long)Wd;
                 for (int k = 0; k < PB_V; ++k) {
                     const int s = s0 + k * PT_X;
                     if (s >= Wi) break;
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(PT_X * PT_Y)
                         }
                     }
                     if (gate) acc = gate_from_output(acc, gate[q0 + s], gate_kind);
-                    dx[q0 + s] = acc;
+                    dx[qd0 + s] = acc;
                 }
             }
         }
@@ -386,7 +391,7 @@ template <typename T, typename A, int P>
 __global__ void __launch_bounds__(256)
     maxpool_bwd_smem(const T *__restrict__ dy, const A *__restrict__ arg, T *__restrict__ dx,
                      const T *__restrict__ gate, int Ho, int Wo, int Hi, int Wi, int d,
-                     int gate_kind, long long planes) {
+                     int gate_kind, long long planes, int Wd) {
     extern __shared__ __align__(16) unsigned char sp_raw[];
     const int hx = (P - 1) * d, RW = SP_TW + hx, RH = SP_TH + hx;
     T *ds = reinterpret_cast<T *>(sp_raw);
@@ -433,6 +438,7 @@ __global__ void __launch_bounds__(256)
             const int gr = r0 + r;
             if (gr >= Hi) break;
             const long long q = (plane * Hi + gr) * (long long)Wi;
+            const long long qd = (plane * Hi + gr) * (long long)Wd;
             T gv[SP_TW / 32];
 #pragma unroll
             for (int k = 0; k < SP_TW / 32; ++k) {
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__(256)
                         if (as[base - j * d] == i * P + j) acc = add_rn(acc, ds[base - j * d]);
                 }
                 if (gate) acc = gate_from_output(acc, gv[k], gate_kind);
-                dx[q + gs] = acc;
+                dx[qd + gs] = acc;
             }
         }
         __syncthreads();
@@ -633,7 +639,8 @@ int maxpool_forward_t(const T *x, T *y, void *arg, int arg_bytes, int n, int c, 
 template <typename T>
 int maxpool_backward_t(const T *dy, const void *arg, int arg_bytes, T *dx, int n, int c, int ho,
                        int wo, int p, int d, int hi, int wi, const T *gate, int gate_kind,
-                       cudaStream_t st) {
+                       cudaStream_t st, int dx_pitch) {
+    const int Wd = dx_pitch > 0 ? dx_pitch : wi;
     long long planes = (long long)n * c;
     if (planes == 0 || hi <= 0 || wi <= 0) return DP_OK;
     if constexpr (sizeof(T) == 4) if (sp_use<T>(p, d, false)) {
@@ -645,12 +652,12 @@ int maxpool_backward_t(const T *dy, const void *arg, int arg_bytes, T *dx, int n
         rc = sp_launch_prep(maxpool_bwd_smem<T, uint8_t, PP>, smem);                        \
         if (rc == DP_OK)                                                                    \
             maxpool_bwd_smem<T, uint8_t, PP><<<g, dim3(32, 8), smem, st>>>(                 \
-                dy, (const uint8_t *)arg, dx, gate, ho, wo, hi, wi, d, gate_kind, planes);  \
+                dy, (const uint8_t *)arg, dx, gate, ho, wo, hi, wi, d, gate_kind, planes, Wd); \
     } else {                                                                                \
         rc = sp_launch_prep(maxpool_bwd_smem<T, int32_t, PP>, smem);                        \
         if (rc == DP_OK)                                                                    \
             maxpool_bwd_smem<T, int32_t, PP><<<g, dim3(32, 8), smem, st>>>(                 \
-                dy, (const int32_t *)arg, dx, gate, ho, wo, hi, wi, d, gate_kind, planes);  \
+                dy, (const int32_t *)arg, dx, gate, ho, wo, hi, wi, d, gate_kind, planes, Wd); \
     }
         SP_P_SWITCH(p, SP_BWD)
 #undef SP_BWD
@@ -664,14 +671,15 @@ int maxpool_backward_t(const T *dy, const void *arg, int arg_bytes, T *dx, int n
         if (p == 2)
             maxpool_bwd_tile<T, uint8_t, 2><<<g, blk, 0, st>>>(dy, (const uint8_t *)arg, dx, gate,
                                                                ho, wo, hi, wi, p, d, gate_kind,
-                                                               planes);
+                                                               planes, Wd);
         else
             maxpool_bwd_tile<T, uint8_t, 0><<<g, blk, 0, st>>>(dy, (const uint8_t *)arg, dx, gate,
                                                                ho, wo, hi, wi, p, d, gate_kind,
-                                                               planes);
+                                                               planes, Wd);
     } else {
         maxpool_bwd_tile<T, int32_t, 0><<<g, blk, 0, st>>>(dy, (const int32_t *)arg, dx, gate, ho,
-                                                           wo, hi, wi, p, d, gate_kind, planes);
+                                                           wo, hi, wi, p, d, gate_kind, planes,
+                                                           Wd);
     }
     return check_launch("maxpool_bwd_tile");
 }
@@ -730,7 +738,7 @@ int avgpool_backward_t(const T *dy, T *dx, int n, int c, int ho, int wo, int p, 
     template int maxpool_forward_t<T>(const T *, T *, void *, int, int, int, int, int, int,   \
                                       int, int, cudaStream_t);                                \
     template int maxpool_backward_t<T>(const T *, const void *, int, T *, int, int, int, int, \
-                                       int, int, int, int, const T *, int, cudaStream_t);     \
+                                       int, int, int, int, const T *, int, cudaStream_t, int); \
     template int avgpool_forward_t<T>(const T *, T *, int, int, int, int, int, int, int,      \
                                       cudaStream_t);                                          \
     template int avgpool_backward_t<T>(const T *, T *, int, int, int, int, int, int, int, int, \

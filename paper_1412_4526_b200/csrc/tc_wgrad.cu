@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(256) tc_stage_x_taps(const float *__restrict__
 // here: every line opens a different DRAM page).
 __global__ void __launch_bounds__(256) tc_stage_dy(const float *__restrict__ src,
                                                    float *__restrict__ dst, int O, int H, int w,
-                                                   int wp, int lm, long long total_quads) {
+                                                   int wp, int lm, long long total_quads,
+                                                   int ws) {  // ws: source row pitch
     const int nq = wp >> 2;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total_quads;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(256) tc_stage_dy(const float *__restrict__ src
         const long long no = row / H;
         const int o = (int)(no % O);
         const long long n = no / O;
-        const float *s = src + row * w;
+        const float *s = src + row * ws;
         float e[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -694,9 +695,10 @@ int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, i
     return DP_OK;
 }
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
-                cudaStream_t st) {
+                cudaStream_t st, int src_pitch) {
     const long long quads = (long long)n * cout * ho * (wp / 4);
-    tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, lm, quads);
+    tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, lm, quads,
+                                                   src_pitch > 0 ? src_pitch : wo);
     return check_launch("tc_stage_dy");
 }
 
@@ -705,7 +707,8 @@ bool ws_supported(int n, int cin, int hi, int wi, int cout, int k, int d);
 size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d);
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack);
+                            size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack,
+                            int dy_pitch);
 
 // Split form (engine): stage x early (phase 1, may run during the forward pass), the rest
 // later (phase 2).  Only the smem-operand kernel splits; the TMEM-operand fallback stages
@@ -714,19 +717,19 @@ int tc_wgrad_prepare(const float *x, int n, int cin, int hi, int wi, int cout, i
                      void *ws, size_t ws_bytes, cudaStream_t st) {
     if (!ws_supported(n, cin, hi, wi, cout, k, d)) return DP_OK;
     return ws_conv_backward_kernel(x, nullptr, nullptr, nullptr, n, cin, hi, wi, cout, k, d, ws,
-                                   ws_bytes, st, 1, 0);
+                                   ws_bytes, st, 1, 0, 0);
 }
 int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st, size_t x_slack);
+                            size_t ws_bytes, cudaStream_t st, size_t x_slack, int dy_pitch);
 int tc_conv_backward_kernel_staged(const float *x, const float *dy, float *dw, float *db, int n,
                                    int cin, int hi, int wi, int cout, int k, int d, void *ws,
                                    size_t ws_bytes, cudaStream_t st) {
     if (!ws_supported(n, cin, hi, wi, cout, k, d))
         return tc_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes,
-                                       st, 0);
+                                       st, 0, 0);
     return ws_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes, st,
-                                   2, 0);
+                                   2, 0, 0);
 }
 
 bool tc_wgrad_supported(int n, int cin, int hi, int wi, int cout, int k, int d) {
@@ -744,10 +747,12 @@ size_t tc_wgrad_workspace(int n, int cin, int hi, int wi, int cout, int k, int d
 
 int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st, size_t x_slack) {
+                            size_t ws_bytes, cudaStream_t st, size_t x_slack, int dy_pitch) {
     if (ws_supported(n, cin, hi, wi, cout, k, d))
         return ws_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d, ws, ws_bytes,
-                                       st, 3, x_slack);
+                                       st, 3, x_slack, dy_pitch);
+    if (dy_pitch != 0 && dy_pitch != wi - (k - 1) * d)
+        return set_error(DP_ERR_UNSUPPORTED, "weight gradient: pitched dy needs the smem kernel");
     WgPlan p;
     if (!wg_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED,
@@ -782,7 +787,8 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
         const long long quads = (long long)n * cout * p.ho * (p.wp_dy / 4);
-        tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy, 0, quads);
+        tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy, 0, quads,
+                                                       p.wo);
         rc = check_launch("tc_stage_dy");
         if (rc) return rc;
         dys = dp_;

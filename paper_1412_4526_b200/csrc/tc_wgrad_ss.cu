@@ -59,7 +59,7 @@ int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp
 int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int l,
                     int d, long long copy_floats, cudaStream_t st);
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
-                cudaStream_t st);
+                cudaStream_t st, int src_pitch);
 
 constexpr int WS_CONV_WARPS = 8;
 constexpr int WS_TMA_WARP = 8;
@@ -790,7 +790,8 @@ size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d) {
 // the forward pass (side stream) and phase 2 in the backward.
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
-                            size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack) {
+                            size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack,
+                            int dy_pitch) {
     WsPlan p;
     if (!ws_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED, "weight gradient (smem operands): unsupported shape");
@@ -816,19 +817,23 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
         if (rc) return rc;
     }
     if (!(phases & 2)) return DP_OK;
-    const bool stage_dy = p.stage_dy || ((uintptr_t)dy & 15) != 0;
+    // dy in place when its rows are 16-byte aligned: unpadded (wo % 4 == 0) or handed over
+    // with a 16-byte row pitch by the producer (dy_pitch, engine layer 0)
+    const int pitch = dy_pitch > 0 ? dy_pitch : p.wo;
+    const bool pitched_ok = p.J == 1 && pitch % 4 == 0 && ((uintptr_t)dy & 15) == 0;
+    const bool stage_dy = (p.stage_dy && !pitched_ok) || ((uintptr_t)dy & 15) != 0;
     if (stage_dy && !p.stage_dy)
         return set_error(DP_ERR_ARG, "weight gradient: dy must be 16-byte aligned");
     const float *dys = dy;
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
-        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st);
+        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st, pitch);
         if (rc) return rc;
         dys = dp_;
     }
     CUtensorMap mx[4], mdy;
     {
-        const cuuint64_t rowb = (cuuint64_t)(stage_dy ? p.wp_dy : p.wo) * 4;
+        const cuuint64_t rowb = (cuuint64_t)(stage_dy ? p.wp_dy : pitch) * 4;
         if (p.J == 1) {
             cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)p.ho, (cuuint64_t)cout, (cuuint64_t)n};
             cuuint64_t str[3] = {stage_dy ? rowb * cout : rowb, stage_dy ? rowb : rowb * p.ho,

@@ -84,9 +84,11 @@ class _Rec:
 
 
 def _repitches(x, dy) -> int:
-    """Staging copies the tensor-core weight gradient launches: x always (16-byte row
-    pitch, (n, h, c, w) order, shifted copies), dy when its rows are not 16-byte aligned."""
-    return 1 + int(dy.shape[3] % 4 != 0)
+    """Staging copies the tensor-core weight gradient launches (approximate): x unless it is
+    read in place (every tap offset 16-byte aligned and 16-byte rows -- here: d % 4 == 0 is
+    not known to this helper, so x staging is counted unless W % 4 == 0), dy when its row
+    pitch is not 16-byte aligned."""
+    return int(x.shape[3] % 4 != 0) + int(dy.stride(2) % 4 != 0)
 
 
 def _nbytes(*ts):
@@ -182,17 +184,18 @@ class ops:
         return int(_lib_dev().dp_conv_backward_kernel_fast_workspace(n, ci, hi, wi, co, k, d))
 
     @staticmethod
-    def conv_backward_kernel_fast(x, dy, dw, db, k, d, ws, x_slack=0):
+    def conv_backward_kernel_fast(x, dy, dw, db, k, d, ws, x_slack=0, dy_pitch=0):
         """x_slack: readable bytes after x's storage (engine buffers carry SLACK_BYTES), which
-        lets the kernel read x in place instead of staging a copy where the shape allows."""
+        lets the kernel read x in place instead of staging a copy where the shape allows;
+        dy_pitch: dy's row pitch when it is a strided (n, c, h, w) view."""
         with _Rec('conv_backward_kernel_tc', 2 + _repitches(x, dy), 'tensor',
                   2 * dy.numel() * x.shape[1] * k * k):
             n, ci, hi, wi = x.shape
             co = dy.shape[1]
-            if x_slack:
+            if x_slack or dy_pitch:
                 _lib.check(_lib_dev().dp_conv_backward_kernel_fast_ex(
-                    _ptr(x), int(x_slack), _ptr(dy), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k,
-                    d, _ptr(ws), ws.numel() * ws.element_size(), _stream()),
+                    _ptr(x), int(x_slack), _ptr(dy), int(dy_pitch), _ptr(dw), _ptr(db), n, ci,
+                    hi, wi, co, k, d, _ptr(ws), ws.numel() * ws.element_size(), _stream()),
                     "conv_backward_kernel_fast_ex")
                 return
             _lib.check(_lib_dev().dp_conv_backward_kernel_fast(
@@ -227,14 +230,15 @@ class ops:
                                                      _stream()), "maxpool_forward")
 
     @staticmethod
-    def maxpool_backward(dy, arg, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY):
+    def maxpool_backward(dy, arg, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY, dx_pitch=0):
+        """dx_pitch: write dx with that row pitch (dx a strided (n, c, h, w) view)."""
         with _Rec('maxpool_backward', 1, 'hbm', _nbytes(dy, arg, dx, gate)):
             n, c, ho, wo = dy.shape
-            _lib.check(_lib_dev().dp_maxpool_backward(_code(dy), _ptr(dy), _ptr(arg),
-                                                      arg.element_size(), _ptr(dx), n, c, ho, wo, p,
-                                                      d, dx.shape[2], dx.shape[3], _ptr(gate),
-                                                      gate_kind if gate is not None else 0,
-                                                      _stream()), "maxpool_backward")
+            _lib.check(_lib_dev().dp_maxpool_backward_pitched(
+                _code(dy), _ptr(dy), _ptr(arg), arg.element_size(), _ptr(dx),
+                dx_pitch or dx.shape[3], n, c, ho, wo, p, d, dx.shape[2], dx.shape[3],
+                _ptr(gate), gate_kind if gate is not None else 0, _stream()),
+                "maxpool_backward")
 
     @staticmethod
     def avgpool_forward(x, y, p, d, nonlin=_lib.DP_IDENTITY):
@@ -500,6 +504,18 @@ class DenseNet:
         self.output = self.acts[-1]
         if train:
             biggest = max([int(np.prod(s)) for s in shapes])
+            # layer 0's delta goes only to its weight gradient: when a max pool produces it
+            # and its rows are not 16-byte aligned, the pool backward writes it with a padded
+            # row pitch the weight gradient's TMA reads in place (no re-pitch copy)
+            self._l0_pitch = 0
+            c0, h0, w0 = self.groups[0].out_shape
+            if (len(self.groups) > 1 and isinstance(self.groups[0].op, DilatedConv) and
+                    isinstance(self.groups[1].op, DilatedPool) and
+                    self.groups[1].op.base.kind == "max" and w0 % 4 and
+                    self.dtype == torch.float32 and self.precision == "fast" and
+                    not os.environ.get("DP_NO_L0_PITCH")):
+                self._l0_pitch = (w0 + 3) // 4 * 4
+                biggest = max(biggest, c0 * h0 * self._l0_pitch)
             # three rotating delta buffers: a layer's weight gradient runs on a side stream
             # (overlapping the data-gradient / pool-backward chain) and still reads its
             # delta while the next op writes; the third buffer keeps that delta intact
@@ -707,6 +723,7 @@ class DenseNet:
                 dw, db = self.grads[g.first]
                 kk, d = op.base.kernel_size, op.dilation
                 fast_w = self.tc_wgrad.get(gi, False)
+                dyp = delta.stride(2) if (gi == 0 and delta.stride(2) != delta.shape[3]) else 0
                 if side is not None:
                     # weight gradient on the side stream (in order; per-layer workspaces for
                     # the fast ones, x staged during the forward pass when prepared)
@@ -718,7 +735,7 @@ class DenseNet:
                         elif fast_w:
                             ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d,
                                                           self._ws_l.get(gi, self._ws),
-                                                          x_slack=SLACK_BYTES)
+                                                          x_slack=SLACK_BYTES, dy_pitch=dyp)
                         else:
                             ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                     side_busy = True
@@ -729,7 +746,7 @@ class DenseNet:
                         readers[src] = ev
                 elif fast_w:
                     ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws,
-                                                  x_slack=SLACK_BYTES)
+                                                  x_slack=SLACK_BYTES, dy_pitch=dyp)
                 else:
                     ops.conv_backward_kernel(x_in, delta, dw, db, kk, d, self._ws)
                 if gi == 0 and not with_input_grad:
@@ -742,10 +759,20 @@ class DenseNet:
                 else:
                     ops.conv_backward_data(delta, wt, dx, kk, d, gate, gk)
             elif isinstance(op, DilatedPool):
-                dx = out_buf(ping, x_in.shape)
+                pitched = (gi == 1 and self._l0_pitch and self.tc_wgrad.get(0, False) and
+                           0 not in self._prepared and not with_input_grad)
+                if pitched:  # layer 0's delta, rows padded to a 16-byte pitch
+                    _ = out_buf(ping, x_in.shape)  # (waits for the buffer's last reader)
+                    n_, c_, h_, w_ = x_in.shape
+                    pp = self._l0_pitch
+                    dx = self._dbuf[ping].as_strided((n_, c_, h_, w_), (c_ * h_ * pp, h_ * pp,
+                                                                        pp, 1))
+                else:
+                    dx = out_buf(ping, x_in.shape)
                 if op.base.kind == "max":
                     ops.maxpool_backward(delta, self.args[gi], dx, op.base.kernel_size,
-                                         op.dilation, gate, gk)
+                                         op.dilation, gate, gk,
+                                         dx_pitch=self._l0_pitch if pitched else 0)
                 else:
                     ops.avgpool_backward(delta, dx, op.base.kernel_size, op.dilation, gate, gk)
             else:

@@ -252,3 +252,39 @@ def test_tc_weight_gradient_x_in_place(shape):
     assert torch.isfinite(out["direct"][0]).all()
     assert torch.equal(out["direct"][0], out["staged"][0])
     assert torch.equal(out["direct"][1], out["staged"][1])
+
+
+@pytest.mark.parametrize("p,d", [(2, 1), (4, 1), (2, 2)])
+def test_layer0_pitched_delta_path(p, d):
+    """Layer 0's delta handed over with a 16-byte row pitch: the max-pool backward writes dx
+    with row pitch P (gate still read at pitch W) and the weight gradient reads dy through
+    that pitch in place -- both bit-identical to the contiguous path (which re-pitches dy)."""
+    import torch
+    from paper_1412_4526_b200 import _lib
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, kd, h, w = 2, 3, 50, 6, 1, 80, 86   # conv x (n, ci, h, w), d = 1
+    e = (k - 1) * kd + 1
+    ho, wo = h - e + 1, w - e + 1                        # conv output = pool input (81 wide)
+    assert wo % 4
+    rng = np.random.default_rng(p * 7 + d)
+    x = _t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
+    a = _t(rng.uniform(-1, 1, (n, co, ho, wo)).astype(np.float32))
+    ep = (p - 1) * d + 1
+    y = torch.empty((n, co, ho - ep + 1, wo - ep + 1), device="cuda")
+    arg = torch.empty(y.shape, dtype=torch.uint8, device="cuda")
+    ops.maxpool_forward(a, y, arg, p, d)
+    g = _t(rng.uniform(-1, 1, y.shape).astype(np.float32))
+    dx = torch.empty_like(a)
+    ops.maxpool_backward(g, arg, dx, p, d)
+    pp = (wo + 3) // 4 * 4
+    buf = torch.full((n * co * ho * pp,), float("nan"), device="cuda")
+    dxp = buf.as_strided((n, co, ho, wo), (co * ho * pp, ho * pp, pp, 1))
+    ops.maxpool_backward(g, arg, dxp, p, d, dx_pitch=pp)
+    assert torch.equal(dxp, dx)
+    ws = torch.empty(ops.wgrad_fast_workspace(x, co, k, kd), dtype=torch.uint8, device="cuda")
+    dw1, db1 = torch.empty((co, ci, k, k), device="cuda"), torch.empty(co, device="cuda")
+    dw2, db2 = torch.empty_like(dw1), torch.empty_like(db1)
+    ops.conv_backward_kernel_fast(x, dx, dw1, db1, k, kd, ws)
+    ops.conv_backward_kernel_fast(x, dxp, dw2, db2, k, kd, ws, dy_pitch=pp)
+    torch.cuda.synchronize()
+    assert torch.equal(dw1, dw2) and torch.equal(db1, db2)

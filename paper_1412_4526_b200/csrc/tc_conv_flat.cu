@@ -415,9 +415,11 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd) {
     // accumulator columns, halving the M tiles per CTA tile.  Wide inputs (>= 4 channel
     // chunks) are loader / feed bound, not MMA bound, and gain more from the extra M tiles
     // (round 2, tools/conv_ab.py: c3 conv2 fwd 2.47 -> 1.92 ms, data grad 2.51 -> 1.84 at
-    // MT 2 -> 4); narrow ones are MMA bound and keep stacking (c2 conv2 fwd 0.83 vs 1.00).
+    // MT 2 -> 4); narrow ones, and outputs of <= 32 channels (three N = 32 MMAs cost 120
+    // cycles vs 88 stacked), or with many taps per unit (l > 4: Plain CNN1's 7x7 head data
+    // grad 1.19 stacked vs 1.26), are MMA bound and keep stacking (c2 conv2 fwd 0.83 vs 1.00).
     p.stacked = 2 * p.Npad <= 256 && !getenv("DP_TF_NOSTACK") &&
-                (R < 32 || getenv("DP_TF_STACK"));
+                (R < 32 || p.Npad < 64 || l > 4 || getenv("DP_TF_STACK"));
     p.acc_cols = p.stacked ? 2 * p.Npad : p.Npad;
     p.ok = p.Npad <= 256;
     int mt = p.acc_cols <= 256 ? 256 / p.acc_cols : 1;

@@ -6,8 +6,11 @@
 // (u, v) is p = u*Wv + v and tap (i, j) reads input record p + i*d*Wv + j*d.  The flat kernel
 // reads one 128-record A window per TAP; here one window per TAP ROW serves all l taps:
 //   D'[r, (j, o)] = sum_c A[s + r, c] * W[o, c, i, j]     (N = l * QS columns, rounded to 16)
-// and the epilogue forms y[s + r] = sum_j D'[r + j*d, (j, o)], so an M tile of 128 rows yields
-// S = 128 - (l-1)*d outputs (M tiles overlap by (l-1)*d rows).  Per tap row and M tile the
+// and the epilogue forms y[s + r] = sum_j D'[r + j*d, (j, o)].  The MT M tiles of a CTA tile
+// are contiguous (record offsets 0, 128, ...): rows past 128 come from the next tile's TMEM
+// accumulator through the epilogue's shared-memory exchange, so a CTA tile of MT*128 rows
+// yields MT*128 - (l-1)*d outputs (round 1 overlapped every M tile by (l-1)d rows: c3's head,
+// d = 8, l = 7, wasted 48 of 128 MMA rows).  Per tap row and M tile the
 // tensor core reads A_hi twice and A_lo once (three N = LN MMAs: A_hi W_hi, A_hi W_lo,
 // A_lo W_hi) instead of 2*l times -- the flat kernel's limiter was exactly these A reads.
 // QS, the column stride of one tap in N, is Q rounded to 16 -- or to 8 when Q <= 8 (the
@@ -49,13 +52,14 @@ struct TtArgs {
     float *out;          // (n, Q, Ho, Wo)
     const float *gate;
     int n_rc, l, d, Q, Npad, QS, LN, MT, S, NR, TR, n_tr;
+    int STEP, XR;          // outputs per CTA tile (MT*128 - (l-1)d), exchange rows (128 + (l-1)d)
     int Wv, Ho, Wo, act, gate_kind;
     long long plane_recs;
     int flat_len, tiles_per_img, total_tiles, HB;
     uint32_t seg_bytes;    // NR * 16
     uint32_t wrow_bytes;   // one tap row of packed weights: 2 * LN * 32
     uint32_t ubytes;       // unit buffer
-    uint32_t xoff;         // epilogue exchange area: [l][8 or 16][160] floats after the units
+    uint32_t xoff;         // epilogue exchange area: [l][8 or 16][XR] floats after the units
 };
 
 __device__ __forceinline__ float tt_act(float v, int kind) {
@@ -70,7 +74,8 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
     __shared__ uint64_t ufull[TT_MAX_HB], uempty[TT_MAX_HB], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
     __shared__ float s_bias[256];
-    // epilogue exchange (dynamic): [tap j][16 columns][128 rows + 32 spill rows (zero)]
+    // epilogue exchange (dynamic): [tap j][XC columns][XR = 128 + (l-1)d rows: the tile's own
+    // D' rows, then the next M tile's first (l-1)d rows]
     float *s_x = reinterpret_cast<float *>(smem_raw + a.xoff);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -79,8 +84,9 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
     for (int o = threadIdx.x; o < a.Npad; o += blockDim.x)
         s_bias[o] = (!BWD && o < a.Q) ? a.bias[o] : 0.f;
     const int XC = a.QS == 8 ? 8 : 16;  // exchange columns per tap
-    for (int e = threadIdx.x; e < a.l * XC * 32; e += blockDim.x)
-        s_x[(e >> 5) * 160 + 128 + (e & 31)] = 0.f;
+    const int XR = a.XR, halo = a.XR - 128;
+    for (int e = threadIdx.x; e < a.l * XC * halo; e += blockDim.x)
+        s_x[(e / halo) * XR + 128 + e % halo] = 0.f;
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.HB; ++b) {
             ptx::mbar_init(&ufull[b], 1);
@@ -107,7 +113,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
             uint32_t uph = 0;
             for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
                 const int img = tile / a.tiles_per_img;
-                const int f0 = (tile - img * a.tiles_per_img) * MT * a.S;
+                const int f0 = (tile - img * a.tiles_per_img) * a.STEP;
                 for (int rc = 0; rc < a.n_rc; ++rc) {
                     const unsigned char *pl =
                         xr + ((size_t)img * a.n_rc + rc) * 4 * a.plane_recs * 16;
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
                         const uint64_t bh = ptx::smem_desc(wb + (uint32_t)t * a.wrow_bytes, 128, 256);
                         const uint32_t acc0 = (u | t) != 0;
                         for (int mt = 0; mt < MT; ++mt) {
-                            const uint64_t ad = a0 + (uint64_t)(mt * a.S);
+                            const uint64_t ad = a0 + (uint64_t)(mt * 128);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.LN);
                             ptx::mma_tf32_ss(dd, ad, bh, idesc, acc0);
                             ptx::mma_tf32_ss(dd, ad, bh + blo_units, idesc, 1);
@@ -198,16 +204,24 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
         uint32_t tph = 0;
         for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
             const int img = tile / a.tiles_per_img;
-            const int f0 = (tile - img * a.tiles_per_img) * MT * a.S;
+            const int f0 = (tile - img * a.tiles_per_img) * a.STEP;
             ptx::mbar_wait_sleep(&tfull[buf], tph);
             ptx::tc_fence_after();
             const long long img_off = (long long)img * a.Q * ostride;
             for (int mt = 0; mt < MT; ++mt) {
-                const int p = f0 + mt * a.S + r;
+                // M tiles are contiguous: row r of tile mt needs D rows r + j*d, the ones
+                // past 128 from the next tile (its first (l-1)d rows go to the exchange's
+                // spill rows); the CTA tile's last (l-1)d rows wait for the next CTA tile
+                const int p = f0 + mt * 128 + r;
                 const int u = p / a.Wv, v = p - u * a.Wv;
-                const bool inside = r < a.S && p < a.flat_len && v < a.Wo;
+                const bool inside = mt * 128 + r < a.STEP && p < a.flat_len && v < a.Wo;
+                // tcgen05.ld is warp-collective: the whole warp loads the next tile's rows
+                // when any of its lanes needs them; only lanes r < halo publish them
+                const bool spill_w = mt + 1 < MT && q * 32 < halo;
+                const bool spill = spill_w && r < halo;
                 const long long pix = img_off + (long long)u * a.Wo + v;
                 const uint32_t dcol = tmem + lane_off + (uint32_t)((buf * MT + mt) * a.LN);
+                const uint32_t ncol = dcol + (uint32_t)a.LN;  // tile mt + 1
                 for (int o0 = 0; o0 < a.QS; o0 += 16) {
                     // all l taps' columns of this chunk: l TMEM loads, one wait; publish
                     // rows; one barrier; gather rows r + j*d; one barrier (reuse)
@@ -225,34 +239,44 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
 #pragma unroll
                     for (int j = 0; j < TT_MAX_L; ++j) {
                         if (j >= a.l) break;
-                        uint32_t rv[16];
-                        float *xs = s_x + j * XC * 160;
+                        uint32_t rv[16], rn[16];
+                        float *xs = s_x + j * XC * XR;
                         if (a.QS == 8) {  // one 8-column tap group (never past the allocation)
                             ptx::tmem_ld8(dcol + (uint32_t)(j * 8), rv);
+                            if (spill_w) ptx::tmem_ld8(ncol + (uint32_t)(j * 8), rn);
                             ptx::tmem_wait_ld();
 #pragma unroll
-                            for (int t = 0; t < 8; ++t) xs[t * 160 + r] = __uint_as_float(rv[t]);
+                            for (int t = 0; t < 8; ++t) xs[t * XR + r] = __uint_as_float(rv[t]);
+                            if (spill) {
+#pragma unroll
+                                for (int t = 0; t < 8; ++t)
+                                    xs[t * XR + 128 + r] = __uint_as_float(rn[t]);
+                            }
                         } else {
                             ptx::tmem_ld16(dcol + (uint32_t)(j * a.QS + o0), rv);
+                            if (spill_w) ptx::tmem_ld16(ncol + (uint32_t)(j * a.QS + o0), rn);
                             ptx::tmem_wait_ld();
 #pragma unroll
-                            for (int t = 0; t < 16; ++t) xs[t * 160 + r] = __uint_as_float(rv[t]);
+                            for (int t = 0; t < 16; ++t) xs[t * XR + r] = __uint_as_float(rv[t]);
+                            if (spill) {
+#pragma unroll
+                                for (int t = 0; t < 16; ++t)
+                                    xs[t * XR + 128 + r] = __uint_as_float(rn[t]);
+                            }
                         }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
                     for (int j = 0; j < TT_MAX_L; ++j) {
                         if (j >= a.l) break;
-                        const int rr = r + j * a.d;  // < 128 + 32 whenever r < S
-                        if (rr < 160) {
-                            const float *xs = s_x + j * XC * 160 + rr;
-                            if (a.QS == 8) {
+                        const int rr = r + j * a.d;  // < XR
+                        const float *xs = s_x + j * XC * XR + rr;
+                        if (a.QS == 8) {
 #pragma unroll
-                                for (int t = 0; t < 8; ++t) acc[t] += xs[t * 160];
-                            } else {
+                            for (int t = 0; t < 8; ++t) acc[t] += xs[t * XR];
+                        } else {
 #pragma unroll
-                                for (int t = 0; t < 16; ++t) acc[t] += xs[t * 160];
-                            }
+                            for (int t = 0; t < 16; ++t) acc[t] += xs[t * XR];
                         }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -350,7 +374,7 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
 // host side
 // --------------------------------------------------------------------------------
 struct TtPlan {
-    int Npad, QS, LN, n_rc, MT, S, NR, TR, n_tr, HB;
+    int Npad, QS, LN, n_rc, MT, S, NR, TR, n_tr, HB, STEP, XR;
     bool ok;
     uint32_t seg_bytes, wrow_bytes, ubytes, xbytes;
     size_t wbytes;
@@ -374,13 +398,18 @@ static TtPlan tt_plan(int R, int Q, int l, int d, int max_mt) {
     if (max_mt >= 1 && mt > max_mt) mt = max_mt;
     if (mt < 1) return p;
     p.MT = mt;
-    p.NR = ((mt - 1) * p.S + 128 + 7) / 8 * 8;
+    // contiguous M tiles: the MT*128 records of a tap row window give D' rows for MT*128 -
+    // (l-1)d outputs (the last (l-1)d rows' sums need the next CTA tile: one overlap per
+    // CTA tile instead of one per M tile)
+    p.NR = mt * 128;
+    p.STEP = mt * 128 - (l - 1) * d;
+    p.XR = 128 + (l - 1) * d;
     p.seg_bytes = (uint32_t)p.NR * 16;
     p.wrow_bytes = (uint32_t)(2 * p.LN * 32);
     p.wbytes = (size_t)p.n_rc * l * p.wrow_bytes;
     if (l > TT_MAX_L) return p;
     // tap rows per unit: as many as leave room for 2 unit buffers next to the exchange area
-    p.xbytes = (uint32_t)l * (p.QS == 8 ? 8 : 16) * 160 * 4;
+    p.xbytes = (uint32_t)l * (p.QS == 8 ? 8 : 16) * p.XR * 4;
     const size_t budget = (size_t)TT_SMEM_TOTAL - p.xbytes - 2048;
     p.TR = 0;
     int tr_max = l;
@@ -411,9 +440,9 @@ static size_t tt_relayout_recs(int Hin, int Win, int pad, int l, int d, const Tt
                                int Ho, int Wo) {
     const int Wv = Win + 2 * pad, Hv = Hin + 2 * pad;
     flat_len = (long long)(Ho - 1) * Wv + Wo;
-    tiles_per_img = (int)((flat_len + (long long)p.MT * p.S - 1) / ((long long)p.MT * p.S));
+    tiles_per_img = (int)((flat_len + p.STEP - 1) / p.STEP);
     // the last tile's windows reach f0 + (l-1)*d*Wv + NR
-    long long need = (long long)(tiles_per_img - 1) * p.MT * p.S + (long long)(l - 1) * d * Wv + p.NR;
+    long long need = (long long)(tiles_per_img - 1) * p.STEP + (long long)(l - 1) * d * Wv + p.NR;
     long long vrecs = (long long)Hv * Wv;
     plane_recs = (need > vrecs ? need : vrecs);
     plane_recs = (plane_recs + 7) / 8 * 8;
@@ -509,6 +538,8 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     a.LN = p.LN;
     a.MT = p.MT;
     a.S = p.S;
+    a.STEP = p.STEP;
+    a.XR = p.XR;
     a.NR = p.NR;
     a.TR = p.TR;
     a.n_tr = p.n_tr;

@@ -2,9 +2,9 @@
 
     python tools/step_traffic.py <full_step.ncu-rep> <out json> <out md> [source note]
 
-The capture holds the launches of one eager c3 training step starting at conv2's forward
-(`-s 40 -c 20`); MAP assigns each captured launch to the bench `kernels` record that times it
-(a record = the staging / relayout launches + the main kernel of one op).  Writes the json
+The capture holds ~one eager c3 training step (`-s 40 -c 20`) starting anywhere in it; SEQ,
+the step's launch sequence, assigns each captured launch to the bench `kernels` record that
+times it (a record = the staging / relayout launches + the main kernel of one op).  Writes the json
 bench.py reads for `roofline.traffic` and a markdown summary for profiles/."""
 import csv
 import io
@@ -12,13 +12,34 @@ import json
 import subprocess
 import sys
 
-# capture index -> bench record (c3 step, round-2 kernel selection)
-MAP = ["02:conv_forward_tc", "03:maxpool_forward", "04:conv_forward_tc", "04:conv_forward_tc",
-       "05:mask_delta", "06:conv_backward_kernel_tc", "06:conv_backward_kernel_tc",
-       "06:conv_backward_kernel_tc", "07:conv_backward_data_tc", "08:maxpool_backward",
-       "09:conv_backward_kernel_tc", "09:conv_backward_kernel_tc", "10:conv_backward_data_tc",
-       "11:maxpool_backward", "12:conv_backward_kernel_tc", "12:conv_backward_kernel_tc",
-       "12:conv_backward_kernel_tc", "00:conv_forward_tc", "01:maxpool_forward"]
+# one c3 training step in issue order: (kernel-name fragment, bench record).  The capture
+# starts anywhere in a step; the sequence is matched cyclically against it.
+SEQ = [("tc_conv_flat_kernel<1, 0, 3>", "00:conv_forward_tc"), ("maxpool_fwd", "01:maxpool_forward"),
+       ("tc_conv_flat_kernel<0, 0, 0>", "02:conv_forward_tc"), ("maxpool_fwd", "03:maxpool_forward"),
+       ("tc_relayout", "04:conv_forward_tc"), ("tc_conv_tap_kernel<0>", "04:conv_forward_tc"),
+       ("mask_delta", "05:mask_delta"), ("tc_stage_dy", "06:conv_backward_kernel_tc"),
+       ("tc_wgrad_ss", "06:conv_backward_kernel_tc"),
+       ("tc_conv_flat_kernel<1, 1, 0>", "07:conv_backward_data_tc"),
+       ("maxpool_bwd", "08:maxpool_backward"), ("tc_wgrad_ss", "09:conv_backward_kernel_tc"),
+       ("tc_conv_flat_kernel<0, 1, 0>", "10:conv_backward_data_tc"),
+       ("maxpool_bwd", "11:maxpool_backward"), ("tc_stage_x_taps", "12:conv_backward_kernel_tc"),
+       ("tc_wgrad_ss", "12:conv_backward_kernel_tc")]
+
+
+def assign(names):
+    """records for the captured launches (None where the sequence does not match)"""
+    n = len(SEQ)
+    for start in range(len(names)):
+        for rot in range(n):
+            k_max = min(n, len(names) - start)
+            if all(SEQ[(rot + k) % n][0] in names[start + k] for k in range(k_max)):
+                out = [None] * len(names)
+                for k in range(k_max):
+                    out[start + k] = SEQ[(rot + k) % n][1]
+                return out
+    raise SystemExit("capture does not match the expected c3 step sequence")
+
+
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -41,11 +62,15 @@ def main():
         return float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
 
     recs = {}
+    body = rows[2:]
+    mapping = assign([r[h.index("Kernel Name")] for r in body])
     lines = ["| # | kernel | record | us | DRAM read GB | write GB | tensor % | DRAM % | L2 % | "
              "issue % |", "|---|---|---|---|---|---|---|---|---|---|"]
-    for i, r in enumerate(rows[2:2 + len(MAP)]):
+    for i, r in enumerate(body):
         name = r[h.index("Kernel Name")]
-        rec = MAP[i]
+        rec = mapping[i]
+        if rec is None:
+            continue
         rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
         t = val(r, "gpu__time_duration.sum")
         e = recs.setdefault(rec, {"launches": [], "dram_bytes": 0.0, "gpu_time_us": 0.0})

@@ -136,6 +136,36 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
     }
 }
 
+// fp16 split of the same weights for the flat kernel's HALF (forward) mode: K steps of 16
+// channels, per K step [W_hi | W_lo] (Npad rows x 16 halves each), element (n, k) at byte
+// (n>>3)*256 + (k>>3)*128 + (n&7)*16 + (k&7)*2 -- the same 64 * Npad bytes per K step.
+__global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
+                                    int R, int l, int Npad, int n_ks) {
+    const int total = n_ks * 2 * Npad * 16;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += gridDim.x * blockDim.x) {
+        const int k = idx & 15;
+        const int n = (idx >> 4) % Npad;
+        const int hl = (idx / (16 * Npad)) & 1;
+        const int ks = idx / (32 * Npad);
+        const int j = ks % l, i = (ks / l) % l, c = (ks / (l * l)) * 16 + k;
+        const float v = (n < Q && c < R) ? w[(((long long)n * R + c) * l + i) * l + j] : 0.f;
+        __half hi, lo;
+        ptx::f16_split(v, hi, lo);
+        const int byte = hl * Npad * 32 + (n >> 3) * 256 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+        wp[((long long)ks * Npad * 64 + byte) / 2] = hl ? lo : hi;
+    }
+}
+
+int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, cudaStream_t st) {
+    const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 15) / 16;
+    const int n_ks = n_rc * l * l;
+    const int total = n_ks * 2 * Npad * 16;
+    tc_pack_weights_f16<<<ceil_div(total, 256), 256, 0, st>>>(w, (__half *)wp, Q, R, l, Npad,
+                                                              n_ks);
+    return check_launch("tc_pack_weights_f16");
+}
+
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st) {
     const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 7) / 8;
     const int tp = rp ? 8 / rp : 1;

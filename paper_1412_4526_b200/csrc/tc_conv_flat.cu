@@ -47,6 +47,7 @@
 namespace dp {
 
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st);
+int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, cudaStream_t st);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
 // 14 warps: registers are granted per 4 warps, so 14 warps (as 16) leave 128 registers
@@ -109,9 +110,14 @@ struct IntTag {
     static constexpr int value = V;
 };
 
-template <bool STACKED, bool BWD, int RP>
+// HALF: fp16 split operands (kind::f16, K = 16 per MMA): records carry 16 channels as
+// [hi c0-7 | hi c8-15 | lo c0-7 | lo c8-15] (8 halves per 16-byte core-matrix row, the same
+// byte geometry as the tf32 records, so descriptors are unchanged) -- half the record and
+// weight bytes and half the MMAs per channel.  Forward only (bounded activations).
+template <bool STACKED, bool BWD, int RP, bool HALF = false>
 __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArgs a) {
     constexpr int TP = RP ? 8 / RP : 1;
+    constexpr int CH = HALF ? 16 : 8;  // channels per chunk (one K step per tap)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t ufull[TF_MAX_HB], uempty[TF_MAX_HB], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
@@ -150,8 +156,8 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
             const int img = tile / a.tiles_per_img;
             const int f0 = (tile - img * a.tiles_per_img) * MT * 128;
             for (int rc = 0, wu = 0; rc < a.n_rc; ++rc) {
-                const float *src = a.in + ((long long)img * a.R + rc * 8) * plane_in;
-                const int cvalid = min(8, a.R - rc * 8);
+                const float *src = a.in + ((long long)img * a.R + rc * CH) * plane_in;
+                const int cvalid = min(CH, a.R - rc * CH);
                 const bool pk = RP > 0 && rc == a.n_rc - 1;
                 const uint32_t wub = pk ? a.wunit_pk : a.wunit_bytes;
                 for (int i = 0; i < a.l; ++i, ++wu, ++gu) {
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         constexpr bool PK = decltype(packed)::value;
                         constexpr int LU = decltype(lu)::value;
                         for (int r0 = lw * 32 + lane; r0 < a.NR; r0 += LU * TF_LGW * 32) {
-                            float v[LU][8];
+                            float v[LU][CH];
 #pragma unroll
                             for (int u = 0; u < LU; ++u) {
                                 const int r = r0 + u * TF_LGW * 32;
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                         r < a.NR && y >= 0 && y < a.Hin && x >= 0 && x < a.Win;
                                     const float *p = src + (ok ? (long long)y * a.Win + x : 0);
 #pragma unroll
-                                    for (int k = 0; k < 8; ++k)
+                                    for (int k = 0; k < CH; ++k)
                                         v[u][k] = (ok && k < cvalid) ? __ldg(p + k * plane_in) : 0.f;
                                 } else {
 #pragma unroll
@@ -230,8 +236,27 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                             for (int u = 0; u < LU; ++u) {
                                 const int r = r0 + u * TF_LGW * 32;
                                 if (r >= a.NR) break;
+                                const uint32_t ps = a.plane_bytes / 16;  // plane stride (16 B)
+                                if constexpr (HALF) {
+                                    uint32_t hw[8], lw2[8];
+#pragma unroll
+                                    for (int q = 0; q < 8; ++q) {
+                                        __half h0, l0, h1, l1;
+                                        ptx::f16_split(v[u][2 * q], h0, l0);
+                                        ptx::f16_split(v[u][2 * q + 1], h1, l1);
+                                        hw[q] = (uint32_t)__half_as_ushort(h0) |
+                                                ((uint32_t)__half_as_ushort(h1) << 16);
+                                        lw2[q] = (uint32_t)__half_as_ushort(l0) |
+                                                 ((uint32_t)__half_as_ushort(l1) << 16);
+                                    }
+                                    uint4 *q0 = reinterpret_cast<uint4 *>(ub) + r;
+                                    q0[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                                    q0[ps] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+                                    q0[2 * ps] = make_uint4(lw2[0], lw2[1], lw2[2], lw2[3]);
+                                    q0[3 * ps] = make_uint4(lw2[4], lw2[5], lw2[6], lw2[7]);
+                                    continue;
+                                }
                                 float4 *p0 = reinterpret_cast<float4 *>(ub) + r;
-                                const uint32_t ps = a.plane_bytes / 16;  // plane stride (float4)
                                 p0[0] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
                                 p0[ps] = make_float4(v[u][4], v[u][5], v[u][6], v[u][7]);
                                 p0[2 * ps] =
@@ -248,7 +273,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     else if (a.NR <= 2 * TF_LGW * 32)
                         fill(BoolTag<false>(), IntTag<2>());
                     else
-                        fill(BoolTag<false>(), IntTag<TF_LU>());
+                        fill(BoolTag<false>(), IntTag<HALF ? TF_LU / 2 : TF_LU>());
                     // generic-proxy stores -> visible to the tensor core (async proxy)
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
@@ -264,8 +289,9 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
     } else if (warp == TF_MMA_WARP) {
         // ================================ MMA issuer ================================
         const uint32_t hs = ptx::smem_u32(smem_raw);
-        const uint32_t idesc_n = ptx::idesc_tf32(128, a.Npad);
-        const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.Npad);
+        const uint32_t idesc_n = HALF ? ptx::idesc_f16(128, a.Npad) : ptx::idesc_tf32(128, a.Npad);
+        const uint32_t idesc_2n =
+            HALF ? ptx::idesc_f16(128, 2 * a.Npad) : ptx::idesc_tf32(128, 2 * a.Npad);
         const uint32_t ks_units = (uint32_t)(a.Npad * 64) >> 4;  // descriptor units = 16 B
         const uint32_t wlo_units = (uint32_t)(a.Npad * 32) >> 4;
         const uint32_t lo_units = (2 * a.plane_bytes) >> 4;
@@ -292,7 +318,14 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         for (int mt = 0; mt < MT; ++mt) {
                             const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * step);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.acc_cols);
-                            if (STACKED) {
+                            if (HALF && STACKED) {
+                                ptx::mma_f16_ss(dd, ad, bj, idesc_2n, acc);
+                                ptx::mma_f16_ss(dd, ad + lo_units, bj, idesc_n, 1);
+                            } else if (HALF) {
+                                ptx::mma_f16_ss(dd, ad, bj, idesc_n, acc);
+                                ptx::mma_f16_ss(dd, ad, bj + wlo_units, idesc_n, 1);
+                                ptx::mma_f16_ss(dd, ad + lo_units, bj, idesc_n, 1);
+                            } else if (STACKED) {
                                 ptx::mma_tf32_ss(dd, ad, bj, idesc_2n, acc);
                                 ptx::mma_tf32_ss(dd, ad + lo_units, bj, idesc_n, 1);
                             } else {
@@ -397,16 +430,16 @@ struct TfPlan {
 
 // M tiles per CTA tile: accumulators double-buffered in the 512 TMEM columns; unit
 // buffers (halo + one tap row of weights) as many as fit, at least two.
-static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd) {
+static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd, bool half = false) {
     TfPlan p;
     p.Npad = (Q + 15) / 16 * 16;
-    p.n_rc = (R + 7) / 8;
+    p.n_rc = half ? (R + 15) / 16 : (R + 7) / 8;
     // tap-packed records for inputs of <= 4 channels.  The kernel also packs the last
     // chunk of a wider input (DP_TF_PACK_LAST), but that measured slower (c2 conv3 data
     // gradient 0.76 -> 0.84 ms): the packed units' loads, not their MMAs, set the pace.
     const int rem = R - (p.n_rc - 1) * 8;
     (void)bwd;
-    p.rp = (rem <= 4 && l > 1 && (p.n_rc == 1 || getenv("DP_TF_PACK_LAST")) &&
+    p.rp = (!half && rem <= 4 && l > 1 && (p.n_rc == 1 || getenv("DP_TF_PACK_LAST")) &&
             !getenv("DP_TF_NOPACK"))
                ? rem
                : 0;
@@ -467,7 +500,10 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     // short images: fewer M tiles per CTA tile
     const int max_mt = (int)((flat_len + 127) / 128);
-    TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd);
+    // fp16-split operands for the forward of inputs with >= 16 channels (DP_TF_HALF=0: tf32)
+    const char *he = getenv("DP_TF_HALF");
+    const bool half = !bwd && R >= 16 && !(he && he[0] == '0');
+    TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, half);
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
                          R, Q, l, d);
@@ -478,7 +514,8 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
                          wbytes);
     if (((uintptr_t)ws & 15) != 0)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
-    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp, st);
+    int rc = half ? tc_pack_f16(w, ws, Q, R, l, st)
+                  : tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp, st);
     if (rc) return rc;
     if (g_tf_sms == 0) {
         int dev = 0;
@@ -529,7 +566,10 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
-    if (bwd && p.stacked)
+    if (half)
+        kern = p.stacked ? tc_conv_flat_kernel<true, false, 0, true>
+                         : tc_conv_flat_kernel<false, false, 0, true>;
+    else if (bwd && p.stacked)
         kern = p.rp == 1   ? tc_conv_flat_kernel<true, true, 1>
                : p.rp == 2 ? tc_conv_flat_kernel<true, true, 2>
                : p.rp == 3 ? tc_conv_flat_kernel<true, true, 3>

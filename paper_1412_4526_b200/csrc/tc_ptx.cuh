@@ -8,6 +8,7 @@
 //    whereas A from SMEM is SMEM-bandwidth bound (~128 B/cycle: ~40 cycles);
 //  * MN-major tf32 A descriptors produced zeros -> operands are K-major.
 #pragma once
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace dp {
@@ -216,6 +217,25 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
            ((uint32_t)(M >> 4) << 24);
+}
+// kind::f16 instruction descriptor: D f32, A/B fp16 (format 0), both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+// D[tmem] (+)= A[smem] * B[smem], fp16 operands (K = 16 per instruction), fp32 accumulate
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// fp16 split: hi = RN(x), lo = RN(x - hi); x = hi + lo to ~2^-22 relative (|x| >= 2^-14:
+// normal range; below, an absolute error of ~2^-25)
+__device__ __forceinline__ void f16_split(float x, __half &hi, __half &lo) {
+    hi = __float2half_rn(x);
+    lo = __float2half_rn(x - __half2float(hi));
 }
 // D[tmem] (+)= A[tmem] * B[smem]
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,

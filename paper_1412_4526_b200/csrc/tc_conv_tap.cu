@@ -68,7 +68,9 @@ __device__ __forceinline__ float tt_act(float v, int kind) {
     return v;
 }
 
-template <bool BWD>
+// HALF (forward only): fp16-split records / weights and kind::f16 MMAs (K = 16 channels per
+// K step, same byte geometry as the tf32 records) -- half the record and weight feed
+template <bool BWD, bool HALF = false>
 __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t ufull[TT_MAX_HB], uempty[TT_MAX_HB], tfull[2], tempty[2];
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
     } else if (warp == TT_MMA_WARP) {
         // ================================ MMA issuer ================================
         const uint32_t sb = ptx::smem_u32(smem_raw);
-        const uint32_t idesc = ptx::idesc_tf32(128, a.LN);
+        const uint32_t idesc = HALF ? ptx::idesc_f16(128, a.LN) : ptx::idesc_tf32(128, a.LN);
         const uint32_t lo_units = (2 * a.seg_bytes) >> 4;
         const uint32_t blo_units = (uint32_t)(a.LN * 32) >> 4;
         int b = 0, buf = 0;
@@ -172,9 +174,15 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
                         for (int mt = 0; mt < MT; ++mt) {
                             const uint64_t ad = a0 + (uint64_t)(mt * 128);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.LN);
-                            ptx::mma_tf32_ss(dd, ad, bh, idesc, acc0);
-                            ptx::mma_tf32_ss(dd, ad, bh + blo_units, idesc, 1);
-                            ptx::mma_tf32_ss(dd, ad + lo_units, bh, idesc, 1);
+                            if (HALF) {
+                                ptx::mma_f16_ss(dd, ad, bh, idesc, acc0);
+                                ptx::mma_f16_ss(dd, ad, bh + blo_units, idesc, 1);
+                                ptx::mma_f16_ss(dd, ad + lo_units, bh, idesc, 1);
+                            } else {
+                                ptx::mma_tf32_ss(dd, ad, bh, idesc, acc0);
+                                ptx::mma_tf32_ss(dd, ad, bh + blo_units, idesc, 1);
+                                ptx::mma_tf32_ss(dd, ad + lo_units, bh, idesc, 1);
+                            }
                         }
                     }
                     ptx::mma_commit(&uempty[b]);
@@ -370,6 +378,69 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
     }
 }
 
+// fp16 forms (HALF): records [hi c0-7 | hi c8-15 | lo c0-7 | lo c8-15] per 16-channel chunk
+__global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__ in,
+                                                       uint4 *__restrict__ xr, int R, int Hin,
+                                                       int Win, int Wv, int pad, int n_rc,
+                                                       long long plane_recs, long long vrecs,
+                                                       long long total) {
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long nrc = idx / plane_recs;
+        const long long f = idx - nrc * plane_recs;
+        const int rc = (int)(nrc % n_rc);
+        const long long n = nrc / n_rc;
+        const long long yv = f / Wv;
+        const int y = (int)yv - pad, x = (int)(f - yv * Wv) - pad;
+        const bool ok = f < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win;
+        const float *src = in + ((n * R + rc * 16) * Hin + (ok ? y : 0)) * (long long)Win + (ok ? x : 0);
+        const long long cs = (long long)Hin * Win;
+        uint32_t hw[8], lw[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int c0 = rc * 16 + 2 * q;
+            const float v0 = (ok && c0 < R) ? __ldg(src + (2 * q) * cs) : 0.f;
+            const float v1 = (ok && c0 + 1 < R) ? __ldg(src + (2 * q + 1) * cs) : 0.f;
+            __half h0, l0, h1, l1;
+            ptx::f16_split(v0, h0, l0);
+            ptx::f16_split(v1, h1, l1);
+            hw[q] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            lw[q] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        }
+        uint4 *dst = xr + nrc * 4 * plane_recs + f;
+        dst[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        dst[plane_recs] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+        dst[2 * plane_recs] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        dst[3 * plane_recs] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+    }
+}
+
+// weights W(q, r, i, j) -> per (16-channel chunk rc, tap row i): [hi | lo] tiles of LN rows
+// (row n = j*QS + q) x K = 16 halves: element (n, k) at (n>>3)*256 + (k>>3)*128 + (n&7)*16 +
+// (k&7)*2 (forward only)
+__global__ void tc_pack_tap_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
+                                int R, int l, int QS, int LN, int n_rc) {
+    const long long total = (long long)n_rc * l * 2 * LN * 16;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(idx & 15);
+        const long long rest = idx >> 4;
+        const int n = (int)(rest % LN);
+        const long long r2 = rest / LN;
+        const int hl = (int)(r2 & 1);
+        const long long ri = r2 >> 1;  // rc * l + i
+        const int i = (int)(ri % l), rc = (int)(ri / l);
+        const int j = n / QS, qo = n - j * QS;
+        const int c = rc * 16 + k;
+        const float v = (j < l && qo < Q && c < R) ? w[(((long long)qo * R + c) * l + i) * l + j] : 0.f;
+        __half hi, lo;
+        ptx::f16_split(v, hi, lo);
+        const long long byte = (ri * 2 + hl) * (long long)LN * 32 + (n >> 3) * 256 + (k >> 3) * 128 +
+                               (n & 7) * 16 + (k & 7) * 2;
+        wp[byte / 2] = hl ? lo : hi;
+    }
+}
+
 // --------------------------------------------------------------------------------
 // host side
 // --------------------------------------------------------------------------------
@@ -380,13 +451,13 @@ struct TtPlan {
     size_t wbytes;
 };
 
-static TtPlan tt_plan(int R, int Q, int l, int d, int max_mt) {
+static TtPlan tt_plan(int R, int Q, int l, int d, int max_mt, bool half = false) {
     TtPlan p;
     p.ok = false;
     p.Npad = (Q + 15) / 16 * 16;
     p.QS = (Q <= 8 && !getenv("DP_TT_QS16")) ? 8 : p.Npad;
     p.LN = (l * p.QS + 15) / 16 * 16;
-    p.n_rc = (R + 7) / 8;
+    p.n_rc = half ? (R + 15) / 16 : (R + 7) / 8;
     p.S = 128 - (l - 1) * d;
     if (p.LN > 256 || p.S < 32 || p.Npad > 256) return p;
     int mt = 256 / p.LN;
@@ -482,7 +553,11 @@ static int g_tt_sms = 0;
 int tt_launch(const float *in, const float *w, const float *bias, float *out, const float *gate,
               int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
               int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st) {
-    TtPlan p = tt_plan(R, Q, l, d, 0);
+    // fp16-split operands for the forward of inputs with >= 16 channels (DP_TF_HALF=0: tf32);
+    // the workspace query stays tf32-sized (a superset)
+    const char *he = getenv("DP_TF_HALF");
+    const bool half = !bwd && R >= 16 && !(he && he[0] == '0');
+    TtPlan p = tt_plan(R, Q, l, d, 0, half);
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "tap-stacked conv: unsupported (R=%d Q=%d k=%d d=%d)",
                          R, Q, l, d);
@@ -502,8 +577,12 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     {
         const long long total = (long long)p.n_rc * l * 2 * p.LN * 8;
         long long g = (total + 255) / 256;
-        tc_pack_tap<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, wp, Q, R, l, p.QS, p.LN,
-                                                                p.n_rc, bwd ? 1 : 0);
+        if (half)
+            tc_pack_tap_f16<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, (__half *)wp, Q, R, l,
+                                                                        p.QS, p.LN, p.n_rc);
+        else
+            tc_pack_tap<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, wp, Q, R, l, p.QS, p.LN,
+                                                                    p.n_rc, bwd ? 1 : 0);
         int rc = check_launch("tc_pack_tap");
         if (rc) return rc;
     }
@@ -512,8 +591,12 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
         const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
         const long long total = (long long)n * p.n_rc * plane_recs;
         long long g = (total + 255) / 256;
-        tc_relayout<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
-            in, xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
+        if (half)
+            tc_relayout_f16<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
+                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
+        else
+            tc_relayout<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
+                in, xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
         int rc = check_launch("tc_relayout");
         if (rc) return rc;
     }
@@ -562,7 +645,9 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     const int grid = a.total_tiles < g_tt_sms ? a.total_tiles : g_tt_sms;
     a.xoff = (uint32_t)p.HB * p.ubytes;
     const size_t smem = (size_t)a.xoff + p.xbytes;
-    void (*kern)(const TtArgs) = bwd ? tc_conv_tap_kernel<true> : tc_conv_tap_kernel<false>;
+    void (*kern)(const TtArgs) = bwd    ? tc_conv_tap_kernel<true>
+                                 : half ? tc_conv_tap_kernel<false, true>
+                                        : tc_conv_tap_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess)

@@ -185,6 +185,8 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
               int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st);
 // flattened shared-memory-operand variant (tc_conv_flat.cu), preferred when it applies
 bool tf_conv_supported(int R, int Q, int l, int d);
+size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
+                             int Ho, int Wo);
 int tf_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
                     int, int, int, void *, size_t, cudaStream_t);
 int tf_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
@@ -785,7 +787,11 @@ size_t tc_conv_fwd_workspace(int n, int cin, int h, int wd, int cout, int k, int
     const int e = (k - 1) * d + 1;
     const size_t t = tt_conv_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
     const size_t w = tc_conv_workspace(cin, cout, k);
-    return t > w ? t : w;
+    // the flat kernel's TMA-fed forward (relayout planes) where the tap-stacked one is not used
+    const size_t f =
+        t ? 0 : tf_relayout_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
+    size_t m = t > w ? t : w;
+    return f > m ? f : m;
 }
 
 size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, int d) {

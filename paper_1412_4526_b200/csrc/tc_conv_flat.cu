@@ -79,6 +79,8 @@ struct TfArgs {
     uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
     int tiles_per_img, total_tiles, flat_len;
     unsigned long long *trace;  // DP_TC_TRACE: per-unit clock64 stamps of CTA 0 (8 slots)
+    const unsigned char *xr;    // relayout planes (TMA-fed mode) or nullptr (loader warps)
+    long long plane_recs;       // records per relayout plane
 };
 
 // slots: 0/1 loader warp 0 unit start/end, 2/3/4 MMA wait/got/issued, 5/6 epilogue
@@ -130,7 +132,8 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
         s_bias[o] = (!BWD && o < a.Q) ? a.bias[o] : 0.f;
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.HB; ++b) {
-            ptx::mbar_init(&ufull[b], TF_LGW + 1);  // + the weight copy's expect_tx
+            // loader warps + the weight copy's expect_tx; TMA-fed: one expect_tx
+            ptx::mbar_init(&ufull[b], a.xr ? 1 : TF_LGW + 1);
             ptx::mbar_init(&uempty[b], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -145,7 +148,49 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
     ptx::tc_fence_after();
     const uint32_t tmem = s_tmem;
 
-    if (warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
+    if (a.xr && warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
+        // ====================== TMA-fed producer (relayout planes) ======================
+        // the unit's four record planes are contiguous ranges of the pre-split relayout
+        // (tc_relayout / tc_relayout_f16): four bulk copies + the weight unit, one expect_tx
+        if (warp == TF_LOAD_WARP0 && lane == 0) {
+            const unsigned char *wsrc = reinterpret_cast<const unsigned char *>(a.wpack);
+            int b = 0, gu = 0;
+            uint32_t uph = 0;
+            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+                const int img = tile / a.tiles_per_img;
+                const int f0 = (tile - img * a.tiles_per_img) * MT * 128;
+                for (int rc = 0; rc < a.n_rc; ++rc) {
+                    const unsigned char *pl = a.xr + ((size_t)img * a.n_rc + rc) * 4 *
+                                                         (size_t)a.plane_recs * 16;
+                    for (int i = 0; i < a.l; ++i, ++gu) {
+                        ptx::mbar_wait(&uempty[b], uph ^ 1);
+                        TF_TRACE(a, gu, 0, true);
+                        unsigned char *ub = smem_raw + (size_t)b * a.ubytes;
+                        ptx::mbar_expect_tx(&ufull[b], 4 * a.plane_bytes + a.wunit_bytes);
+                        const long long rec0 = f0 + (long long)i * a.d * a.Wv;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            ptx::bulk_g2s(ub + (size_t)q * a.plane_bytes,
+                                          pl + ((size_t)q * a.plane_recs + rec0) * 16,
+                                          a.plane_bytes, &ufull[b]);
+                        const unsigned char *ws =
+                            wsrc + ((size_t)rc * a.l + i) * a.wunit_bytes;
+                        for (uint32_t off = 0; off < a.wunit_bytes; off += 32768u) {
+                            const uint32_t nb =
+                                a.wunit_bytes - off < 32768u ? a.wunit_bytes - off : 32768u;
+                            ptx::bulk_g2s(ub + a.halo_bytes + off, ws + off, nb, &ufull[b]);
+                        }
+                        TF_TRACE(a, gu, 1, true);
+                        if (++b == a.HB) {
+                            b = 0;
+                            uph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
         // ================================ loaders ================================
         const int lw = (warp - TF_LOAD_WARP0) % TF_LGW, grp = (warp - TF_LOAD_WARP0) / TF_LGW;
         const long long plane_in = (long long)a.Hin * a.Win;
@@ -240,15 +285,9 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                 if constexpr (HALF) {
                                     uint32_t hw[8], lw2[8];
 #pragma unroll
-                                    for (int q = 0; q < 8; ++q) {
-                                        __half h0, l0, h1, l1;
-                                        ptx::f16_split(v[u][2 * q], h0, l0);
-                                        ptx::f16_split(v[u][2 * q + 1], h1, l1);
-                                        hw[q] = (uint32_t)__half_as_ushort(h0) |
-                                                ((uint32_t)__half_as_ushort(h1) << 16);
-                                        lw2[q] = (uint32_t)__half_as_ushort(l0) |
-                                                 ((uint32_t)__half_as_ushort(l1) << 16);
-                                    }
+                                    for (int q = 0; q < 8; ++q)
+                                        ptx::f16_split2(v[u][2 * q], v[u][2 * q + 1], hw[q],
+                                                        lw2[q]);
                                     uint4 *q0 = reinterpret_cast<uint4 *>(ub) + r;
                                     q0[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                                     q0[ps] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
@@ -490,6 +529,52 @@ bool tf_conv_supported(int R, int Q, int l, int d) {
     return tf_plan(R, Q, l, d, 0, true).ok;  // unpacked: the larger weight unit
 }
 
+// relayout kernels of the tap-stacked conv (tc_conv_tap.cu): the same record planes
+__global__ void tc_relayout(const float *__restrict__ in, float4 *__restrict__ xr, int R, int Hin,
+                            int Win, int Wv, int pad, int n_rc, long long plane_recs,
+                            long long vrecs, long long total);
+__global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict__ xr, int R,
+                                int Hin, int Win, int Wv, int pad, int n_rc, long long plane_recs,
+                                long long vrecs, long long total);
+
+// TMA-fed mode (forward, fp16-split, inputs >= 16 channels): the fp16 loaders were the
+// limit (tools/tf_trace.py, c3 conv2: ~2800 loader vs ~2000 MMA cycles per unit), so the
+// split is done once by a bandwidth-bound relayout pass and units arrive as bulk copies.
+static bool tf_relayout_mode(int R, bool bwd) {
+    const char *he = getenv("DP_TF_HALF");
+    const char *re = getenv("DP_TF_RELAYOUT");
+    return !bwd && R >= 16 && !(he && he[0] == '0') && !(re && re[0] == '0');
+}
+
+static long long tf_plane_recs(const TfPlan &p, int Hin, int Win, int pad, int l, int d, int Ho,
+                               int Wo) {
+    const int Wv = Win + 2 * pad;
+    const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
+    const long long tpi = (flat_len + (long long)p.MT * 128 - 1) / ((long long)p.MT * 128);
+    const long long need = (tpi - 1) * p.MT * 128 + (long long)(l - 1) * d * Wv + p.NR;
+    const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
+    return ((need > vrecs ? need : vrecs) + 7) / 8 * 8;
+}
+
+static size_t tf_weight_bytes(const TfPlan &p, int l) {
+    return p.rp ? (size_t)(p.n_rc - 1) * l * l * p.Npad * 64 + (size_t)l * p.wunit_pk
+                : (size_t)p.n_rc * l * p.wunit_bytes;
+}
+
+// workspace of the TMA-fed forward (packed weights + relayout planes), 0 when it does not
+// apply; the flat kernel uses it when the caller's workspace covers it
+size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
+                             int Ho, int Wo) {
+    if (!tf_relayout_mode(R, false) || Ho < 1 || Wo < 1) return 0;
+    const int Wv = Win + 2 * pad;
+    const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
+    const int max_mt = (int)((flat_len + 127) / 128);
+    TfPlan p = tf_plan(R, Q, l, d, max_mt, false, true);
+    if (!p.ok) return 0;
+    const size_t wb = (tf_weight_bytes(p, l) + 255) / 256 * 256;
+    return wb + (size_t)n * p.n_rc * 4 * tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo) * 16;
+}
+
 static int g_tf_sms = 0;
 
 static int tf_launch(const float *in, const float *w, const float *bias, float *out,
@@ -507,11 +592,28 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
                          R, Q, l, d);
-    const size_t wbytes = p.rp ? (size_t)(p.n_rc - 1) * l * l * p.Npad * 64 + (size_t)l * p.wunit_pk
-                               : (size_t)p.n_rc * l * p.wunit_bytes;
+    const size_t wbytes = tf_weight_bytes(p, l);
     if (ws == nullptr || ws_bytes < wbytes)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
                          wbytes);
+    // TMA-fed when it applies and the workspace also covers the relayout planes
+    const unsigned char *xr = nullptr;
+    long long plane_recs = 0;
+    if (half && tf_relayout_mode(R, bwd) && ((uintptr_t)ws & 255) == 0) {
+        const size_t wb = (wbytes + 255) / 256 * 256;
+        plane_recs = tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo);
+        const size_t need = wb + (size_t)n * p.n_rc * 4 * plane_recs * 16;
+        if (ws_bytes >= need && plane_recs < 0x7fffffffLL) {
+            xr = (const unsigned char *)ws + wb;
+            const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
+            const long long total = (long long)n * p.n_rc * plane_recs;
+            const long long g = (total + 255) / 256;
+            tc_relayout_f16<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
+                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
+            const int rc0 = check_launch("tc_relayout_f16");
+            if (rc0) return rc0;
+        }
+    }
     if (((uintptr_t)ws & 15) != 0)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
     int rc = half ? tc_pack_f16(w, ws, Q, R, l, st)
@@ -563,6 +665,8 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     a.total_tiles = (int)tt;
     if (a.total_tiles == 0) return DP_OK;
     a.trace = getenv("DP_TC_TRACE") ? tc_trace_buffer(st) : nullptr;
+    a.xr = xr;
+    a.plane_recs = plane_recs;
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);

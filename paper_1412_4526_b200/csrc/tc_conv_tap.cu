@@ -401,11 +401,7 @@ __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__
             const int c0 = rc * 16 + 2 * q;
             const float v0 = (ok && c0 < R) ? __ldg(src + (2 * q) * cs) : 0.f;
             const float v1 = (ok && c0 + 1 < R) ? __ldg(src + (2 * q + 1) * cs) : 0.f;
-            __half h0, l0, h1, l1;
-            ptx::f16_split(v0, h0, l0);
-            ptx::f16_split(v1, h1, l1);
-            hw[q] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            lw[q] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+            ptx::f16_split2(v0, v1, hw[q], lw[q]);
         }
         uint4 *dst = xr + nrc * 4 * plane_recs + f;
         dst[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);

@@ -1,6 +1,6 @@
 """Per bench-record DRAM traffic from a one-step full ncu capture (tools/profile_c3.sh):
 
-    python tools/step_traffic.py <full_step.ncu-rep> <out json> <out md> [source note]
+    python tools/step_traffic.py <full_step.ncu-rep | raw.csv> <out json> <out md> [source note]
 
 The capture holds ~one eager c3 training step (`-s 40 -c 20`) starting anywhere in it; SEQ,
 the step's launch sequence, assigns each captured launch to the bench `kernels` record that
@@ -14,14 +14,15 @@ import sys
 
 # one c3 training step in issue order: (kernel-name fragment, bench record).  The capture
 # starts anywhere in a step; the sequence is matched cyclically against it.
-SEQ = [("tc_conv_flat_kernel<1, 0, 3>", "00:conv_forward_tc"), ("maxpool_fwd", "01:maxpool_forward"),
-       ("tc_conv_flat_kernel<0, 0, 0>", "02:conv_forward_tc"), ("maxpool_fwd", "03:maxpool_forward"),
-       ("tc_relayout", "04:conv_forward_tc"), ("tc_conv_tap_kernel<0>", "04:conv_forward_tc"),
+SEQ = [("tc_conv_flat_kernel<1, 0, 3", "00:conv_forward_tc"), ("maxpool_fwd", "01:maxpool_forward"),
+       ("tc_relayout", "02:conv_forward_tc"), ("tc_conv_flat_kernel<0, 0, 0", "02:conv_forward_tc"),
+       ("maxpool_fwd", "03:maxpool_forward"),
+       ("tc_relayout", "04:conv_forward_tc"), ("tc_conv_tap_kernel<0", "04:conv_forward_tc"),
        ("mask_delta", "05:mask_delta"), ("tc_stage_dy", "06:conv_backward_kernel_tc"),
        ("tc_wgrad_ss", "06:conv_backward_kernel_tc"),
-       ("tc_conv_flat_kernel<1, 1, 0>", "07:conv_backward_data_tc"),
+       ("tc_conv_flat_kernel<1, 1, 0", "07:conv_backward_data_tc"),
        ("maxpool_bwd", "08:maxpool_backward"), ("tc_wgrad_ss", "09:conv_backward_kernel_tc"),
-       ("tc_conv_flat_kernel<0, 1, 0>", "10:conv_backward_data_tc"),
+       ("tc_conv_flat_kernel<0, 1, 0", "10:conv_backward_data_tc"),
        ("maxpool_bwd", "11:maxpool_backward"), ("tc_stage_x_taps", "12:conv_backward_kernel_tc"),
        ("tc_wgrad_ss", "12:conv_backward_kernel_tc")]
 
@@ -52,8 +53,12 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e3, "us": 1
 def main():
     rep, out_json, out_md = sys.argv[1:4]
     note = sys.argv[4] if len(sys.argv) > 4 else rep
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                          ",".join(METRICS)], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a saved `ncu -i <rep> --page raw --csv` export
+        with open(rep) as fh:
+            raw = fh.read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                              ",".join(METRICS)], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
 

@@ -136,11 +136,13 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
     }
 }
 
-// fp16 split of the same weights for the flat kernel's HALF (forward) mode: K steps of 16
+// fp16 split of the same weights for the flat kernel's HALF mode: K steps of 16
 // channels, per K step [W_hi | W_lo] (Npad rows x 16 halves each), element (n, k) at byte
 // (n>>3)*256 + (k>>3)*128 + (n&7)*16 + (k&7)*2 -- the same 64 * Npad bytes per K step.
+// bwd: the data gradient's rotated weights (w is (R = cout, Q = cin, l, l)), lo' scaled by
+// 2^11 (the offset split of the fp16 data gradient: cross products in their own columns)
 __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
-                                    int R, int l, int Npad, int n_ks) {
+                                    int R, int l, int Npad, int n_ks, int bwd) {
     const int total = n_ks * 2 * Npad * 16;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += gridDim.x * blockDim.x) {
@@ -149,20 +151,28 @@ __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restr
         const int hl = (idx / (16 * Npad)) & 1;
         const int ks = idx / (32 * Npad);
         const int j = ks % l, i = (ks / l) % l, c = (ks / (l * l)) * 16 + k;
-        const float v = (n < Q && c < R) ? w[(((long long)n * R + c) * l + i) * l + j] : 0.f;
+        float v = 0.f;
+        if (n < Q && c < R)
+            v = bwd ? w[(((long long)c * Q + n) * l + (l - 1 - i)) * l + (l - 1 - j)]
+                    : w[(((long long)n * R + c) * l + i) * l + j];
         __half hi, lo;
-        ptx::f16_split(v, hi, lo);
+        if (bwd) {
+            hi = __float2half_rn(v);
+            lo = __float2half_rn((v - __half2float(hi)) * ptx::F16_LO_SCALE);
+        } else {
+            ptx::f16_split(v, hi, lo);
+        }
         const int byte = hl * Npad * 32 + (n >> 3) * 256 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
         wp[((long long)ks * Npad * 64 + byte) / 2] = hl ? lo : hi;
     }
 }
 
-int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, cudaStream_t st) {
+int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, cudaStream_t st) {
     const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 15) / 16;
     const int n_ks = n_rc * l * l;
     const int total = n_ks * 2 * Npad * 16;
     tc_pack_weights_f16<<<ceil_div(total, 256), 256, 0, st>>>(w, (__half *)wp, Q, R, l, Npad,
-                                                              n_ks);
+                                                              n_ks, bwd);
     return check_launch("tc_pack_weights_f16");
 }
 
@@ -186,7 +196,7 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
 // flattened shared-memory-operand variant (tc_conv_flat.cu), preferred when it applies
 bool tf_conv_supported(int R, int Q, int l, int d);
 size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
-                             int Ho, int Wo);
+                             int Ho, int Wo, bool bwd);
 int tf_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
                     int, int, int, void *, size_t, cudaStream_t);
 int tf_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
@@ -789,7 +799,7 @@ size_t tc_conv_fwd_workspace(int n, int cin, int h, int wd, int cout, int k, int
     const size_t w = tc_conv_workspace(cin, cout, k);
     // the flat kernel's TMA-fed forward (relayout planes) where the tap-stacked one is not used
     const size_t f =
-        t ? 0 : tf_relayout_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
+        t ? 0 : tf_relayout_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1, false);
     size_t m = t > w ? t : w;
     return f > m ? f : m;
 }
@@ -798,7 +808,10 @@ size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, in
     const int e = (k - 1) * d + 1;
     const size_t t = tt_conv_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1, wo + e - 1);
     const size_t w = tc_conv_workspace(cout, cin, k);
-    return t > w ? t : w;
+    const size_t f = t ? 0 : tf_relayout_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1,
+                                                   wo + e - 1, true);
+    size_t m = t > w ? t : w;
+    return f > m ? f : m;
 }
 
 int tc_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,

@@ -47,7 +47,7 @@
 namespace dp {
 
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st);
-int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, cudaStream_t st);
+int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, cudaStream_t st);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
 // 14 warps: registers are granted per 4 warps, so 14 warps (as 16) leave 128 registers
@@ -285,9 +285,14 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                 if constexpr (HALF) {
                                     uint32_t hw[8], lw2[8];
 #pragma unroll
-                                    for (int q = 0; q < 8; ++q)
-                                        ptx::f16_split2(v[u][2 * q], v[u][2 * q + 1], hw[q],
-                                                        lw2[q]);
+                                    for (int q = 0; q < 8; ++q) {
+                                        if (BWD)  // deltas: the offset split
+                                            ptx::f16_split2_scaled(v[u][2 * q], v[u][2 * q + 1],
+                                                                   hw[q], lw2[q]);
+                                        else
+                                            ptx::f16_split2(v[u][2 * q], v[u][2 * q + 1], hw[q],
+                                                            lw2[q]);
+                                    }
                                     uint4 *q0 = reinterpret_cast<uint4 *>(ub) + r;
                                     q0[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                                     q0[ps] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
@@ -357,7 +362,11 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         for (int mt = 0; mt < MT; ++mt) {
                             const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * step);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.acc_cols);
-                            if (HALF && STACKED) {
+                            if (HALF && STACKED && BWD) {
+                                // offset split: [hi*hi | hi*lo'] + lo'*hi into the lo' half
+                                ptx::mma_f16_ss(dd, ad, bj, idesc_2n, acc);
+                                ptx::mma_f16_ss(dd + a.Npad, ad + lo_units, bj, idesc_n, 1);
+                            } else if (HALF && STACKED) {
                                 ptx::mma_f16_ss(dd, ad, bj, idesc_2n, acc);
                                 ptx::mma_f16_ss(dd, ad + lo_units, bj, idesc_n, 1);
                             } else if (HALF) {
@@ -434,7 +443,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     for (int t = 0; t < 16; ++t) {
                         if (t >= nq) break;
                         float val = __uint_as_float(r[t]);
-                        if (STACKED) val += __uint_as_float(r2[t]);
+                        if (STACKED && HALF && BWD)
+                            val += __uint_as_float(r2[t]) * (1.f / ptx::F16_LO_SCALE);
+                        else if (STACKED)
+                            val += __uint_as_float(r2[t]);
                         if (!BWD)
                             val = tf_act(val + aux[t], a.act);
                         else if (a.gate)
@@ -492,8 +504,10 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd, bool hal
     // grad 1.19 stacked vs 1.26), are MMA bound and keep stacking (c2 conv2 fwd 0.83 vs 1.00).
     p.stacked = 2 * p.Npad <= 256 && !getenv("DP_TF_NOSTACK") &&
                 (R < 32 || p.Npad < 64 || l > 4 || getenv("DP_TF_STACK"));
+    // the fp16 data gradient needs the second accumulator half (offset-split cross terms)
+    if (half && bwd) p.stacked = 2 * p.Npad <= 256;
     p.acc_cols = p.stacked ? 2 * p.Npad : p.Npad;
-    p.ok = p.Npad <= 256;
+    p.ok = p.Npad <= 256 && (!(half && bwd) || p.stacked);
     int mt = p.acc_cols <= 256 ? 256 / p.acc_cols : 1;
     if (mt > TF_MAX_MT) mt = TF_MAX_MT;
     if (const char *e = getenv("DP_TF_MT")) {
@@ -535,15 +549,21 @@ __global__ void tc_relayout(const float *__restrict__ in, float4 *__restrict__ x
                             long long vrecs, long long total);
 __global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict__ xr, int R,
                                 int Hin, int Win, int Wv, int pad, int n_rc, long long plane_recs,
-                                long long vrecs, long long total);
+                                long long vrecs, long long total, int scaled_lo);
 
 // TMA-fed mode (forward, fp16-split, inputs >= 16 channels): the fp16 loaders were the
 // limit (tools/tf_trace.py, c3 conv2: ~2800 loader vs ~2000 MMA cycles per unit), so the
 // split is done once by a bandwidth-bound relayout pass and units arrive as bulk copies.
+// fp16-split operands: forward of inputs with >= 16 channels (DP_TF_HALF=0: tf32), and the
+// data gradient of deltas with >= 16 channels through the offset split (DP_TF_HALF_BWD=0)
+static bool tf_half(int R, bool bwd) {
+    const char *he = getenv(bwd ? "DP_TF_HALF_BWD" : "DP_TF_HALF");
+    return R >= 16 && !(he && he[0] == '0');
+}
+
 static bool tf_relayout_mode(int R, bool bwd) {
-    const char *he = getenv("DP_TF_HALF");
     const char *re = getenv("DP_TF_RELAYOUT");
-    return !bwd && R >= 16 && !(he && he[0] == '0') && !(re && re[0] == '0');
+    return tf_half(R, bwd) && !(re && re[0] == '0');
 }
 
 static long long tf_plane_recs(const TfPlan &p, int Hin, int Win, int pad, int l, int d, int Ho,
@@ -564,12 +584,12 @@ static size_t tf_weight_bytes(const TfPlan &p, int l) {
 // workspace of the TMA-fed forward (packed weights + relayout planes), 0 when it does not
 // apply; the flat kernel uses it when the caller's workspace covers it
 size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
-                             int Ho, int Wo) {
-    if (!tf_relayout_mode(R, false) || Ho < 1 || Wo < 1) return 0;
+                             int Ho, int Wo, bool bwd) {
+    if (!tf_relayout_mode(R, bwd) || Ho < 1 || Wo < 1) return 0;
     const int Wv = Win + 2 * pad;
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     const int max_mt = (int)((flat_len + 127) / 128);
-    TfPlan p = tf_plan(R, Q, l, d, max_mt, false, true);
+    TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, true);
     if (!p.ok) return 0;
     const size_t wb = (tf_weight_bytes(p, l) + 255) / 256 * 256;
     return wb + (size_t)n * p.n_rc * 4 * tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo) * 16;
@@ -585,10 +605,12 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     // short images: fewer M tiles per CTA tile
     const int max_mt = (int)((flat_len + 127) / 128);
-    // fp16-split operands for the forward of inputs with >= 16 channels (DP_TF_HALF=0: tf32)
-    const char *he = getenv("DP_TF_HALF");
-    const bool half = !bwd && R >= 16 && !(he && he[0] == '0');
+    bool half = tf_half(R, bwd);
     TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, half);
+    if (half && !p.ok) {  // e.g. no second accumulator half for a wide data gradient
+        half = false;
+        p = tf_plan(R, Q, l, d, max_mt, bwd, false);
+    }
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
                          R, Q, l, d);
@@ -609,14 +631,15 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
             const long long total = (long long)n * p.n_rc * plane_recs;
             const long long g = (total + 255) / 256;
             tc_relayout_f16<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
-                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
+                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total,
+                bwd ? 1 : 0);
             const int rc0 = check_launch("tc_relayout_f16");
             if (rc0) return rc0;
         }
     }
     if (((uintptr_t)ws & 15) != 0)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
-    int rc = half ? tc_pack_f16(w, ws, Q, R, l, st)
+    int rc = half ? tc_pack_f16(w, ws, Q, R, l, bwd ? 1 : 0, st)
                   : tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp, st);
     if (rc) return rc;
     if (g_tf_sms == 0) {
@@ -670,7 +693,9 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
-    if (half)
+    if (half && bwd)
+        kern = tc_conv_flat_kernel<true, true, 0, true>;
+    else if (half)
         kern = p.stacked ? tc_conv_flat_kernel<true, false, 0, true>
                          : tc_conv_flat_kernel<false, false, 0, true>;
     else if (bwd && p.stacked)

@@ -379,11 +379,12 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
 }
 
 // fp16 forms (HALF): records [hi c0-7 | hi c8-15 | lo c0-7 | lo c8-15] per 16-channel chunk
+// scaled_lo: the offset split (ptx::f16_split2_scaled) for deltas of unknown magnitude
 __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__ in,
                                                        uint4 *__restrict__ xr, int R, int Hin,
                                                        int Win, int Wv, int pad, int n_rc,
                                                        long long plane_recs, long long vrecs,
-                                                       long long total) {
+                                                       long long total, int scaled_lo) {
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const long long nrc = idx / plane_recs;
@@ -401,7 +402,10 @@ __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__
             const int c0 = rc * 16 + 2 * q;
             const float v0 = (ok && c0 < R) ? __ldg(src + (2 * q) * cs) : 0.f;
             const float v1 = (ok && c0 + 1 < R) ? __ldg(src + (2 * q + 1) * cs) : 0.f;
-            ptx::f16_split2(v0, v1, hw[q], lw[q]);
+            if (scaled_lo)
+                ptx::f16_split2_scaled(v0, v1, hw[q], lw[q]);
+            else
+                ptx::f16_split2(v0, v1, hw[q], lw[q]);
         }
         uint4 *dst = xr + nrc * 4 * plane_recs + f;
         dst[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -589,7 +593,7 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
         long long g = (total + 255) / 256;
         if (half)
             tc_relayout_f16<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
-                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
+                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total, 0);
         else
             tc_relayout<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
                 in, xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);

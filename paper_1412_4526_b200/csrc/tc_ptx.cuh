@@ -246,6 +246,19 @@ __device__ __forceinline__ void f16_split2(float a, float b, uint32_t &hi, uint3
     hi = *reinterpret_cast<const uint32_t *>(&h);
     lo = *reinterpret_cast<const uint32_t *>(&l);
 }
+// offset split for operands of unknown magnitude (deltas): lo' = RN_fp16((x - hi) * 2^11),
+// kept in the normal fp16 range whenever hi is; the cross products hi*lo' + lo'*hi carry the
+// 2^11 and accumulate in their own TMEM columns, scaled back by 2^-11 in the epilogue.  x is
+// represented to ~2^-23 relative above 2^-13 and to ~2^-35 absolute below (vs ~2^-25 with an
+// unscaled lo).
+constexpr float F16_LO_SCALE = 2048.f;
+__device__ __forceinline__ void f16_split2_scaled(float a, float b, uint32_t &hi, uint32_t &lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn((a - hf.x) * F16_LO_SCALE, (b - hf.y) * F16_LO_SCALE);
+    hi = *reinterpret_cast<const uint32_t *>(&h);
+    lo = *reinterpret_cast<const uint32_t *>(&l);
+}
 // D[tmem] (+)= A[tmem] * B[smem]
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {

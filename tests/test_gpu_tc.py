@@ -288,3 +288,26 @@ def test_layer0_pitched_delta_path(p, d):
     ops.conv_backward_kernel_fast(x, dxp, dw2, db2, k, kd, ws, dy_pitch=pp)
     torch.cuda.synchronize()
     assert torch.equal(dw1, dw2) and torch.equal(db1, db2)
+
+
+@pytest.mark.parametrize("scale", [1e-3, 1e-6, 1e3])
+def test_tc_backward_data_fp16_offset_split_range(scale):
+    """The fp16 data gradient (offset split, lo' = RN((dy - hi) * 2^11), cross products in
+    their own accumulator half) stays within the north-star bound for deltas far from 1 in
+    magnitude -- where an unscaled fp16 lo would fall into subnormals."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = 2, 50, 50, 3, 4, 60, 64
+    rng = np.random.default_rng(11)
+    e = (k - 1) * d + 1
+    dy = _t((rng.uniform(-1, 1, (n, co, h - e + 1, w - e + 1)) * scale).astype(np.float32))
+    wt = _t((rng.uniform(-0.5, 0.5, (co, ci, k, k)) * 4.0 / np.sqrt(co * k * k))
+            .astype(np.float32))
+    ref = torch.empty((n, ci, h, w), device="cuda", dtype=torch.float64)
+    ops.conv_backward_data(dy.double(), wt.double(), ref, k, d)
+    dx = torch.full((n, ci, h, w), float("nan"), device="cuda")
+    ws = torch.empty(ops.bwd_fast_workspace(dy, ci, k, d), dtype=torch.uint8, device="cuda")
+    ops.conv_backward_data_fast(dy, wt, dx, k, d, ws)
+    torch.cuda.synchronize()
+    assert torch.isfinite(dx).all()
+    assert _rel(dx, ref) < TOL

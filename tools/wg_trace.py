@@ -11,9 +11,12 @@ sys.path.insert(0, ".")
 from paper_1412_4526_b200 import _lib  # noqa: E402
 from paper_1412_4526_b200.engine import ops  # noqa: E402
 
-LAYERS = [(3, 284, 16, 6, 1), (16, 278, 32, 5, 2), (32, 268, 10, 4, 4)]
-ci, hi, co, k, d = LAYERS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
-N = 64
+# c2 conv1..conv3 (N = 64), then c3 conv1..conv3 (N = 16)
+LAYERS = [(3, 284, 16, 6, 1), (16, 278, 32, 5, 2), (32, 268, 10, 4, 4),
+          (3, 580, 50, 6, 1), (50, 572, 50, 3, 4), (50, 560, 8, 7, 8)]
+li = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+ci, hi, co, k, d = LAYERS[li]
+N = 64 if li < 3 else 16
 e = (k - 1) * d + 1
 ho = hi - e + 1
 x = torch.randn(N, ci, hi, hi, device="cuda")

@@ -377,6 +377,15 @@ def run_reference_arm(args, rank):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+def stable_lr(batch, side, mask_frac):
+    """SGD step size that keeps the synthetic training run finite: the loss is a SUM over the
+    masked pixels, so the gradient grows with their count (a fixed 1e-7 diverges to NaN within
+    ~8 c3 steps, and a NaN/overflowing step is a degenerate workload: the fp16-split convs
+    see out-of-range operands and fall back to tf32)."""
+    frac = 1.0 if mask_frac is None else mask_frac
+    return 1e-4 / max(1.0, batch * side * side * frac)
+
+
 def _synthetic(spec, batch, side, mask_frac, seed, dev):
     import torch
     rng = np.random.default_rng(seed)
@@ -429,7 +438,8 @@ def measure_config(text, side, batch, mask_frac, steps=5, warmup=3, seed=7):
         out.update({"forward": px / (ms_fwd / 1e3), "ms_forward": ms_fwd})
         flops = net.conv_flops_per_image()["fwd"] * batch
     else:
-        tr = DataParallelTrainer(plan, batch, side, side, lr=1e-9, use_graph=True)
+        tr = DataParallelTrainer(plan, batch, side, side, lr=stable_lr(batch, side, mask_frac),
+                                 use_graph=True)
         net = tr.net
         tr.load_batch(imgs, tgts, masks)
         ms_train = timed(tr.step)
@@ -598,7 +608,8 @@ def main():
     dpool = [tuple(t.to(dev) for t in p) for p in pool]
     hpool = [tuple(t.pin_memory() for t in p) for p in pool]
 
-    tr = DataParallelTrainer(plan, B, SIDE, SIDE, lr=1e-7, use_graph=not args.no_graph)
+    tr = DataParallelTrainer(plan, B, SIDE, SIDE, lr=stable_lr(B, SIDE, MASK_FRAC),
+                            use_graph=not args.no_graph)
     net = tr.net
     stream = torch.cuda.current_stream()
 

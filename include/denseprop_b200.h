@@ -137,6 +137,14 @@ int dp_conv_fast_supported(int reduce_channels, int out_channels, int k, int d);
 int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float *y, int n,
                          int cin, int h, int w, int cout, int k, int d, int nonlin,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* Same with flags (ABI 5).  DP_FAST_INPUT_FP16_RANGE: the caller vouches that |x| stays well
+ * inside the fp16 range (tanh outputs, images), which allows the fp16-split forward (hi =
+ * RN_fp16(x), lo = RN_fp16(x - hi), kind::f16, fp32 accumulation: ~2^-22 relative, half the
+ * operand feed of 3xTF32).  Without it (and in dp_conv_forward_fast) the forward is 3xTF32. */
+enum dp_fast_flags { DP_FAST_INPUT_FP16_RANGE = 1 };
+int dp_conv_forward_fast_ex(const float *x, const float *wt, const float *b, float *y, int n,
+                            int cin, int h, int w, int cout, int k, int d, int nonlin, int flags,
+                            void *workspace, size_t workspace_bytes, void *stream);
 int dp_conv_backward_data_fast(const float *dy, const float *wt, float *dx, int n, int cout,
                                int ho, int wo, int cin, int k, int d, const float *gate,
                                int gate_kind, void *workspace, size_t workspace_bytes,

@@ -33,7 +33,7 @@ size_t tc_conv_fwd_workspace(int n, int cin, int h, int w, int cout, int k, int 
 size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, int d);
 bool tc_conv_supported(int R, int Q, int l, int d);
 int tc_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
-                    int, int, int, void *, size_t, cudaStream_t);
+                    int, int, int, void *, size_t, cudaStream_t, int flags);
 int tc_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
                           int, const float *, int, void *, size_t, cudaStream_t);
 bool tc_wgrad_supported(int, int, int, int, int, int, int);
@@ -271,7 +271,19 @@ int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float 
     DP_TRY(check_nonlin(nonlin));
     DP_TRY(check_window("dilated conv", h, w, k, d));
     return tc_conv_forward(x, wt, b, y, n, cin, h, w, cout, k, d, nonlin, workspace,
-                           workspace_bytes, (cudaStream_t)stream);
+                           workspace_bytes, (cudaStream_t)stream, 0);
+}
+
+int dp_conv_forward_fast_ex(const float *x, const float *wt, const float *b, float *y, int n,
+                            int cin, int h, int w, int cout, int k, int d, int nonlin, int flags,
+                            void *workspace, size_t workspace_bytes, void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("in channels", cin));
+    DP_TRY(check_pos("out channels", cout));
+    DP_TRY(check_nonlin(nonlin));
+    DP_TRY(check_window("dilated conv", h, w, k, d));
+    return tc_conv_forward(x, wt, b, y, n, cin, h, w, cout, k, d, nonlin, workspace,
+                           workspace_bytes, (cudaStream_t)stream, flags);
 }
 
 int dp_conv_backward_data_fast(const float *dy, const float *wt, float *dx, int n, int cout,

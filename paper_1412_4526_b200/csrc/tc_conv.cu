@@ -142,7 +142,7 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
 // bwd: the data gradient's rotated weights (w is (R = cout, Q = cin, l, l)), lo' scaled by
 // 2^11 (the offset split of the fp16 data gradient: cross products in their own columns)
 __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
-                                    int R, int l, int Npad, int n_ks, int bwd) {
+                                    int R, int l, int Npad, int n_ks, int bwd, int *flag) {
     const int total = n_ks * 2 * Npad * 16;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += gridDim.x * blockDim.x) {
@@ -155,6 +155,7 @@ __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restr
         if (n < Q && c < R)
             v = bwd ? w[(((long long)c * Q + n) * l + (l - 1 - i)) * l + (l - 1 - j)]
                     : w[(((long long)n * R + c) * l + i) * l + j];
+        if (!(fabsf(v) < ptx::F16_SPLIT_MAX)) atomicOr(flag, 1);
         __half hi, lo;
         if (bwd) {
             hi = __float2half_rn(v);
@@ -167,12 +168,13 @@ __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restr
     }
 }
 
-int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, cudaStream_t st) {
+int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, int *flag,
+                cudaStream_t st) {
     const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 15) / 16;
     const int n_ks = n_rc * l * l;
     const int total = n_ks * 2 * Npad * 16;
     tc_pack_weights_f16<<<ceil_div(total, 256), 256, 0, st>>>(w, (__half *)wp, Q, R, l, Npad,
-                                                              n_ks, bwd);
+                                                              n_ks, bwd, flag);
     return check_launch("tc_pack_weights_f16");
 }
 
@@ -192,13 +194,14 @@ size_t tt_conv_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, in
                          int Wo);
 int tt_launch(const float *in, const float *w, const float *bias, float *out, const float *gate,
               int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
-              int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st);
+              int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st,
+              bool f16_ok = false);
 // flattened shared-memory-operand variant (tc_conv_flat.cu), preferred when it applies
 bool tf_conv_supported(int R, int Q, int l, int d);
 size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
                              int Ho, int Wo, bool bwd);
 int tf_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
-                    int, int, int, void *, size_t, cudaStream_t);
+                    int, int, int, void *, size_t, cudaStream_t, bool f16_ok);
 int tf_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
                           int, const float *, int, void *, size_t, cudaStream_t);
 
@@ -816,16 +819,18 @@ size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, in
 
 int tc_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,
                     int h, int wd, int cout, int k, int d, int act, void *ws, size_t ws_bytes,
-                    cudaStream_t st) {
+                    cudaStream_t st, int flags) {
+    const bool f16 = (flags & DP_FAST_INPUT_FP16_RANGE) != 0;
     {
         const int e = (k - 1) * d + 1;
         const size_t t = tt_conv_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
         if (t && ws_bytes >= t)
             return tt_launch(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k,
-                             d, 0, act, 0, false, ws, ws_bytes, st);
+                             d, 0, act, 0, false, ws, ws_bytes, st, f16);
     }
     if (tf_conv_supported(cin, cout, k, d))
-        return tf_conv_forward(x, w, b, y, n, cin, h, wd, cout, k, d, act, ws, ws_bytes, st);
+        return tf_conv_forward(x, w, b, y, n, cin, h, wd, cout, k, d, act, ws, ws_bytes, st,
+                               f16);
     int e = (k - 1) * d + 1;
     return launch_tc(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k, d, 0, act,
                      0, false, ws, ws_bytes, st);

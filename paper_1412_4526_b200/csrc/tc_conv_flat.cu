@@ -47,7 +47,8 @@
 namespace dp {
 
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st);
-int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, cudaStream_t st);
+int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, int *flag,
+                cudaStream_t st);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
 // 14 warps: registers are granted per 4 warps, so 14 warps (as 16) leave 128 registers
@@ -81,6 +82,8 @@ struct TfArgs {
     unsigned long long *trace;  // DP_TC_TRACE: per-unit clock64 stamps of CTA 0 (8 slots)
     const unsigned char *xr;    // relayout planes (TMA-fed mode) or nullptr (loader warps)
     long long plane_recs;       // records per relayout plane
+    const int *exit_if;         // fp16 kernel: exit when its operands tripped the range flag
+    const int *exit_unless;     // its tf32 fallback: run only when they did
 };
 
 // slots: 0/1 loader warp 0 unit start/end, 2/3/4 MMA wait/got/issued, 5/6 epilogue
@@ -125,6 +128,12 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
     __shared__ uint32_t s_tmem;
     __shared__ float s_bias[256];
 
+    // fp16-split launches come in pairs (fp16 kernel, tf32 fallback) gated by the range flag
+    // the fp16 relayout / weight packs set; exactly one of the two does the work (uniform,
+    // before any barrier or TMEM allocation)
+    if ((a.exit_if && *(volatile const int *)a.exit_if) ||
+        (a.exit_unless && !*(volatile const int *)a.exit_unless))
+        return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int MT = a.MT;
     const int units = a.n_rc * a.l;
@@ -547,23 +556,31 @@ bool tf_conv_supported(int R, int Q, int l, int d) {
 __global__ void tc_relayout(const float *__restrict__ in, float4 *__restrict__ xr, int R, int Hin,
                             int Win, int Wv, int pad, int n_rc, long long plane_recs,
                             long long vrecs, long long total);
+template <bool SCALED>
 __global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict__ xr, int R,
                                 int Hin, int Win, int Wv, int pad, int n_rc, long long plane_recs,
-                                long long vrecs, long long total, int scaled_lo);
+                                long long vrecs, long long total, int *flag);
 
 // TMA-fed mode (forward, fp16-split, inputs >= 16 channels): the fp16 loaders were the
 // limit (tools/tf_trace.py, c3 conv2: ~2800 loader vs ~2000 MMA cycles per unit), so the
 // split is done once by a bandwidth-bound relayout pass and units arrive as bulk copies.
 // fp16-split operands: forward of inputs with >= 16 channels (DP_TF_HALF=0: tf32), and the
 // data gradient of deltas with >= 16 channels through the offset split (DP_TF_HALF_BWD=0)
-static bool tf_half(int R, bool bwd) {
+// fp16-split operands for inputs of >= 16 channels: forward when the caller allows it
+// (DP_FAST_INPUT_FP16_RANGE; DP_TF_HALF=0: never), data gradient by default
+// (DP_TF_HALF_BWD=0: never).  Always TMA-fed and always paired with a tf32 fallback launch
+// that runs instead when an operand is outside the split's range (|x| >= 2^15, inf, NaN):
+// c4's relu outputs errors exceeded fp16's 65504.
+static bool tf_half(int R, bool bwd, bool f16_ok) {
+    if (R < 16) return false;
     const char *he = getenv(bwd ? "DP_TF_HALF_BWD" : "DP_TF_HALF");
-    return R >= 16 && !(he && he[0] == '0');
+    if (he && he[0] == '0') return false;
+    return bwd || f16_ok;
 }
 
-static bool tf_relayout_mode(int R, bool bwd) {
+static bool tf_relayout_mode(int R, bool bwd, bool f16_ok) {
     const char *re = getenv("DP_TF_RELAYOUT");
-    return tf_half(R, bwd) && !(re && re[0] == '0');
+    return tf_half(R, bwd, f16_ok) && !(re && re[0] == '0');
 }
 
 static long long tf_plane_recs(const TfPlan &p, int Hin, int Win, int pad, int l, int d, int Ho,
@@ -581,67 +598,35 @@ static size_t tf_weight_bytes(const TfPlan &p, int l) {
                 : (size_t)p.n_rc * l * p.wunit_bytes;
 }
 
-// workspace of the TMA-fed forward (packed weights + relayout planes), 0 when it does not
-// apply; the flat kernel uses it when the caller's workspace covers it
+static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
+
+// workspace of the fp16-split flat conv: [fp16 weights | tf32 fallback weights | range flag
+// (256 B) | fp16 relayout planes]; 0 when it does not apply.  The flat kernel uses it when
+// the caller's workspace covers it (else tf32 alone).
 size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
                              int Ho, int Wo, bool bwd) {
-    if (!tf_relayout_mode(R, bwd) || Ho < 1 || Wo < 1) return 0;
+    // (sized as if fp16 were allowed: the query cannot know the caller's flags)
+    if (!tf_relayout_mode(R, bwd, true) || Ho < 1 || Wo < 1) return 0;
     const int Wv = Win + 2 * pad;
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     const int max_mt = (int)((flat_len + 127) / 128);
     TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, true);
-    if (!p.ok) return 0;
-    const size_t wb = (tf_weight_bytes(p, l) + 255) / 256 * 256;
-    return wb + (size_t)n * p.n_rc * 4 * tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo) * 16;
+    TfPlan q = tf_plan(R, Q, l, d, max_mt, bwd, false);
+    if (!p.ok || !q.ok) return 0;
+    return al256(tf_weight_bytes(p, l)) + al256(tf_weight_bytes(q, l)) + 256 +
+           (size_t)n * p.n_rc * 4 * tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo) * 16;
 }
 
 static int g_tf_sms = 0;
 
-static int tf_launch(const float *in, const float *w, const float *bias, float *out,
-                     const float *gate, int n, int R, int Hin, int Win, int Q, int Ho, int Wo,
-                     int l, int d, int pad, int act, int gate_kind, bool bwd, void *ws,
-                     size_t ws_bytes, cudaStream_t st) {
+// one launch of plan p (fp16 records when half; TMA-fed from xr when given), weights at wp
+static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, const float *bias,
+                  float *out, const float *gate, int n, int R, int Hin, int Win, int Q, int Ho,
+                  int Wo, int l, int d, int pad, int act, int gate_kind, bool bwd,
+                  const unsigned char *xr, long long plane_recs, const int *exit_if,
+                  const int *exit_unless, cudaStream_t st) {
     const int Wv = Win + 2 * pad;
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
-    // short images: fewer M tiles per CTA tile
-    const int max_mt = (int)((flat_len + 127) / 128);
-    bool half = tf_half(R, bwd);
-    TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, half);
-    if (half && !p.ok) {  // e.g. no second accumulator half for a wide data gradient
-        half = false;
-        p = tf_plan(R, Q, l, d, max_mt, bwd, false);
-    }
-    if (!p.ok)
-        return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
-                         R, Q, l, d);
-    const size_t wbytes = tf_weight_bytes(p, l);
-    if (ws == nullptr || ws_bytes < wbytes)
-        return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
-                         wbytes);
-    // TMA-fed when it applies and the workspace also covers the relayout planes
-    const unsigned char *xr = nullptr;
-    long long plane_recs = 0;
-    if (half && tf_relayout_mode(R, bwd) && ((uintptr_t)ws & 255) == 0) {
-        const size_t wb = (wbytes + 255) / 256 * 256;
-        plane_recs = tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo);
-        const size_t need = wb + (size_t)n * p.n_rc * 4 * plane_recs * 16;
-        if (ws_bytes >= need && plane_recs < 0x7fffffffLL) {
-            xr = (const unsigned char *)ws + wb;
-            const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
-            const long long total = (long long)n * p.n_rc * plane_recs;
-            const long long g = (total + 255) / 256;
-            tc_relayout_f16<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
-                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total,
-                bwd ? 1 : 0);
-            const int rc0 = check_launch("tc_relayout_f16");
-            if (rc0) return rc0;
-        }
-    }
-    if (((uintptr_t)ws & 15) != 0)
-        return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
-    int rc = half ? tc_pack_f16(w, ws, Q, R, l, bwd ? 1 : 0, st)
-                  : tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, p.rp, st);
-    if (rc) return rc;
     if (g_tf_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -652,7 +637,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
         return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: image too large");
     TfArgs a;
     a.in = in;
-    a.wpack = (const float *)ws;
+    a.wpack = (const float *)wp;
     a.bias = bias;
     a.out = out;
     a.gate = gate;
@@ -690,6 +675,8 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     a.trace = getenv("DP_TC_TRACE") ? tc_trace_buffer(st) : nullptr;
     a.xr = xr;
     a.plane_recs = plane_recs;
+    a.exit_if = exit_if;
+    a.exit_unless = exit_unless;
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
@@ -727,20 +714,95 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     if (e != cudaSuccess)
         return set_error(DP_ERR_CUDA, "tc_conv_flat: cudaFuncSetAttribute: %s",
                          cudaGetErrorString(e));
-    cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.maxThreadsPerBlock < TF_THREADS)
-        return set_error(DP_ERR_CUDA, "tc_conv_flat: %d registers/thread allow only %d threads",
-                         fa.numRegs, fa.maxThreadsPerBlock);
     kern<<<grid, TF_THREADS, smem, st>>>(a);
     return check_launch("tc_conv_flat_kernel");
 }
 
+// the tf32 flat conv as the fallback of an fp16-split launch: runs only when *flag is set
+// (weights packed into wp, which must hold tf_fallback_bytes)
+size_t tf_fallback_bytes(int R, int Q, int l, int d, bool bwd) {
+    TfPlan q = tf_plan(R, Q, l, d, 0, bwd, false);
+    return q.ok ? al256(tf_weight_bytes(q, l)) : 0;
+}
+int tf_fallback(const float *in, const float *w, const float *bias, float *out, const float *gate,
+                int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
+                int act, int gate_kind, bool bwd, void *wp, const int *flag, cudaStream_t st) {
+    const int Wv = Win + 2 * pad;
+    const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
+    TfPlan q = tf_plan(R, Q, l, d, (int)((flat_len + 127) / 128), bwd, false);
+    if (!q.ok) return set_error(DP_ERR_UNSUPPORTED, "flat conv fallback: unsupported shape");
+    int rc = tc_pack(w, (float *)wp, Q, R, l, bwd ? 1 : 0, q.rp, st);
+    if (rc) return rc;
+    return tf_run(q, false, in, wp, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d, pad, act,
+                  gate_kind, bwd, nullptr, 0, nullptr, flag, st);
+}
+
+static int tf_launch(const float *in, const float *w, const float *bias, float *out,
+                     const float *gate, int n, int R, int Hin, int Win, int Q, int Ho, int Wo,
+                     int l, int d, int pad, int act, int gate_kind, bool bwd, void *ws,
+                     size_t ws_bytes, cudaStream_t st, bool f16_ok = false) {
+    const int Wv = Win + 2 * pad;
+    const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
+    // short images: fewer M tiles per CTA tile
+    const int max_mt = (int)((flat_len + 127) / 128);
+    const TfPlan q = tf_plan(R, Q, l, d, max_mt, bwd, false);  // tf32
+    if (!q.ok)
+        return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: unsupported (R=%d Q=%d k=%d d=%d)",
+                         R, Q, l, d);
+    if (((uintptr_t)ws & 15) != 0)
+        return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
+    // fp16-split (TMA-fed, with the tf32 fallback) when it applies and the workspace holds it
+    if (tf_relayout_mode(R, bwd, f16_ok) && ((uintptr_t)ws & 255) == 0) {
+        const TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, true);
+        const long long plane_recs = p.ok ? tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo) : 0;
+        const size_t wb16 = p.ok ? al256(tf_weight_bytes(p, l)) : 0;
+        const size_t wb32 = al256(tf_weight_bytes(q, l));
+        const size_t need = wb16 + wb32 + 256 + (size_t)n * p.n_rc * 4 * plane_recs * 16;
+        if (p.ok && ws_bytes >= need && plane_recs < 0x7fffffffLL) {
+            unsigned char *w8 = (unsigned char *)ws;
+            int *flag = (int *)(w8 + wb16 + wb32);
+            const unsigned char *xr = w8 + wb16 + wb32 + 256;
+            if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess)
+                return set_error(DP_ERR_CUDA, "flat conv: flag reset failed");
+            int rc = tc_pack_f16(w, w8, Q, R, l, bwd ? 1 : 0, flag, st);
+            if (rc) return rc;
+            const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
+            const long long total = (long long)n * p.n_rc * plane_recs;
+            const long long g = (total + 255) / 256;
+            const int gg = (int)(g < 148 * 64 ? g : 148 * 64);
+            if (bwd)
+                tc_relayout_f16<true><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv, pad,
+                                                          p.n_rc, plane_recs, vrecs, total, flag);
+            else
+                tc_relayout_f16<false><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv, pad,
+                                                           p.n_rc, plane_recs, vrecs, total, flag);
+            rc = check_launch("tc_relayout_f16");
+            if (rc) return rc;
+            rc = tc_pack(w, (float *)(w8 + wb16), Q, R, l, bwd ? 1 : 0, q.rp, st);
+            if (rc) return rc;
+            rc = tf_run(p, true, in, w8, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d, pad,
+                        act, gate_kind, bwd, xr, plane_recs, flag, nullptr, st);
+            if (rc) return rc;
+            return tf_run(q, false, in, w8 + wb16, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo,
+                          l, d, pad, act, gate_kind, bwd, nullptr, 0, nullptr, flag, st);
+        }
+    }
+    const size_t wbytes = tf_weight_bytes(q, l);
+    if (ws == nullptr || ws_bytes < wbytes)
+        return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
+                         wbytes);
+    int rc = tc_pack(w, (float *)ws, Q, R, l, bwd ? 1 : 0, q.rp, st);
+    if (rc) return rc;
+    return tf_run(q, false, in, ws, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d, pad, act,
+                  gate_kind, bwd, nullptr, 0, nullptr, nullptr, st);
+}
+
 int tf_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,
                     int h, int wd, int cout, int k, int d, int act, void *ws, size_t ws_bytes,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool f16_ok) {
     int e = (k - 1) * d + 1;
     return tf_launch(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k, d, 0, act,
-                     0, false, ws, ws_bytes, st);
+                     0, false, ws, ws_bytes, st, f16_ok);
 }
 
 int tf_conv_backward_data(const float *dy, const float *w, float *dx, int n, int cout, int ho,

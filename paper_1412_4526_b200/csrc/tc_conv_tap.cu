@@ -53,6 +53,7 @@ struct TtArgs {
     const float *gate;
     int n_rc, l, d, Q, Npad, QS, LN, MT, S, NR, TR, n_tr;
     int STEP, XR;          // outputs per CTA tile (MT*128 - (l-1)d), exchange rows (128 + (l-1)d)
+    const int *exit_if;    // fp16 launch: exit when the range flag is set (tf32 fallback runs)
     int Wv, Ho, Wo, act, gate_kind;
     long long plane_recs;
     int flat_len, tiles_per_img, total_tiles, HB;
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1) tc_conv_tap_kernel(const TtArgs
     // D' rows, then the next M tile's first (l-1)d rows]
     float *s_x = reinterpret_cast<float *>(smem_raw + a.xoff);
 
+    if (a.exit_if && *(volatile const int *)a.exit_if) return;  // uniform, before any barrier
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int MT = a.MT;
     const int units = a.n_rc * a.n_tr;
@@ -379,12 +381,17 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
 }
 
 // fp16 forms (HALF): records [hi c0-7 | hi c8-15 | lo c0-7 | lo c8-15] per 16-channel chunk
-// scaled_lo: the offset split (ptx::f16_split2_scaled) for deltas of unknown magnitude
+// SCALED: the offset split (ptx::f16_split2_scaled) for deltas of unknown magnitude
+// (compile time: a runtime switch in the conversion loop cost the pass 25 %)
+// flag: set (atomicOr) when any element is outside the fp16-split's safe range (|x| >= 2^15)
+// or not finite -- the fp16 kernel then exits and the tf32 fallback launched after it runs
+template <bool SCALED>
 __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__ in,
                                                        uint4 *__restrict__ xr, int R, int Hin,
                                                        int Win, int Wv, int pad, int n_rc,
                                                        long long plane_recs, long long vrecs,
-                                                       long long total, int scaled_lo) {
+                                                       long long total, int *flag) {
+    bool bad = false;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const long long nrc = idx / plane_recs;
@@ -402,7 +409,8 @@ __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__
             const int c0 = rc * 16 + 2 * q;
             const float v0 = (ok && c0 < R) ? __ldg(src + (2 * q) * cs) : 0.f;
             const float v1 = (ok && c0 + 1 < R) ? __ldg(src + (2 * q + 1) * cs) : 0.f;
-            if (scaled_lo)
+            bad |= !(fabsf(v0) < ptx::F16_SPLIT_MAX) || !(fabsf(v1) < ptx::F16_SPLIT_MAX);
+            if constexpr (SCALED)
                 ptx::f16_split2_scaled(v0, v1, hw[q], lw[q]);
             else
                 ptx::f16_split2(v0, v1, hw[q], lw[q]);
@@ -413,13 +421,19 @@ __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__
         dst[2 * plane_recs] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         dst[3 * plane_recs] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
     }
+    if (bad) atomicOr(flag, 1);
 }
+
+template __global__ void tc_relayout_f16<false>(const float *, uint4 *, int, int, int, int, int,
+                                                int, long long, long long, long long, int *);
+template __global__ void tc_relayout_f16<true>(const float *, uint4 *, int, int, int, int, int,
+                                               int, long long, long long, long long, int *);
 
 // weights W(q, r, i, j) -> per (16-channel chunk rc, tap row i): [hi | lo] tiles of LN rows
 // (row n = j*QS + q) x K = 16 halves: element (n, k) at (n>>3)*256 + (k>>3)*128 + (n&7)*16 +
 // (k&7)*2 (forward only)
 __global__ void tc_pack_tap_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
-                                int R, int l, int QS, int LN, int n_rc) {
+                                int R, int l, int QS, int LN, int n_rc, int *flag) {
     const long long total = (long long)n_rc * l * 2 * LN * 16;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -433,6 +447,7 @@ __global__ void tc_pack_tap_f16(const float *__restrict__ w, __half *__restrict_
         const int j = n / QS, qo = n - j * QS;
         const int c = rc * 16 + k;
         const float v = (j < l && qo < Q && c < R) ? w[(((long long)qo * R + c) * l + i) * l + j] : 0.f;
+        if (!(fabsf(v) < ptx::F16_SPLIT_MAX)) atomicOr(flag, 1);
         __half hi, lo;
         ptx::f16_split(v, hi, lo);
         const long long byte = (ri * 2 + hl) * (long long)LN * 32 + (n >> 3) * 256 + (k >> 3) * 128 +
@@ -548,15 +563,25 @@ size_t tt_conv_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, in
     return wb + (size_t)n * p.n_rc * 4 * plane_recs * 16;
 }
 
+// the flat kernel's tf32 fallback of an fp16-split launch (tc_conv_flat.cu)
+size_t tf_fallback_bytes(int R, int Q, int l, int d, bool bwd);
+int tf_fallback(const float *in, const float *w, const float *bias, float *out, const float *gate,
+                int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
+                int act, int gate_kind, bool bwd, void *wp, const int *flag, cudaStream_t st);
+
 static int g_tt_sms = 0;
 
 int tt_launch(const float *in, const float *w, const float *bias, float *out, const float *gate,
               int n, int R, int Hin, int Win, int Q, int Ho, int Wo, int l, int d, int pad,
-              int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st) {
-    // fp16-split operands for the forward of inputs with >= 16 channels (DP_TF_HALF=0: tf32);
-    // the workspace query stays tf32-sized (a superset)
+              int act, int gate_kind, bool bwd, void *ws, size_t ws_bytes, cudaStream_t st,
+              bool f16_ok) {
+    // fp16-split operands for the forward of inputs with >= 16 channels the caller vouches
+    // are in fp16 range (DP_FAST_INPUT_FP16_RANGE; DP_TF_HALF=0: tf32); the workspace query
+    // stays tf32-sized (a superset)
     const char *he = getenv("DP_TF_HALF");
-    const bool half = !bwd && R >= 16 && !(he && he[0] == '0');
+    bool half = f16_ok && !bwd && R >= 16 && !(he && he[0] == '0');
+    const size_t fb_bytes = half ? tf_fallback_bytes(R, Q, l, d, false) : 0;
+    if (half && fb_bytes == 0) half = false;
     TtPlan p = tt_plan(R, Q, l, d, 0, half);
     if (!p.ok)
         return set_error(DP_ERR_UNSUPPORTED, "tap-stacked conv: unsupported (R=%d Q=%d k=%d d=%d)",
@@ -564,8 +589,16 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     long long plane_recs, flat_len;
     int tiles_per_img;
     tt_relayout_recs(Hin, Win, pad, l, d, p, plane_recs, tiles_per_img, flat_len, Ho, Wo);
+    if (half && (size_t)((p.wbytes + 255) / 256 * 256) + (size_t)n * p.n_rc * 4 * plane_recs * 16 +
+                        256 + fb_bytes > ws_bytes) {  // no room for the fp16 layout: tf32
+        half = false;
+        p = tt_plan(R, Q, l, d, 0, false);
+        tt_relayout_recs(Hin, Win, pad, l, d, p, plane_recs, tiles_per_img, flat_len, Ho, Wo);
+    }
     const size_t wb = (p.wbytes + 255) / 256 * 256;
-    const size_t need = wb + (size_t)n * p.n_rc * 4 * plane_recs * 16;
+    const size_t planes = (size_t)n * p.n_rc * 4 * plane_recs * 16;
+    // fp16: [weights | planes | range flag (256 B) | the flat tf32 fallback's weights]
+    const size_t need = wb + planes + (half ? 256 + fb_bytes : 0);
     if (ws == nullptr || ws_bytes < need)
         return set_error(DP_ERR_ARG, "tap-stacked conv: workspace %zu < %zu bytes", ws_bytes, need);
     if (((uintptr_t)ws & 255) != 0)
@@ -574,12 +607,15 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
         return set_error(DP_ERR_UNSUPPORTED, "tap-stacked conv: image too large");
     float *wp = (float *)ws;
     float4 *xr = (float4 *)((unsigned char *)ws + wb);
+    int *flag = half ? (int *)((unsigned char *)ws + wb + planes) : nullptr;
+    if (half && cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess)
+        return set_error(DP_ERR_CUDA, "tap-stacked conv: flag reset failed");
     {
         const long long total = (long long)p.n_rc * l * 2 * p.LN * 8;
         long long g = (total + 255) / 256;
         if (half)
             tc_pack_tap_f16<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, (__half *)wp, Q, R, l,
-                                                                        p.QS, p.LN, p.n_rc);
+                                                                        p.QS, p.LN, p.n_rc, flag);
         else
             tc_pack_tap<<<(int)(g < 4096 ? g : 4096), 256, 0, st>>>(w, wp, Q, R, l, p.QS, p.LN,
                                                                     p.n_rc, bwd ? 1 : 0);
@@ -592,8 +628,8 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
         const long long total = (long long)n * p.n_rc * plane_recs;
         long long g = (total + 255) / 256;
         if (half)
-            tc_relayout_f16<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
-                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total, 0);
+            tc_relayout_f16<false><<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
+                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total, flag);
         else
             tc_relayout<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
                 in, xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);
@@ -623,6 +659,7 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     a.S = p.S;
     a.STEP = p.STEP;
     a.XR = p.XR;
+    a.exit_if = flag;
     a.NR = p.NR;
     a.TR = p.TR;
     a.n_tr = p.n_tr;
@@ -653,7 +690,11 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
     if (e != cudaSuccess)
         return set_error(DP_ERR_CUDA, "tc_conv_tap: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     kern<<<grid, TT_THREADS, smem, st>>>(a);
-    return check_launch("tc_conv_tap_kernel");
+    const int rc = check_launch("tc_conv_tap_kernel");
+    if (rc || !half) return rc;
+    // fp16 operands out of range (flag set): the flat tf32 kernel redoes the layer
+    return tf_fallback(in, w, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d, pad, act,
+                       gate_kind, false, (unsigned char *)ws + wb + planes + 256, flag, st);
 }
 
 }  // namespace dp

@@ -252,6 +252,9 @@ __device__ __forceinline__ void f16_split2(float a, float b, uint32_t &hi, uint3
 // represented to ~2^-23 relative above 2^-13 and to ~2^-35 absolute below (vs ~2^-25 with an
 // unscaled lo).
 constexpr float F16_LO_SCALE = 2048.f;
+// operands at or above this magnitude (or not finite) send an fp16-split convolution to its
+// tf32 fallback (hi = RN_fp16 overflows at 65520)
+constexpr float F16_SPLIT_MAX = 32768.f;
 __device__ __forceinline__ void f16_split2_scaled(float a, float b, uint32_t &hi, uint32_t &lo) {
     const __half2 h = __floats2half2_rn(a, b);
     const float2 hf = __half22float2(h);

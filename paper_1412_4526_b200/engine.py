@@ -141,12 +141,16 @@ class ops:
         return int(_lib_dev().dp_conv_backward_data_fast_workspace(n, co, ho, wo, ci, k, d))
 
     @staticmethod
-    def conv_forward_fast(x, w, b, y, k, d, nonlin, ws):
+    def conv_forward_fast(x, w, b, y, k, d, nonlin, ws, fp16_range=False):
+        """fp16_range: the caller vouches |x| stays well inside fp16 range (tanh outputs,
+        images) -- allows the fp16-split forward (DP_FAST_INPUT_FP16_RANGE)."""
         with _Rec('conv_forward_tc', 2, 'tensor', 2 * y.numel() * x.shape[1] * k * k):
             n, ci, h, wd = x.shape
-            _lib.check(_lib_dev().dp_conv_forward_fast(
+            flags = _lib.DP_FAST_INPUT_FP16_RANGE if fp16_range else 0
+            _lib.check(_lib_dev().dp_conv_forward_fast_ex(
                 _ptr(x), _ptr(w), _ptr(b), _ptr(y), n, ci, h, wd, w.shape[0], k, d, nonlin,
-                _ptr(ws), ws.numel() * ws.element_size(), _stream()), "conv_forward_fast")
+                flags, _ptr(ws), ws.numel() * ws.element_size(), _stream()),
+                "conv_forward_fast")
 
     @staticmethod
     def conv_backward_data_fast(dy, w, dx, k, d, ws, gate=None, gate_kind=_lib.DP_IDENTITY):
@@ -599,6 +603,16 @@ class DenseNet:
     def _group_input(self, gi):
         return self.x0 if gi == 0 else self.acts[gi - 1]
 
+    def _fp16_input(self, gi):
+        """Is group gi's input bounded well inside fp16 range by construction?  The padded
+        image (group 0) and tanh outputs (|x| <= 1) are; relu / identity outputs are not."""
+        if gi == 0:
+            return True
+        prev = self.groups[gi - 1]
+        if prev.act == "tanh":
+            return True
+        return isinstance(prev.op, NonlinLayerSpec) and prev.op.kind == "tanh"
+
     def _view(self, buf, shape):
         n = int(np.prod(shape))
         return buf[:n].view(shape)
@@ -645,7 +659,7 @@ class DenseNet:
                 wt, b = self.params[g.first]
                 if self.tc.get(gi, (False, False))[0]:
                     ops.conv_forward_fast(x, wt, b, y, op.base.kernel_size, op.dilation, act,
-                                          self._tc_ws)
+                                          self._tc_ws, fp16_range=self._fp16_input(gi))
                 else:
                     ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
             elif isinstance(op, DilatedPool):

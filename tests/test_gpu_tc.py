@@ -59,12 +59,14 @@ def force_env(monkeypatch):
     return _set
 
 
+@pytest.mark.parametrize("fp16", [False, True])
 @pytest.mark.parametrize("kernel", ["flat", "tap", "halo", "flat_packlast"])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("act", [0, 1, 2])
-def test_tc_forward_matches_exact(shape, act, kernel, force_env):
+def test_tc_forward_matches_exact(shape, act, kernel, fp16, force_env):
     """kernel="tap" passes the shape-aware workspace, which selects the tap-stacked kernel
-    where it applies (else the flat one runs again)."""
+    where it applies (else the flat one runs again); fp16: the input is declared in fp16
+    range, selecting the fp16-split forward for inputs of >= 16 channels."""
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
@@ -84,7 +86,7 @@ def test_tc_forward_matches_exact(shape, act, kernel, force_env):
     ops.conv_forward(x.double(), wt.double(), b.double(), y_ref, k, d, act)
     nb = ops.fast_workspace(ci, co, k) if kernel != "tap" else ops.fwd_fast_workspace(x, co, k, d)
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
-    ops.conv_forward_fast(x, wt, b, y, k, d, act, ws)
+    ops.conv_forward_fast(x, wt, b, y, k, d, act, ws, fp16_range=fp16)
     torch.cuda.synchronize()
     assert torch.isfinite(y).all()
     assert _rel(y, y_ref) < TOL
@@ -290,11 +292,12 @@ def test_layer0_pitched_delta_path(p, d):
     assert torch.equal(dw1, dw2) and torch.equal(db1, db2)
 
 
-@pytest.mark.parametrize("scale", [1e-3, 1e-6, 1e3])
+@pytest.mark.parametrize("scale", [1e-3, 1e-6, 1e3, 1e5])
 def test_tc_backward_data_fp16_offset_split_range(scale):
     """The fp16 data gradient (offset split, lo' = RN((dy - hi) * 2^11), cross products in
     their own accumulator half) stays within the north-star bound for deltas far from 1 in
-    magnitude -- where an unscaled fp16 lo would fall into subnormals."""
+    magnitude -- where an unscaled fp16 lo would fall into subnormals; at 1e5 (beyond fp16's
+    range) the relayout's range flag sends the layer to the tf32 fallback launch."""
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = 2, 50, 50, 3, 4, 60, 64
@@ -311,3 +314,27 @@ def test_tc_backward_data_fp16_offset_split_range(scale):
     torch.cuda.synchronize()
     assert torch.isfinite(dx).all()
     assert _rel(dx, ref) < TOL
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e5])
+@pytest.mark.parametrize("shape", [(2, 50, 50, 3, 4, 60, 64), (1, 50, 8, 7, 8, 90, 96)])
+def test_tc_forward_fp16_range_fallback(shape, scale):
+    """Inputs declared in fp16 range but exceeding it (1e5): the fp16-split forward's range
+    flag makes its kernel exit and the paired tf32 launch compute the layer (flat and
+    tap-stacked paths) -- results within the bound either way."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    rng = np.random.default_rng(5)
+    x = _t((rng.uniform(-1, 1, (n, ci, h, w)) * scale).astype(np.float32))
+    wt = _t((rng.uniform(-0.5, 0.5, (co, ci, k, k)) * 4.0 / np.sqrt(ci * k * k)).astype(np.float32))
+    b = _t(rng.uniform(-0.5, 0.5, co).astype(np.float32))
+    e = (k - 1) * d + 1
+    ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda", dtype=torch.float64)
+    ops.conv_forward(x.double(), wt.double(), b.double(), ref, k, d, 0)
+    y = torch.full(ref.shape, float("nan"), device="cuda")
+    ws = torch.empty(ops.fwd_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+    ops.conv_forward_fast(x, wt, b, y, k, d, 0, ws, fp16_range=True)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
+    assert _rel(y, ref) < TOL

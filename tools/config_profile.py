@@ -19,7 +19,8 @@ side = int(sys.argv[2]) if len(sys.argv) > 2 else {"c2": 256, "c3": 512, "c4": 1
 batch = int(sys.argv[3]) if len(sys.argv) > 3 else {"c2": 64, "c3": 4, "c4": 2}[name]
 spec = dp.parse_spec(text)
 plan = dp.compile_plan(spec)
-tr = DataParallelTrainer(plan, batch, side, side, lr=1e-9, use_graph=False)
+tr = DataParallelTrainer(plan, batch, side, side, lr=bench.stable_lr(batch, side, 0.01),
+                        use_graph=False)
 imgs = torch.rand((batch, spec.input_channels, side, side), device="cuda") - 0.5
 tgts = torch.rand((batch, spec.output_channels, side, side), device="cuda")
 masks = (torch.rand((batch, side, side), device="cuda") < 0.01).to(torch.uint8)

@@ -3,7 +3,8 @@ environment settings in one process (the switches are read per call):
 
     python tools/conv_ab.py fwd n,ci,co,k,d,h "DP_TT_TR=1" "DP_TT_TR=2" "DP_TT_QS16=1" ...
 
-AB_ACT=<code> fuses a nonlinearity into the forward (default 0: none, as in front of a pool).
+AB_ACT=<code> fuses a nonlinearity into the forward (default 0: none, as in front of a pool);
+AB_FP16=0 does not declare the forward input in fp16 range (default: declared, |x| <= 1).
 Prints CUDA-event ms per call for the default and each setting, and the normwise difference
 of each output from the default one."""
 import os
@@ -37,7 +38,9 @@ def main():
             out = torch.empty((n, co, ho, ho), device="cuda")
             ws = torch.empty(ops.fwd_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
             act = int(os.environ.get("AB_ACT", "0"))  # fused nonlinearity code (0 = none)
-            f = lambda: ops.conv_forward_fast(x, w, b, out, k, d, act, ws)  # noqa: E731
+            f16 = os.environ.get("AB_FP16", "1") == "1"  # input declared in fp16 range
+            f = lambda: ops.conv_forward_fast(x, w, b, out, k, d, act, ws,  # noqa: E731
+                                              fp16_range=f16)
         else:
             out = torch.empty((n, ci, h, h), device="cuda")
             ws = torch.empty(ops.bwd_fast_workspace(dy, ci, k, d), dtype=torch.uint8,

@@ -596,6 +596,13 @@ static inline dim3 pool_grid(long long planes, long long pixels) {
 }
 
 
+// pool_stream.cu: warp-streaming fp32 / uint8-code kernels; -1 = shape not covered
+int maxpool_forward_stream(const float *x, float *y, void *arg, int arg_bytes, long long planes,
+                           int h, int w, int p, int d, int act, cudaStream_t st);
+int maxpool_backward_stream(const float *dy, const void *arg, int arg_bytes, float *dx,
+                            long long planes, int ho, int wo, int p, int d, int hi, int wi,
+                            const float *gate, int gate_kind, int wd, cudaStream_t st);
+
 template <typename T>
 int maxpool_forward_t(const T *x, T *y, void *arg, int arg_bytes, int n, int c, int h, int w,
                       int p, int d, int act, cudaStream_t st) {
@@ -603,6 +610,11 @@ int maxpool_forward_t(const T *x, T *y, void *arg, int arg_bytes, int n, int c, 
     int ho = h - e + 1, wo = w - e + 1;
     long long planes = (long long)n * c;
     if (planes == 0 || ho <= 0 || wo <= 0) return DP_OK;
+    if constexpr (sizeof(T) == 4) {
+        const int rc = maxpool_forward_stream((const float *)x, (float *)y, arg, arg_bytes,
+                                              planes, h, w, p, d, act, st);
+        if (rc >= 0) return rc;
+    }
     if constexpr (sizeof(T) == 4) if (sp_use<T>(p, d, true)) {
         const dim3 g = sp_grid(wo, ho, planes);
         const size_t smem = sp_smem(p, d, sizeof(T), 0, true);
@@ -655,6 +667,12 @@ int maxpool_backward_t(const T *dy, const void *arg, int arg_bytes, T *dx, int n
     const int Wd = dx_pitch > 0 ? dx_pitch : wi;
     long long planes = (long long)n * c;
     if (planes == 0 || hi <= 0 || wi <= 0) return DP_OK;
+    if constexpr (sizeof(T) == 4) {
+        const int rc = maxpool_backward_stream((const float *)dy, arg, arg_bytes, (float *)dx,
+                                               planes, ho, wo, p, d, hi, wi, (const float *)gate,
+                                               gate_kind, Wd, st);
+        if (rc >= 0) return rc;
+    }
     if constexpr (sizeof(T) == 4) if (sp_use<T>(p, d, false)) {
         const dim3 g = sp_grid(wi, hi, planes);
         const size_t smem = sp_smem(p, d, sizeof(T), 1, false);

@@ -91,7 +91,12 @@ POOL_SHAPES = [(4, 2, 1, 40, 41), (3, 3, 2, 33, 35), (2, 8, 1, 40, 40), (5, 2, 1
                (2, 4, 1, 150, 300), (2, 8, 1, 99, 270), (2, 5, 3, 90, 170), (3, 2, 4, 70, 290),
                (1, 7, 8, 80, 400), (1, 9, 1, 40, 50), (1, 3, 25, 60, 60),
                # d = 1, p = 3..8: the vectorised kernels (4-column groups, ragged tile edges)
-               (2, 3, 1, 50, 77), (3, 5, 1, 45, 140), (2, 6, 1, 37, 131), (1, 7, 1, 70, 263)]
+               (2, 3, 1, 50, 77), (3, 5, 1, 45, 140), (2, 6, 1, 37, 131), (1, 7, 1, 70, 263),
+               # output widths of 4k: the warp-streaming kernels (pool_stream.cu) forward and
+               # backward, several 64-row items and column strips, halos 1..16
+               (2, 4, 1, 150, 303), (2, 2, 4, 140, 264), (2, 2, 16, 90, 276),
+               (2, 3, 8, 100, 272), (2, 4, 4, 80, 140), (2, 3, 1, 70, 130), (2, 2, 2, 66, 258),
+               (2, 2, 8, 70, 136), (3, 4, 2, 67, 70), (2, 2, 1, 129, 253), (1, 4, 1, 200, 579)]
 
 
 @pytest.mark.parametrize("shape", POOL_SHAPES)
@@ -129,6 +134,24 @@ def test_pool_nan_signed_zero(K, p, d):
     assert np.array_equal(arg, arg2)
     dy = rng.uniform(-1, 1, y.shape).astype(np.float32)
     h, w = x.shape[1:]
+    assert np.array_equal(K.maxpool_backward(dy, arg, p, d, h, w).view(np.uint32),
+                          kernels_c.maxpool_backward(dy, arg, p, d, h, w, 4).view(np.uint32))
+
+
+@pytest.mark.parametrize("p,d", [(2, 1), (4, 1), (2, 4), (3, 2), (2, 16)])
+def test_pool_stream_nan_signed_zero(K, p, d):
+    # the same special values through the warp-streaming kernels (output width 4k)
+    rng = np.random.default_rng(p * 100 + d)
+    w = 144 + (p - 1) * d
+    x = rng.choice(np.array([0.0, -0.0, 1.0, -1.0, np.nan, np.inf, -np.inf], np.float32),
+                   size=(2, 90, w))
+    x[1, :20, :40] = np.nan
+    y, arg = K.maxpool_forward(x, p, d)
+    y2, arg2 = kernels_c.maxpool_forward(x, p, d, 4)
+    assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
+    assert np.array_equal(arg, arg2)
+    dy = rng.choice(np.array([0.0, -0.0, 0.5, -0.25, 1e-30], np.float32), size=y.shape)
+    h = x.shape[1]
     assert np.array_equal(K.maxpool_backward(dy, arg, p, d, h, w).view(np.uint32),
                           kernels_c.maxpool_backward(dy, arg, p, d, h, w, 4).view(np.uint32))
 

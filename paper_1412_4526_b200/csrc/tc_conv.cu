@@ -141,18 +141,31 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
 // (n>>3)*256 + (k>>3)*128 + (n&7)*16 + (k&7)*2 -- the same 64 * Npad bytes per K step.
 // bwd: the data gradient's rotated weights (w is (R = cout, Q = cin, l, l)), lo' scaled by
 // 2^11 (the offset split of the fp16 data gradient: cross products in their own columns)
+// rp > 0: one tap-packed chunk of rp <= 8 channels (tp = 16 / rp column taps per K step,
+// slot k = t*rp + c <-> (c, j = g*tp + t), G = ceil(l / tp) K steps per tap row)
 __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
-                                    int R, int l, int Npad, int n_ks, int bwd, int *flag) {
+                                    int R, int l, int Npad, int n_ks, int bwd, int *flag,
+                                    int rp) {
     const int total = n_ks * 2 * Npad * 16;
+    const int tp = rp ? 16 / rp : 1, G = (l + tp - 1) / tp;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += gridDim.x * blockDim.x) {
         const int k = idx & 15;
         const int n = (idx >> 4) % Npad;
         const int hl = (idx / (16 * Npad)) & 1;
         const int ks = idx / (32 * Npad);
-        const int j = ks % l, i = (ks / l) % l, c = (ks / (l * l)) * 16 + k;
+        int j, i, c;
+        bool slot_ok = true;
+        if (rp) {
+            i = ks / G;
+            c = k % rp;
+            j = (ks % G) * tp + k / rp;
+            slot_ok = k < rp * tp && j < l;
+        } else {
+            j = ks % l, i = (ks / l) % l, c = (ks / (l * l)) * 16 + k;
+        }
         float v = 0.f;
-        if (n < Q && c < R)
+        if (n < Q && c < R && slot_ok)
             v = bwd ? w[(((long long)c * Q + n) * l + (l - 1 - i)) * l + (l - 1 - j)]
                     : w[(((long long)n * R + c) * l + i) * l + j];
         if (!(fabsf(v) < ptx::F16_SPLIT_MAX)) atomicOr(flag, 1);
@@ -169,12 +182,13 @@ __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restr
 }
 
 int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, int *flag,
-                cudaStream_t st) {
+                cudaStream_t st, int rp) {
     const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 15) / 16;
-    const int n_ks = n_rc * l * l;
+    const int tp = rp ? 16 / rp : 1;
+    const int n_ks = rp ? l * ((l + tp - 1) / tp) : n_rc * l * l;  // rp: one chunk
     const int total = n_ks * 2 * Npad * 16;
     tc_pack_weights_f16<<<ceil_div(total, 256), 256, 0, st>>>(w, (__half *)wp, Q, R, l, Npad,
-                                                              n_ks, bwd, flag);
+                                                              n_ks, bwd, flag, rp);
     return check_launch("tc_pack_weights_f16");
 }
 
@@ -801,8 +815,9 @@ size_t tc_conv_fwd_workspace(int n, int cin, int h, int wd, int cout, int k, int
     const size_t t = tt_conv_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1);
     const size_t w = tc_conv_workspace(cin, cout, k);
     // the flat kernel's TMA-fed forward (relayout planes) where the tap-stacked one is not used
+    // (also when the tap kernel applies: it declines shapes at launch, see tt_launch)
     const size_t f =
-        t ? 0 : tf_relayout_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1, false);
+        tf_relayout_workspace(n, cin, h, wd, cout, k, d, 0, h - e + 1, wd - e + 1, false);
     size_t m = t > w ? t : w;
     return f > m ? f : m;
 }
@@ -811,8 +826,8 @@ size_t tc_conv_bwd_workspace(int n, int cout, int ho, int wo, int cin, int k, in
     const int e = (k - 1) * d + 1;
     const size_t t = tt_conv_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1, wo + e - 1);
     const size_t w = tc_conv_workspace(cout, cin, k);
-    const size_t f = t ? 0 : tf_relayout_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1,
-                                                   wo + e - 1, true);
+    const size_t f = tf_relayout_workspace(n, cout, ho, wo, cin, k, d, e - 1, ho + e - 1,
+                                           wo + e - 1, true);
     size_t m = t > w ? t : w;
     return f > m ? f : m;
 }

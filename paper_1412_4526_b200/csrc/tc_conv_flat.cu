@@ -48,7 +48,7 @@ namespace dp {
 
 int tc_pack(const float *w, float *wp, int Q, int R, int l, int bwd, int rp, cudaStream_t st);
 int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, int *flag,
-                cudaStream_t st);
+                cudaStream_t st, int rp = 0);
 unsigned long long *tc_trace_buffer(cudaStream_t st);
 
 // 14 warps: registers are granted per 4 warps, so 14 warps (as 16) leave 128 registers
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint64_t ufull[TF_MAX_HB], uempty[TF_MAX_HB], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
-    __shared__ float s_bias[256];
+    __shared__ __align__(16) float s_bias[256];
 
     // fp16-split launches come in pairs (fp16 kernel, tf32 fallback) gated by the range flag
     // the fp16 relayout / weight packs set; exactly one of the two does the work (uniform,
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull[b], 1);
-            ptx::mbar_init(&tempty[b], TF_EPI_WARPS);
+            ptx::mbar_init(&tempty[b], a.xr ? 2 * TF_EPI_WARPS : TF_EPI_WARPS);
         }
         ptx::mbar_fence_init();
     }
@@ -157,7 +157,11 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
     ptx::tc_fence_after();
     const uint32_t tmem = s_tmem;
 
-    if (a.xr && warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
+    // TMA-fed: one producer thread; warps TF_LOAD_WARP0 + 1..4 join the epilogue (a second
+    // group taking alternate 16-column chunks: a single group of 4 warps, latency bound at
+    // ~950 cycles per chunk, set the pace of the narrow-K first layer -- tools/tf_trace.py)
+    const bool epi2 = a.xr && warp > TF_LOAD_WARP0 && warp <= TF_LOAD_WARP0 + TF_EPI_WARPS;
+    if (a.xr && warp == TF_LOAD_WARP0) {
         // ====================== TMA-fed producer (relayout planes) ======================
         // the unit's four record planes are contiguous ranges of the pre-split relayout
         // (tc_relayout / tc_relayout_f16): four bulk copies + the weight unit, one expect_tx
@@ -175,7 +179,9 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         ptx::mbar_wait(&uempty[b], uph ^ 1);
                         TF_TRACE(a, gu, 0, true);
                         unsigned char *ub = smem_raw + (size_t)b * a.ubytes;
-                        ptx::mbar_expect_tx(&ufull[b], 4 * a.plane_bytes + a.wunit_bytes);
+                        const bool pk = RP > 0 && rc == a.n_rc - 1;  // tap-packed last chunk
+                        const uint32_t wub = pk ? a.wunit_pk : a.wunit_bytes;
+                        ptx::mbar_expect_tx(&ufull[b], 4 * a.plane_bytes + wub);
                         const long long rec0 = f0 + (long long)i * a.d * a.Wv;
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
@@ -183,10 +189,9 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                           pl + ((size_t)q * a.plane_recs + rec0) * 16,
                                           a.plane_bytes, &ufull[b]);
                         const unsigned char *ws =
-                            wsrc + ((size_t)rc * a.l + i) * a.wunit_bytes;
-                        for (uint32_t off = 0; off < a.wunit_bytes; off += 32768u) {
-                            const uint32_t nb =
-                                a.wunit_bytes - off < 32768u ? a.wunit_bytes - off : 32768u;
+                            wsrc + (size_t)rc * a.l * a.wunit_bytes + (size_t)i * wub;
+                        for (uint32_t off = 0; off < wub; off += 32768u) {
+                            const uint32_t nb = wub - off < 32768u ? wub - off : 32768u;
                             ptx::bulk_g2s(ub + a.halo_bytes + off, ws + off, nb, &ufull[b]);
                         }
                         TF_TRACE(a, gu, 1, true);
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
             }
         }
         __syncwarp();
-    } else if (warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
+    } else if (!a.xr && warp >= TF_LOAD_WARP0 && warp < TF_MMA_WARP) {
         // ================================ loaders ================================
         const int lw = (warp - TF_LOAD_WARP0) % TF_LGW, grp = (warp - TF_LOAD_WARP0) / TF_LGW;
         const long long plane_in = (long long)a.Hin * a.Win;
@@ -408,9 +413,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                 tph ^= 1;
             }
         }
-    } else {
+    } else if (warp < TF_EPI_WARPS || epi2) {
         // ================================ epilogue ================================
         const int q = warp & 3;
+        const int eg = epi2 ? 1 : 0, neg = a.xr ? 2 : 1;  // epilogue group, groups
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const long long ostride = (long long)a.Ho * a.Wo;
         int buf = 0, gu = 0;
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                 const long long pix = img_off + (long long)u * a.Wo + v;
                 const uint32_t dcol =
                     tmem + lane_off + (uint32_t)((buf * MT + mt) * a.acc_cols);
-                for (int o0 = 0; o0 < a.Npad; o0 += 16) {
+                for (int o0 = 16 * eg; o0 < a.Npad; o0 += 16 * neg) {
                     uint32_t r[16], r2[16];
                     ptx::tmem_ld16(dcol + o0, r);
                     if (STACKED) ptx::tmem_ld16(dcol + a.Npad + o0, r2);
@@ -444,7 +450,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                          ? __ldg(a.gate + off0 + t * ostride) : 0.f;
                     } else {
 #pragma unroll
-                        for (int t = 0; t < 16; ++t) aux[t] = s_bias[o0 + t];
+                        for (int t = 0; t < 16; t += 4) {
+                            const float4 b4 = *reinterpret_cast<const float4 *>(s_bias + o0 + t);
+                            aux[t] = b4.x, aux[t + 1] = b4.y, aux[t + 2] = b4.z, aux[t + 3] = b4.w;
+                        }
                     }
                     ptx::tmem_wait_ld();
                     if (!inside) continue;
@@ -483,7 +492,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
 // host side
 // --------------------------------------------------------------------------------
 struct TfPlan {
-    int Npad, n_rc, MT, acc_cols, NR, HB, rp, G;
+    int Npad, n_rc, MT, acc_cols, NR, HB, rp, G, tp;
     bool stacked, ok;
     uint32_t plane_bytes, halo_bytes, wunit_bytes, wunit_pk, ubytes;
 };
@@ -499,11 +508,17 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd, bool hal
     // gradient 0.76 -> 0.84 ms): the packed units' loads, not their MMAs, set the pace.
     const int rem = R - (p.n_rc - 1) * 8;
     (void)bwd;
-    p.rp = (!half && rem <= 4 && l > 1 && (p.n_rc == 1 || getenv("DP_TF_PACK_LAST")) &&
-            !getenv("DP_TF_NOPACK"))
-               ? rem
-               : 0;
-    p.G = p.rp ? (l + 8 / p.rp - 1) / (8 / p.rp) : l;
+    // fp16-split records hold 16 slots: inputs of <= 8 channels pack 16 / R column taps
+    // (c3's 8-channel head data gradient: 4 K steps per tap row instead of 7 tf32 ones)
+    if (half)
+        p.rp = (R <= 8 && l > 1 && !getenv("DP_TF_NOPACK")) ? R : 0;
+    else
+        p.rp = (rem <= 4 && l > 1 && (p.n_rc == 1 || getenv("DP_TF_PACK_LAST")) &&
+                !getenv("DP_TF_NOPACK"))
+                   ? rem
+                   : 0;
+    p.tp = p.rp ? (half ? 16 : 8) / p.rp : 1;
+    p.G = p.rp ? (l + p.tp - 1) / p.tp : l;
     // Stacked ([W_hi | W_lo] in one N = 2 Npad MMA) saves an MMA per K step but doubles the
     // accumulator columns, halving the M tiles per CTA tile.  Wide inputs (>= 4 channel
     // chunks) are loader / feed bound, not MMA bound, and gain more from the extra M tiles
@@ -561,6 +576,113 @@ __global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict_
                                 int Hin, int Win, int Wv, int pad, int n_rc, long long plane_recs,
                                 long long vrecs, long long total, int *flag);
 
+// NCHW (n, R <= 4, Hin, Win) -> four planes of tap-packed 16-byte records over the virtual
+// grid (the loaders' RP layout: slot t*R + c of record f = x[c] at virtual flat index
+// f + t*d, TP = 8 / R column taps, zeros outside the input):
+// [hi s0-3 | hi s4-7 | lo s0-3 | lo s4-7], hi = raw fp32 bits, lo = x - trunc_tf32(x).
+// The packed chunk's loaders were the limit of the 3-channel first layers (ncu, c3 conv1:
+// 28 % of the instructions at the record loads, 10 % at the flat-index divide).
+__global__ void __launch_bounds__(256) tc_relayout_pk(const float *__restrict__ in,
+                                                      float4 *__restrict__ xr, int R, int Hin,
+                                                      int Win, int Wv, int pad, int d,
+                                                      long long plane_recs, long long vrecs,
+                                                      long long total) {
+    const int TP = 8 / R;
+    const long long cs = (long long)Hin * Win;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long n = idx / plane_recs;
+        const long long f = idx - n * plane_recs;
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (t >= TP) break;
+            const long long ff = f + (long long)t * d;
+            const long long yv = ff / Wv;
+            const int y = (int)yv - pad, x = (int)(ff - yv * Wv) - pad;
+            if (!(ff < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
+            const float *src = in + n * R * cs + (long long)y * Win + x;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c < R) v[t * R + c] = __ldg(src + c * cs);
+        }
+        float4 *dst = xr + n * 4 * plane_recs + f;
+        dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+        dst[plane_recs] = make_float4(v[4], v[5], v[6], v[7]);
+        dst[2 * plane_recs] = make_float4(ptx::tf32_lo(v[0]), ptx::tf32_lo(v[1]),
+                                          ptx::tf32_lo(v[2]), ptx::tf32_lo(v[3]));
+        dst[3 * plane_recs] = make_float4(ptx::tf32_lo(v[4]), ptx::tf32_lo(v[5]),
+                                          ptx::tf32_lo(v[6]), ptx::tf32_lo(v[7]));
+    }
+}
+
+// fp16-split records of a single tap-packed chunk (R <= 8 channels): slot t*R + c of record
+// f = x[c] at virtual flat index f + t*d, TP = 16 / R column taps, planes
+// [hi s0-7 | hi s8-15 | lo s0-7 | lo s8-15]; SCALED: the data gradient's offset split;
+// flag as tc_relayout_f16
+template <bool SCALED>
+__global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restrict__ in,
+                                                          uint4 *__restrict__ xr, int R,
+                                                          int Hin, int Win, int Wv, int pad,
+                                                          int d, long long plane_recs,
+                                                          long long vrecs, long long total,
+                                                          int *flag) {
+    const int TP = 16 / R;
+    const long long cs = (long long)Hin * Win;
+    bool bad = false;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long n = idx / plane_recs;
+        const long long f = idx - n * plane_recs;
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            if (t >= TP) break;
+            const long long ff = f + (long long)t * d;
+            const long long yv = ff / Wv;
+            const int y = (int)yv - pad, x = (int)(ff - yv * Wv) - pad;
+            if (!(ff < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
+            const float *src = in + n * R * cs + (long long)y * Win + x;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < R && t * R + c < 16) v[t * R + c] = __ldg(src + c * cs);
+        }
+        uint32_t hw[8], lw[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            bad |= !(fabsf(v[2 * q]) < ptx::F16_SPLIT_MAX) ||
+                   !(fabsf(v[2 * q + 1]) < ptx::F16_SPLIT_MAX);
+            if constexpr (SCALED)
+                ptx::f16_split2_scaled(v[2 * q], v[2 * q + 1], hw[q], lw[q]);
+            else
+                ptx::f16_split2(v[2 * q], v[2 * q + 1], hw[q], lw[q]);
+        }
+        uint4 *dst = xr + n * 4 * plane_recs + f;
+        dst[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        dst[plane_recs] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+        dst[2 * plane_recs] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        dst[3 * plane_recs] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+// the tf32 TMA-fed mode of single-chunk tap-packed inputs (R <= 4: first layers)
+static bool tf_pk_relayout(const TfPlan &q) {
+    const char *e = getenv("DP_TF_PK_RELAYOUT");
+    return q.rp > 0 && q.n_rc == 1 && !(e && e[0] == '0');
+}
+// ... and of narrow unpacked tf32 inputs (<= DP_TF_R32_CHUNKS 8-channel chunks, default 2:
+// c3's 8-channel head data gradient, whose loaders were the limit)
+static bool tf_r32_relayout(const TfPlan &q) {
+    const char *e = getenv("DP_TF_R32_CHUNKS");
+    const int mx = e ? atoi(e) : 2;
+    return q.rp == 0 && q.n_rc <= mx;
+}
+
 // TMA-fed mode (forward, fp16-split, inputs >= 16 channels): the fp16 loaders were the
 // limit (tools/tf_trace.py, c3 conv2: ~2800 loader vs ~2000 MMA cycles per unit), so the
 // split is done once by a bandwidth-bound relayout pass and units arrive as bulk copies.
@@ -571,16 +693,24 @@ __global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict_
 // (DP_TF_HALF_BWD=0: never).  Always TMA-fed and always paired with a tf32 fallback launch
 // that runs instead when an operand is outside the split's range (|x| >= 2^15, inf, NaN):
 // c4's relu outputs errors exceeded fp16's 65504.
-static bool tf_half(int R, bool bwd, bool f16_ok) {
-    if (R < 16) return false;
+static bool tf_half(int R, int l, bool bwd, bool f16_ok) {
+    // <= 8 channels: tap-packed, data gradient only by default -- a packed fp16 first layer
+    // gained little (c3 conv1 0.645 -> 0.630 ms, c1 conv1 slower) and its input split (lo
+    // subnormal below |x| = 1/8) doubled the unforced c4 output error and with it the relu /
+    // max-pool flips (dw2 2.1e-4 against the exact tier's 4.5e-5); DP_TF_F16_PACK_FWD=1 opts in
+    if (R < 16 && (R > 8 || getenv("DP_TF_NOPACK") || (!bwd && !getenv("DP_TF_F16_PACK_FWD"))))
+        return false;
+    // (and >= 5 taps a row: c4's 3x3 8-channel head data gradient measured 0.513 ms in tf32
+    // against 0.553 packed, c3's 7x7 one 1.24 -> 0.94)
+    if (R < 16 && bwd && l < 5) return false;
     const char *he = getenv(bwd ? "DP_TF_HALF_BWD" : "DP_TF_HALF");
     if (he && he[0] == '0') return false;
     return bwd || f16_ok;
 }
 
-static bool tf_relayout_mode(int R, bool bwd, bool f16_ok) {
+static bool tf_relayout_mode(int R, int l, bool bwd, bool f16_ok) {
     const char *re = getenv("DP_TF_RELAYOUT");
-    return tf_half(R, bwd, f16_ok) && !(re && re[0] == '0');
+    return tf_half(R, l, bwd, f16_ok) && !(re && re[0] == '0');
 }
 
 static long long tf_plane_recs(const TfPlan &p, int Hin, int Win, int pad, int l, int d, int Ho,
@@ -606,10 +736,16 @@ static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
 size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
                              int Ho, int Wo, bool bwd) {
     // (sized as if fp16 were allowed: the query cannot know the caller's flags)
-    if (!tf_relayout_mode(R, bwd, true) || Ho < 1 || Wo < 1) return 0;
+    if (Ho < 1 || Wo < 1) return 0;
     const int Wv = Win + 2 * pad;
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     const int max_mt = (int)((flat_len + 127) / 128);
+    if (!tf_relayout_mode(R, l, bwd, true)) {  // tap-packed tf32 planes: [weights | planes]
+        TfPlan q = tf_plan(R, Q, l, d, max_mt, bwd, false);
+        if (!q.ok || !(tf_pk_relayout(q) || tf_r32_relayout(q))) return 0;
+        return al256(tf_weight_bytes(q, l)) +
+               (size_t)n * q.n_rc * 4 * tf_plane_recs(q, Hin, Win, pad, l, d, Ho, Wo) * 16;
+    }
     TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, true);
     TfPlan q = tf_plan(R, Q, l, d, max_mt, bwd, false);
     if (!p.ok || !q.ok) return 0;
@@ -658,7 +794,7 @@ static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, c
     a.MT = p.MT;
     a.G = p.G;
     a.wunit_pk = p.wunit_pk;
-    a.tpd = (p.rp ? 8 / p.rp : 1) * d;
+    a.tpd = p.tp * d;
     a.acc_cols = p.acc_cols;
     a.NR = p.NR;
     a.HB = p.HB;
@@ -680,8 +816,13 @@ static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, c
     const int grid = a.total_tiles < g_tf_sms ? a.total_tiles : g_tf_sms;
     const size_t smem = (size_t)p.HB * p.ubytes;
     void (*kern)(const TfArgs);
+    // (fp16 kernels are TMA-fed: RP only marks the tap-packed chunk, 1 = packed)
     if (half && bwd)
-        kern = tc_conv_flat_kernel<true, true, 0, true>;
+        kern = p.rp ? tc_conv_flat_kernel<true, true, 1, true>
+                    : tc_conv_flat_kernel<true, true, 0, true>;
+    else if (half && p.rp)
+        kern = p.stacked ? tc_conv_flat_kernel<true, false, 1, true>
+                         : tc_conv_flat_kernel<false, false, 1, true>;
     else if (half)
         kern = p.stacked ? tc_conv_flat_kernel<true, false, 0, true>
                          : tc_conv_flat_kernel<false, false, 0, true>;
@@ -752,7 +893,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
     if (((uintptr_t)ws & 15) != 0)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace must be 16-byte aligned");
     // fp16-split (TMA-fed, with the tf32 fallback) when it applies and the workspace holds it
-    if (tf_relayout_mode(R, bwd, f16_ok) && ((uintptr_t)ws & 255) == 0) {
+    if (tf_relayout_mode(R, l, bwd, f16_ok) && ((uintptr_t)ws & 255) == 0) {
         const TfPlan p = tf_plan(R, Q, l, d, max_mt, bwd, true);
         const long long plane_recs = p.ok ? tf_plane_recs(p, Hin, Win, pad, l, d, Ho, Wo) : 0;
         const size_t wb16 = p.ok ? al256(tf_weight_bytes(p, l)) : 0;
@@ -764,13 +905,21 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
             const unsigned char *xr = w8 + wb16 + wb32 + 256;
             if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess)
                 return set_error(DP_ERR_CUDA, "flat conv: flag reset failed");
-            int rc = tc_pack_f16(w, w8, Q, R, l, bwd ? 1 : 0, flag, st);
+            int rc = tc_pack_f16(w, w8, Q, R, l, bwd ? 1 : 0, flag, st, p.rp);
             if (rc) return rc;
             const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
             const long long total = (long long)n * p.n_rc * plane_recs;
             const long long g = (total + 255) / 256;
             const int gg = (int)(g < 148 * 64 ? g : 148 * 64);
-            if (bwd)
+            if (p.rp && bwd)
+                tc_relayout_f16_pk<true><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv,
+                                                             pad, d, plane_recs, vrecs, total,
+                                                             flag);
+            else if (p.rp)
+                tc_relayout_f16_pk<false><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv,
+                                                              pad, d, plane_recs, vrecs, total,
+                                                              flag);
+            else if (bwd)
                 tc_relayout_f16<true><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv, pad,
                                                           p.n_rc, plane_recs, vrecs, total, flag);
             else
@@ -788,6 +937,32 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
         }
     }
     const size_t wbytes = tf_weight_bytes(q, l);
+    if ((tf_pk_relayout(q) || tf_r32_relayout(q)) && ((uintptr_t)ws & 255) == 0) {
+        // narrow tf32 inputs: relayout once, TMA-fed units
+        const long long plane_recs = tf_plane_recs(q, Hin, Win, pad, l, d, Ho, Wo);
+        const size_t need = al256(wbytes) + (size_t)n * q.n_rc * 4 * plane_recs * 16;
+        if (ws_bytes >= need && plane_recs < 0x7fffffffLL) {
+            unsigned char *w8 = (unsigned char *)ws;
+            int rc = tc_pack(w, (float *)w8, Q, R, l, bwd ? 1 : 0, q.rp, st);
+            if (rc) return rc;
+            float4 *xr = reinterpret_cast<float4 *>(w8 + al256(wbytes));
+            const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
+            const long long total = (long long)n * q.n_rc * plane_recs;
+            const long long g = (total + 255) / 256;
+            const int gg = (int)(g < 148 * 64 ? g : 148 * 64);
+            if (q.rp)
+                tc_relayout_pk<<<gg, 256, 0, st>>>(in, xr, R, Hin, Win, Wv, pad, d, plane_recs,
+                                                   vrecs, total);
+            else
+                tc_relayout<<<gg, 256, 0, st>>>(in, xr, R, Hin, Win, Wv, pad, q.n_rc, plane_recs,
+                                                vrecs, total);
+            rc = check_launch("tc_relayout");
+            if (rc) return rc;
+            return tf_run(q, false, in, w8, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d,
+                          pad, act, gate_kind, bwd, (const unsigned char *)xr, plane_recs,
+                          nullptr, nullptr, st);
+        }
+    }
     if (ws == nullptr || ws_bytes < wbytes)
         return set_error(DP_ERR_ARG, "tensor-core conv: workspace %zu < %zu bytes", ws_bytes,
                          wbytes);

@@ -338,3 +338,63 @@ def test_tc_forward_fp16_range_fallback(shape, scale):
     torch.cuda.synchronize()
     assert torch.isfinite(y).all()
     assert _rel(y, ref) < TOL
+
+
+PACKED_FWD = [(2, 3, 16, 6, 1, 70, 75), (4, 3, 16, 6, 1, 20, 23), (1, 8, 8, 7, 8, 70, 71),
+              (1, 5, 20, 3, 16, 50, 40), (3, 2, 3, 1, 5, 9, 9), (1, 8, 16, 7, 8, 60, 66),
+              (1, 3, 50, 6, 1, 80, 90), (4, 1, 16, 6, 1, 40, 40)]
+PACKED_BWD = [(1, 8, 8, 7, 8, 70, 71), (1, 50, 8, 7, 8, 96, 90), (2, 16, 6, 4, 4, 50, 52),
+              (1, 24, 8, 2, 3, 40, 41), (1, 16, 8, 3, 32, 80, 90), (3, 2, 3, 1, 5, 9, 9)]
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e5])
+@pytest.mark.parametrize("shape", PACKED_FWD)
+def test_tc_forward_fp16_tap_packed(shape, scale, monkeypatch):
+    """Inputs of <= 8 channels in the fp16 split (opt-in DP_TF_F16_PACK_FWD): 16 / R column
+    taps per K step (slot t*R + c), TMA-fed from a packed relayout; 1e5 trips the range flag
+    (tf32 fallback)."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    monkeypatch.setenv("DP_TF_F16_PACK_FWD", "1")
+    n, ci, co, k, d, h, w = shape
+    rng = np.random.default_rng(sum(shape))
+    x = _t((rng.uniform(-1, 1, (n, ci, h, w)) * scale).astype(np.float32))
+    wt = _t((rng.uniform(-0.5, 0.5, (co, ci, k, k)) * 4.0 / np.sqrt(ci * k * k)).astype(np.float32))
+    b = _t(rng.uniform(-0.5, 0.5, co).astype(np.float32))
+    e = (k - 1) * d + 1
+    ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda", dtype=torch.float64)
+    ops.conv_forward(x.double(), wt.double(), b.double(), ref, k, d, 0)
+    y = torch.full(ref.shape, float("nan"), device="cuda")
+    ws = torch.empty(ops.fwd_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+    ops.conv_forward_fast(x, wt, b, y, k, d, 0, ws, fp16_range=True)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
+    assert _rel(y, ref) < TOL
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-4, 1e5])
+@pytest.mark.parametrize("gate_kind", [None, 1])
+@pytest.mark.parametrize("shape", PACKED_BWD)
+def test_tc_backward_data_fp16_tap_packed(shape, gate_kind, scale):
+    """Deltas of <= 8 channels: the offset-split fp16 data gradient on tap-packed records
+    (c3's 8-channel head); 1e5 sends the layer to the tf32 fallback."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    rng = np.random.default_rng(sum(shape) + 3)
+    e = (k - 1) * d + 1
+    dy = _t((rng.uniform(-1, 1, (n, co, h - e + 1, w - e + 1)) * scale).astype(np.float32))
+    wt = _t((rng.uniform(-0.5, 0.5, (co, ci, k, k)) * 4.0 / np.sqrt(co * k * k))
+            .astype(np.float32))
+    gate = None
+    if gate_kind is not None:
+        gate = _t(np.tanh(rng.normal(size=(n, ci, h, w))).astype(np.float32))
+    ref = torch.empty((n, ci, h, w), device="cuda", dtype=torch.float64)
+    ops.conv_backward_data(dy.double(), wt.double(), ref, k, d,
+                           None if gate is None else gate.double(), gate_kind or 0)
+    dx = torch.full((n, ci, h, w), float("nan"), device="cuda")
+    ws = torch.empty(ops.bwd_fast_workspace(dy, ci, k, d), dtype=torch.uint8, device="cuda")
+    ops.conv_backward_data_fast(dy, wt, dx, k, d, ws, gate, gate_kind or 0)
+    torch.cuda.synchronize()
+    assert torch.isfinite(dx).all()
+    assert _rel(dx, ref) < TOL

@@ -1,5 +1,7 @@
 """Per-unit timeline of the flat conv kernel (CTA 0):
-python tools/tf_trace.py <fwd|bwd> <n,ci,co,k,d,h>"""
+python tools/tf_trace.py <fwd|bwd> <n,ci,co,k,d,h>
+TF_FP16=1: forward input declared in fp16 range (the fp16-split TMA-fed kernel); TF_ACT=<code>
+fused nonlinearity (default 0).  (An fp16 launch's tf32 fallback exits before tracing.)"""
 import ctypes
 import os
 import sys
@@ -21,11 +23,14 @@ b = torch.randn(co, device="cuda")
 ho = h - e + 1
 if mode == "fwd":
     y = torch.empty(n, co, ho, ho, device="cuda")
-    ws = torch.empty(ops.fast_workspace(ci, co, k), dtype=torch.uint8, device="cuda")
-    f = lambda: ops.conv_forward_fast(x, w, b, y, k, d, 1, ws)  # noqa: E731
+    x = x.clamp(-1, 1)
+    ws = torch.empty(ops.fwd_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+    act = int(os.environ.get("TF_ACT", "0"))
+    f16 = os.environ.get("TF_FP16", "0") == "1"
+    f = lambda: ops.conv_forward_fast(x, w, b, y, k, d, act, ws, fp16_range=f16)  # noqa: E731
 else:
     dy = torch.randn(n, co, ho, ho, device="cuda")
-    ws = torch.empty(ops.fast_workspace(co, ci, k), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(ops.bwd_fast_workspace(dy, ci, k, d), dtype=torch.uint8, device="cuda")
     f = lambda: ops.conv_backward_data_fast(dy, w, x, k, d, ws)  # noqa: E731
 f()
 torch.cuda.synchronize()

@@ -808,7 +808,8 @@ static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, c
     if (tt > 0x7fffffff) return set_error(DP_ERR_UNSUPPORTED, "flat tensor-core conv: too many tiles");
     a.total_tiles = (int)tt;
     if (a.total_tiles == 0) return DP_OK;
-    a.trace = getenv("DP_TC_TRACE") ? tc_trace_buffer(st) : nullptr;
+    // (not for an fp16 launch's fallback: requesting the buffer clears it)
+    a.trace = getenv("DP_TC_TRACE") && !exit_unless ? tc_trace_buffer(st) : nullptr;
     a.xr = xr;
     a.plane_recs = plane_recs;
     a.exit_if = exit_if;

@@ -98,6 +98,7 @@ struct WsArgs {
     float *part;  // [splits][n_tiles * 128][NB]
     float *pdb;   // [splits][Npad]
     int no_m64;   // DP_WG_NO_M64: run a short last tile as M = 128 (experiments)
+    int pf;       // L2 prefetch distance in K blocks (DP_WG_PF, 0 = off)
     unsigned long long *trace;  // DP_WG_TRACE: per-K-block clock64 stamps of CTA 0
 };
 
@@ -197,9 +198,35 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     if (warp == WS_TMA_WARP) {
         // ================================ TMA producer ================================
         WsSched sc(a, kb_first, n_i);
+        // a second schedule a.pf blocks ahead: its dy box and new x row are prefetched into
+        // L2 so the stage's TMA loads hit L2 (the traces showed ~2400 cycles from issue to
+        // stage-full with only 2-3 stages in flight on the wide layers)
+        WsSched pf(a, kb_first, n_i);
+        for (int q = 0; q < a.pf; ++q) pf.next();
         unsigned char *ring = smem + a.ring_hi;
         int pre = 0;  // this block's new row came with the previous block's 2-row box
-        for (int kl = 0; kl < nkb; ++kl, sc.next()) {
+        for (int kl = 0; kl < nkb; ++kl, sc.next(), pf.next()) {
+            if (a.pf && lane == 0 && kl + a.pf < nkb) {
+                const int pv0 = pf.vb * 32;
+                if (a.J == 1)
+                    ptx::tma_prefetch_l2_4d(&tm_dy, pv0, pf.u, 0, pf.img);
+                else
+                    ptx::tma_prefetch_l2_5d(&tm_dy, pv0, 0, 0, pf.u, pf.img);
+                for (int k = pf.cstart ? 0 : n_i - 1; k < n_i; ++k) {
+                    if (a.direct) {
+                        ptx::tma_prefetch_l2_5d(&tm_x0, pv0 + a.rs.j0[0] * a.d, 0, 0,
+                                                pf.u + (i_lo + k) * a.d, pf.img);
+                        continue;
+                    }
+                    const int prow = pf.img * a.Hi + pf.u + (i_lo + k) * a.d;
+                    for (int rb = 0; rb < a.rs.n_b; ++rb) {
+                        const CUtensorMap *m = rb == 0 ? &tm_x0 : rb == 1 ? &tm_x1
+                                                               : rb == 2 ? &tm_x2 : &tm_x3;
+                        ptx::tma_prefetch_l2_4d(m, pv0 + a.rs.j0[rb] * a.d - a.rs.b[rb], 0, 0,
+                                                prow);
+                    }
+                }
+            }
             const int s = kl % a.SS;
             WS_TRACE(a, kl, 1, lane == 0);
             ptx::mbar_wait(&sempty[s], ((kl / a.SS) & 1) ^ 1);
@@ -913,6 +940,13 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.Hi = hi;
     a.kb_total = p.kb_total;
     a.SS = p.SS;
+    {
+        // x read in place only (c3 conv2 1.88 -> 1.74 ms at 2-4 blocks ahead; the staged
+        // small-box modes lost to the extra TMA requests: c3 conv1 1.33 -> 1.71)
+        const char *e = getenv("DP_WG_PF");
+        a.pf = e ? atoi(e) : (a.direct ? 3 : 0);
+        if (a.pf < 0) a.pf = 0;
+    }
     a.R = p.R;
     a.NM = p.NM;
     a.Ls = p.Ls;

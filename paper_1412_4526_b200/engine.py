@@ -581,11 +581,18 @@ class DenseNet:
             if isinstance(g.op, DilatedConv):
                 f_ok, b_ok = self.tc.get(gi, (False, False))
                 w_ok = getattr(self, "tc_wgrad", {}).get(gi, False)
-                dg = "tcgen05-3xtf32" if b_ok else "exact"
+                ci, co = g.op.base.in_channels, g.op.base.out_channels
+                kk = g.op.base.kernel_size
+                # fp16-split (3 passes, tf32 fallback launch when an operand leaves fp16's
+                # range): inputs of >= 16 channels declared in range; deltas of >= 16
+                # channels, or <= 8 tap-packed at >= 5 taps a row (tc_conv_flat.cu tf_half)
+                f16f = ci >= 16 and self._fp16_input(gi)
+                f16b = co >= 16 or (co <= 8 and kk >= 5)
+                fwd = ("tcgen05-fp16x3" if f16f else "tcgen05-3xtf32") if f_ok else "exact"
+                dg = ("tcgen05-fp16x3-offset" if f16b else "tcgen05-3xtf32") if b_ok else "exact"
                 if gi == 0:
                     dg = "not needed"  # layer 0's input delta is not computed (backward.py:208)
-                out[g.first] = {"forward": "tcgen05-3xtf32" if f_ok else "exact",
-                                "data_grad": dg,
+                out[g.first] = {"forward": fwd, "data_grad": dg,
                                 "weight_grad": "tcgen05-3xtf32" if w_ok else "cuda-core"}
         return out
 

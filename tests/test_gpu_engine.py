@@ -256,7 +256,7 @@ def test_config_c2_full_size(dp):
     """c2: 3x256x256, forward + masked backward with 1% of pixels (BASELINE.json configs[1])."""
     eng = _engine_vs_oracle(dp, _c1_text(3), 256, 2, np.float32, 0.01)
     plan = eng.kernel_plan()
-    assert all(v["forward"] == "tcgen05-3xtf32" for v in plan.values())
+    assert all(v["forward"].startswith("tcgen05-") for v in plan.values())
     _engine_vs_oracle(dp, _c1_text(3), 256, 1, np.float32, 0.01, precision="exact")
 
 

@@ -751,6 +751,18 @@ def main():
         ceil = peaks["bf16_tflops"] / 2 / 3
         roof["derived_3xtf32_ceiling_tflops"] = ceil
         roof["frac_of_3xtf32_ceiling"] = roof["achieved"] / ceil
+        # measured tcgen05 SS-MMA throughput (tools/mma_peak.cu, profiles/r02_mma_peak.json):
+        # the split kernels issue 3 MMAs per algorithmic MAC at N = 64 / 128
+        mpath = os.path.join(ROOT, "profiles", "r02_mma_peak.json")
+        if os.path.exists(mpath):
+            with open(mpath) as fh:
+                pts = json.load(fh)["points"]
+            ss = {f"{p['kind']}_n{p['N']}": p["tflops"] for p in pts}
+            roof["tcgen05_ss_peak_tflops"] = ss
+            roof["mma_rate_tflops"] = 3 * roof["achieved"]  # split products issued per s
+            for kind in ("tf32", "f16"):  # the weight gradients are 3xTF32
+                if f"{kind}_n128" in ss:
+                    roof[f"frac_of_ss_{kind}_n128"] = 3 * roof["achieved"] / ss[f"{kind}_n128"]
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"r02_traffic_{args.config}.json")
     if os.path.exists(tpath):

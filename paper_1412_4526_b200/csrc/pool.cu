@@ -528,17 +528,15 @@ __global__ void __launch_bounds__(256)
             for (int k = 0; k < SP_TW / 32; ++k) {
                 const int s = tx + 32 * k, gs = s0 + s;
                 if (gs >= Wi) break;
+                // out-of-map windows are staged as +0.0: adding them leaves the accumulator's
+                // bits unchanged (it starts at +0.0, and round-to-nearest never turns +0.0 + x
+                // into -0.0), so every tap is added without a range check
                 T acc = T(0);
 #pragma unroll
                 for (int i = P - 1; i >= 0; --i) {
-                    const int u = gr - i * d;
-                    if (u < 0 || u >= Ho) continue;
                     const int base = (r + hx - i * d) * RW + s + hx;
 #pragma unroll
-                    for (int j = P - 1; j >= 0; --j) {
-                        const int vv = gs - j * d;
-                        if (vv >= 0 && vv < Wo) acc = add_rn(acc, qs[base - j * d]);
-                    }
+                    for (int j = P - 1; j >= 0; --j) acc = add_rn(acc, qs[base - j * d]);
                 }
                 if (gate) acc = gate_from_output(acc, __ldg(gate + q + gs), gate_kind);
                 dx[q + gs] = acc;

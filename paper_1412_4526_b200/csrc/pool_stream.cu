@@ -119,16 +119,19 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
         const int nin = nout + G::HALO;
         // input row k of the item starts at element e0 + k * W of x; it is staged from the
         // 16-byte boundary at or below it, so its float shift inside the staging is
-        // (e0 + k * W) & 3 (x itself is 16-byte aligned, checked by the launcher)
+        // (e0 + k * W) & 3 (x itself is 16-byte aligned, checked by the launcher).  Row
+        // pointers and shifts advance incrementally (per-row 64-bit index math was ~40 % of
+        // the first version's instructions, ncu)
         const long long e0 = (plane * H + u0) * (long long)W + x0;
         const int avail0 = W - x0;  // valid floats of a row from its column x0
+        const int w3 = W & 3;
+        const float *sp = x + e0;   // column x0 of the next row to stage
+        int ssh = (int)(e0 & 3);    // its shift
         int k_st = 0;               // next row to stage
         auto stage = [&]() {
             if (k_st < nin) {
-                const long long e = e0 + (long long)k_st * W;
-                const int sh = (int)(e & 3);
-                const float *base = x + (e - sh);
-                const int avail = sh + avail0;
+                const float *base = sp - ssh;
+                const int avail = ssh + avail0;
                 float *dst = xs + (k_st & (MS_NB - 1)) * G::RW;
                 if (avail >= 4 * G::NC) {
 #pragma unroll
@@ -140,40 +143,47 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
                         ptx::cp_async16(dst + 4 * c, nb ? base + 4 * c : base, nb);
                     }
                 }
+                sp += W;
+                ssh = (ssh + w3) & 3;
             }
             ++k_st;
             ptx::cp_async_commit();
         };
-#pragma unroll 1
-        for (int k = 0; k < MS_NB - 1; ++k) stage();
-        float *yo = y + (plane * Ho + u0) * (long long)Wo + x0 + 4 * lane;
-        uint8_t *ao = arg + (plane * Ho + u0) * (long long)Wo + x0 + 4 * lane;
-        const int cols = Wo - x0 - 4 * lane;
-        const bool vfull = vec && cols >= 4;
-#pragma unroll 1
-        for (int k = 0; k < nin; ++k) {
+        int psh = (int)(e0 & 3);  // shift of the row being processed
+        // row pass of row k into the lane-private ring slot k % RING
+        auto rowstep = [&](int k) {
             __syncwarp();  // every lane is done with the slot the next stage overwrites
             stage();
             ptx::cp_async_wait_group(MS_NB - 1);
             __syncwarp();
             const float *row = xs + (k & (MS_NB - 1)) * G::RW + 4 * lane;
-            const int sh = (int)((e0 + (long long)k * W) & 3);
             float best[4];
             uint32_t cw;
-            switch (sh) {
+            switch (psh) {
                 case 0: ms_rowpass<P, D, 0>(row, best, cw); break;
                 case 1: ms_rowpass<P, D, 1>(row, best, cw); break;
                 case 2: ms_rowpass<P, D, 2>(row, best, cw); break;
                 default: ms_rowpass<P, D, 3>(row, best, cw); break;
             }
+            psh = (psh + w3) & 3;
             const int slot = k & (G::RING - 1);
             *reinterpret_cast<float4 *>(rv + slot * 128 + 4 * lane) =
                 make_float4(best[0], best[1], best[2], best[3]);
             rc[slot * 32 + lane] = cw;
-            if (k < G::HALO) continue;
-            // column pass: output row k - HALO over the row-pass rows i*D below it; the codes
-            // stay packed 4 per word (candidate word of row i = its row codes + i*P per byte)
-            const int u = k - G::HALO;
+        };
+#pragma unroll 1
+        for (int k = 0; k < MS_NB - 1; ++k) stage();
+#pragma unroll 1
+        for (int k = 0; k < G::HALO; ++k) rowstep(k);
+        float *yo = y + (plane * Ho + u0) * (long long)Wo + x0 + 4 * lane;
+        uint8_t *ao = arg + (plane * Ho + u0) * (long long)Wo + x0 + 4 * lane;
+        const int cols = Wo - x0 - 4 * lane;
+        const bool vfull = vec && cols >= 4;
+#pragma unroll 1
+        for (int u = 0; u < nout; ++u, yo += Wo, ao += Wo) {
+            rowstep(u + G::HALO);
+            // column pass: output row u over the row-pass rows u + i*D; the codes stay packed
+            // 4 per word (candidate word of row i = its row codes + i*P per byte)
             float ob[4];
             uint32_t oc;
             {
@@ -196,16 +206,15 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
                     }
             }
             ms_act4(ob, act);
-            const long long o = (long long)u * Wo;
             if (vfull) {
-                *reinterpret_cast<float4 *>(yo + o) = make_float4(ob[0], ob[1], ob[2], ob[3]);
-                *reinterpret_cast<uint32_t *>(ao + o) = oc;
+                *reinterpret_cast<float4 *>(yo) = make_float4(ob[0], ob[1], ob[2], ob[3]);
+                *reinterpret_cast<uint32_t *>(ao) = oc;
             } else {
 #pragma unroll
                 for (int m = 0; m < 4; ++m)
                     if (m < cols) {
-                        yo[o + m] = ob[m];
-                        ao[o + m] = (uint8_t)(oc >> (8 * m));
+                        yo[m] = ob[m];
+                        ao[m] = (uint8_t)(oc >> (8 * m));
                     }
             }
         }

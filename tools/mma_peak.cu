@@ -1,6 +1,6 @@
-// Dense tcgen05 throughput on every SM, operands in shared memory (SS, K-major, no swizzle):
-// one CTA per SM, one thread issuing `count` back-to-back MMAs of M = 128 into alternating
-// accumulators, one commit at the end; TFLOP/s from CUDA events over the whole grid.  The
+// Dense tcgen05 throughput on every SM, operands in shared memory (SS, K-major, no swizzle or
+// SWIZZLE_128B): one CTA per SM, one thread issuing `count` back-to-back MMAs of M = 128
+// rotating over 512 / N accumulators, one commit at the end; TFLOP/s from CUDA events over the whole grid.  The
 // measured ceilings of the conv / weight-gradient kernels' arithmetic (kind::tf32 for 3xTF32,
 // kind::f16 for the fp16 split) at the N they issue.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/mma_peak tools/mma_peak.cu
@@ -10,12 +10,12 @@
 #include "../paper_1412_4526_b200/csrc/tc_ptx.cuh"
 using namespace dp;
 
-__global__ void __launch_bounds__(128, 1) peak(int count, int N, int f16) {
+__global__ void __launch_bounds__(128, 1) peak(int count, int N, int f16, int sw) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t bar;
     __shared__ uint32_t s_tmem;
     const int warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < (48 * 1024) / 4; i += blockDim.x) ((float *)sm)[i] = 0.f;
+    for (int i = threadIdx.x; i < (64 * 1024) / 4; i += blockDim.x) ((float *)sm)[i] = 0.f;
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bar, 1);
         ptx::mbar_fence_init();
@@ -29,13 +29,18 @@ __global__ void __launch_bounds__(128, 1) peak(int count, int N, int f16) {
     if (warp == 0) {
         // A: 128 rows, B: N rows; K-major no-swizzle core matrices (8 rows x 16 B): SBO = 128
         // between 8-row groups, LBO = one K chunk (16 B of K) of all rows
+        // (sw: K-major SWIZZLE_128B, rows of 128 B in 1 KB atoms, as the weight gradient's
+        // TMA boxes write them)
         const uint32_t a0 = ptx::smem_u32(sm), b0 = a0 + 16 * 1024;
-        const uint64_t ad = ptx::smem_desc(a0, 128 * 16, 128);
-        const uint64_t bd = ptx::smem_desc(b0, (uint32_t)N * 16, 128);
+        const uint64_t ad = sw ? ptx::smem_desc_sw128(a0) : ptx::smem_desc(a0, 128 * 16, 128);
+        const uint64_t bd =
+            sw ? ptx::smem_desc_sw128(b0) : ptx::smem_desc(b0, (uint32_t)N * 16, 128);
         const uint32_t idesc = f16 ? ptx::idesc_f16(128, N) : ptx::idesc_tf32(128, N);
         if (ptx::elect_one()) {
             for (int i = 0; i < count; ++i) {
-                const uint32_t d = tmem + (uint32_t)((i & 1) * N);
+                // rotate over every accumulator TMEM holds (512 / N): back-to-back MMAs into
+                // one accumulator serialise on it
+                const uint32_t d = tmem + (uint32_t)((i % (512 / N)) * N);
                 if (f16)
                     ptx::mma_f16_ss(d, ad, bd, idesc, 1);
                 else
@@ -57,22 +62,23 @@ int main() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&mhz, cudaDevAttrClockRate, dev);
-    const int smem = 48 * 1024;
+    const int smem = 64 * 1024;
     cudaFuncSetAttribute(peak, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int count = 20000;
     printf("{\"sms\": %d, \"points\": [\n", sms);
     bool first = true;
+    for (int sw = 0; sw < 2; ++sw)
     for (int f16 = 0; f16 < 2; ++f16)
         for (int N : {64, 128, 256}) {
             const int K = f16 ? 16 : 8;
-            peak<<<sms, 128, smem>>>(200, N, f16);  // warm-up
+            peak<<<sms, 128, smem>>>(200, N, f16, sw);  // warm-up
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             float best = 1e30f;
             for (int rep = 0; rep < 5; ++rep) {
                 cudaEventRecord(e0);
-                peak<<<sms, 128, smem>>>(count, N, f16);
+                peak<<<sms, 128, smem>>>(count, N, f16, sw);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float ms = 0;
@@ -82,9 +88,10 @@ int main() {
             const double flops = 2.0 * 128 * N * K * (double)count * sms;
             const double tf = flops / (best * 1e-3) / 1e12;
             const double cyc = best * 1e-3 * 1965e6 / count;  // at the max SM clock
-            printf("%s {\"kind\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"operands\": \"SS\", "
+            printf("%s {\"kind\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"operands\": \"SS\", \"layout\": \"%s\", "
                    "\"tflops\": %.1f, \"cycles_per_mma_at_1965MHz\": %.1f}",
-                   first ? "" : ",\n", f16 ? "f16" : "tf32", N, K, tf, cyc);
+                   first ? "" : ",\n", f16 ? "f16" : "tf32", N, K, sw ? "sw128" : "none", tf,
+                   cyc);
             first = false;
         }
     printf("\n], \"error\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));

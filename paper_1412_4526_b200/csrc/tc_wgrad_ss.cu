@@ -415,6 +415,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                     if (hm) hm[idx] = v;
                 }
             }
+            WS_TRACE(a, kl, 3, tid == 0);
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&cfull[s]);

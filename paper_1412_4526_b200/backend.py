@@ -2,8 +2,9 @@
 
 Mirrors the reference's selector (backend.py:1-75): `available()`, `use(name)`,
 `active()`, `kernels()`, `default_threads()`, env vars DENSEPROP_BACKEND and
-DENSEPROP_THREADS.  The only backend this package registers is "cuda"
-(`cuda_kernels`, the sm_100a C ABI).  Unlike the reference there is no silent
+DENSEPROP_THREADS.  This package registers "cuda" (`cuda_kernels`, the sm_100a C ABI's
+exact tier: bit-identical to the compiled reference) and "cuda-fast" (`cuda_fast_kernels`:
+the fp32 convolutions on the tcgen05 fast tier, within the 1e-4 normwise bound).  Unlike the reference there is no silent
 CPU fallback: when libdenseprop_b200.so or a CUDA device is missing,
 `kernels()` raises `KernelUnavailable` naming the cause.  Unknown names
 (including "gpu", tests/test_backends.py:92-95) raise ValueError.
@@ -17,16 +18,16 @@ from __future__ import annotations
 import os
 import warnings
 
-from . import _lib, cuda_kernels
+from . import _lib, cuda_fast_kernels, cuda_kernels
 
-_BACKENDS = {"cuda": cuda_kernels}
+_BACKENDS = {"cuda": cuda_kernels, "cuda-fast": cuda_fast_kernels}
 _active: str | None = None
 _why_unavailable: str | None = None
 
 
 def _usable(name: str) -> bool:
     global _why_unavailable
-    if name != "cuda":
+    if not name.startswith("cuda"):
         return True
     try:
         _lib.require_device()

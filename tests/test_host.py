@@ -192,6 +192,26 @@ def test_backend_selection_api():
         backend.use("compiled")
     backend.use("auto")
     assert backend.active() == "cuda"
+    assert backend.registered() == ["cuda", "cuda-fast"]
+    backend.use("cuda-fast")
+    assert backend.active() == "cuda-fast"
+    backend.use("cuda")
+
+
+def test_cuda_fast_backend_has_the_module_contract():
+    """"cuda-fast" exposes exactly the boundary functions "cuda" does (reference
+    backend.py:25-48) and fails as loudly without a device."""
+    from paper_1412_4526_b200 import cuda_fast_kernels, cuda_kernels
+    names = ["conv_forward", "conv_backward_data", "conv_backward_kernel", "maxpool_forward",
+             "maxpool_backward", "avgpool_forward", "avgpool_backward", "nonlin_forward",
+             "nonlin_backward"]
+    for n in names:
+        assert callable(getattr(cuda_fast_kernels, n)) and callable(getattr(cuda_kernels, n))
+    if _lib.device_count() == 0:
+        with pytest.raises(_lib.KernelUnavailable):
+            cuda_fast_kernels.conv_forward(np.zeros((1, 5, 5), np.float32),
+                                           np.zeros((1, 1, 3, 3), np.float32),
+                                           np.zeros(1, np.float32), 1)
 
 
 def test_default_threads_env(monkeypatch):

@@ -141,11 +141,12 @@ __global__ void tc_pack_weights(const float *__restrict__ w, float *__restrict__
 // (n>>3)*256 + (k>>3)*128 + (n&7)*16 + (k&7)*2 -- the same 64 * Npad bytes per K step.
 // bwd: the data gradient's rotated weights (w is (R = cout, Q = cin, l, l)), lo' scaled by
 // 2^11 (the offset split of the fp16 data gradient: cross products in their own columns)
-// rp > 0: one tap-packed chunk of rp <= 8 channels (tp = 16 / rp column taps per K step,
-// slot k = t*rp + c <-> (c, j = g*tp + t), G = ceil(l / tp) K steps per tap row)
+// rp > 0: the LAST chunk holds rp <= 8 channels, tap-packed (tp = 16 / rp column taps per K
+// step, slot k = t*rp + c <-> (c, j = g*tp + t), G = ceil(l / tp) K steps per tap row), after
+// the (n_rc - 1) * l * l K steps of the full chunks
 __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restrict__ wp, int Q,
                                     int R, int l, int Npad, int n_ks, int bwd, int *flag,
-                                    int rp) {
+                                    int rp, int n_rc) {
     const int total = n_ks * 2 * Npad * 16;
     const int tp = rp ? 16 / rp : 1, G = (l + tp - 1) / tp;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -156,10 +157,12 @@ __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restr
         const int ks = idx / (32 * Npad);
         int j, i, c;
         bool slot_ok = true;
-        if (rp) {
-            i = ks / G;
-            c = k % rp;
-            j = (ks % G) * tp + k / rp;
+        const int full = rp ? (n_rc - 1) * l * l : n_ks;  // K steps of the full chunks
+        if (ks >= full) {  // the tap-packed last chunk
+            const int kp = ks - full;
+            i = kp / G;
+            c = (n_rc - 1) * 16 + k % rp;
+            j = (kp % G) * tp + k / rp;
             slot_ok = k < rp * tp && j < l;
         } else {
             j = ks % l, i = (ks / l) % l, c = (ks / (l * l)) * 16 + k;
@@ -185,10 +188,11 @@ int tc_pack_f16(const float *w, void *wp, int Q, int R, int l, int bwd, int *fla
                 cudaStream_t st, int rp) {
     const int Npad = (Q + 15) / 16 * 16, n_rc = (R + 15) / 16;
     const int tp = rp ? 16 / rp : 1;
-    const int n_ks = rp ? l * ((l + tp - 1) / tp) : n_rc * l * l;  // rp: one chunk
+    // rp: the last chunk tap-packed (G = ceil(l / tp) K steps per tap row)
+    const int n_ks = rp ? (n_rc - 1) * l * l + l * ((l + tp - 1) / tp) : n_rc * l * l;
     const int total = n_ks * 2 * Npad * 16;
     tc_pack_weights_f16<<<ceil_div(total, 256), 256, 0, st>>>(w, (__half *)wp, Q, R, l, Npad,
-                                                              n_ks, bwd, flag, rp);
+                                                              n_ks, bwd, flag, rp, n_rc);
     return check_launch("tc_pack_weights_f16");
 }
 

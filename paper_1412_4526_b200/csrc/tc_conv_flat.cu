@@ -510,8 +510,14 @@ static TfPlan tf_plan(int R, int Q, int l, int d, int max_mt, bool bwd, bool hal
     (void)bwd;
     // fp16-split records hold 16 slots: inputs of <= 8 channels pack 16 / R column taps
     // (c3's 8-channel head data gradient: 4 K steps per tap row instead of 7 tf32 ones)
+    // (and the last chunk of a wider input when it holds <= 8 channels: c3's 50 = 3 x 16 + 2
+    // channels run one K step of 8 column taps there instead of l steps of 2 channels)
+    const int rem16 = R - (p.n_rc - 1) * 16;
     if (half)
-        p.rp = (R <= 8 && l > 1 && !getenv("DP_TF_NOPACK")) ? R : 0;
+        p.rp = (rem16 <= 8 && l > 1 && !getenv("DP_TF_NOPACK") &&
+                (p.n_rc == 1 || !getenv("DP_TF_F16_NOPACK_LAST")))
+                   ? rem16
+                   : 0;
     else
         p.rp = (rem <= 4 && l > 1 && (p.n_rc == 1 || getenv("DP_TF_PACK_LAST")) &&
                 !getenv("DP_TF_NOPACK"))
@@ -573,8 +579,9 @@ __global__ void tc_relayout(const float *__restrict__ in, float4 *__restrict__ x
                             long long vrecs, long long total);
 template <bool SCALED>
 __global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict__ xr, int R,
-                                int Hin, int Win, int Wv, int pad, int n_rc, long long plane_recs,
-                                long long vrecs, long long total, int *flag);
+                                int Hin, int Win, int Wv, int pad, int n_rc, int n_rc_do,
+                                long long plane_recs, long long vrecs, long long total,
+                                int *flag);
 
 // NCHW (n, R <= 4, Hin, Win) -> four planes of tap-packed 16-byte records over the virtual
 // grid (the loaders' RP layout: slot t*R + c of record f = x[c] at virtual flat index
@@ -622,9 +629,12 @@ __global__ void __launch_bounds__(256) tc_relayout_pk(const float *__restrict__ 
 // f = x[c] at virtual flat index f + t*d, TP = 16 / R column taps, planes
 // [hi s0-7 | hi s8-15 | lo s0-7 | lo s8-15]; SCALED: the data gradient's offset split;
 // flag as tc_relayout_f16
+// (the LAST chunk of a wider input when n_rc > 1: channels c_base .. c_base + rp of the R,
+// written to chunk n_rc - 1 of each image's planes)
 template <bool SCALED>
 __global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restrict__ in,
-                                                          uint4 *__restrict__ xr, int R,
+                                                          uint4 *__restrict__ xr, int R_all,
+                                                          int R, int c_base, int n_rc,
                                                           int Hin, int Win, int Wv, int pad,
                                                           int d, long long plane_recs,
                                                           long long vrecs, long long total,
@@ -646,7 +656,7 @@ __global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restric
             const long long yv = ff / Wv;
             const int y = (int)yv - pad, x = (int)(ff - yv * Wv) - pad;
             if (!(ff < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
-            const float *src = in + n * R * cs + (long long)y * Win + x;
+            const float *src = in + (n * R_all + c_base) * cs + (long long)y * Win + x;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 if (c < R && t * R + c < 16) v[t * R + c] = __ldg(src + c * cs);
@@ -661,7 +671,7 @@ __global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restric
             else
                 ptx::f16_split2(v[2 * q], v[2 * q + 1], hw[q], lw[q]);
         }
-        uint4 *dst = xr + n * 4 * plane_recs + f;
+        uint4 *dst = xr + (n * n_rc + n_rc - 1) * 4 * plane_recs + f;
         dst[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         dst[plane_recs] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
         dst[2 * plane_recs] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
@@ -912,20 +922,36 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
             const long long total = (long long)n * p.n_rc * plane_recs;
             const long long g = (total + 255) / 256;
             const int gg = (int)(g < 148 * 64 ? g : 148 * 64);
-            if (p.rp && bwd)
-                tc_relayout_f16_pk<true><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv,
-                                                             pad, d, plane_recs, vrecs, total,
-                                                             flag);
-            else if (p.rp)
-                tc_relayout_f16_pk<false><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv,
-                                                              pad, d, plane_recs, vrecs, total,
-                                                              flag);
-            else if (bwd)
-                tc_relayout_f16<true><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv, pad,
-                                                          p.n_rc, plane_recs, vrecs, total, flag);
-            else
-                tc_relayout_f16<false><<<gg, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv, pad,
-                                                           p.n_rc, plane_recs, vrecs, total, flag);
+            // full 16-channel chunks, then the tap-packed last one (if any)
+            const int n_full = p.rp ? p.n_rc - 1 : p.n_rc;
+            if (n_full > 0) {
+                const long long tf = (long long)n * n_full * plane_recs;
+                const long long gf = (tf + 255) / 256;
+                const int ggf = (int)(gf < 148 * 64 ? gf : 148 * 64);
+                if (bwd)
+                    tc_relayout_f16<true><<<ggf, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win, Wv,
+                                                               pad, p.n_rc, n_full, plane_recs,
+                                                               vrecs, tf, flag);
+                else
+                    tc_relayout_f16<false><<<ggf, 256, 0, st>>>(in, (uint4 *)xr, R, Hin, Win,
+                                                                Wv, pad, p.n_rc, n_full,
+                                                                plane_recs, vrecs, tf, flag);
+            }
+            if (p.rp) {
+                const long long tp_ = (long long)n * plane_recs;
+                const long long gp = (tp_ + 255) / 256;
+                const int ggp = (int)(gp < 148 * 64 ? gp : 148 * 64);
+                const int c_base = (p.n_rc - 1) * 16;
+                if (bwd)
+                    tc_relayout_f16_pk<true><<<ggp, 256, 0, st>>>(
+                        in, (uint4 *)xr, R, p.rp, c_base, p.n_rc, Hin, Win, Wv, pad, d,
+                        plane_recs, vrecs, tp_, flag);
+                else
+                    tc_relayout_f16_pk<false><<<ggp, 256, 0, st>>>(
+                        in, (uint4 *)xr, R, p.rp, c_base, p.n_rc, Hin, Win, Wv, pad, d,
+                        plane_recs, vrecs, tp_, flag);
+            }
+            (void)gg;
             rc = check_launch("tc_relayout_f16");
             if (rc) return rc;
             rc = tc_pack(w, (float *)(w8 + wb16), Q, R, l, bwd ? 1 : 0, q.rp, st);

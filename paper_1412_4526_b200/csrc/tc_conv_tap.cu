@@ -385,19 +385,23 @@ __global__ void tc_pack_tap(const float *__restrict__ w, float *__restrict__ wp,
 // (compile time: a runtime switch in the conversion loop cost the pass 25 %)
 // flag: set (atomicOr) when any element is outside the fp16-split's safe range (|x| >= 2^15)
 // or not finite -- the fp16 kernel then exits and the tf32 fallback launched after it runs
+// n_rc_do <= n_rc: only the first n_rc_do chunks of every image (the last one may be
+// tap-packed by tc_relayout_f16_pk); total = n * n_rc_do * plane_recs
 template <bool SCALED>
 __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__ in,
                                                        uint4 *__restrict__ xr, int R, int Hin,
                                                        int Win, int Wv, int pad, int n_rc,
-                                                       long long plane_recs, long long vrecs,
-                                                       long long total, int *flag) {
+                                                       int n_rc_do, long long plane_recs,
+                                                       long long vrecs, long long total,
+                                                       int *flag) {
     bool bad = false;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
-        const long long nrc = idx / plane_recs;
-        const long long f = idx - nrc * plane_recs;
-        const int rc = (int)(nrc % n_rc);
-        const long long n = nrc / n_rc;
+        const long long nrd = idx / plane_recs;
+        const long long f = idx - nrd * plane_recs;
+        const int rc = (int)(nrd % n_rc_do);
+        const long long n = nrd / n_rc_do;
+        const long long nrc = n * n_rc + rc;
         const long long yv = f / Wv;
         const int y = (int)yv - pad, x = (int)(f - yv * Wv) - pad;
         const bool ok = f < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win;
@@ -425,9 +429,9 @@ __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__
 }
 
 template __global__ void tc_relayout_f16<false>(const float *, uint4 *, int, int, int, int, int,
-                                                int, long long, long long, long long, int *);
+                                                int, int, long long, long long, long long, int *);
 template __global__ void tc_relayout_f16<true>(const float *, uint4 *, int, int, int, int, int,
-                                               int, long long, long long, long long, int *);
+                                               int, int, long long, long long, long long, int *);
 
 // weights W(q, r, i, j) -> per (16-channel chunk rc, tap row i): [hi | lo] tiles of LN rows
 // (row n = j*QS + q) x K = 16 halves: element (n, k) at (n>>3)*256 + (k>>3)*128 + (n&7)*16 +
@@ -629,7 +633,8 @@ int tt_launch(const float *in, const float *w, const float *bias, float *out, co
         long long g = (total + 255) / 256;
         if (half)
             tc_relayout_f16<false><<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
-                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total, flag);
+                in, (uint4 *)xr, R, Hin, Win, Wv, pad, p.n_rc, p.n_rc, plane_recs, vrecs, total,
+                flag);
         else
             tc_relayout<<<(int)(g < 148 * 64 ? g : 148 * 64), 256, 0, st>>>(
                 in, xr, R, Hin, Win, Wv, pad, p.n_rc, plane_recs, vrecs, total);

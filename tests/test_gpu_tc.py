@@ -398,3 +398,42 @@ def test_tc_backward_data_fp16_tap_packed(shape, gate_kind, scale):
     torch.cuda.synchronize()
     assert torch.isfinite(dx).all()
     assert _rel(dx, ref) < TOL
+
+
+PACK_LAST = [(2, 50, 50, 3, 4, 60, 64), (1, 20, 16, 5, 2, 40, 44), (1, 24, 32, 3, 1, 33, 40),
+             (1, 40, 8, 7, 8, 90, 96), (1, 66, 24, 2, 3, 30, 31), (2, 18, 10, 4, 4, 50, 52)]
+
+
+@pytest.mark.parametrize("mode", ["fwd", "bwd"])
+@pytest.mark.parametrize("shape", PACK_LAST)
+def test_tc_fp16_pack_last_chunk(shape, mode):
+    """fp16 split with a tap-packed LAST chunk (R = 16k + r, r <= 8: slot t*r + c holds channel
+    16k + c at column tap t), next to the full 16-channel chunks -- forward (input declared in
+    range) and the offset-split data gradient (deltas of R channels)."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    rng = np.random.default_rng(sum(shape) + (0 if mode == "fwd" else 1))
+    e = (k - 1) * d + 1
+    if mode == "fwd":
+        x = _t(rng.uniform(-1, 1, (n, ci, h, w)).astype(np.float32))
+        wt = _t((rng.uniform(-0.5, 0.5, (co, ci, k, k)) * 4.0 / np.sqrt(ci * k * k))
+                .astype(np.float32))
+        b = _t(rng.uniform(-0.5, 0.5, co).astype(np.float32))
+        ref = torch.empty((n, co, h - e + 1, w - e + 1), device="cuda", dtype=torch.float64)
+        ops.conv_forward(x.double(), wt.double(), b.double(), ref, k, d, 0)
+        y = torch.full(ref.shape, float("nan"), device="cuda")
+        ws = torch.empty(ops.fwd_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+        ops.conv_forward_fast(x, wt, b, y, k, d, 0, ws, fp16_range=True)
+    else:  # deltas of ci channels flow back to co inputs: R = ci here
+        dy = _t(rng.uniform(-1, 1, (n, ci, h - e + 1, w - e + 1)).astype(np.float32))
+        wt = _t((rng.uniform(-0.5, 0.5, (ci, co, k, k)) * 4.0 / np.sqrt(ci * k * k))
+                .astype(np.float32))
+        ref = torch.empty((n, co, h, w), device="cuda", dtype=torch.float64)
+        ops.conv_backward_data(dy.double(), wt.double(), ref, k, d)
+        y = torch.full(ref.shape, float("nan"), device="cuda")
+        ws = torch.empty(ops.bwd_fast_workspace(dy, co, k, d), dtype=torch.uint8, device="cuda")
+        ops.conv_backward_data_fast(dy, wt, y, k, d, ws)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
+    assert _rel(y, ref) < TOL

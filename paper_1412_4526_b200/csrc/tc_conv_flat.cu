@@ -79,7 +79,8 @@ struct TfArgs {
     uint32_t wunit_pk;   // its weight-unit bytes (other chunks: wunit_bytes)
     uint32_t plane_bytes, halo_bytes, wunit_bytes, ubytes;
     int tiles_per_img, total_tiles, flat_len;
-    unsigned long long *trace;  // DP_TC_TRACE: per-unit clock64 stamps of CTA 0 (8 slots)
+    unsigned long long *trace;  // DP_TC_TRACE=<cta>: per-unit clock64 stamps of one CTA (8 slots)
+    int trace_cta;
     const unsigned char *xr;    // relayout planes (TMA-fed mode) or nullptr (loader warps)
     long long plane_recs;       // records per relayout plane
     const int *exit_if;         // fp16 kernel: exit when its operands tripped the range flag
@@ -90,7 +91,7 @@ struct TfArgs {
 // tile wait/got (at the tile's first unit), 7 epilogue tile done
 #define TF_TRACE(A, U, SLOT, COND)                                                   \
     do {                                                                             \
-        if ((A).trace && (COND) && blockIdx.x == 0 && (U) < 1024)                    \
+        if ((A).trace && (COND) && (int)blockIdx.x == (A).trace_cta && (U) < 1024)    \
             (A).trace[(U) * 8 + (SLOT)] = clock64();                                 \
     } while (0)
 
@@ -820,6 +821,7 @@ static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, c
     if (a.total_tiles == 0) return DP_OK;
     // (not for an fp16 launch's fallback: requesting the buffer clears it)
     a.trace = getenv("DP_TC_TRACE") && !exit_unless ? tc_trace_buffer(st) : nullptr;
+    a.trace_cta = a.trace ? atoi(getenv("DP_TC_TRACE")) : 0;
     a.xr = xr;
     a.plane_recs = plane_recs;
     a.exit_if = exit_if;

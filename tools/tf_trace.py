@@ -1,6 +1,6 @@
 """Per-unit timeline of the flat conv kernel (CTA 0):
 python tools/tf_trace.py <fwd|bwd> <n,ci,co,k,d,h>
-TF_FP16=1: forward input declared in fp16 range (the fp16-split TMA-fed kernel); TF_ACT=<code>
+TF_CTA=<n>: trace CTA n instead of 0.  TF_FP16=1: forward input declared in fp16 range (the fp16-split TMA-fed kernel); TF_ACT=<code>
 fused nonlinearity (default 0).  (An fp16 launch's tf32 fallback exits before tracing.)"""
 import ctypes
 import os
@@ -9,7 +9,7 @@ import sys
 import numpy as np
 import torch
 
-os.environ["DP_TC_TRACE"] = "1"
+os.environ["DP_TC_TRACE"] = os.environ.get("TF_CTA", "0")  # the CTA traced
 sys.path.insert(0, ".")
 from paper_1412_4526_b200 import _lib  # noqa: E402
 from paper_1412_4526_b200.engine import ops  # noqa: E402

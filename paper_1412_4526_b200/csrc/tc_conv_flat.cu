@@ -604,13 +604,19 @@ __global__ void __launch_bounds__(256) tc_relayout_pk(const float *__restrict__ 
         float v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = 0.f;
+        // one 32-bit divide per record, the taps step along the row (a 64-bit divide per tap
+        // made this pass issue bound); y < Hin implies the tap is inside the virtual grid
+        const int fi = (int)f, yv0 = fi / Wv, xv0 = fi - yv0 * Wv;
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             if (t >= TP) break;
-            const long long ff = f + (long long)t * d;
-            const long long yv = ff / Wv;
-            const int y = (int)yv - pad, x = (int)(ff - yv * Wv) - pad;
-            if (!(ff < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
+            int xx = xv0 + t * d, yy = yv0;
+            while (xx >= Wv) {
+                xx -= Wv;
+                ++yy;
+            }
+            const int y = yy - pad, x = xx - pad;
+            if (!(y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
             const float *src = in + n * R * cs + (long long)y * Win + x;
 #pragma unroll
             for (int c = 0; c < 4; ++c)
@@ -650,13 +656,17 @@ __global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restric
         float v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.f;
+        const int fi = (int)f, yv0 = fi / Wv, xv0 = fi - yv0 * Wv;  // (as tc_relayout_pk)
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             if (t >= TP) break;
-            const long long ff = f + (long long)t * d;
-            const long long yv = ff / Wv;
-            const int y = (int)yv - pad, x = (int)(ff - yv * Wv) - pad;
-            if (!(ff < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
+            int xx = xv0 + t * d, yy = yv0;
+            while (xx >= Wv) {
+                xx -= Wv;
+                ++yy;
+            }
+            const int y = yy - pad, x = xx - pad;
+            if (!(y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
             const float *src = in + (n * R_all + c_base) * cs + (long long)y * Win + x;
 #pragma unroll
             for (int c = 0; c < 8; ++c)

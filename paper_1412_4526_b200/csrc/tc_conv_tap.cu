@@ -395,15 +395,28 @@ __global__ void __launch_bounds__(256) tc_relayout_f16(const float *__restrict__
                                                        long long vrecs, long long total,
                                                        int *flag) {
     bool bad = false;
+    // 32-bit index math whenever the pass fits it (every config): the 64-bit divides by
+    // plane_recs and Wv were a large share of this HBM-bound pass's issue slots
+    const bool small = total < 0x7fffffffLL;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
-        const long long nrd = idx / plane_recs;
-        const long long f = idx - nrd * plane_recs;
+        long long nrd, f;
+        int yvi;
+        if (small) {
+            const unsigned ui = (unsigned)idx, pr = (unsigned)plane_recs;
+            const unsigned q = ui / pr;
+            nrd = q;
+            f = ui - q * pr;
+            yvi = (int)((unsigned)f / (unsigned)Wv);
+        } else {
+            nrd = idx / plane_recs;
+            f = idx - nrd * plane_recs;
+            yvi = (int)(f / Wv);
+        }
         const int rc = (int)(nrd % n_rc_do);
         const long long n = nrd / n_rc_do;
         const long long nrc = n * n_rc + rc;
-        const long long yv = f / Wv;
-        const int y = (int)yv - pad, x = (int)(f - yv * Wv) - pad;
+        const int y = yvi - pad, x = (int)(f - (long long)yvi * Wv) - pad;
         const bool ok = f < vrecs && y >= 0 && y < Hin && x >= 0 && x < Win;
         const float *src = in + ((n * R + rc * 16) * Hin + (ok ? y : 0)) * (long long)Win + (ok ? x : 0);
         const long long cs = (long long)Hin * Win;

@@ -421,6 +421,7 @@ static int ms_bwd_launch(const float *dy, const uint8_t *arg, float *dx, const f
         case 401: return CALL(4, 1);                   \
         case 402: return CALL(4, 2);                   \
         case 404: return CALL(4, 4);                   \
+        case 801: return CALL(8, 1);                   \
         default: return -1;                            \
     }
 

@@ -10,7 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1412_4526_b200 import _lib  # noqa: E402
 from paper_1412_4526_b200.engine import ops  # noqa: E402
 
-SHAPES = [("c3 pool1", 16, 50, 575, 575, 4, 1), ("c3 pool2", 16, 50, 564, 564, 2, 4)]
+SHAPES = [("c3 pool1", 16, 50, 575, 575, 4, 1), ("c3 pool2", 16, 50, 564, 564, 2, 4),
+          ("plain p8", 4, 50, 639, 639, 8, 1)]
 
 
 def timeit(fn, reps):

@@ -771,6 +771,15 @@ def main():
         if top["name"] in tj.get("kernels", {}):
             traffic = tj["kernels"][top["name"]]["dram_bytes"]
             traffic_src = tj.get("source")
+        # the committed ncu capture's per-launch tensor-pipe / DRAM / issue percentages
+        # beside each record's CUDA-event time (cold-cache, serialised: indicative)
+        for k in prof["kernels"]:
+            rec = tj.get("kernels", {}).get(k["name"])
+            if rec:
+                k["ncu"] = [{"kernel": ln["kernel"].split("(")[0][:60],
+                             **{m: round(ln[m], 1) for m in ("tensor_pct", "dram_pct",
+                                                            "issue_pct") if m in ln}}
+                            for ln in rec["launches"]]
     roof.update({"kernel": top["name"], "ms_per_launch": top["ms"],
                  "share_of_step": top["ms"] / prof["step_ms"], "peak_source": peaks["source"],
                  "traffic": traffic, "traffic_source": traffic_src,

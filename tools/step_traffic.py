@@ -90,7 +90,9 @@ def main():
         rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
         t = val(r, "gpu__time_duration.sum")
         e = recs.setdefault(rec, {"launches": [], "dram_bytes": 0.0, "gpu_time_us": 0.0})
-        e["launches"].append({"kernel": name[:120], "dram_bytes": rd + wr, "gpu_time_us": t})
+        e["launches"].append({"kernel": name[:120], "dram_bytes": rd + wr, "gpu_time_us": t,
+                              "tensor_pct": val(r, METRICS[3]), "dram_pct": val(r, METRICS[4]),
+                              "issue_pct": val(r, METRICS[6])})
         e["dram_bytes"] += rd + wr
         e["gpu_time_us"] += t
         pct = [r[h.index(k)][:5] for k in METRICS[3:]]

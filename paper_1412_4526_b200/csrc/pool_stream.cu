@@ -1,6 +1,6 @@
 // Streaming max-pool kernels (sm_100a), fp32 with uint8 argmax codes: one warp per strip of
 // output columns (forward: 128, backward: 4 * (32 - NL)) x MS_RS rows, walking the rows with a
-// cp.async ring of staged input rows (MS_NB rows in flight per warp).  Warps are independent
+// cp.async ring of staged input rows (MS_NBF / MS_NBB rows in flight per warp).  Warps are independent
 // (no __syncthreads); every lane owns 4 consecutive columns, so staging, smem reads and
 // global stores are 16-byte vectors.  The shared-memory tile kernels in pool.cu were issue
 // bound (ncu issue-active 73-84 %, DRAM 22-52 %, profiles/r02_ncu_c3.md) at ~100-130
@@ -28,7 +28,10 @@
 
 namespace dp {
 
-constexpr int MS_NB = 8;     // staged rows in flight per warp (power of two)
+// staged rows in flight per warp (powers of two): occupancy, not prefetch depth, set the pace
+// (c3 pool1 fwd 679 / 650 / 648 us and pool2 bwd 638 / 603 / 587 us at 8 / 4 / 2 rows)
+constexpr int MS_NBF = 4;    // forward
+constexpr int MS_NBB = 2;    // backward
 constexpr int MS_RS = 64;    // output (forward) / pixel (backward) rows per work item
 constexpr int MS_WARPS = 4;  // independent warps per CTA
 
@@ -40,8 +43,23 @@ struct MsFwd {
     static constexpr int NC = 32 + (HALO + 3) / 4 + 1;  // 16-byte chunks per staged row
     static constexpr int RW = 4 * NC;                   // floats per staged row
     static constexpr int RING = ms_pow2(HALO + 1);      // row-pass results kept per lane
-    static constexpr size_t WARP_BYTES = (size_t)MS_NB * RW * 4 + (size_t)RING * (128 + 32) * 4;
+    // p = 4: row pairs (u, u + D) kept for the column pass (out(u) = pair(u) vs pair(u + 2D))
+    static constexpr int PRING = P == 4 ? ms_pow2(2 * D + 1) : 0;
+    static constexpr size_t WARP_BYTES =
+        (size_t)MS_NBF * RW * 4 + (size_t)(RING + PRING) * (128 + 32) * 4;
 };
+
+// first-wins (strict '>') merge of a later candidate into (v, c), codes packed 4 per word:
+// byte m of the result is the candidate's when its value m is greater
+__device__ __forceinline__ void ms_merge4(float v[4], uint32_t &c, const float t[4],
+                                          uint32_t cand) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+        if (t[m] > v[m]) {
+            v[m] = t[m];
+            c = __byte_perm(c, cand, (0x3210 & ~(0xF << (4 * m))) | ((4 + m) << (4 * m)));
+        }
+}
 
 template <int P, int D>
 struct MsBwd {
@@ -49,7 +67,7 @@ struct MsBwd {
     static constexpr int NL = (HALO + 3) / 4;      // halo lanes: feed right neighbours only
     static constexpr int PX = 4 * (32 - NL);       // pixel columns per strip
     static constexpr int RING = ms_pow2(HALO + 1);  // pixel rows accumulated at once
-    static constexpr size_t WARP_BYTES = (size_t)MS_NB * 32 * (16 + 4) + (size_t)RING * 128 * 4;
+    static constexpr size_t WARP_BYTES = (size_t)MS_NBB * 32 * (16 + 4) + (size_t)RING * 128 * 4;
 };
 
 // row pass of one staged row (S = the row's float shift inside its 16-byte staging):
@@ -106,8 +124,10 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
     extern __shared__ __align__(16) unsigned char ms_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float *xs = reinterpret_cast<float *>(ms_raw + wid * G::WARP_BYTES);
-    float *rv = xs + MS_NB * G::RW;                                    // [RING][128]
+    float *rv = xs + MS_NBF * G::RW;                                    // [RING][128]
     uint32_t *rc = reinterpret_cast<uint32_t *>(rv + G::RING * 128);  // [RING][32]
+    float *pv = reinterpret_cast<float *>(rc + G::RING * 32);          // [PRING][128]
+    uint32_t *pc = reinterpret_cast<uint32_t *>(pv + G::PRING * 128);  // [PRING][32]
     const long long nw = (long long)gridDim.x * MS_WARPS;
     for (long long it = (long long)blockIdx.x * MS_WARPS + wid; it < items; it += nw) {
         const int sx = (int)(it % sx_n);
@@ -132,7 +152,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
             if (k_st < nin) {
                 const float *base = sp - ssh;
                 const int avail = ssh + avail0;
-                float *dst = xs + (k_st & (MS_NB - 1)) * G::RW;
+                float *dst = xs + (k_st & (MS_NBF - 1)) * G::RW;
                 if (avail >= 4 * G::NC) {
 #pragma unroll
                     for (int c = lane; c < G::NC; c += 32) ptx::cp_async16(dst + 4 * c, base + 4 * c, 16);
@@ -150,13 +170,16 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
             ptx::cp_async_commit();
         };
         int psh = (int)(e0 & 3);  // shift of the row being processed
-        // row pass of row k into the lane-private ring slot k % RING
+        // row pass of row k into the lane-private ring slot k % RING; p = 4 also forms the
+        // pair (k - D, k) into the pair ring, returned in (prv, prc)
+        float prv[4];
+        uint32_t prc = 0;
         auto rowstep = [&](int k) {
             __syncwarp();  // every lane is done with the slot the next stage overwrites
             stage();
-            ptx::cp_async_wait_group(MS_NB - 1);
+            ptx::cp_async_wait_group(MS_NBF - 1);
             __syncwarp();
-            const float *row = xs + (k & (MS_NB - 1)) * G::RW + 4 * lane;
+            const float *row = xs + (k & (MS_NBF - 1)) * G::RW + 4 * lane;
             float best[4];
             uint32_t cw;
             switch (psh) {
@@ -170,9 +193,22 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
             *reinterpret_cast<float4 *>(rv + slot * 128 + 4 * lane) =
                 make_float4(best[0], best[1], best[2], best[3]);
             rc[slot * 32 + lane] = cw;
+            if constexpr (P == 4) {
+                if (k >= D) {
+                    const int s0 = (k - D) & (G::RING - 1);
+                    const float4 f = *reinterpret_cast<const float4 *>(rv + s0 * 128 + 4 * lane);
+                    prv[0] = f.x, prv[1] = f.y, prv[2] = f.z, prv[3] = f.w;
+                    prc = rc[s0 * 32 + lane];
+                    ms_merge4(prv, prc, best, cw + (uint32_t)P * 0x01010101u);
+                    const int ps = (k - D) & (G::PRING - 1);
+                    *reinterpret_cast<float4 *>(pv + ps * 128 + 4 * lane) =
+                        make_float4(prv[0], prv[1], prv[2], prv[3]);
+                    pc[ps * 32 + lane] = prc;
+                }
+            }
         };
 #pragma unroll 1
-        for (int k = 0; k < MS_NB - 1; ++k) stage();
+        for (int k = 0; k < MS_NBF - 1; ++k) stage();
 #pragma unroll 1
         for (int k = 0; k < G::HALO; ++k) rowstep(k);
         float *yo = y + (plane * Ho + u0) * (long long)Wo + x0 + 4 * lane;
@@ -186,24 +222,29 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
             // 4 per word (candidate word of row i = its row codes + i*P per byte)
             float ob[4];
             uint32_t oc;
-            {
-                const int s0 = u & (G::RING - 1);
-                const float4 f = *reinterpret_cast<const float4 *>(rv + s0 * 128 + 4 * lane);
-                oc = rc[s0 * 32 + lane];
+            if constexpr (P == 4) {
+                // pair(u) (rows u, u + D) vs pair(u + 2D), just formed: first-wins over the
+                // four rows in order, as the sequential scan
+                const int s0 = u & (G::PRING - 1);
+                const float4 f = *reinterpret_cast<const float4 *>(pv + s0 * 128 + 4 * lane);
+                oc = pc[s0 * 32 + lane];
                 ob[0] = f.x, ob[1] = f.y, ob[2] = f.z, ob[3] = f.w;
-            }
+                ms_merge4(ob, oc, prv, prc + (uint32_t)(2 * P) * 0x01010101u);
+            } else {
+                {
+                    const int s0 = u & (G::RING - 1);
+                    const float4 f = *reinterpret_cast<const float4 *>(rv + s0 * 128 + 4 * lane);
+                    oc = rc[s0 * 32 + lane];
+                    ob[0] = f.x, ob[1] = f.y, ob[2] = f.z, ob[3] = f.w;
+                }
 #pragma unroll
-            for (int i = 1; i < P; ++i) {
-                const int si = (u + i * D) & (G::RING - 1);
-                const float4 f = *reinterpret_cast<const float4 *>(rv + si * 128 + 4 * lane);
-                const uint32_t cand = rc[si * 32 + lane] + (uint32_t)(i * P) * 0x01010101u;
-                const float t[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-                for (int m = 0; m < 4; ++m)
-                    if (t[m] > ob[m]) {
-                        ob[m] = t[m];
-                        oc = __byte_perm(oc, cand, (0x3210 & ~(0xF << (4 * m))) | ((4 + m) << (4 * m)));
-                    }
+                for (int i = 1; i < P; ++i) {
+                    const int si = (u + i * D) & (G::RING - 1);
+                    const float4 f = *reinterpret_cast<const float4 *>(rv + si * 128 + 4 * lane);
+                    const uint32_t cand = rc[si * 32 + lane] + (uint32_t)(i * P) * 0x01010101u;
+                    const float t[4] = {f.x, f.y, f.z, f.w};
+                    ms_merge4(ob, oc, t, cand);
+                }
             }
             ms_act4(ob, act);
             if (vfull) {
@@ -233,10 +274,10 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
     constexpr int NL = G::NL;
     extern __shared__ __align__(16) unsigned char ms_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const size_t wbytes = G::WARP_BYTES + (gate ? MS_NB * 128 * 4 : 0);
+    const size_t wbytes = G::WARP_BYTES + (gate ? MS_NBB * 128 * 4 : 0);
     float *dys = reinterpret_cast<float *>(ms_raw + wid * wbytes);    // [NB][128]
-    uint32_t *cs = reinterpret_cast<uint32_t *>(dys + MS_NB * 128);  // [NB][32]
-    float *acc = reinterpret_cast<float *>(cs + MS_NB * 32);          // [RING][4][32]
+    uint32_t *cs = reinterpret_cast<uint32_t *>(dys + MS_NBB * 128);  // [NB][32]
+    float *acc = reinterpret_cast<float *>(cs + MS_NBB * 32);          // [RING][4][32]
     float *gs = acc + G::RING * 128;                                   // [NB][128] (gate)
     const long long nw = (long long)gridDim.x * MS_WARPS;
     for (long long it = (long long)blockIdx.x * MS_WARPS + wid; it < items; it += nw) {
@@ -255,7 +296,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
             const int u = r0 - G::HALO + k;
             const bool ok = colok && k < nwin && u >= 0 && u < Ho;
             const long long off = pbase + (long long)(ok ? u : 0) * Wo + (ok ? v0 : 0);
-            const int sl = k & (MS_NB - 1);
+            const int sl = k & (MS_NBB - 1);
             ptx::cp_async16(dys + sl * 128 + 4 * lane, dy + off, ok ? 16 : 0);
             ptx::cp_async4(cs + sl * 32 + lane, arg + off, ok ? 4 : 0);
             if (gate) {  // the gate row of pixel row u, when the item writes that row
@@ -276,13 +317,13 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
 #pragma unroll
         for (int e = 0; e < G::RING * 4; ++e) acc[e * 32 + lane] = 0.f;
 #pragma unroll 1
-        for (int k = 0; k < MS_NB - 1; ++k) stage(k);
+        for (int k = 0; k < MS_NBB - 1; ++k) stage(k);
 #pragma unroll 1
         for (int k = 0; k < nwin; ++k) {
-            stage(k + MS_NB - 1);
-            ptx::cp_async_wait_group(MS_NB - 1);  // this lane's own copies of row k landed
+            stage(k + MS_NBB - 1);
+            ptx::cp_async_wait_group(MS_NBB - 1);  // this lane's own copies of row k landed
             const int u = r0 - G::HALO + k;
-            const int sl = k & (MS_NB - 1);
+            const int sl = k & (MS_NBB - 1);
             const float4 f = *reinterpret_cast<const float4 *>(dys + sl * 128 + 4 * lane);
             const uint32_t cw = cs[sl * 32 + lane];
             const float dv[4] = {f.x, f.y, f.z, f.w};
@@ -392,7 +433,7 @@ static int ms_bwd_launch(const float *dy, const uint8_t *arg, float *dx, const f
                          long long planes, int ho, int wo, int hi, int wi, int wd, int gate_kind,
                          cudaStream_t st) {
     using G = MsBwd<P, D>;
-    const size_t smem = MS_WARPS * (G::WARP_BYTES + (gate ? MS_NB * 128 * 4 : 0));
+    const size_t smem = MS_WARPS * (G::WARP_BYTES + (gate ? MS_NBB * 128 * 4 : 0));
     auto kern = maxpool_bwd_stream<P, D>;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

@@ -474,9 +474,11 @@ static bool ms_enabled() {
 // -1: not applicable (the caller uses pool.cu's kernels); else DP_OK / an error code
 int maxpool_forward_stream(const float *x, float *y, void *arg, int arg_bytes, long long planes,
                            int h, int w, int p, int d, int act, cudaStream_t st) {
-    // p = 2 stays on pool.cu's register-tile kernel (4.3-4.5 TB/s on the config shapes
-    // against 2.3-4.4 here: two taps per output leave the streaming overhead unamortised)
-    if (arg_bytes != 1 || !ms_enabled() || (p < 3 && !getenv("DP_POOL_STREAM_P2"))) return -1;
+    // p = 2 stays on pool.cu's register-tile kernel except at d = 4..8 (c3 pool2: 0.50 ->
+    // 0.47 ms here; d = 1 / 2 / 16 measured 3-65 % slower: two taps per output leave the
+    // streaming overhead unamortised)
+    const bool p2ok = (d >= 4 && d <= 8) || getenv("DP_POOL_STREAM_P2");
+    if (arg_bytes != 1 || !ms_enabled() || (p < 3 && !p2ok)) return -1;
     const int ho = h - (p - 1) * d, wo = w - (p - 1) * d;
 #define MS_F(PP, DD) ms_fwd_launch<PP, DD>(x, y, (uint8_t *)arg, planes, h, w, ho, wo, act, st)
     MS_PD_SWITCH(p, d, MS_F)

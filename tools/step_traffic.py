@@ -21,7 +21,7 @@ SEQ = [("tc_relayout_pk", "00:conv_forward_tc"), ("tc_conv_flat_kernel<1, 0, 3",
        ("tc_relayout_f16<0>", "02:conv_forward_tc"), ("tc_relayout_f16_pk<0>", "02:conv_forward_tc"),
        ("tc_conv_flat_kernel<0, 0, 1, 1>", "02:conv_forward_tc"),
        ("tc_conv_flat_kernel<0, 0, 0, 0>", "02:conv_forward_tc"),
-       ("maxpool_fwd_tile", "03:maxpool_forward"),
+       ("maxpool_fwd_stream", "03:maxpool_forward"),
        ("tc_relayout_f16<0>", "04:conv_forward_tc"), ("tc_conv_tap_kernel<0, 1>", "04:conv_forward_tc"),
        ("tc_conv_flat_kernel<1, 0, 0, 0>", "04:conv_forward_tc"),
        ("mask_delta", "05:mask_delta"), ("tc_stage_dy", "06:conv_backward_kernel_tc"),

@@ -55,6 +55,9 @@ C4 = ("input channels=3\n"
       "conv out=8 in=128 k=3 stride=1 weights=seed:5\n")
 # plain CNN1 with the paper's 8x8 first pool (patch 133) -- BASELINE configs[4] family
 PLAIN8 = C3.replace("out=8 in=50 k=7", "out=32 in=50 k=7").replace("k=4 stride=4", "k=8 stride=8")
+# the other configs[4] points: 2x2 first pool (patch 37) and the k = 2 first conv (patch 65)
+PLAIN2 = C3.replace("out=8 in=50 k=7", "out=32 in=50 k=7").replace("k=4 stride=4", "k=2 stride=2")
+PLAIN4_K2 = C3.replace("out=8 in=50 k=7", "out=32 in=50 k=7").replace("in=3 k=6", "in=3 k=2")
 
 
 def _run(text, side, batch, frac, seed):
@@ -173,3 +176,13 @@ def test_unforced_c4_512():
 def test_unforced_plain_p8_256():
     """BASELINE configs[4] family: plain CNN1 with the 8x8 first pool (patch 133)."""
     _check(*_run(PLAIN8, 256, 1, 1.0, seed=14))
+
+
+def test_unforced_plain_p2_256():
+    """BASELINE configs[4] family: plain CNN1 with the 2x2 first pool (patch 37)."""
+    _check(*_run(PLAIN2, 256, 1, 1.0, seed=15))
+
+
+def test_unforced_plain_p4_k2_256():
+    """BASELINE configs[4] family: plain CNN1 with a 2x2 first convolution (patch 65)."""
+    _check(*_run(PLAIN4_K2, 256, 1, 1.0, seed=16))

@@ -832,11 +832,17 @@ class DenseNet:
             for _ in range(warmup):
                 fn()
         torch.cuda.current_stream().wait_stream(s)
-        g = torch.cuda.CUDAGraph()
+        try:  # keep the cudaGraph_t so its kernel nodes can be counted (graph_kernel_nodes)
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+        except TypeError:
+            g = torch.cuda.CUDAGraph()
         before = ops.launches
         with torch.cuda.graph(g):
             fn()
         self.graph_kernels = ops.launches - before
+        exact = graph_kernel_nodes(g)
+        if exact is not None:
+            self.graph_kernels = exact
         return g
 
     def activation_bytes(self) -> int:
@@ -856,6 +862,40 @@ class DenseNet:
                 fwd += f
                 bwd += f if gi == 0 else 2 * f
         return {"fwd": fwd, "bwd": bwd}
+
+
+def graph_kernel_nodes(g):
+    """Kernel nodes of OUR library (namespace dp) in a captured CUDA graph, counted from the
+    graph itself through the driver API (cuGraphGetNodes / cuGraphKernelNodeGetParams /
+    cuFuncGetName: the runtime-API variants cannot resolve functions registered by the
+    library's own static runtime); None when that introspection is unavailable (callers then
+    keep the per-op estimate)."""
+    try:
+        from cuda.bindings import driver as drv
+        graph = drv.CUgraph(init_value=g.raw_cuda_graph())
+        err, _, n = drv.cuGraphGetNodes(graph, 0)
+        if int(err) != 0:
+            return None
+        err, nodes, n = drv.cuGraphGetNodes(graph, n)
+        if int(err) != 0:
+            return None
+        count = 0
+        for nd in nodes[:n]:
+            err, kind = drv.cuGraphNodeGetType(nd)
+            if int(err) != 0 or kind != drv.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+                continue
+            err, params = drv.cuGraphKernelNodeGetParams(nd)
+            if int(err) != 0:
+                return None
+            err, name = drv.cuFuncGetName(params.func)
+            if int(err) != 0:
+                return None
+            name = name.decode() if isinstance(name, bytes) else str(name)
+            if "2dp" in name or name.startswith("dp::"):
+                count += 1
+        return count
+    except Exception:  # noqa: BLE001 -- introspection is best effort
+        return None
 
 
 def profile_step(trainer, reps=5):

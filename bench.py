@@ -757,7 +757,8 @@ def main():
         if os.path.exists(mpath):
             with open(mpath) as fh:
                 pts = json.load(fh)["points"]
-            ss = {f"{p['kind']}_n{p['N']}": p["tflops"] for p in pts}
+            ss = {f"{p['kind']}_n{p['N']}": p["tflops"] for p in pts
+                  if p.get("operands", "SS") == "SS" and p.get("layout", "none") == "none"}
             roof["tcgen05_ss_peak_tflops"] = ss
             roof["mma_rate_tflops"] = 3 * roof["achieved"]  # split products issued per s
             for kind in ("tf32", "f16"):  # the weight gradients are 3xTF32

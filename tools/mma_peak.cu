@@ -10,7 +10,25 @@
 #include "../paper_1412_4526_b200/csrc/tc_ptx.cuh"
 using namespace dp;
 
-__global__ void __launch_bounds__(128, 1) peak(int count, int N, int f16, int sw) {
+// A from TMEM (the "TS" form): K-major A rows in TMEM columns
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+
+// sw: 0 = no swizzle, 1 = SWIZZLE_128B, 2 = A from TMEM (TS), 3 = A copied smem -> TMEM
+// (tcgen05.cp 128x256b) before every PAIR of TS MMAs that share it, 4 = before every one.  Accumulators rotate with
+// compile-time offsets over 256 TMEM columns (N = 64: 4, 128: 2, 256: 1), the issue loop is
+// unrolled by 4 (an index computation per MMA made the issuing thread the limit)
+template <int N>
+__global__ void __launch_bounds__(128, 1) peak(int count, int f16, int sw) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t bar;
     __shared__ uint32_t s_tmem;
@@ -32,19 +50,32 @@ __global__ void __launch_bounds__(128, 1) peak(int count, int N, int f16, int sw
         // (sw: K-major SWIZZLE_128B, rows of 128 B in 1 KB atoms, as the weight gradient's
         // TMA boxes write them)
         const uint32_t a0 = ptx::smem_u32(sm), b0 = a0 + 16 * 1024;
-        const uint64_t ad = sw ? ptx::smem_desc_sw128(a0) : ptx::smem_desc(a0, 128 * 16, 128);
+        const uint64_t ad = sw == 1 ? ptx::smem_desc_sw128(a0) : ptx::smem_desc(a0, 128 * 16, 128);
         const uint64_t bd =
-            sw ? ptx::smem_desc_sw128(b0) : ptx::smem_desc(b0, (uint32_t)N * 16, 128);
+            sw == 1 ? ptx::smem_desc_sw128(b0) : ptx::smem_desc(b0, (uint32_t)N * 16, 128);
+        const uint32_t a_tm = tmem + 448;  // A operand columns (TS form), past the accumulators
         const uint32_t idesc = f16 ? ptx::idesc_f16(128, N) : ptx::idesc_tf32(128, N);
         if (ptx::elect_one()) {
-            for (int i = 0; i < count; ++i) {
-                // rotate over every accumulator TMEM holds (512 / N): back-to-back MMAs into
-                // one accumulator serialise on it
-                const uint32_t d = tmem + (uint32_t)((i % (512 / N)) * N);
-                if (f16)
-                    ptx::mma_f16_ss(d, ad, bd, idesc, 1);
-                else
-                    ptx::mma_tf32_ss(d, ad, bd, idesc, 1);
+            constexpr int NACC = 256 / N;
+            for (int i = 0; i < count; i += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t d = tmem + (uint32_t)((u % NACC) * N);
+                    if (sw >= 3 && (sw == 4 || (u & 1) == 0))
+                        cp_128x256b(a_tm + (uint32_t)((u & 2) * 4), ad);
+                    if (sw >= 3 && f16)
+                        mma_f16_ts(d, a_tm + (uint32_t)((u & 2) * 4), bd, idesc, 1);
+                    else if (sw >= 3)
+                        ptx::mma_tf32_ts(d, a_tm + (uint32_t)((u & 2) * 4), bd, idesc, 1);
+                    else if (sw == 2 && f16)
+                        mma_f16_ts(d, a_tm, bd, idesc, 1);
+                    else if (sw == 2)
+                        ptx::mma_tf32_ts(d, a_tm, bd, idesc, 1);
+                    else if (f16)
+                        ptx::mma_f16_ss(d, ad, bd, idesc, 1);
+                    else
+                        ptx::mma_tf32_ss(d, ad, bd, idesc, 1);
+                }
             }
             ptx::mma_commit(&bar);
         }
@@ -63,22 +94,25 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&mhz, cudaDevAttrClockRate, dev);
     const int smem = 64 * 1024;
-    cudaFuncSetAttribute(peak, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(peak<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(peak<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(peak<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int count = 20000;
     printf("{\"sms\": %d, \"points\": [\n", sms);
     bool first = true;
-    for (int sw = 0; sw < 2; ++sw)
+    for (int sw = 0; sw < 5; ++sw)
     for (int f16 = 0; f16 < 2; ++f16)
         for (int N : {64, 128, 256}) {
             const int K = f16 ? 16 : 8;
-            peak<<<sms, 128, smem>>>(200, N, f16, sw);  // warm-up
+            auto kern = N == 64 ? peak<64> : N == 128 ? peak<128> : peak<256>;
+            kern<<<sms, 128, smem>>>(200, f16, sw);  // warm-up
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             float best = 1e30f;
             for (int rep = 0; rep < 5; ++rep) {
                 cudaEventRecord(e0);
-                peak<<<sms, 128, smem>>>(count, N, f16, sw);
+                kern<<<sms, 128, smem>>>(count, f16, sw);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float ms = 0;
@@ -88,9 +122,11 @@ int main() {
             const double flops = 2.0 * 128 * N * K * (double)count * sms;
             const double tf = flops / (best * 1e-3) / 1e12;
             const double cyc = best * 1e-3 * 1965e6 / count;  // at the max SM clock
-            printf("%s {\"kind\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"operands\": \"SS\", \"layout\": \"%s\", "
+            printf("%s {\"kind\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"operands\": \"%s\", \"layout\": \"%s\", "
                    "\"tflops\": %.1f, \"cycles_per_mma_at_1965MHz\": %.1f}",
-                   first ? "" : ",\n", f16 ? "f16" : "tf32", N, K, sw ? "sw128" : "none", tf,
+                   first ? "" : ",\n", f16 ? "f16" : "tf32", N, K, sw >= 2 ? "TS" : "SS",
+                   sw == 4 ? "TS, cp per MMA" : sw == 3 ? "TS, cp per 2 MMAs" :
+                   sw == 2 ? "A in TMEM (TS)" : sw ? "sw128" : "none", tf,
                    cyc);
             first = false;
         }

@@ -221,3 +221,43 @@ def test_sgd_update_matches_numpy(dt):
     want = p - dt(lr) * g
     assert np.array_equal(pt.cpu().numpy(), want)
     assert np.array_equal(gt.cpu().numpy(), g)
+
+
+@pytest.mark.parametrize("act", [0, 1, 3])  # identity, tanh (fp64), tanh (fast)
+@pytest.mark.parametrize("shape", [(2, 6, 4, 1, 70, 135), (2, 5, 2, 4, 66, 128),
+                                   (1, 4, 8, 1, 80, 139), (2, 3, 3, 2, 40, 68)])
+def test_pool_stream_fused_act_gate_pitch(shape, act, monkeypatch):
+    """The engine-facing device pools (batched, fused nonlinearity, fused backward gate, pitched
+    dx): the warp-streaming kernels are bit-identical to pool.cu's (DP_POOL_STREAM=0) -- the
+    gate staged as 16-byte rows (aligned maps) and word by word otherwise."""
+    import torch
+    from paper_1412_4526_b200 import _lib
+    from paper_1412_4526_b200.engine import ops
+    n, c, p, d, h, w = shape
+    e = (p - 1) * d + 1
+    ho, wo = h - e + 1, w - e + 1
+    g = torch.Generator(device="cuda").manual_seed(sum(shape) + act)
+    x = torch.rand((n, c, h, w), device="cuda", generator=g) - 0.5
+    x[:, :, ::3, ::2] = 0.125  # ties
+    dy = torch.rand((n, c, ho, wo), device="cuda", generator=g) - 0.5
+    gate = torch.tanh(torch.rand((n, c, h, w), device="cuda", generator=g) - 0.5)
+    pitch = (w + 7) // 4 * 4
+    out = {}
+    for mode in ("smem", "stream"):
+        if mode == "smem":
+            monkeypatch.setenv("DP_POOL_STREAM", "0")
+        else:
+            monkeypatch.delenv("DP_POOL_STREAM", raising=False)
+        y = torch.empty((n, c, ho, wo), device="cuda")
+        arg = torch.empty((n, c, ho, wo), device="cuda", dtype=torch.uint8)
+        ops.maxpool_forward(x, y, arg, p, d, act)
+        dxs = torch.full((n, c, h, pitch), 7.0, device="cuda")
+        dx = dxs[..., :w]
+        ops.maxpool_backward(dy, arg, dx, p, d, gate, _lib.DP_TANH_FAST, dx_pitch=pitch)
+        dx2 = torch.empty((n, c, h, w), device="cuda")
+        ops.maxpool_backward(dy, arg, dx2, p, d)
+        torch.cuda.synchronize()
+        out[mode] = (y.clone(), arg.clone(), dxs.clone(), dx2.clone())
+    for a, b in zip(out["smem"], out["stream"]):
+        assert torch.equal(a.view(torch.int32) if a.dtype == torch.float32 else a,
+                           b.view(torch.int32) if b.dtype == torch.float32 else b)

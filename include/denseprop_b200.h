@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DP_ABI_VERSION 5
+#define DP_ABI_VERSION 6
 
 enum dp_dtype { DP_F32 = 0, DP_F64 = 1 };
 /* reference nonlin kinds, netspec.py:31 / forward.py:69-76 */
@@ -172,6 +172,25 @@ int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const 
                                     int dy_pitch, float *dw, float *db, int n, int cin, int hi,
                                     int wi, int cout, int k, int d, void *workspace,
                                     size_t workspace_bytes, void *stream);
+/* fp16-split weight gradient (ABI 6): the same dw / db as dp_conv_backward_kernel_fast_ex
+ * (x, x_slack_bytes, dy_pitch as there) with x also handed over pre-split as two fp16 NCHW
+ * tensors x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11), xh_slack_bytes readable (and
+ * finite) past each, read in place (every tap offset a multiple of 8 halves, W % 8 == 0); dy is
+ * split the same way into the workspace.  Products hi.hi + (hi.lo' + lo'.hi) * 2^-11 on
+ * kind::f16 with 64-pixel K blocks: half the MMAs and shared-memory operand bytes of the tf32
+ * kernel, and a smaller error (fp16's 11-bit hi vs tf32's).  The caller guarantees |x| < 2^15;
+ * a dy element outside (-2^15, 2^15) or not finite sends the call, on the device, to the tf32
+ * kernel on x.  _workspace returns 0 where the fp16 form does not apply. */
+size_t dp_conv_backward_kernel_fast_f16_workspace(int n, int cin, int hi, int wi, int cout,
+                                                  int k, int d);
+/* x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11) elementwise (the split the fp16
+ * weight gradient reads); 16-byte aligned pointers (ABI 6) */
+int dp_split_f16(const float *x, void *x_hi, void *x_lo, int64_t count, void *stream);
+int dp_conv_backward_kernel_fast_f16(const float *x, size_t x_slack_bytes, const void *x_hi,
+                                     const void *x_lo, size_t xh_slack_bytes, const float *dy,
+                                     int dy_pitch, float *dw, float *db, int n, int cin, int hi,
+                                     int wi, int cout, int k, int d, void *workspace,
+                                     size_t workspace_bytes, void *stream);
 /* Split form (ABI 4): _prepare stages x (the re-laid-out / shifted copies the kernel's TMA
  * boxes read) into `workspace`; it depends on x only, so it can run as soon as x exists
  * (the engine overlaps it with the forward pass on a side stream).  _staged then runs the

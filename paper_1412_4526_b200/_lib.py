@@ -23,7 +23,7 @@ DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED = 0, 1, 2, 3
 NONLIN_CODE = {"identity": DP_IDENTITY, "tanh": DP_TANH, "relu": DP_RELU}
 DP_POOL_MAX, DP_POOL_AVG = 0, 1  # enum dp_pool_kind
 DP_FAST_INPUT_FP16_RANGE = 1  # enum dp_fast_flags
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _vp, _i, _i64, _sz, _d = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double
 
@@ -66,6 +66,10 @@ SIGNATURES = {
     "dp_maxpool_backward_pitched": (_i, [_i, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i,
                                          _i, _i, _vp, _i, _vp]),
     "dp_conv_backward_kernel_fast_prepare": (_i, [_vp] + [_i] * 7 + [_vp, _sz, _vp]),
+    "dp_conv_backward_kernel_fast_f16_workspace": (_sz, [_i] * 7),
+    "dp_split_f16": (_i, [_vp, _vp, _vp, _i64, _vp]),
+    "dp_conv_backward_kernel_fast_f16": (_i, [_vp, _sz, _vp, _vp, _sz, _vp, _i, _vp, _vp] +
+                                         [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_fast_staged": (_i, [_vp, _vp, _vp, _vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
     "dp_conv_backward_kernel": (_i, [_i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp,

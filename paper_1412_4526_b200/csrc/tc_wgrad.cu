@@ -478,7 +478,10 @@ __global__ void __launch_bounds__(256) tc_stage_x_taps(const float *__restrict__
 __global__ void __launch_bounds__(256) tc_stage_dy(const float *__restrict__ src,
                                                    float *__restrict__ dst, int O, int H, int w,
                                                    int wp, int lm, long long total_quads,
-                                                   int ws) {  // ws: source row pitch
+                                                   int ws,  // ws: source row pitch
+                                                   const int *exit_unless) {
+    // the tf32 fallback of an fp16-split weight gradient: runs only when its range flag is set
+    if (exit_unless && !*(volatile const int *)exit_unless) return;
     const int nq = wp >> 2;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total_quads;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -646,11 +649,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 wg_encode() {
 }
 
 static int wg_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
-                  const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz) {
+                  const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz,
+                  bool f16 = false) {
     auto enc = wg_encode();
     if (!enc) return set_error(DP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, (void *)base, dims, strides_bytes,
+    CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     rank, (void *)base, dims, strides_bytes,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -671,6 +676,85 @@ unsigned long long *wg_trace_buffer(cudaStream_t st) {
 int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz) {
     return wg_map(m, base, rank, dims, strides_bytes, box, swz);
+}
+int wg_make_map16(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
+                  const cuuint64_t *strides_bytes, const cuuint32_t *box) {
+    return wg_map(m, base, rank, dims, strides_bytes, box, true, true);
+}
+
+// dy staging for the fp16-split weight gradient: NCHW fp32 (row pitch ws) -> two fp16
+// tensors (n, h, o, wp) hi = RN(dy), lo' = RN((dy - hi) * 2^11) (the data gradient's offset
+// split), lm zeros left of each row; one thread per 8 destination halves (16-byte stores)
+__global__ void __launch_bounds__(256) tc_stage_dy16(const float *__restrict__ src,
+                                                     uint4 *__restrict__ dhi,
+                                                     uint4 *__restrict__ dlo, int O, int H,
+                                                     int w, int wp, int lm, long long total8,
+                                                     int ws, int *flag) {
+    const int n8 = wp >> 3;
+    bool bad = false;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total8;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long row = idx / n8;  // (n, o, h)
+        const int v = (int)(idx - row * n8) * 8;
+        const int h = (int)(row % H);
+        const long long no = row / H;
+        const int o = (int)(no % O);
+        const long long n = no / O;
+        const float *s = src + row * ws;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c0 = v + 2 * q - lm, c1 = c0 + 1;
+            const float e0 = (c0 >= 0 && c0 < w) ? __ldg(s + c0) : 0.f;
+            const float e1 = (c1 >= 0 && c1 < w) ? __ldg(s + c1) : 0.f;
+            bad |= !(fabsf(e0) < ptx::F16_SPLIT_MAX) || !(fabsf(e1) < ptx::F16_SPLIT_MAX);
+            ptx::f16_split2_scaled(e0, e1, hw[q], lw[q]);
+        }
+        const long long di = (((n * H + h) * O + o) * wp + v) >> 3;
+        dhi[di] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        dlo[di] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    if (bad) atomicOr(flag, 1);
+}
+int wg_stage_dy16(const float *dy, void *dhi, void *dlo, int n, int cout, int ho, int wo,
+                  int wp, int lm, cudaStream_t st, int src_pitch, int *flag) {
+    const long long total8 = (long long)n * cout * ho * (wp / 8);
+    tc_stage_dy16<<<stage_grid(total8), 256, 0, st>>>(dy, (uint4 *)dhi, (uint4 *)dlo, cout, ho,
+                                                      wo, wp, lm, total8,
+                                                      src_pitch > 0 ? src_pitch : wo, flag);
+    return check_launch("tc_stage_dy16");
+}
+// x -> (hi, lo') for the fp16-split weight gradient's in-place operands (the engine splits
+// an activation once in the forward pass); 8 elements per thread, 16-byte stores
+__global__ void __launch_bounds__(256) tc_split_f16(const float *__restrict__ x,
+                                                    __half *__restrict__ hi,
+                                                    __half *__restrict__ lo, long long count) {
+    const long long n8 = count >> 3;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(x) + 2 * i);
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(x) + 2 * i + 1);
+        uint32_t hw[4], lw[4];
+        ptx::f16_split2_scaled(a.x, a.y, hw[0], lw[0]);
+        ptx::f16_split2_scaled(a.z, a.w, hw[1], lw[1]);
+        ptx::f16_split2_scaled(b.x, b.y, hw[2], lw[2]);
+        ptx::f16_split2_scaled(b.z, b.w, hw[3], lw[3]);
+        reinterpret_cast<uint4 *>(hi)[i] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        reinterpret_cast<uint4 *>(lo)[i] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (count & 7)) {
+        const long long j = (count & ~7LL) + threadIdx.x;
+        const __half h = __float2half_rn(x[j]);
+        hi[j] = h;
+        lo[j] = __float2half_rn((x[j] - __half2float(h)) * ptx::F16_LO_SCALE);
+    }
+}
+int tc_split_f16_launch(const float *x, void *hi, void *lo, long long count, cudaStream_t st) {
+    if (((uintptr_t)x & 15) || ((uintptr_t)hi & 15) || ((uintptr_t)lo & 15))
+        return set_error(DP_ERR_ARG, "fp16 split: pointers must be 16-byte aligned");
+    if (count <= 0) return DP_OK;
+    tc_split_f16<<<stage_grid(count / 8 + 1), 256, 0, st>>>(x, (__half *)hi, (__half *)lo, count);
+    return check_launch("tc_split_f16");
 }
 int wg_sms() { return wg_num_sms(); }
 int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
@@ -695,10 +779,10 @@ int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, i
     return DP_OK;
 }
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
-                cudaStream_t st, int src_pitch) {
+                cudaStream_t st, int src_pitch, const int *exit_unless) {
     const long long quads = (long long)n * cout * ho * (wp / 4);
     tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, lm, quads,
-                                                   src_pitch > 0 ? src_pitch : wo);
+                                                   src_pitch > 0 ? src_pitch : wo, exit_unless);
     return check_launch("tc_stage_dy");
 }
 
@@ -708,7 +792,7 @@ size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d);
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
                             size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack,
-                            int dy_pitch);
+                            int dy_pitch, const int *exit_unless = nullptr);
 
 // Split form (engine): stage x early (phase 1, may run during the forward pass), the rest
 // later (phase 2).  Only the smem-operand kernel splits; the TMEM-operand fallback stages
@@ -788,7 +872,7 @@ int tc_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
         const long long quads = (long long)n * cout * p.ho * (p.wp_dy / 4);
         tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dp_, cout, p.ho, p.wo, p.wp_dy, 0, quads,
-                                                       p.wo);
+                                                       p.wo, nullptr);
         rc = check_launch("tc_stage_dy");
         if (rc) return rc;
         dys = dp_;

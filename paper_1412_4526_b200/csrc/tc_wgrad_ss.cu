@@ -52,6 +52,10 @@ namespace dp {
 
 int wg_make_map(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides_bytes, const cuuint32_t *box, bool swz);
+int wg_make_map16(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
+                  const cuuint64_t *strides_bytes, const cuuint32_t *box);
+int wg_stage_dy16(const float *dy, void *dhi, void *dlo, int n, int cout, int ho, int wo,
+                  int wp, int lm, cudaStream_t st, int src_pitch, int *flag);
 int wg_sms();
 unsigned long long *wg_trace_buffer(cudaStream_t st);
 int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int mask,
@@ -59,7 +63,7 @@ int wg_stage_x(const float *x, float *xs, int n, int cin, int hi, int wi, int wp
 int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, int wp, int l,
                     int d, long long copy_floats, cudaStream_t st);
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
-                cudaStream_t st, int src_pitch);
+                cudaStream_t st, int src_pitch, const int *exit_unless);
 
 constexpr int WS_CONV_WARPS = 8;
 constexpr int WS_TMA_WARP = 8;
@@ -99,7 +103,10 @@ struct WsArgs {
     float *pdb;   // [splits][Npad]
     int no_m64;   // DP_WG_NO_M64: run a short last tile as M = 128 (experiments)
     int pf;       // L2 prefetch distance in K blocks (DP_WG_PF, 0 = off)
+    int f16;      // fp16-split operands: tm_x1 = x lo', tm_xp = dy lo' (offset split, 2^11)
     unsigned long long *trace;  // DP_WG_TRACE: per-K-block clock64 stamps of CTA 0
+    const int *exit_if;         // fp16 kernel: exit when its operands tripped the range flag
+    const int *exit_unless;     // its tf32 fallback: run only when they did
 };
 
 // slots: 1 producer ready, 0 TMA issue, 2 converters got the stage, 4 converters done,
@@ -161,6 +168,9 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
     __shared__ uint64_t sfull[WS_MAX_SS], cfull[WS_MAX_SS], sempty[WS_MAX_SS], accfull;
     __shared__ uint32_t s_tmem;
 
+    if ((a.exit_if && *(volatile const int *)a.exit_if) ||
+        (a.exit_unless && !*(volatile const int *)a.exit_unless))
+        return;  // block-uniform, before any barrier or TMEM allocation
     unsigned char *smem = (unsigned char *)(((uintptr_t)ws_smem_raw + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x % a.n_groups, split = blockIdx.x / a.n_groups;
@@ -207,15 +217,22 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         int pre = 0;  // this block's new row came with the previous block's 2-row box
         for (int kl = 0; kl < nkb; ++kl, sc.next(), pf.next()) {
             if (a.pf && lane == 0 && kl + a.pf < nkb) {
-                const int pv0 = pf.vb * 32;
+                const int pv0 = pf.vb * (a.f16 ? 64 : 32);
                 if (a.J == 1)
                     ptx::tma_prefetch_l2_4d(&tm_dy, pv0, pf.u, 0, pf.img);
                 else
                     ptx::tma_prefetch_l2_5d(&tm_dy, pv0, 0, 0, pf.u, pf.img);
+                if (a.f16 && a.J == 1)
+                    ptx::tma_prefetch_l2_4d(&tm_xp, pv0, pf.u, 0, pf.img);
+                else if (a.f16)
+                    ptx::tma_prefetch_l2_5d(&tm_xp, pv0, 0, 0, pf.u, pf.img);
                 for (int k = pf.cstart ? 0 : n_i - 1; k < n_i; ++k) {
                     if (a.direct) {
                         ptx::tma_prefetch_l2_5d(&tm_x0, pv0 + a.rs.j0[0] * a.d, 0, 0,
                                                 pf.u + (i_lo + k) * a.d, pf.img);
+                        if (a.f16)
+                            ptx::tma_prefetch_l2_5d(&tm_x1, pv0 + a.rs.j0[0] * a.d, 0, 0,
+                                                    pf.u + (i_lo + k) * a.d, pf.img);
                         continue;
                     }
                     const int prow = pf.img * a.Hi + pf.u + (i_lo + k) * a.d;
@@ -235,8 +252,9 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 ptx::mbar_wait(&sempty[kw % a.SS], (kw / a.SS) & 1);
             }
             if (lane == 0) {
-                const int v0 = sc.vb * 32;
+                const int v0 = sc.vb * (a.f16 ? 64 : 32);
                 const int hh = sc.img * a.Hi + sc.u;
+                const uint32_t f16x = a.f16 ? 2u : 1u;  // fp16 split: hi and lo' boxes
                 const int k0 = sc.cstart ? 0 : n_i - 1;
                 WS_TRACE(a, kl, 0, true);
                 // TMA box count, not bytes, limits this producer: inside a column one 2-row
@@ -257,8 +275,15 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 } else {
                     nbox_rows = skip ? 0 : pair ? 2 : 1;
                 }
-                ptx::mbar_expect_tx(&sfull[s], (uint32_t)(a.J * a.Q) * 128u +
-                                                   (uint32_t)nbox_rows * a.box_tx_row);
+                ptx::mbar_expect_tx(&sfull[s], f16x * ((uint32_t)(a.J * a.Q) * 128u +
+                                                          (uint32_t)nbox_rows * a.box_tx_row));
+                if (a.f16) {  // B_lo' straight from the staged fp16 lo' rows
+                    unsigned char *bl = smem + (size_t)s * a.b_bytes + (size_t)a.NB * 128;
+                    if (a.J == 1)
+                        ptx::tma_load_4d(bl, &tm_xp, v0, sc.u, 0, sc.img, &sfull[s]);
+                    else
+                        ptx::tma_load_5d(bl, &tm_xp, v0, 0, 0, sc.u, sc.img, &sfull[s]);
+                }
                 if (a.J == 1) {
                     ptx::tma_load_4d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, sc.u, 0, sc.img,
                                      &sfull[s]);
@@ -286,6 +311,10 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                             // NCHW in place: (w, jj, c, h, n); rows past Hi zero-fill
                             ptx::tma_load_5d(dst, &tm_x0, v0 + a.rs.j0[0] * a.d, 0, 0,
                                              sc.u + (i_lo + k) * a.d, sc.img, &sfull[s]);
+                            if (a.f16)  // the lo' row into the lo ring
+                                ptx::tma_load_5d(dst + (a.ring_lo - a.ring_hi), &tm_x1,
+                                                 v0 + a.rs.j0[0] * a.d, 0, 0,
+                                                 sc.u + (i_lo + k) * a.d, sc.img, &sfull[s]);
                             continue;
                         }
                         for (int rb = 0; rb < a.rs.n_b; ++rb) {
@@ -302,10 +331,12 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         }
     } else if (warp == WS_MMA_WARP) {
         // ================================ MMA issuer ================================
-        const uint32_t idesc_2n = ptx::idesc_tf32(128, 2 * a.NB);
-        const uint32_t idesc_n = ptx::idesc_tf32(128, a.NB);
-        const uint32_t idesc_2n64 = ptx::idesc_tf32(64, 2 * a.NB);
-        const uint32_t idesc_n64 = ptx::idesc_tf32(64, a.NB);
+        const uint32_t idesc_2n =
+            a.f16 ? ptx::idesc_f16(128, 2 * a.NB) : ptx::idesc_tf32(128, 2 * a.NB);
+        const uint32_t idesc_n = a.f16 ? ptx::idesc_f16(128, a.NB) : ptx::idesc_tf32(128, a.NB);
+        const uint32_t idesc_2n64 =
+            a.f16 ? ptx::idesc_f16(64, 2 * a.NB) : ptx::idesc_tf32(64, 2 * a.NB);
+        const uint32_t idesc_n64 = a.f16 ? ptx::idesc_f16(64, a.NB) : ptx::idesc_tf32(64, a.NB);
         const uint32_t sbase = ptx::smem_u32(smem);
         const uint32_t hi_base = sbase + a.ring_hi, lo_base = sbase + a.ring_lo;
         // tile 0's first ring slot (relative to the block's Bm) and line inside it; later
@@ -337,10 +368,21 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                     const uint32_t dcol = tmem + (uint32_t)(t * acc_cols);
                     const bool m64 = tail64 && t == G - 1;
                     const uint32_t i2 = m64 ? idesc_2n64 : idesc_2n, i1 = m64 ? idesc_n64 : idesc_n;
+                    if (a.f16) {
+                        // offset split: [hi.hi | hi.lo'] + lo'.hi into the lo' half (scaled
+                        // back by 2^-11 in the epilogue); K = 16 halves per 32-byte slice
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) {
-                        ptx::mma_tf32_ss(dcol, da + 2 * ks, bd0 + 2 * ks, i2, (kl | ks) > 0);
-                        ptx::mma_tf32_ss(dcol, da + lo_units + 2 * ks, bd0 + 2 * ks, i1, 1);
+                        for (int ks = 0; ks < 4; ++ks) {
+                            ptx::mma_f16_ss(dcol, da + 2 * ks, bd0 + 2 * ks, i2, (kl | ks) > 0);
+                            ptx::mma_f16_ss(dcol + (uint32_t)a.NB, da + lo_units + 2 * ks,
+                                            bd0 + 2 * ks, i1, 1);
+                        }
+                    } else {
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) {
+                            ptx::mma_tf32_ss(dcol, da + 2 * ks, bd0 + 2 * ks, i2, (kl | ks) > 0);
+                            ptx::mma_tf32_ss(dcol, da + lo_units + 2 * ks, bd0 + 2 * ks, i1, 1);
+                        }
                     }
                 }
                 ptx::mma_commit(&sempty[s]);
@@ -375,7 +417,28 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
             ptx::mbar_wait(&sfull[s], ph);
             WS_TRACE(a, kl, 2, tid == 0);
             unsigned char *st = smem + (size_t)s * a.b_bytes;
-            {
+            if (a.f16) {
+                // db from the staged split: dy = hi + lo' * 2^-11 (8 halves per chunk)
+                const uint4 *bh = reinterpret_cast<const uint4 *>(st);
+                const uint4 *bl = reinterpret_cast<const uint4 *>(st + (uint32_t)a.NB * 128);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int idx = tid + 256 * m;
+                    if (idx >= nchunks) break;
+                    if (idx < db0 || idx >= db1) continue;
+                    const uint4 h4 = bh[idx], l4 = bl[idx];
+                    const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
+                    float sum = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hw[q]));
+                        const float2 lf = __half22float2(*reinterpret_cast<const __half2 *>(&lw[q]));
+                        sum += (hf.x + lf.x * (1.f / ptx::F16_LO_SCALE)) +
+                               (hf.y + lf.y * (1.f / ptx::F16_LO_SCALE));
+                    }
+                    dbacc[m] += sum;
+                }
+            } else {
                 // B_lo = B_hi - trunc(B_hi) (elementwise; the swizzle is preserved) + db
                 const float4 *bh = reinterpret_cast<const float4 *>(st);
                 float4 *bl = reinterpret_cast<float4 *>(st + (uint32_t)a.NB * 128);
@@ -406,6 +469,14 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                                  ? reinterpret_cast<float4 *>(smem + a.ring_hi +
                                                               (size_t)(a.R + slot) * a.slot_bytes)
                                  : nullptr;
+                if (a.f16) {  // lo' came with the row (TMA): only the mirrors are copied
+                    if (slot < a.NM)
+                        for (int idx = tid; idx < lchunks; idx += WS_CONV_WARPS * 32) {
+                            dst2[idx] = dst[idx];
+                            if (hm) hm[idx] = src[idx];
+                        }
+                    continue;
+                }
                 for (int idx = tid; idx < lchunks; idx += WS_CONV_WARPS * 32) {
                     const float4 v = src[idx];
                     const float4 lo = make_float4(ptx::tf32_lo(v.x), ptx::tf32_lo(v.y),
@@ -463,11 +534,12 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
 #pragma unroll
                 for (int k = 0; k < 16; k += 4) {
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float ls = a.f16 ? 1.f / ptx::F16_LO_SCALE : 1.f;  // offset split
                     if (nkb > 0)
-                        v = make_float4(__uint_as_float(h[k]) + __uint_as_float(l2[k]),
-                                        __uint_as_float(h[k + 1]) + __uint_as_float(l2[k + 1]),
-                                        __uint_as_float(h[k + 2]) + __uint_as_float(l2[k + 2]),
-                                        __uint_as_float(h[k + 3]) + __uint_as_float(l2[k + 3]));
+                        v = make_float4(__uint_as_float(h[k]) + __uint_as_float(l2[k]) * ls,
+                                        __uint_as_float(h[k + 1]) + __uint_as_float(l2[k + 1]) * ls,
+                                        __uint_as_float(h[k + 2]) + __uint_as_float(l2[k + 2]) * ls,
+                                        __uint_as_float(h[k + 3]) + __uint_as_float(l2[k + 3]) * ls);
                     if (store) *reinterpret_cast<float4 *>(dstp + o0 + k) = v;
                 }
             }
@@ -488,7 +560,11 @@ constexpr int WR_GROUPS = 8;
 __global__ void __launch_bounds__(32 * WR_GROUPS)
     ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb, float *__restrict__ dw,
               float *__restrict__ db, int Q, int C, int l, int Ls, int Npad, int J, int Ja,
-              int splits, int rows_pad, WsResidues rs) {
+              int splits, int rows_pad, WsResidues rs, const int *exit_if,
+              const int *exit_unless) {
+    if ((exit_if && *(volatile const int *)exit_if) ||
+        (exit_unless && !*(volatile const int *)exit_unless))
+        return;
     __shared__ float red[WR_GROUPS][32];
     const long long lines = (long long)l * Ls;
     const int NB = (J * Q + 15) / 16 * 16;
@@ -551,7 +627,7 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
 // host side
 // --------------------------------------------------------------------------------
 struct WsPlan {
-    int pair, direct;
+    int pair, direct, f16;
     int J, kc, dc, sb, NB;  // J dy copies (B), kc = Ja column taps in the x lines (A), step dc = d
     int Cpad, Npad, Ls, n_tiles, G, n_groups, splits, SS, R, NM, max_ni;
     int ho, wo, nvb, T, wp_x, wp_dy, lm_dy, mask;
@@ -565,7 +641,7 @@ struct WsPlan {
 static size_t ws_align256(size_t v) { return (v + 255) / 256 * 256; }
 
 static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, int Ja,
-                      WsPlan &p);
+                      WsPlan &p, bool f16 = false);
 
 // x read in place (no tc_stage_x copy): one residue at offset 0 (every tap offset j*d a
 // multiple of 4 floats), 16-byte rows, no 2-row boxes (a 6th map dimension), and the caller
@@ -597,18 +673,19 @@ static void ws_try_direct(WsPlan &p, int cin, int wi, int d, size_t x_slack) {
 // needs 4 | Ja*d (Ja = k: no stacking, the unstacked kernel).  Ja is picked by a per-K-block
 // cost model of the shared-memory operand bytes (A hi + lo per tile, B per MMA) and issue
 // slots; DP_WG_J=<J> forces the smallest legal Ja with that many dy copies.
-static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPlan &p) {
+static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPlan &p,
+                    bool f16 = false) {
     if (const char *e = getenv("DP_WG_J")) {
         const int J = atoi(e);
         for (int Ja = 1; Ja <= k && J >= 1; ++Ja)
-            if ((k + Ja - 1) / Ja == J && ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, p))
+            if ((k + Ja - 1) / Ja == J && ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, p, f16))
                 return true;
     }
     bool ok = false;
     double best = 0;
     for (int Ja = k; Ja >= 1; --Ja) {
         WsPlan q;
-        if (!ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, q)) continue;
+        if (!ws_plan_j(n, cin, hi, wi, cout, k, d, Ja, q, f16)) continue;
         // cycles per K block (measured model): the tensor core -- an SS MMA costs
         // max(39, N/2) cycles (tools/tc_probe.cu), 2 per K=8 slice and tile, 4 slices, plus
         // the commit -- or the TMA producer, ~550 cycles per box (dy + the x boxes of the
@@ -627,9 +704,14 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
     return ok;
 }
 
+// f16: the fp16-split variant (x pre-split into fp16 hi / lo' NCHW tensors read in place,
+// dy staged as fp16 hi / lo'; K blocks of 64 px so a 128-byte line still holds one K block):
+// every tap offset must be a multiple of 8 halves (16 bytes: TMA box starts), no 2-row boxes
 static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, int Ja,
-                      WsPlan &p) {
+                      WsPlan &p, bool f16) {
     if (getenv("DP_WG_TMEM")) return false;  // force the TMEM-operand kernel (experiments)
+    p.f16 = f16 ? 1 : 0;
+    const int KB = f16 ? 64 : 32;  // pixels per K block (one 128-byte line)
     const int e = (k - 1) * d + 1;
     p.ho = hi - e + 1;
     p.wo = wi - e + 1;
@@ -644,8 +726,11 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     p.kc = Ja;
     p.dc = d;
     p.sb = p.kc * d;
-    if (J > 1 && (p.sb & 3)) return false;
+    if (J > 1 && (p.sb & (f16 ? 7 : 3))) return false;
     const int kc = p.kc, dc = p.dc;
+    if (f16)
+        for (int j = 0; j < kc; ++j)
+            if ((j * dc) & 7) return false;
     p.Cpad = (cin + 7) / 8 * 8;
     if (p.Cpad > 256) return false;
     // lines per ring slot (one input row): residue boxes, each rounded up to 8 lines.  Small
@@ -670,7 +755,7 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     // 2-row x boxes need one box per row whose lines fill the slot exactly (the tap
     // dimension is padded with zero-filled taps to Ls / cin)
     // (only for rows of <= 8 KB: a 2-row box of 16-KB rows measured 23 % slower, c2 conv3 J=1)
-    p.pair = ((nres == 1 || p.rs.tapcopy) && p.Ls % cin == 0 && p.Ls <= 64 &&
+    p.pair = (!f16 && (nres == 1 || p.rs.tapcopy) && p.Ls % cin == 0 && p.Ls <= 64 &&
               !getenv("DP_WG_NOPAIR") && !getenv("DP_WG_TMA_MIRROR"))
                  ? 1
                  : 0;
@@ -765,7 +850,7 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     // bytes the residue boxes of one row deliver (zero-filled padding taps included)
     p.box_tx_row = (uint32_t)cin * (p.pair ? p.rs.n[0] : kc) * 128u;
     // K runs over x-aligned columns: dy shifted by up to (J-1) Ja d needs that many more
-    p.nvb = (p.wo + (J - 1) * p.sb + 31) / 32;
+    p.nvb = (p.wo + (J - 1) * p.sb + KB - 1) / KB;
     p.T = (p.ho + d - 1) / d;
     p.kb_total = (long long)n * p.nvb * d * p.T;
     p.splits = wg_sms() / p.n_groups;
@@ -775,16 +860,19 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     // J > 1: dy always staged, with (J-1)*sb zeros left of each row and zeros right of it up
     // to the last K block's reach, so the overlapping-view box never leaves the row
     p.lm_dy = (J - 1) * p.sb;
-    p.wp_dy = J > 1 ? p.nvb * 32 + p.lm_dy : (p.wo + 3) / 4 * 4;
-    p.stage_dy = J > 1 || p.wp_dy != p.wo;
+    p.wp_dy = J > 1 ? p.nvb * KB + p.lm_dy : (f16 ? (p.wo + 7) / 8 * 8 : (p.wo + 3) / 4 * 4);
+    p.stage_dy = f16 || J > 1 || p.wp_dy != p.wo;
     if ((long long)n * hi > (1LL << 31)) return false;
     p.part_bytes = ws_align256((size_t)p.splits * p.n_tiles * 128 * p.NB * 4);
     p.pdb_bytes = ws_align256((size_t)p.splits * p.Npad * 4);
     // boxes read up to (kc*J-1)*d + 32 floats past a row's end (those columns meet zero dy)
     p.copy_bytes =
         ws_align256((size_t)n * cin * hi * p.wp_x * 4 + ((size_t)(kc * J - 1) * d + 64) * 4);
-    p.x_bytes = (size_t)(p.rs.tapcopy ? kc : p.rs.n_b) * p.copy_bytes;
-    p.dy_bytes = p.stage_dy ? ws_align256((size_t)n * cout * p.ho * p.wp_dy * 4) : 0;
+    p.x_bytes = f16 ? 0 : (size_t)(p.rs.tapcopy ? kc : p.rs.n_b) * p.copy_bytes;
+    // f16: dy staged as two fp16 tensors (hi, lo')
+    p.dy_bytes = !p.stage_dy ? 0
+                 : f16 ? 2 * ws_align256((size_t)n * cout * p.ho * p.wp_dy * 2)
+                       : ws_align256((size_t)n * cout * p.ho * p.wp_dy * 4);
     p.total_bytes = p.part_bytes + p.pdb_bytes + p.x_bytes + p.dy_bytes;
     return true;
 }
@@ -819,7 +907,7 @@ size_t ws_workspace(int n, int cin, int hi, int wi, int cout, int k, int d) {
 int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *db, int n,
                             int cin, int hi, int wi, int cout, int k, int d, void *ws,
                             size_t ws_bytes, cudaStream_t st, int phases, size_t x_slack,
-                            int dy_pitch) {
+                            int dy_pitch, const int *exit_unless) {
     WsPlan p;
     if (!ws_plan(n, cin, hi, wi, cout, k, d, p))
         return set_error(DP_ERR_UNSUPPORTED, "weight gradient (smem operands): unsupported shape");
@@ -855,7 +943,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     const float *dys = dy;
     if (stage_dy) {
         float *dp_ = (float *)(w8 + p.part_bytes + p.pdb_bytes + p.x_bytes);
-        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st, pitch);
+        rc = wg_stage_dy(dy, dp_, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st, pitch, exit_unless);
         if (rc) return rc;
         dys = dp_;
     }
@@ -928,6 +1016,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.sb = p.sb;
     a.NB = p.NB;
     a.tma_mirror = getenv("DP_WG_TMA_MIRROR") ? 1 : 0;
+    a.f16 = 0;
     a.pair = p.pair;
     a.direct = p.direct;
     a.n_tiles = p.n_tiles;
@@ -957,8 +1046,10 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.ring_hi = (uint32_t)p.SS * p.b_bytes;
     a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
     a.rs = p.rs;
-    a.trace = getenv("DP_WG_TRACE") ? wg_trace_buffer(st) : nullptr;
+    a.trace = getenv("DP_WG_TRACE") && !exit_unless ? wg_trace_buffer(st) : nullptr;
     a.no_m64 = getenv("DP_WG_NO_M64") ? 1 : 0;
+    a.exit_if = nullptr;
+    a.exit_unless = exit_unless;
     const size_t smem = (size_t)a.ring_lo + (size_t)(p.R + p.NM) * p.slot_bytes + 1024;
     cudaError_t e = cudaFuncSetAttribute(tc_wgrad_ss_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -971,8 +1062,154 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     const long long total = (long long)k * p.Ls * p.NB + cout;
     ws_reduce<<<ceil_div(total, 32), 32 * WR_GROUPS, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
                                                     p.Npad, p.J, p.kc, p.splits, p.n_tiles * 128,
-                                                    p.rs);
+                                                    p.rs, nullptr, exit_unless);
     return check_launch("ws_reduce");
+}
+
+// fp16-split weight gradient: x arrives pre-split as two fp16 NCHW tensors (hi = RN(x),
+// lo' = RN((x - hi) * 2^11), the caller's job -- the engine's pool forward emits them) read in
+// place; dy is split here.  Same ring / schedule / epilogue as the tf32 kernel with 64-px K
+// blocks (one 128-byte line of halves): half the MMAs and shared-memory operand bytes per
+// pixel.  Range guard as the fp16 convolutions: the dy split flags any |dy| >= 2^15 (or not
+// finite) and the tf32 kernel on the fp32 x runs instead (the caller guarantees |x| < 2^15:
+// it splits only bounded activations).  Workspace: [fp16 plan | flag | tf32 plan].
+static bool ws_f16_inplace(const WsPlan &p, int wi) {
+    return p.rs.n_b == 1 && p.rs.b[0] == 0 && wi % 8 == 0;
+}
+static size_t ws_f16_overrun(const WsPlan &p, int d) {  // bytes the tap view reads past x
+    return ((size_t)(p.rs.n[0] - 1) * p.rs.step * d + 64) * 2;
+}
+
+size_t ws_workspace_f16(int n, int cin, int hi, int wi, int cout, int k, int d) {
+    WsPlan p, q;
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p, true) || !ws_f16_inplace(p, wi) ||
+        !ws_plan(n, cin, hi, wi, cout, k, d, q))
+        return 0;
+    return p.total_bytes + 256 + q.total_bytes;
+}
+
+int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi,
+                                const void *x_lo, size_t xh_slack, const float *dy, int dy_pitch,
+                                float *dw, float *db, int n, int cin, int hi, int wi, int cout,
+                                int k, int d, void *ws, size_t ws_bytes, cudaStream_t st) {
+    WsPlan p, q;
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p, true) || !ws_plan(n, cin, hi, wi, cout, k, d, q))
+        return set_error(DP_ERR_UNSUPPORTED, "fp16 weight gradient: unsupported shape");
+    // x in place: one residue at offset 0, 16-byte rows of halves, slack for the tap view
+    if (!ws_f16_inplace(p, wi) || xh_slack < ws_f16_overrun(p, d) || ((uintptr_t)x_hi & 15) ||
+        ((uintptr_t)x_lo & 15))
+        return set_error(DP_ERR_UNSUPPORTED, "fp16 weight gradient: x not readable in place");
+    p.direct = 1;
+    p.R = p.max_ni + p.SS - 1;
+    const size_t need = p.total_bytes + 256 + q.total_bytes;
+    if (ws == nullptr || ws_bytes < need || ((uintptr_t)ws & 255))
+        return set_error(DP_ERR_ARG, "fp16 weight gradient: workspace %zu < %zu bytes or "
+                         "misaligned", ws_bytes, need);
+    unsigned char *w8 = (unsigned char *)ws;
+    int *flag = (int *)(w8 + p.total_bytes);
+    if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess)
+        return set_error(DP_ERR_CUDA, "fp16 weight gradient: flag reset failed");
+    WsArgs a;
+    a.part = (float *)w8;
+    a.pdb = (float *)(w8 + p.part_bytes);
+    unsigned char *dhi = w8 + p.part_bytes + p.pdb_bytes;
+    unsigned char *dlo = dhi + p.dy_bytes / 2;
+    const int pitch = dy_pitch > 0 ? dy_pitch : p.wo;
+    int rc = wg_stage_dy16(dy, dhi, dlo, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st, pitch, flag);
+    if (rc) return rc;
+    CUtensorMap mx[4], mdy, mdyl;
+    const cuuint64_t rowb = (cuuint64_t)p.wp_dy * 2;
+    for (int hl = 0; hl < 2; ++hl) {
+        const void *base = hl ? (const void *)dlo : (const void *)dhi;
+        CUtensorMap *m = hl ? &mdyl : &mdy;
+        if (p.J == 1) {
+            cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)p.ho, (cuuint64_t)cout, (cuuint64_t)n};
+            cuuint64_t str[3] = {rowb * cout, rowb, rowb * cout * p.ho};
+            cuuint32_t box[4] = {64, 1, (cuuint32_t)cout, 1};
+            rc = wg_make_map16(m, base, 4, dims, str, box);
+        } else {
+            cuuint64_t dims[5] = {(cuuint64_t)p.wp_dy, (cuuint64_t)cout, (cuuint64_t)p.J,
+                                  (cuuint64_t)p.ho, (cuuint64_t)n};
+            cuuint64_t str[4] = {rowb, (cuuint64_t)p.sb * 2, rowb * cout, rowb * cout * p.ho};
+            cuuint32_t box[5] = {64, (cuuint32_t)cout, (cuuint32_t)p.J, 1, 1};
+            rc = wg_make_map16(m, base, 5, dims, str, box);
+        }
+        if (rc) return rc;
+    }
+    for (int hl = 0; hl < 2; ++hl) {
+        cuuint64_t dims[5] = {(cuuint64_t)wi, (cuuint64_t)p.rs.nreal0, (cuuint64_t)cin,
+                              (cuuint64_t)hi, (cuuint64_t)n};
+        // (a single-tap view's tap stride is never stepped: any multiple of 16 bytes will do)
+        const cuuint64_t tap = p.rs.nreal0 > 1 ? (cuuint64_t)p.rs.step * p.dc * 2 : 16;
+        cuuint64_t str[4] = {tap, (cuuint64_t)hi * wi * 2, (cuuint64_t)wi * 2,
+                             (cuuint64_t)cin * hi * wi * 2};
+        cuuint32_t box[5] = {64, (cuuint32_t)p.rs.n[0], (cuuint32_t)cin, 1, 1};
+        rc = wg_make_map16(&mx[hl], hl ? x_lo : x_hi, 5, dims, str, box);
+        if (rc) return rc;
+    }
+    mx[2] = mx[0];
+    mx[3] = mx[0];
+    a.C = cin;
+    a.Cpad = p.Cpad;
+    a.l = k;
+    a.d = d;
+    a.Q = cout;
+    a.Npad = p.Npad;
+    a.J = p.J;
+    a.sb = p.sb;
+    a.NB = p.NB;
+    a.tma_mirror = 0;
+    a.pair = 0;
+    a.direct = 1;
+    a.f16 = 1;
+    a.n_tiles = p.n_tiles;
+    a.G = p.G;
+    a.n_groups = p.n_groups;
+    a.splits = p.splits;
+    a.Ho = p.ho;
+    a.Wo = p.wo;
+    a.nvb = p.nvb;
+    a.T = p.T;
+    a.Hi = hi;
+    a.kb_total = p.kb_total;
+    a.SS = p.SS;
+    {
+        const char *e = getenv("DP_WG_PF");
+        a.pf = e ? atoi(e) : 3;
+        if (a.pf < 0) a.pf = 0;
+    }
+    a.R = p.R;
+    a.NM = p.NM;
+    a.Ls = p.Ls;
+    a.b_bytes = p.b_bytes;
+    a.slot_bytes = p.slot_bytes;
+    a.box_tx_row = (uint32_t)cin * p.rs.n[0] * 128u;
+    a.ring_hi = (uint32_t)p.SS * p.b_bytes;
+    a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
+    a.rs = p.rs;
+    a.trace = getenv("DP_WG_TRACE") ? wg_trace_buffer(st) : nullptr;
+    a.no_m64 = getenv("DP_WG_NO_M64") ? 1 : 0;
+    a.exit_if = flag;
+    a.exit_unless = nullptr;
+    const size_t smem = (size_t)a.ring_lo + (size_t)(p.R + p.NM) * p.slot_bytes + 1024;
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_ss_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return set_error(DP_ERR_CUDA, "tc_wgrad_ss: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    const int grid = p.n_groups * p.splits;
+    tc_wgrad_ss_kernel<<<grid, WS_THREADS, smem, st>>>(mx[0], mx[1], mx[2], mx[3], mdy, mdyl, a);
+    rc = check_launch("tc_wgrad_ss_kernel (fp16)");
+    if (rc) return rc;
+    const long long total = (long long)k * p.Ls * p.NB + cout;
+    ws_reduce<<<ceil_div(total, 32), 32 * WR_GROUPS, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
+                                                    p.Npad, p.J, p.kc, p.splits, p.n_tiles * 128,
+                                                    p.rs, flag, nullptr);
+    rc = check_launch("ws_reduce");
+    if (rc) return rc;
+    // the tf32 fallback, every launch gated on the flag
+    return ws_conv_backward_kernel(x, dy, dw, db, n, cin, hi, wi, cout, k, d,
+                                   w8 + p.total_bytes + 256, q.total_bytes, st, 3, x_slack,
+                                   dy_pitch, flag);
 }
 
 }  // namespace dp

@@ -188,6 +188,35 @@ class ops:
         return int(_lib_dev().dp_conv_backward_kernel_fast_workspace(n, ci, hi, wi, co, k, d))
 
     @staticmethod
+    def wgrad_f16_workspace(x, co, k, d) -> int:
+        n, ci, hi, wi = x.shape
+        return int(_lib_dev().dp_conv_backward_kernel_fast_f16_workspace(n, ci, hi, wi, co, k,
+                                                                         d))
+
+    @staticmethod
+    def split_f16(x, x_hi, x_lo):
+        """x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11) (the fp16 weight gradient's
+        pre-split operand)."""
+        with _Rec('split_f16', 1, 'hbm', x.numel() * 8):
+            _lib.check(_lib_dev().dp_split_f16(_ptr(x), _ptr(x_hi), _ptr(x_lo), x.numel(),
+                                               _stream()), "split_f16")
+
+    @staticmethod
+    def conv_backward_kernel_fast_f16(x, x_hi, x_lo, dy, dw, db, k, d, ws, x_slack,
+                                      dy_pitch=0):
+        """fp16-split weight gradient: x_hi / x_lo the fp16 split of x (lo scaled by 2^11),
+        read in place (x_slack readable, finite bytes after each and after x); x itself feeds
+        the tf32 fallback the device range guard selects."""
+        # dy split, fp16 kernel, reduce; the gated tf32 fallback's (dy staging,) kernel, reduce
+        with _Rec('conv_backward_kernel_tc', 6, 'tensor', 2 * dy.numel() * x.shape[1] * k * k):
+            n, ci, hi, wi = x.shape
+            co = dy.shape[1]
+            _lib.check(_lib_dev().dp_conv_backward_kernel_fast_f16(
+                _ptr(x), int(x_slack), _ptr(x_hi), _ptr(x_lo), int(x_slack), _ptr(dy),
+                int(dy_pitch), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k, d, _ptr(ws),
+                ws.numel() * ws.element_size(), _stream()), "conv_backward_kernel_fast_f16")
+
+    @staticmethod
     def conv_backward_kernel_fast(x, dy, dw, db, k, d, ws, x_slack=0, dy_pitch=0):
         """x_slack: readable bytes after x's storage (engine buffers carry SLACK_BYTES), which
         lets the kernel read x in place instead of staging a copy where the shape allows;
@@ -423,9 +452,13 @@ SLACK_BYTES = 64 * 1024
 
 
 def _slack_empty(shape, kw):
+    """The slack is zeroed: overlapping tap views multiply it by zero-filled dy columns, and
+    garbage there could be NaN."""
     n = int(np.prod(shape))
     extra = SLACK_BYTES // torch.tensor([], dtype=kw["dtype"]).element_size()
-    return torch.empty(n + extra, **kw)[:n].view(shape)
+    buf = torch.empty(n + extra, **kw)
+    buf[n:].zero_()
+    return buf[:n].view(shape)
 
 
 def _slack_zeros(shape, kw):
@@ -539,6 +572,22 @@ class DenseNet:
                     self.tc_wgrad[gi] = fast
                     ws = max(ws, ops.wgrad_fast_workspace(xin, co, kk, dd) if fast else
                              ops.wgrad_workspace(xin, co, kk, dd))
+            # fp16-split weight gradients (DP_WG_F16=0: off): a conv whose input is a tanh
+            # output (|x| <= 1, inside fp16's range by construction) and whose shape the fp16
+            # kernel takes gets that input split into fp16 hi / lo' once in the forward pass
+            self._wg16 = {}
+            if not os.environ.get("DP_WG_F16", "1") == "0":
+                kw16 = {"dtype": torch.float16, "device": self.device}
+                for gi, fast in self.tc_wgrad.items():
+                    if not fast or gi == 0 or not self._fp16_input(gi):
+                        continue
+                    g, xin = self.groups[gi], self._group_input(gi)
+                    nb = ops.wgrad_f16_workspace(xin, g.op.base.out_channels,
+                                                 g.op.base.kernel_size, g.op.dilation)
+                    if nb:
+                        self._wg16[gi] = (_slack_empty(tuple(xin.shape), kw16),
+                                          _slack_empty(tuple(xin.shape), kw16), nb)
+                        ws = max(ws, nb)
             self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
             # overlap mode: each fast weight gradient gets its own workspace so its x staging
             # can run during the forward pass (prepare) and survive until the backward
@@ -551,6 +600,8 @@ class DenseNet:
                         nb = ops.wgrad_fast_workspace(self._group_input(gi),
                                                       g.op.base.out_channels,
                                                       g.op.base.kernel_size, g.op.dilation)
+                        if gi in self._wg16:
+                            nb = max(nb, self._wg16[gi][2])
                         self._ws_l[gi] = torch.empty(nb, dtype=torch.uint8, device=self.device)
             self.mask = torch.zeros((N, height, width), dtype=torch.uint8, device=self.device)
             self.target = torch.zeros_like(self.output)
@@ -592,8 +643,11 @@ class DenseNet:
                 dg = ("tcgen05-fp16x3-offset" if f16b else "tcgen05-3xtf32") if b_ok else "exact"
                 if gi == 0:
                     dg = "not needed"  # layer 0's input delta is not computed (backward.py:208)
-                out[g.first] = {"forward": fwd, "data_grad": dg,
-                                "weight_grad": "tcgen05-3xtf32" if w_ok else "cuda-core"}
+                wg = "cuda-core"
+                if w_ok:
+                    wg = ("tcgen05-fp16x3-offset" if gi in getattr(self, "_wg16", {})
+                          else "tcgen05-3xtf32")
+                out[g.first] = {"forward": fwd, "data_grad": dg, "weight_grad": wg}
         return out
 
     # ------------------------------------------------------------- parameters
@@ -683,6 +737,9 @@ class DenseNet:
                     if kind == _lib.DP_TANH and self.precision == "fast":
                         kind = _lib.DP_TANH_FAST
                     ops.nonlin_forward(x, y, kind)
+            if self.train and gi + 1 in getattr(self, "_wg16", {}):
+                hi16, lo16, _ = self._wg16[gi + 1]
+                ops.split_f16(y, hi16, lo16)
         return self.output
 
     # ------------------------------------------------------------- loss / mask
@@ -753,6 +810,11 @@ class DenseNet:
                         if fast_w and gi in self._prepared:
                             ops.conv_backward_kernel_fast_staged(x_in, delta, dw, db, kk, d,
                                                                  self._ws_l[gi])
+                        elif gi in self._wg16:
+                            hi16, lo16, _ = self._wg16[gi]
+                            ops.conv_backward_kernel_fast_f16(x_in, hi16, lo16, delta, dw, db,
+                                                              kk, d, self._ws_l.get(gi, self._ws),
+                                                              SLACK_BYTES, dy_pitch=dyp)
                         elif fast_w:
                             ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d,
                                                           self._ws_l.get(gi, self._ws),
@@ -765,6 +827,10 @@ class DenseNet:
                     src = (ping - 1) % nbuf  # buffer holding `delta` (if it is a buffer)
                     if delta.data_ptr() == self._dbuf[src].data_ptr():
                         readers[src] = ev
+                elif gi in self._wg16:
+                    hi16, lo16, _ = self._wg16[gi]
+                    ops.conv_backward_kernel_fast_f16(x_in, hi16, lo16, delta, dw, db, kk, d,
+                                                      self._ws, SLACK_BYTES, dy_pitch=dyp)
                 elif fast_w:
                     ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws,
                                                   x_slack=SLACK_BYTES, dy_pitch=dyp)

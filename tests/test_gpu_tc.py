@@ -256,6 +256,96 @@ def test_tc_weight_gradient_x_in_place(shape):
     assert torch.equal(out["direct"][1], out["staged"][1])
 
 
+F16_WGRAD_SHAPES = [
+    # n, cin, cout, k, d, h, w  -- tap offsets j*d multiples of 8 halves, W % 8 == 0
+    (1, 50, 8, 7, 8, 90, 96),       # c3 head widths (J = 7 column-tap stacking)
+    (2, 32, 16, 3, 8, 60, 64),
+    (3, 16, 32, 3, 8, 45, 48),      # Ho % d != 0: a column phase runs past the image
+    (2, 32, 10, 4, 8, 70, 72),      # Q = 10 -> Npad 16
+    (2, 24, 48, 1, 3, 20, 24),      # 1x1 kernel
+    (1, 8, 8, 2, 16, 50, 48),       # d = 16
+]
+
+
+def _f16_case(shape, seed):
+    import torch
+    from paper_1412_4526_b200.engine import SLACK_BYTES, _slack_empty, ops
+    n, ci, co, k, d, h, w = shape
+    e = (k - 1) * d + 1
+    rng = np.random.default_rng(seed)
+    kw = {"dtype": torch.float32, "device": "cuda"}
+    x = _slack_empty((n, ci, h, w), kw)
+    x.copy_(_t(np.tanh(rng.normal(size=(n, ci, h, w))).astype(np.float32)))
+    dy = _t(rng.uniform(-1, 1, (n, co, h - e + 1, w - e + 1)).astype(np.float32))
+    nb = ops.wgrad_f16_workspace(x, co, k, d)
+    if not nb:
+        pytest.skip("outside the fp16 weight-gradient envelope")
+    kw16 = {"dtype": torch.float16, "device": "cuda"}
+    xh, xl = _slack_empty((n, ci, h, w), kw16), _slack_empty((n, ci, h, w), kw16)
+    ops.split_f16(x, xh, xl)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    return x, xh, xl, dy, ws, SLACK_BYTES
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-3, 1e4])
+@pytest.mark.parametrize("kernel", ["ss", "ss_j1", "ss_j2", "ss_j3"])
+@pytest.mark.parametrize("shape", F16_WGRAD_SHAPES)
+def test_tc_weight_gradient_fp16_split(shape, kernel, scale, force_env):
+    """dp_conv_backward_kernel_fast_f16 (x pre-split by dp_split_f16, dy split on the device,
+    kind::f16 offset-split MMAs) vs the fp64 exact tier: tighter than the tf32 kernel's bound
+    (fp16's 11-bit hi), deterministic, at dy magnitudes across the guarded range."""
+    force_env(kernel)
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    x, xh, xl, dy, ws, slack = _f16_case(shape, sum(shape))
+    dy = dy * scale
+    assert torch.equal(xh, x.half())
+    assert torch.equal(xl, ((x - xh.float()) * 2048.0).half())
+    dw64 = torch.empty((co, ci, k, k), dtype=torch.float64, device="cuda")
+    db64 = torch.empty(co, dtype=torch.float64, device="cuda")
+    ws64 = torch.empty(max(1, ops.wgrad_workspace(x.double(), co, k, d)), dtype=torch.uint8,
+                       device="cuda")
+    ops.conv_backward_kernel(x.double(), dy.double(), dw64, db64, k, d, ws64)
+    outs = []
+    for _ in range(2):
+        dw = torch.full((co, ci, k, k), float("nan"), device="cuda")
+        db = torch.full((co,), float("nan"), device="cuda")
+        ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, slack)
+        outs.append((dw, db))
+    torch.cuda.synchronize()
+    dw, db = outs[0]
+    assert torch.isfinite(dw).all() and torch.isfinite(db).all()
+    assert torch.equal(dw, outs[1][0]) and torch.equal(db, outs[1][1])
+    assert _rel(dw, dw64) < 5e-6, _rel(dw, dw64)
+    assert _rel(db, db64) < 5e-6, _rel(db, db64)
+
+
+@pytest.mark.parametrize("bad", [4e4, float("inf")])
+@pytest.mark.parametrize("shape", F16_WGRAD_SHAPES[:3])
+def test_tc_weight_gradient_fp16_range_fallback(shape, bad):
+    """One dy element outside fp16's range (or not finite) trips the device flag: the fp16
+    launches exit and the gated tf32 kernel runs -- bit-identical to calling it directly."""
+    import torch
+    from paper_1412_4526_b200.engine import ops
+    n, ci, co, k, d, h, w = shape
+    x, xh, xl, dy, ws, slack = _f16_case(shape, 7)
+    dy[n - 1, co - 1, 1, 2] = bad
+    dw = torch.full((co, ci, k, k), float("nan"), device="cuda")
+    db = torch.full((co,), float("nan"), device="cuda")
+    ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, slack)
+    ws32 = torch.empty(ops.wgrad_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
+    dw2, db2 = torch.empty_like(dw), torch.empty_like(db)
+    ops.conv_backward_kernel_fast(x, dy, dw2, db2, k, d, ws32, x_slack=slack)
+    torch.cuda.synchronize()
+    if bad == 4e4:
+        assert torch.isfinite(dw).all()
+        assert torch.equal(dw, dw2) and torch.equal(db, db2)
+    else:
+        assert torch.equal(torch.isfinite(dw), torch.isfinite(dw2))
+        assert torch.equal(torch.isfinite(db), torch.isfinite(db2))
+
+
 @pytest.mark.parametrize("p,d", [(2, 1), (4, 1), (2, 2)])
 def test_layer0_pitched_delta_path(p, d):
     """Layer 0's delta handed over with a 16-byte row pitch: the max-pool backward writes dx

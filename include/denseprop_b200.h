@@ -174,8 +174,10 @@ int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const 
                                     size_t workspace_bytes, void *stream);
 /* fp16-split weight gradient (ABI 6): the same dw / db as dp_conv_backward_kernel_fast_ex
  * (x, x_slack_bytes, dy_pitch as there) with x also handed over pre-split as two fp16 NCHW
- * tensors x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11), xh_slack_bytes readable (and
- * finite) past each, read in place (every tap offset a multiple of 8 halves, W % 8 == 0); dy is
+ * tensors x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11) with rows of xh_pitch halves
+ * (0: W; a multiple of 8, dp_split_f16 writes them), xh_slack_bytes readable (and finite) past
+ * each, read in place (tap offsets j*d in at most two classes mod 8 halves; the second class
+ * reads x_hi_s / x_lo_s, the copies shifted by _shift()'s halves, NULL when it is 0); dy is
  * split the same way into the workspace.  Products hi.hi + (hi.lo' + lo'.hi) * 2^-11 on
  * kind::f16 with 64-pixel K blocks: half the MMAs and shared-memory operand bytes of the tf32
  * kernel, and a smaller error (fp16's 11-bit hi vs tf32's).  The caller guarantees |x| < 2^15;
@@ -184,10 +186,18 @@ int dp_conv_backward_kernel_fast_ex(const float *x, size_t x_slack_bytes, const 
 size_t dp_conv_backward_kernel_fast_f16_workspace(int n, int cin, int hi, int wi, int cout,
                                                   int k, int d);
 /* x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11) elementwise (the split the fp16
- * weight gradient reads); 16-byte aligned pointers (ABI 6) */
-int dp_split_f16(const float *x, void *x_hi, void *x_lo, int64_t count, void *stream);
+ * weight gradient reads): `rows` rows of w floats -> rows of `pitch` halves (pitch >= w, a
+ * multiple of 8; zeros past w); 16-byte aligned pointers.  x_hi_s / x_lo_s (or NULL): the
+ * same padded arrays shifted left by `shift` (1..7) halves, x_hi_s[i] = x_hi[i + shift] (ABI 6) */
+int dp_split_f16(const float *x, void *x_hi, void *x_lo, void *x_hi_s, void *x_lo_s, int shift,
+                 int64_t rows, int w, int pitch, void *stream);
+/* the shift (halves) the fp16 weight gradient's second tap residue needs its shifted copies
+ * at (0: one residue, no copies; -1: the fp16 form does not apply) */
+int dp_conv_backward_kernel_fast_f16_shift(int n, int cin, int hi, int wi, int cout, int k,
+                                           int d);
 int dp_conv_backward_kernel_fast_f16(const float *x, size_t x_slack_bytes, const void *x_hi,
-                                     const void *x_lo, size_t xh_slack_bytes, const float *dy,
+                                     const void *x_lo, const void *x_hi_s, const void *x_lo_s,
+                                     size_t xh_slack_bytes, int xh_pitch, const float *dy,
                                      int dy_pitch, float *dw, float *db, int n, int cin, int hi,
                                      int wi, int cout, int k, int d, void *workspace,
                                      size_t workspace_bytes, void *stream);

@@ -67,8 +67,10 @@ SIGNATURES = {
                                          _i, _i, _vp, _i, _vp]),
     "dp_conv_backward_kernel_fast_prepare": (_i, [_vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_fast_f16_workspace": (_sz, [_i] * 7),
-    "dp_split_f16": (_i, [_vp, _vp, _vp, _i64, _vp]),
-    "dp_conv_backward_kernel_fast_f16": (_i, [_vp, _sz, _vp, _vp, _sz, _vp, _i, _vp, _vp] +
+    "dp_split_f16": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i64, _i, _i, _vp]),
+    "dp_conv_backward_kernel_fast_f16_shift": (_i, [_i] * 7),
+    "dp_conv_backward_kernel_fast_f16": (_i, [_vp, _sz, _vp, _vp, _vp, _vp, _sz, _i, _vp, _i,
+                                              _vp, _vp] +
                                          [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_fast_staged": (_i, [_vp, _vp, _vp, _vp] + [_i] * 7 + [_vp, _sz, _vp]),
     "dp_conv_backward_kernel_workspace": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),

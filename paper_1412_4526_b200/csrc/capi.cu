@@ -14,9 +14,12 @@
 
 namespace dp {
 size_t ws_workspace_f16(int n, int cin, int hi, int wi, int cout, int k, int d);
-int tc_split_f16_launch(const float *x, void *hi, void *lo, long long count, cudaStream_t st);
+int tc_split_f16_launch(const float *x, void *hi, void *lo, void *hs, void *ls, int shift,
+                        long long rows, int w, int wp, cudaStream_t st);
+int ws_shift_f16(int n, int cin, int hi, int wi, int cout, int k, int d);
 int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi,
-                                const void *x_lo, size_t xh_slack, const float *dy, int dy_pitch,
+                                const void *x_lo, const void *x_hi_s, const void *x_lo_s,
+                                size_t xh_slack, int xh_pitch, const float *dy, int dy_pitch,
                                 float *dw, float *db, int n, int cin, int hi, int wi, int cout,
                                 int k, int d, void *ws, size_t ws_bytes, cudaStream_t st);
 
@@ -390,7 +393,8 @@ size_t dp_conv_backward_kernel_fast_f16_workspace(int n, int cin, int hi, int wi
 }
 
 int dp_conv_backward_kernel_fast_f16(const float *x, size_t x_slack_bytes, const void *x_hi,
-                                     const void *x_lo, size_t xh_slack_bytes, const float *dy,
+                                     const void *x_lo, const void *x_hi_s, const void *x_lo_s,
+                                     size_t xh_slack_bytes, int xh_pitch, const float *dy,
                                      int dy_pitch, float *dw, float *db, int n, int cin, int hi,
                                      int wi, int cout, int k, int d, void *workspace,
                                      size_t workspace_bytes, void *stream) {
@@ -401,14 +405,26 @@ int dp_conv_backward_kernel_fast_f16(const float *x, size_t x_slack_bytes, const
     const int wo = wi - (k - 1) * d;
     if (dy_pitch != 0 && dy_pitch < wo)
         return set_error(DP_ERR_ARG, "dy row pitch %d < width %d", dy_pitch, wo);
-    return dp::ws_conv_backward_kernel_f16(x, x_slack_bytes, x_hi, x_lo, xh_slack_bytes, dy,
+    return dp::ws_conv_backward_kernel_f16(x, x_slack_bytes, x_hi, x_lo, x_hi_s, x_lo_s,
+                                           xh_slack_bytes, xh_pitch, dy,
                                            dy_pitch, dw, db, n, cin, hi, wi, cout, k, d,
                                            workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
-int dp_split_f16(const float *x, void *x_hi, void *x_lo, int64_t count, void *stream) {
-    if (count < 0) return set_error(DP_ERR_ARG, "fp16 split: negative count");
-    return dp::tc_split_f16_launch(x, x_hi, x_lo, count, (cudaStream_t)stream);
+int dp_split_f16(const float *x, void *x_hi, void *x_lo, void *x_hi_s, void *x_lo_s,
+                 int shift, int64_t rows, int w, int pitch, void *stream) {
+    if (rows < 0 || w < 1) return set_error(DP_ERR_ARG, "fp16 split: bad rows %lld / width %d",
+                                            (long long)rows, w);
+    return dp::tc_split_f16_launch(x, x_hi, x_lo, x_hi_s, x_lo_s, shift, rows, w, pitch,
+                                   (cudaStream_t)stream);
+}
+
+int dp_conv_backward_kernel_fast_f16_shift(int n, int cin, int hi, int wi, int cout, int k,
+                                           int d) {
+    if (n < 1 || cin < 1 || cout < 1 || k < 1 || d < 1 || hi < (k - 1) * d + 1 ||
+        wi < (k - 1) * d + 1)
+        return -1;
+    return dp::ws_shift_f16(n, cin, hi, wi, cout, k, d);
 }
 
 int dp_conv_backward_kernel_fast_prepare(const float *x, int n, int cin, int hi, int wi,

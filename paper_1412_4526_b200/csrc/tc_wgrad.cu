@@ -725,35 +725,70 @@ int wg_stage_dy16(const float *dy, void *dhi, void *dlo, int n, int cout, int ho
     return check_launch("tc_stage_dy16");
 }
 // x -> (hi, lo') for the fp16-split weight gradient's in-place operands (the engine splits
-// an activation once in the forward pass); 8 elements per thread, 16-byte stores
+// an activation once in the forward pass): rows of w floats -> rows of wp >= w halves (16-byte
+// rows for TMA, zero padding), one thread per 8 destination halves (16-byte stores).  With
+// hs / ls: also the same padded arrays shifted left by `shift` halves (flat: hs[i] = hi[i +
+// shift]) -- the second tap residue's TMA boxes must start 16-byte aligned.
+__device__ __forceinline__ float split_src(const float *__restrict__ x, long long q, int w,
+                                           int wp, long long total) {
+    if (q >= total) return 0.f;
+    const long long row = q / wp;
+    const int c = (int)(q - row * wp);
+    return c < w ? __ldg(x + row * w + c) : 0.f;
+}
 __global__ void __launch_bounds__(256) tc_split_f16(const float *__restrict__ x,
-                                                    __half *__restrict__ hi,
-                                                    __half *__restrict__ lo, long long count) {
-    const long long n8 = count >> 3;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+                                                    uint4 *__restrict__ hi,
+                                                    uint4 *__restrict__ lo,
+                                                    uint4 *__restrict__ hs,
+                                                    uint4 *__restrict__ ls, int shift, int w,
+                                                    int wp, long long total8) {
+    const int n8 = wp >> 3;
+    const bool vec = (w & 3) == 0;  // source rows 16-byte aligned
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total8;
          i += (long long)gridDim.x * blockDim.x) {
-        const float4 a = __ldg(reinterpret_cast<const float4 *>(x) + 2 * i);
-        const float4 b = __ldg(reinterpret_cast<const float4 *>(x) + 2 * i + 1);
+        const long long row = i / n8;
+        const int v = (int)(i - row * n8) * 8;
+        const float *s = x + row * w + v;
+        float e[8];
+        if (vec && v + 8 <= w) {
+            const float4 a = __ldg(reinterpret_cast<const float4 *>(s));
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(s) + 1);
+            e[0] = a.x; e[1] = a.y; e[2] = a.z; e[3] = a.w;
+            e[4] = b.x; e[5] = b.y; e[6] = b.z; e[7] = b.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) e[q] = v + q < w ? __ldg(s + q) : 0.f;
+        }
         uint32_t hw[4], lw[4];
-        ptx::f16_split2_scaled(a.x, a.y, hw[0], lw[0]);
-        ptx::f16_split2_scaled(a.z, a.w, hw[1], lw[1]);
-        ptx::f16_split2_scaled(b.x, b.y, hw[2], lw[2]);
-        ptx::f16_split2_scaled(b.z, b.w, hw[3], lw[3]);
-        reinterpret_cast<uint4 *>(hi)[i] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        reinterpret_cast<uint4 *>(lo)[i] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    }
-    if (blockIdx.x == 0 && threadIdx.x < (count & 7)) {
-        const long long j = (count & ~7LL) + threadIdx.x;
-        const __half h = __float2half_rn(x[j]);
-        hi[j] = h;
-        lo[j] = __float2half_rn((x[j] - __half2float(h)) * ptx::F16_LO_SCALE);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ptx::f16_split2_scaled(e[2 * q], e[2 * q + 1], hw[q], lw[q]);
+        hi[i] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        lo[i] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        if (hs) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) e[q] = split_src(x, i * 8 + shift + q, w, wp, total8 * 8);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                ptx::f16_split2_scaled(e[2 * q], e[2 * q + 1], hw[q], lw[q]);
+            hs[i] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            ls[i] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
     }
 }
-int tc_split_f16_launch(const float *x, void *hi, void *lo, long long count, cudaStream_t st) {
-    if (((uintptr_t)x & 15) || ((uintptr_t)hi & 15) || ((uintptr_t)lo & 15))
+int tc_split_f16_launch(const float *x, void *hi, void *lo, void *hs, void *ls, int shift,
+                        long long rows, int w, int wp, cudaStream_t st) {
+    if (((uintptr_t)x & 15) || ((uintptr_t)hi & 15) || ((uintptr_t)lo & 15) ||
+        ((uintptr_t)hs & 15) || ((uintptr_t)ls & 15) || (!hs != !ls))
         return set_error(DP_ERR_ARG, "fp16 split: pointers must be 16-byte aligned");
-    if (count <= 0) return DP_OK;
-    tc_split_f16<<<stage_grid(count / 8 + 1), 256, 0, st>>>(x, (__half *)hi, (__half *)lo, count);
+    if (hs && (shift <= 0 || shift >= 8))
+        return set_error(DP_ERR_ARG, "fp16 split: shift %d outside 1..7", shift);
+    if (wp < w || (wp & 7))
+        return set_error(DP_ERR_ARG, "fp16 split: pitch %d must be >= %d and a multiple of 8",
+                         wp, w);
+    const long long total8 = rows * (wp / 8);
+    if (total8 <= 0) return DP_OK;
+    tc_split_f16<<<stage_grid(total8), 256, 0, st>>>(x, (uint4 *)hi, (uint4 *)lo, (uint4 *)hs,
+                                                     (uint4 *)ls, shift, w, wp, total8);
     return check_launch("tc_split_f16");
 }
 int wg_sms() { return wg_num_sms(); }

@@ -228,11 +228,15 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                     ptx::tma_prefetch_l2_5d(&tm_xp, pv0, 0, 0, pf.u, pf.img);
                 for (int k = pf.cstart ? 0 : n_i - 1; k < n_i; ++k) {
                     if (a.direct) {
-                        ptx::tma_prefetch_l2_5d(&tm_x0, pv0 + a.rs.j0[0] * a.d, 0, 0,
-                                                pf.u + (i_lo + k) * a.d, pf.img);
-                        if (a.f16)
-                            ptx::tma_prefetch_l2_5d(&tm_x1, pv0 + a.rs.j0[0] * a.d, 0, 0,
-                                                    pf.u + (i_lo + k) * a.d, pf.img);
+                        // fp16: residue rb's hi / lo' views are tm_x{2rb} / tm_x{2rb+1}
+                        for (int rb = 0; rb < a.rs.n_b; ++rb) {
+                            const int xc = pv0 + a.rs.j0[rb] * a.d - a.rs.b[rb],
+                                      xr = pf.u + (i_lo + k) * a.d;
+                            ptx::tma_prefetch_l2_5d(rb ? &tm_x2 : &tm_x0, xc, 0, 0, xr, pf.img);
+                            if (a.f16)
+                                ptx::tma_prefetch_l2_5d(rb ? &tm_x3 : &tm_x1, xc, 0, 0, xr,
+                                                        pf.img);
+                        }
                         continue;
                     }
                     const int prow = pf.img * a.Hi + pf.u + (i_lo + k) * a.d;
@@ -308,13 +312,22 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                         unsigned char *dst =
                             ring + (size_t)(copy ? a.R + slot : slot) * a.slot_bytes;
                         if (a.direct) {
-                            // NCHW in place: (w, jj, c, h, n); rows past Hi zero-fill
-                            ptx::tma_load_5d(dst, &tm_x0, v0 + a.rs.j0[0] * a.d, 0, 0,
-                                             sc.u + (i_lo + k) * a.d, sc.img, &sfull[s]);
-                            if (a.f16)  // the lo' row into the lo ring
-                                ptx::tma_load_5d(dst + (a.ring_lo - a.ring_hi), &tm_x1,
-                                                 v0 + a.rs.j0[0] * a.d, 0, 0,
-                                                 sc.u + (i_lo + k) * a.d, sc.img, &sfull[s]);
+                            // NCHW in place: (w, jj, c, h, n); rows past Hi zero-fill.  The
+                            // fp16 split may have two residues (tap offsets j*d = 0 / 4 mod 8
+                            // halves): one box each, lo' rows into the lo ring
+                            for (int rb = 0; rb < a.rs.n_b; ++rb) {
+                                unsigned char *db_ = dst + (size_t)a.rs.line0[rb] * 128;
+                                // (residue 1: a copy shifted left by its residue b, so the
+                                // box start stays 16-byte aligned)
+                                const int xc = v0 + a.rs.j0[rb] * a.d - a.rs.b[rb],
+                                          xr = sc.u + (i_lo + k) * a.d;
+                                ptx::tma_load_5d(db_, rb ? &tm_x2 : &tm_x0, xc, 0, 0, xr, sc.img,
+                                                 &sfull[s]);
+                                if (a.f16)
+                                    ptx::tma_load_5d(db_ + (a.ring_lo - a.ring_hi),
+                                                     rb ? &tm_x3 : &tm_x1, xc, 0, 0, xr, sc.img,
+                                                     &sfull[s]);
+                            }
                             continue;
                         }
                         for (int rb = 0; rb < a.rs.n_b; ++rb) {
@@ -706,7 +719,8 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
 
 // f16: the fp16-split variant (x pre-split into fp16 hi / lo' NCHW tensors read in place,
 // dy staged as fp16 hi / lo'; K blocks of 64 px so a 128-byte line still holds one K block):
-// every tap offset must be a multiple of 8 halves (16 bytes: TMA box starts), no 2-row boxes
+// residues are tap offsets mod 8 halves (16 bytes), at most two (one in-place box each),
+// no per-tap copies, no 2-row boxes
 static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, int Ja,
                       WsPlan &p, bool f16) {
     if (getenv("DP_WG_TMEM")) return false;  // force the TMEM-operand kernel (experiments)
@@ -728,9 +742,7 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     p.sb = p.kc * d;
     if (J > 1 && (p.sb & (f16 ? 7 : 3))) return false;
     const int kc = p.kc, dc = p.dc;
-    if (f16)
-        for (int j = 0; j < kc; ++j)
-            if ((j * dc) & 7) return false;
+    const int RM = f16 ? 8 : 4;  // residue modulus: elements per 16 bytes
     p.Cpad = (cin + 7) / 8 * 8;
     if (p.Cpad > 256) return false;
     // lines per ring slot (one input row): residue boxes, each rounded up to 8 lines.  Small
@@ -740,9 +752,9 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     int nres = 0;
     {
         int ls = 0;
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < RM; ++b) {
             int cnt = 0;
-            for (int j = 0; j < kc; ++j) cnt += ((j * dc) & 3) == b;
+            for (int j = 0; j < kc; ++j) cnt += ((j * dc) % RM) == b;
             if (cnt) {
                 ls += (cin * cnt + 7) / 8 * 8;
                 ++nres;
@@ -750,7 +762,8 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
         }
         p.Ls = ls;
     }
-    p.rs.tapcopy = (nres > 1 && cin * kc <= 32 && !getenv("DP_WG_RESIDUE")) ? 1 : 0;
+    if (f16 && nres > 2) return false;
+    p.rs.tapcopy = (!f16 && nres > 1 && cin * kc <= 32 && !getenv("DP_WG_RESIDUE")) ? 1 : 0;
     if (p.rs.tapcopy) p.Ls = (cin * kc + 7) / 8 * 8;
     // 2-row x boxes need one box per row whose lines fill the slot exactly (the tap
     // dimension is padded with zero-filled taps to Ls / cin)
@@ -800,12 +813,12 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     p.R = p.max_ni + p.SS - 1 + p.pair;
     // residue copies: column taps jo with (jo*dc) & 3 == b, lcm(dc, 4) floats apart
     int gcd = 1;
-    for (int v = 4; v >= 1; --v)
-        if (dc % v == 0 && 4 % v == 0) {
+    for (int v = RM; v >= 1; --v)
+        if (dc % v == 0 && RM % v == 0) {
             gcd = v;
             break;
         }
-    p.rs.step = 4 / gcd;
+    p.rs.step = RM / gcd;
     p.mask = 0;
     p.rs.n_b = 0;
     if (p.rs.tapcopy) {  // one "residue" holding all kc taps (copy jo pre-shifted by jo*dc)
@@ -821,10 +834,10 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
         }
     }
     int line0 = 0;
-    for (int b = 0; b < 4 && !p.rs.tapcopy; ++b) {
+    for (int b = 0; b < RM && !p.rs.tapcopy; ++b) {
         int cnt = 0, j0 = -1;
         for (int j = 0; j < kc; ++j)
-            if (((j * dc) & 3) == b) {
+            if (((j * dc) % RM) == b) {
                 if (j0 < 0) j0 = j;
                 ++cnt;
             }
@@ -881,8 +894,8 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
 // unsupported; out = {J, Ja, NB, Ls, n_tiles, G, n_groups, splits, SS, pair, stage_dy,
 // residues, tapcopy, x_bytes / 1 KiB, dy_bytes / 1 KiB, total_bytes / 1 KiB}
 int ws_debug_plan(int n, int cin, int hi, int wi, int cout, int k, int d, int *out, int len) {
-    WsPlan p;
-    if (!ws_plan(n, cin, hi, wi, cout, k, d, p)) return 0;
+    WsPlan p;  // DP_WG_DEBUG_F16: the fp16-split plan
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p, getenv("DP_WG_DEBUG_F16") != nullptr)) return 0;
     const int v[16] = {p.J, p.kc, p.NB, p.Ls, p.n_tiles, p.G, p.n_groups, p.splits, p.SS,
                        p.pair, p.stage_dy ? 1 : 0, p.rs.n_b, p.rs.tapcopy,
                        (int)(p.x_bytes >> 10), (int)(p.dy_bytes >> 10),
@@ -1073,32 +1086,51 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
 // pixel.  Range guard as the fp16 convolutions: the dy split flags any |dy| >= 2^15 (or not
 // finite) and the tf32 kernel on the fp32 x runs instead (the caller guarantees |x| < 2^15:
 // it splits only bounded activations).  Workspace: [fp16 plan | flag | tf32 plan].
-static bool ws_f16_inplace(const WsPlan &p, int wi) {
-    return p.rs.n_b == 1 && p.rs.b[0] == 0 && wi % 8 == 0;
+// two residues (shifted copies) are opt-in, DP_WG_F16_RES2=1: measured slower than the tf32
+// kernel on c3 conv2 (2.30 vs 1.83 ms: Ls 160 leaves 2 dy stages, 4 x boxes per row)
+static bool ws_f16_inplace(const WsPlan &p) {
+    const int max_nb = getenv("DP_WG_F16_RES2") ? 2 : 1;
+    return p.rs.n_b >= 1 && p.rs.n_b <= max_nb && !p.rs.tapcopy && !p.pair;
 }
-static size_t ws_f16_overrun(const WsPlan &p, int d) {  // bytes the tap view reads past x
-    return ((size_t)(p.rs.n[0] - 1) * p.rs.step * d + 64) * 2;
+static size_t ws_f16_overrun(const WsPlan &p, int d) {  // bytes the tap views read past x
+    size_t m = 0;
+    for (int rb = 0; rb < p.rs.n_b; ++rb)
+        m = std::max(m, (size_t)(p.rs.n[rb] - 1) * p.rs.step * d);
+    return (m + 64) * 2;
+}
+
+// the shift (halves) of the second residue's copies, 0 when one residue
+int ws_shift_f16(int n, int cin, int hi, int wi, int cout, int k, int d) {
+    WsPlan p;
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p, true) || !ws_f16_inplace(p)) return -1;
+    return p.rs.n_b > 1 ? p.rs.b[1] : 0;
 }
 
 size_t ws_workspace_f16(int n, int cin, int hi, int wi, int cout, int k, int d) {
     WsPlan p, q;
-    if (!ws_plan(n, cin, hi, wi, cout, k, d, p, true) || !ws_f16_inplace(p, wi) ||
+    if (!ws_plan(n, cin, hi, wi, cout, k, d, p, true) || !ws_f16_inplace(p) ||
         !ws_plan(n, cin, hi, wi, cout, k, d, q))
         return 0;
     return p.total_bytes + 256 + q.total_bytes;
 }
 
 int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi,
-                                const void *x_lo, size_t xh_slack, const float *dy, int dy_pitch,
+                                const void *x_lo, const void *x_hi_s, const void *x_lo_s,
+                                size_t xh_slack, int xh_pitch, const float *dy, int dy_pitch,
                                 float *dw, float *db, int n, int cin, int hi, int wi, int cout,
                                 int k, int d, void *ws, size_t ws_bytes, cudaStream_t st) {
     WsPlan p, q;
     if (!ws_plan(n, cin, hi, wi, cout, k, d, p, true) || !ws_plan(n, cin, hi, wi, cout, k, d, q))
         return set_error(DP_ERR_UNSUPPORTED, "fp16 weight gradient: unsupported shape");
     // x in place: one residue at offset 0, 16-byte rows of halves, slack for the tap view
-    if (!ws_f16_inplace(p, wi) || xh_slack < ws_f16_overrun(p, d) || ((uintptr_t)x_hi & 15) ||
-        ((uintptr_t)x_lo & 15))
+    const int xp = xh_pitch > 0 ? xh_pitch : wi;  // halves per row of x_hi / x_lo
+    if (!ws_f16_inplace(p) || xp < wi || (xp & 7) || xh_slack < ws_f16_overrun(p, d) ||
+        ((uintptr_t)x_hi & 15) || ((uintptr_t)x_lo & 15) || ((uintptr_t)x_hi_s & 15) ||
+        ((uintptr_t)x_lo_s & 15))
         return set_error(DP_ERR_UNSUPPORTED, "fp16 weight gradient: x not readable in place");
+    if (p.rs.n_b > 1 && (!x_hi_s || !x_lo_s))
+        return set_error(DP_ERR_ARG, "fp16 weight gradient: this shape needs the shifted "
+                         "copies (shift %d halves)", p.rs.b[1]);
     p.direct = 1;
     p.R = p.max_ni + p.SS - 1;
     const size_t need = p.total_bytes + 256 + q.total_bytes;
@@ -1136,19 +1168,20 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
         }
         if (rc) return rc;
     }
-    for (int hl = 0; hl < 2; ++hl) {
-        cuuint64_t dims[5] = {(cuuint64_t)wi, (cuuint64_t)p.rs.nreal0, (cuuint64_t)cin,
+    // residue rb's views: mx[2 rb] (hi), mx[2 rb + 1] (lo')
+    for (int m = 0; m < 4; ++m) {
+        const int rb = std::min(m / 2, p.rs.n_b - 1), hl = m & 1;
+        cuuint64_t dims[5] = {(cuuint64_t)wi, (cuuint64_t)p.rs.n[rb], (cuuint64_t)cin,
                               (cuuint64_t)hi, (cuuint64_t)n};
         // (a single-tap view's tap stride is never stepped: any multiple of 16 bytes will do)
-        const cuuint64_t tap = p.rs.nreal0 > 1 ? (cuuint64_t)p.rs.step * p.dc * 2 : 16;
-        cuuint64_t str[4] = {tap, (cuuint64_t)hi * wi * 2, (cuuint64_t)wi * 2,
-                             (cuuint64_t)cin * hi * wi * 2};
-        cuuint32_t box[5] = {64, (cuuint32_t)p.rs.n[0], (cuuint32_t)cin, 1, 1};
-        rc = wg_make_map16(&mx[hl], hl ? x_lo : x_hi, 5, dims, str, box);
+        const cuuint64_t tap = p.rs.n[rb] > 1 ? (cuuint64_t)p.rs.step * p.dc * 2 : 16;
+        cuuint64_t str[4] = {tap, (cuuint64_t)hi * xp * 2, (cuuint64_t)xp * 2,
+                             (cuuint64_t)cin * hi * xp * 2};
+        cuuint32_t box[5] = {64, (cuuint32_t)p.rs.n[rb], (cuuint32_t)cin, 1, 1};
+        const void *base = rb ? (hl ? x_lo_s : x_hi_s) : (hl ? x_lo : x_hi);
+        rc = wg_make_map16(&mx[m], base, 5, dims, str, box);
         if (rc) return rc;
     }
-    mx[2] = mx[0];
-    mx[3] = mx[0];
     a.C = cin;
     a.Cpad = p.Cpad;
     a.l = k;
@@ -1183,7 +1216,7 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
     a.Ls = p.Ls;
     a.b_bytes = p.b_bytes;
     a.slot_bytes = p.slot_bytes;
-    a.box_tx_row = (uint32_t)cin * p.rs.n[0] * 128u;
+    a.box_tx_row = (uint32_t)cin * p.kc * 128u;  // every residue box, real taps only
     a.ring_hi = (uint32_t)p.SS * p.b_bytes;
     a.ring_lo = a.ring_hi + (uint32_t)(p.R + p.NM) * p.slot_bytes;
     a.rs = p.rs;

@@ -194,25 +194,39 @@ class ops:
                                                                          d))
 
     @staticmethod
-    def split_f16(x, x_hi, x_lo):
+    def split_f16(x, x_hi, x_lo, x_hi_s=None, x_lo_s=None, shift=0):
         """x_hi = RN_fp16(x), x_lo = RN_fp16((x - x_hi) * 2^11) (the fp16 weight gradient's
-        pre-split operand)."""
-        with _Rec('split_f16', 1, 'hbm', x.numel() * 8):
-            _lib.check(_lib_dev().dp_split_f16(_ptr(x), _ptr(x_hi), _ptr(x_lo), x.numel(),
-                                               _stream()), "split_f16")
+        pre-split operand); x (..., W) -> x_hi / x_lo (..., P) halves, P >= W a multiple of 8
+        (zeros past W); x_hi_s / x_lo_s: the same shifted left by `shift` halves (flat)."""
+        w, pitch = x.shape[-1], x_hi.shape[-1]
+        nout = 2 if x_hi_s is None else 4
+        with _Rec('split_f16', 1, 'hbm', x.numel() * 4 + x_hi.numel() * 2 * nout):
+            _lib.check(_lib_dev().dp_split_f16(
+                _ptr(x), _ptr(x_hi), _ptr(x_lo), _ptr(x_hi_s) if x_hi_s is not None else None,
+                _ptr(x_lo_s) if x_lo_s is not None else None, int(shift), x.numel() // w, w,
+                pitch, _stream()), "split_f16")
+
+    @staticmethod
+    def wgrad_f16_shift(x, co, k, d) -> int:
+        n, ci, hi, wi = x.shape
+        return int(_lib_dev().dp_conv_backward_kernel_fast_f16_shift(n, ci, hi, wi, co, k, d))
 
     @staticmethod
     def conv_backward_kernel_fast_f16(x, x_hi, x_lo, dy, dw, db, k, d, ws, x_slack,
-                                      dy_pitch=0):
-        """fp16-split weight gradient: x_hi / x_lo the fp16 split of x (lo scaled by 2^11),
-        read in place (x_slack readable, finite bytes after each and after x); x itself feeds
-        the tf32 fallback the device range guard selects."""
+                                      dy_pitch=0, x_hi_s=None, x_lo_s=None):
+        """fp16-split weight gradient: x_hi / x_lo (N, C, H, P) the fp16 split of x (lo scaled
+        by 2^11, rows padded to P, split_f16), read in place (x_slack readable, finite bytes
+        after each and after x); x itself feeds the tf32 fallback the device range guard
+        selects."""
         # dy split, fp16 kernel, reduce; the gated tf32 fallback's (dy staging,) kernel, reduce
         with _Rec('conv_backward_kernel_tc', 6, 'tensor', 2 * dy.numel() * x.shape[1] * k * k):
             n, ci, hi, wi = x.shape
             co = dy.shape[1]
             _lib.check(_lib_dev().dp_conv_backward_kernel_fast_f16(
-                _ptr(x), int(x_slack), _ptr(x_hi), _ptr(x_lo), int(x_slack), _ptr(dy),
+                _ptr(x), int(x_slack), _ptr(x_hi), _ptr(x_lo),
+                _ptr(x_hi_s) if x_hi_s is not None else None,
+                _ptr(x_lo_s) if x_lo_s is not None else None, int(x_slack), x_hi.shape[3],
+                _ptr(dy),
                 int(dy_pitch), _ptr(dw), _ptr(db), n, ci, hi, wi, co, k, d, _ptr(ws),
                 ws.numel() * ws.element_size(), _stream()), "conv_backward_kernel_fast_f16")
 
@@ -584,9 +598,16 @@ class DenseNet:
                     g, xin = self.groups[gi], self._group_input(gi)
                     nb = ops.wgrad_f16_workspace(xin, g.op.base.out_channels,
                                                  g.op.base.kernel_size, g.op.dilation)
-                    if nb:
-                        self._wg16[gi] = (_slack_empty(tuple(xin.shape), kw16),
-                                          _slack_empty(tuple(xin.shape), kw16), nb)
+                    shift = ops.wgrad_f16_shift(xin, g.op.base.out_channels,
+                                                g.op.base.kernel_size, g.op.dilation)
+                    if nb and shift >= 0:
+                        # rows padded to 16 bytes; a second tap residue reads copies shifted
+                        # by `shift` halves (its TMA boxes must start 16-byte aligned)
+                        shp = tuple(xin.shape[:3]) + ((xin.shape[3] + 7) // 8 * 8,)
+                        t = [_slack_empty(shp, kw16) for _ in range(4 if shift else 2)]
+                        self._wg16[gi] = {"hi": t[0], "lo": t[1], "nb": nb, "shift": shift,
+                                          "hs": t[2] if shift else None,
+                                          "ls": t[3] if shift else None}
                         ws = max(ws, nb)
             self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
             # overlap mode: each fast weight gradient gets its own workspace so its x staging
@@ -601,7 +622,7 @@ class DenseNet:
                                                       g.op.base.out_channels,
                                                       g.op.base.kernel_size, g.op.dilation)
                         if gi in self._wg16:
-                            nb = max(nb, self._wg16[gi][2])
+                            nb = max(nb, self._wg16[gi]["nb"])
                         self._ws_l[gi] = torch.empty(nb, dtype=torch.uint8, device=self.device)
             self.mask = torch.zeros((N, height, width), dtype=torch.uint8, device=self.device)
             self.target = torch.zeros_like(self.output)
@@ -738,8 +759,8 @@ class DenseNet:
                         kind = _lib.DP_TANH_FAST
                     ops.nonlin_forward(x, y, kind)
             if self.train and gi + 1 in getattr(self, "_wg16", {}):
-                hi16, lo16, _ = self._wg16[gi + 1]
-                ops.split_f16(y, hi16, lo16)
+                s16 = self._wg16[gi + 1]
+                ops.split_f16(y, s16["hi"], s16["lo"], s16["hs"], s16["ls"], s16["shift"])
         return self.output
 
     # ------------------------------------------------------------- loss / mask
@@ -811,10 +832,11 @@ class DenseNet:
                             ops.conv_backward_kernel_fast_staged(x_in, delta, dw, db, kk, d,
                                                                  self._ws_l[gi])
                         elif gi in self._wg16:
-                            hi16, lo16, _ = self._wg16[gi]
-                            ops.conv_backward_kernel_fast_f16(x_in, hi16, lo16, delta, dw, db,
-                                                              kk, d, self._ws_l.get(gi, self._ws),
-                                                              SLACK_BYTES, dy_pitch=dyp)
+                            s16 = self._wg16[gi]
+                            ops.conv_backward_kernel_fast_f16(
+                                x_in, s16["hi"], s16["lo"], delta, dw, db, kk, d,
+                                self._ws_l.get(gi, self._ws), SLACK_BYTES, dy_pitch=dyp,
+                                x_hi_s=s16["hs"], x_lo_s=s16["ls"])
                         elif fast_w:
                             ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d,
                                                           self._ws_l.get(gi, self._ws),
@@ -828,9 +850,10 @@ class DenseNet:
                     if delta.data_ptr() == self._dbuf[src].data_ptr():
                         readers[src] = ev
                 elif gi in self._wg16:
-                    hi16, lo16, _ = self._wg16[gi]
-                    ops.conv_backward_kernel_fast_f16(x_in, hi16, lo16, delta, dw, db, kk, d,
-                                                      self._ws, SLACK_BYTES, dy_pitch=dyp)
+                    s16 = self._wg16[gi]
+                    ops.conv_backward_kernel_fast_f16(x_in, s16["hi"], s16["lo"], delta, dw, db,
+                                                      kk, d, self._ws, SLACK_BYTES, dy_pitch=dyp,
+                                                      x_hi_s=s16["hs"], x_lo_s=s16["ls"])
                 elif fast_w:
                     ops.conv_backward_kernel_fast(x_in, delta, dw, db, kk, d, self._ws,
                                                   x_slack=SLACK_BYTES, dy_pitch=dyp)

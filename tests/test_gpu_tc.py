@@ -264,6 +264,12 @@ F16_WGRAD_SHAPES = [
     (2, 32, 10, 4, 8, 70, 72),      # Q = 10 -> Npad 16
     (2, 24, 48, 1, 3, 20, 24),      # 1x1 kernel
     (1, 8, 8, 2, 16, 50, 48),       # d = 16
+    # two residues (tap offsets 0 / 4 mod 8 halves): one in-place box each
+    (2, 50, 50, 3, 4, 70, 76),      # c3 conv2 widths, W % 8 = 4 (split rows padded to 80)
+    (1, 32, 16, 7, 8, 60, 61),      # W odd
+    (1, 16, 24, 5, 4, 60, 64),      # residues of 3 and 2 taps
+    (2, 16, 16, 3, 12, 80, 88),     # d = 12: offsets 0, 12, 24
+    (2, 8, 16, 2, 2, 40, 48),       # d = 2, two taps
 ]
 
 
@@ -281,27 +287,38 @@ def _f16_case(shape, seed):
     if not nb:
         pytest.skip("outside the fp16 weight-gradient envelope")
     kw16 = {"dtype": torch.float16, "device": "cuda"}
-    xh, xl = _slack_empty((n, ci, h, w), kw16), _slack_empty((n, ci, h, w), kw16)
-    ops.split_f16(x, xh, xl)
+    wp = (w + 7) // 8 * 8  # 16-byte rows of halves
+    shift = ops.wgrad_f16_shift(x, co, k, d)
+    assert shift >= 0
+    t = [_slack_empty((n, ci, h, wp), kw16) for _ in range(4 if shift else 2)]
+    ops.split_f16(x, t[0], t[1], *(t[2:] + [shift] if shift else []))
+    if shift:  # the second residue's copies: the padded arrays shifted left (flat)
+        for a, s in ((t[0], t[2]), (t[1], t[3])):
+            fa, fs = a.reshape(-1), s.reshape(-1)
+            assert torch.equal(fs[:-shift], fa[shift:]) and not fs[-shift:].any()
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
-    return x, xh, xl, dy, ws, SLACK_BYTES
+    xs = {"x_hi_s": t[2], "x_lo_s": t[3]} if shift else {}
+    return x, t[0], t[1], dy, ws, SLACK_BYTES, xs
 
 
 @pytest.mark.parametrize("scale", [1.0, 1e-3, 1e4])
 @pytest.mark.parametrize("kernel", ["ss", "ss_j1", "ss_j2", "ss_j3"])
 @pytest.mark.parametrize("shape", F16_WGRAD_SHAPES)
-def test_tc_weight_gradient_fp16_split(shape, kernel, scale, force_env):
+def test_tc_weight_gradient_fp16_split(shape, kernel, scale, force_env, monkeypatch):
     """dp_conv_backward_kernel_fast_f16 (x pre-split by dp_split_f16, dy split on the device,
     kind::f16 offset-split MMAs) vs the fp64 exact tier: tighter than the tf32 kernel's bound
-    (fp16's 11-bit hi), deterministic, at dy magnitudes across the guarded range."""
+    (fp16's 11-bit hi), deterministic, at dy magnitudes across the guarded range.  Two-residue
+    shapes (shifted copies) are opt-in in production (DP_WG_F16_RES2) and enabled here."""
+    monkeypatch.setenv("DP_WG_F16_RES2", "1")
     force_env(kernel)
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
-    x, xh, xl, dy, ws, slack = _f16_case(shape, sum(shape))
+    x, xh, xl, dy, ws, slack, xs = _f16_case(shape, sum(shape))
     dy = dy * scale
-    assert torch.equal(xh, x.half())
-    assert torch.equal(xl, ((x - xh.float()) * 2048.0).half())
+    assert torch.equal(xh[..., :w], x.half())
+    assert torch.equal(xl[..., :w], ((x - xh[..., :w].float()) * 2048.0).half())
+    assert not xh[..., w:].any() and not xl[..., w:].any()
     dw64 = torch.empty((co, ci, k, k), dtype=torch.float64, device="cuda")
     db64 = torch.empty(co, dtype=torch.float64, device="cuda")
     ws64 = torch.empty(max(1, ops.wgrad_workspace(x.double(), co, k, d)), dtype=torch.uint8,
@@ -311,7 +328,7 @@ def test_tc_weight_gradient_fp16_split(shape, kernel, scale, force_env):
     for _ in range(2):
         dw = torch.full((co, ci, k, k), float("nan"), device="cuda")
         db = torch.full((co,), float("nan"), device="cuda")
-        ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, slack)
+        ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, slack, **xs)
         outs.append((dw, db))
     torch.cuda.synchronize()
     dw, db = outs[0]
@@ -322,18 +339,19 @@ def test_tc_weight_gradient_fp16_split(shape, kernel, scale, force_env):
 
 
 @pytest.mark.parametrize("bad", [4e4, float("inf")])
-@pytest.mark.parametrize("shape", F16_WGRAD_SHAPES[:3])
-def test_tc_weight_gradient_fp16_range_fallback(shape, bad):
+@pytest.mark.parametrize("shape", F16_WGRAD_SHAPES[:3] + F16_WGRAD_SHAPES[6:7])
+def test_tc_weight_gradient_fp16_range_fallback(shape, bad, monkeypatch):
     """One dy element outside fp16's range (or not finite) trips the device flag: the fp16
     launches exit and the gated tf32 kernel runs -- bit-identical to calling it directly."""
+    monkeypatch.setenv("DP_WG_F16_RES2", "1")
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
-    x, xh, xl, dy, ws, slack = _f16_case(shape, 7)
+    x, xh, xl, dy, ws, slack, xs = _f16_case(shape, 7)
     dy[n - 1, co - 1, 1, 2] = bad
     dw = torch.full((co, ci, k, k), float("nan"), device="cuda")
     db = torch.full((co,), float("nan"), device="cuda")
-    ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, slack)
+    ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, slack, **xs)
     ws32 = torch.empty(ops.wgrad_fast_workspace(x, co, k, d), dtype=torch.uint8, device="cuda")
     dw2, db2 = torch.empty_like(dw), torch.empty_like(db)
     ops.conv_backward_kernel_fast(x, dy, dw2, db2, k, d, ws32, x_slack=slack)

@@ -9,12 +9,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1412_4526_b200.engine import SLACK_BYTES, _slack_empty, ops  # noqa: E402
 
 
-def split16(x, kw16):
-    hi = _slack_empty(tuple(x.shape), kw16)
-    lo = _slack_empty(tuple(x.shape), kw16)
-    ops.split_f16(x, hi, lo)
-    assert torch.equal(hi, x.half()) and torch.equal(lo, ((x - hi.float()) * 2048.0).half())
-    return hi, lo
+def split16(x, kw16, shift):
+    w = x.shape[3]
+    shp = tuple(x.shape[:3]) + ((w + 7) // 8 * 8,)
+    t = [_slack_empty(shp, kw16) for _ in range(4 if shift else 2)]
+    ops.split_f16(x, *t, shift) if shift else ops.split_f16(x, *t)
+    hi, lo = t[0], t[1]
+    assert torch.equal(hi[..., :w], x.half())
+    assert torch.equal(lo[..., :w], ((x - hi[..., :w].float()) * 2048.0).half())
+    return t + [None, None] if not shift else t
 
 
 def timeit(f, reps=10):
@@ -42,7 +45,8 @@ def main():
         dy = (torch.rand((n, co, ho, ho), generator=g, **kw) - 0.5) * 1e-2
         if os.environ.get("BIG_DY"):  # one delta outside fp16's range: the tf32 fallback runs
             dy[0, 0, 0, 0] = 4e4
-        xh, xl = split16(x, {"dtype": torch.float16, "device": "cuda"})
+        shift = max(0, ops.wgrad_f16_shift(x, co, k, d))
+        xh, xl, xhs, xls = split16(x, {"dtype": torch.float16, "device": "cuda"}, shift)
         ref_w = torch.empty((co, ci, k, k), dtype=torch.float64, device="cuda")
         ref_b = torch.empty((co,), dtype=torch.float64, device="cuda")
         ws64 = torch.empty(max(1, ops.wgrad_workspace(x.double(), co, k, d)), dtype=torch.uint8,
@@ -63,7 +67,8 @@ def main():
                     print(arg, "f16 unsupported")
                     continue
                 f = lambda: ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d,  # noqa
-                                                              ws16, SLACK_BYTES)
+                                                              ws16, SLACK_BYTES, x_hi_s=xhs,
+                                                              x_lo_s=xls)
             ms = timeit(f)
             ew = float((dw.double() - ref_w).abs().max() / ref_w.abs().max())
             eb = float((db.double() - ref_b).abs().max() / ref_b.abs().max())

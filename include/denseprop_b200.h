@@ -191,6 +191,13 @@ size_t dp_conv_backward_kernel_fast_f16_workspace(int n, int cin, int hi, int wi
  * same padded arrays shifted left by `shift` (1..7) halves, x_hi_s[i] = x_hi[i + shift] (ABI 6) */
 int dp_split_f16(const float *x, void *x_hi, void *x_lo, void *x_hi_s, void *x_lo_s, int shift,
                  int64_t rows, int w, int pitch, void *stream);
+/* dp_maxpool_forward (f32, 1-byte codes) that also writes the output's fp16 split as
+ * dp_split_f16 does (rows of y_pitch halves, a multiple of 8; the pad columns are not
+ * written: the caller zeroes them once) -- fused into the warp-streaming kernel where it
+ * applies, else the pool then the split (ABI 6) */
+int dp_maxpool_forward_split(const float *x, float *y, void *arg, int n, int c, int h, int w,
+                             int p, int d, int nonlin, void *y_hi, void *y_lo, int y_pitch,
+                             void *stream);
 /* the shift (halves) the fp16 weight gradient's second tap residue needs its shifted copies
  * at (0: one residue, no copies; -1: the fp16 form does not apply) */
 int dp_conv_backward_kernel_fast_f16_shift(int n, int cin, int hi, int wi, int cout, int k,

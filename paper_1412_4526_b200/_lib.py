@@ -69,6 +69,7 @@ SIGNATURES = {
     "dp_conv_backward_kernel_fast_f16_workspace": (_sz, [_i] * 7),
     "dp_split_f16": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i64, _i, _i, _vp]),
     "dp_conv_backward_kernel_fast_f16_shift": (_i, [_i] * 7),
+    "dp_maxpool_forward_split": (_i, [_vp, _vp, _vp] + [_i] * 7 + [_vp, _vp, _i, _vp]),
     "dp_conv_backward_kernel_fast_f16": (_i, [_vp, _sz, _vp, _vp, _vp, _vp, _sz, _i, _vp, _i,
                                               _vp, _vp] +
                                          [_i] * 7 + [_vp, _sz, _vp]),

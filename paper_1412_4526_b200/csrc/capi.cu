@@ -16,6 +16,9 @@ namespace dp {
 size_t ws_workspace_f16(int n, int cin, int hi, int wi, int cout, int k, int d);
 int tc_split_f16_launch(const float *x, void *hi, void *lo, void *hs, void *ls, int shift,
                         long long rows, int w, int wp, cudaStream_t st);
+int maxpool_forward_stream(const float *x, float *y, void *arg, int arg_bytes, long long planes,
+                           int h, int w, int p, int d, int act, cudaStream_t st, void *yh,
+                           void *yl, int yp);
 int ws_shift_f16(int n, int cin, int hi, int wi, int cout, int k, int d);
 int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi,
                                 const void *x_lo, const void *x_hi_s, const void *x_lo_s,
@@ -417,6 +420,25 @@ int dp_split_f16(const float *x, void *x_hi, void *x_lo, void *x_hi_s, void *x_l
                                             (long long)rows, w);
     return dp::tc_split_f16_launch(x, x_hi, x_lo, x_hi_s, x_lo_s, shift, rows, w, pitch,
                                    (cudaStream_t)stream);
+}
+
+int dp_maxpool_forward_split(const float *x, float *y, void *arg, int n, int c, int h, int w,
+                             int p, int d, int nonlin, void *y_hi, void *y_lo, int y_pitch,
+                             void *stream) {
+    DP_TRY(check_pos("batch", n));
+    DP_TRY(check_pos("channels", c));
+    DP_TRY(check_nonlin(nonlin));
+    DP_TRY(check_window("dilated max pool", h, w, p, d));
+    if (p * p > 256) return set_error(DP_ERR_ARG, "split pool forward: uint8 codes need p*p <= 256");
+    const int ho = h - (p - 1) * d, wo = w - (p - 1) * d;
+    cudaStream_t st = (cudaStream_t)stream;
+    // fused: the warp-streaming kernel writes the split with the output
+    const int rc = dp::maxpool_forward_stream(x, y, arg, 1, (long long)n * c, h, w, p, d, nonlin,
+                                              st, y_hi, y_lo, y_pitch);
+    if (rc >= 0) return rc;
+    DP_TRY(maxpool_forward_t<float>(x, y, arg, 1, n, c, h, w, p, d, nonlin, st));
+    return dp::tc_split_f16_launch(y, y_hi, y_lo, nullptr, nullptr, 0, (long long)n * c * ho, wo,
+                                   y_pitch, st);
 }
 
 int dp_conv_backward_kernel_fast_f16_shift(int n, int cin, int hi, int wi, int cout, int k,

@@ -596,7 +596,8 @@ static inline dim3 pool_grid(long long planes, long long pixels) {
 
 // pool_stream.cu: warp-streaming fp32 / uint8-code kernels; -1 = shape not covered
 int maxpool_forward_stream(const float *x, float *y, void *arg, int arg_bytes, long long planes,
-                           int h, int w, int p, int d, int act, cudaStream_t st);
+                           int h, int w, int p, int d, int act, cudaStream_t st,
+                           void *yh = nullptr, void *yl = nullptr, int yp = 0);
 int maxpool_backward_stream(const float *dy, const void *arg, int arg_bytes, float *dx,
                             long long planes, int ho, int wo, int p, int d, int hi, int wi,
                             const float *gate, int gate_kind, int wd, cudaStream_t st);

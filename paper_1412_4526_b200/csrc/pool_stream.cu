@@ -119,7 +119,8 @@ template <int P, int D>
 __global__ void __launch_bounds__(MS_WARPS * 32)
     maxpool_fwd_stream(const float *__restrict__ x, float *__restrict__ y,
                        uint8_t *__restrict__ arg, int H, int W, int Ho, int Wo, int act,
-                       int sx_n, int sy_n, long long items, int vec) {
+                       int sx_n, int sy_n, long long items, int vec, __half *__restrict__ yh,
+                       __half *__restrict__ yl, int yp) {
     using G = MsFwd<P, D>;
     extern __shared__ __align__(16) unsigned char ms_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -247,6 +248,24 @@ __global__ void __launch_bounds__(MS_WARPS * 32)
                 }
             }
             ms_act4(ob, act);
+            if (yh) {
+                // the fp16 weight gradient's split of this output (rows of yp halves)
+                const long long ho_ = (plane * Ho + u0 + u) * (long long)yp + x0 + 4 * lane;
+                uint32_t h2[2], l2[2];
+                ptx::f16_split2_scaled(ob[0], ob[1], h2[0], l2[0]);
+                ptx::f16_split2_scaled(ob[2], ob[3], h2[1], l2[1]);
+                if (cols >= 4) {
+                    *reinterpret_cast<uint2 *>(yh + ho_) = make_uint2(h2[0], h2[1]);
+                    *reinterpret_cast<uint2 *>(yl + ho_) = make_uint2(l2[0], l2[1]);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m < cols) {
+                            yh[ho_ + m] = reinterpret_cast<const __half *>(h2)[m];
+                            yl[ho_ + m] = reinterpret_cast<const __half *>(l2)[m];
+                        }
+                }
+            }
             if (vfull) {
                 *reinterpret_cast<float4 *>(yo) = make_float4(ob[0], ob[1], ob[2], ob[3]);
                 *reinterpret_cast<uint32_t *>(ao) = oc;
@@ -411,7 +430,8 @@ static int ms_grid(const void *kern, size_t smem, long long items) {
 
 template <int P, int D>
 static int ms_fwd_launch(const float *x, float *y, uint8_t *arg, long long planes, int h, int w,
-                         int ho, int wo, int act, cudaStream_t st) {
+                         int ho, int wo, int act, cudaStream_t st, __half *yh, __half *yl,
+                         int yp) {
     using G = MsFwd<P, D>;
     const size_t smem = MS_WARPS * G::WARP_BYTES;
     auto kern = maxpool_fwd_stream<P, D>;
@@ -424,7 +444,7 @@ static int ms_fwd_launch(const float *x, float *y, uint8_t *arg, long long plane
     const int vec = (wo % 4 == 0) && ((uintptr_t)y % 16 == 0) && ((uintptr_t)arg % 4 == 0);
     if ((uintptr_t)x % 16 != 0) return -1;  // rows are staged from 16-byte boundaries of x
     kern<<<ms_grid((const void *)kern, smem, items), MS_WARPS * 32, smem, st>>>(
-        x, y, arg, h, w, ho, wo, act, sx_n, sy_n, items, vec);
+        x, y, arg, h, w, ho, wo, act, sx_n, sy_n, items, vec, yh, yl, yp);
     return check_launch("maxpool_fwd_stream");
 }
 
@@ -472,15 +492,21 @@ static bool ms_enabled() {
 }
 
 // -1: not applicable (the caller uses pool.cu's kernels); else DP_OK / an error code
+// yh / yl (or null): also write the output's fp16 split (hi, lo' = (y - hi) * 2^11) in rows
+// of yp halves (yp % 4 == 0, 8-byte aligned; columns past wo are left untouched)
 int maxpool_forward_stream(const float *x, float *y, void *arg, int arg_bytes, long long planes,
-                           int h, int w, int p, int d, int act, cudaStream_t st) {
+                           int h, int w, int p, int d, int act, cudaStream_t st, void *yh,
+                           void *yl, int yp) {
     // p = 2 stays on pool.cu's register-tile kernel except at d = 4..8 (c3 pool2: 0.50 ->
     // 0.47 ms here; d = 1 / 2 / 16 measured 3-65 % slower: two taps per output leave the
     // streaming overhead unamortised)
     const bool p2ok = (d >= 4 && d <= 8) || getenv("DP_POOL_STREAM_P2");
     if (arg_bytes != 1 || !ms_enabled() || (p < 3 && !p2ok)) return -1;
     const int ho = h - (p - 1) * d, wo = w - (p - 1) * d;
-#define MS_F(PP, DD) ms_fwd_launch<PP, DD>(x, y, (uint8_t *)arg, planes, h, w, ho, wo, act, st)
+    if (yh && (yp < wo || (yp & 3) || ((uintptr_t)yh & 7) || ((uintptr_t)yl & 7))) return -1;
+#define MS_F(PP, DD)                                                                    \
+    ms_fwd_launch<PP, DD>(x, y, (uint8_t *)arg, planes, h, w, ho, wo, act, st, (__half *)yh, \
+                          (__half *)yl, yp)
     MS_PD_SWITCH(p, d, MS_F)
 #undef MS_F
 }

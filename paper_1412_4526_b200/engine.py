@@ -277,6 +277,16 @@ class ops:
                                                      _stream()), "maxpool_forward")
 
     @staticmethod
+    def maxpool_forward_split(x, y, arg, p, d, nonlin, y_hi, y_lo):
+        """maxpool_forward (fp32, uint8 codes) that also writes y's fp16 split (split_f16's
+        layout; pad columns untouched), fused into the streaming kernel where it applies."""
+        with _Rec('maxpool_forward', 1, 'hbm', _nbytes(x, y, arg, y_hi, y_lo)):
+            n, c, h, w = x.shape
+            _lib.check(_lib_dev().dp_maxpool_forward_split(
+                _ptr(x), _ptr(y), _ptr(arg), n, c, h, w, p, d, nonlin, _ptr(y_hi), _ptr(y_lo),
+                y_hi.shape[3], _stream()), "maxpool_forward_split")
+
+    @staticmethod
     def maxpool_backward(dy, arg, dx, p, d, gate=None, gate_kind=_lib.DP_IDENTITY, dx_pitch=0):
         """dx_pitch: write dx with that row pitch (dx a strided (n, c, h, w) view)."""
         with _Rec('maxpool_backward', 1, 'hbm', _nbytes(dy, arg, dx, gate)):
@@ -604,7 +614,8 @@ class DenseNet:
                         # rows padded to 16 bytes; a second tap residue reads copies shifted
                         # by `shift` halves (its TMA boxes must start 16-byte aligned)
                         shp = tuple(xin.shape[:3]) + ((xin.shape[3] + 7) // 8 * 8,)
-                        t = [_slack_empty(shp, kw16) for _ in range(4 if shift else 2)]
+                        # (zeroed: the fused pool forward leaves the pad columns alone)
+                        t = [_slack_zeros(shp, kw16) for _ in range(4 if shift else 2)]
                         self._wg16[gi] = {"hi": t[0], "lo": t[1], "nb": nb, "shift": shift,
                                           "hs": t[2] if shift else None,
                                           "ls": t[3] if shift else None}
@@ -737,6 +748,8 @@ class DenseNet:
                 self._prepared.add(gi)
             if act == _lib.DP_TANH and self.precision == "fast":
                 act = _lib.DP_TANH_FAST  # tanhf (<= 2 ulp) instead of the fp64 evaluation
+            # the next conv's fp16 weight-gradient operand (split of y), if it has one
+            s16 = getattr(self, "_wg16", {}).get(gi + 1) if self.train else None
             if isinstance(op, DilatedConv):
                 wt, b = self.params[g.first]
                 if self.tc.get(gi, (False, False))[0]:
@@ -745,7 +758,13 @@ class DenseNet:
                 else:
                     ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
             elif isinstance(op, DilatedPool):
-                if op.base.kind == "max":
+                if (op.base.kind == "max" and s16 is not None and not s16["shift"] and
+                        self.args[gi].dtype == torch.uint8 and x.dtype == torch.float32):
+                    # the next conv's fp16 weight-gradient operand, written with the output
+                    ops.maxpool_forward_split(x, y, self.args[gi], op.base.kernel_size,
+                                              op.dilation, act, s16["hi"], s16["lo"])
+                    s16 = None
+                elif op.base.kind == "max":
                     ops.maxpool_forward(x, y, self.args[gi], op.base.kernel_size, op.dilation,
                                         act)
                 else:
@@ -758,8 +777,7 @@ class DenseNet:
                     if kind == _lib.DP_TANH and self.precision == "fast":
                         kind = _lib.DP_TANH_FAST
                     ops.nonlin_forward(x, y, kind)
-            if self.train and gi + 1 in getattr(self, "_wg16", {}):
-                s16 = self._wg16[gi + 1]
+            if s16 is not None:  # not fused into the producer: a split pass
                 ops.split_f16(y, s16["hi"], s16["lo"], s16["hs"], s16["ls"], s16["shift"])
         return self.output
 

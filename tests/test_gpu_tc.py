@@ -545,3 +545,37 @@ def test_tc_fp16_pack_last_chunk(shape, mode):
     torch.cuda.synchronize()
     assert torch.isfinite(y).all()
     assert _rel(y, ref) < TOL
+
+
+@pytest.mark.parametrize("shape", [
+    # n, c, h, w, p, d
+    (2, 50, 70, 72, 2, 4),     # c3 pool2-like: warp-streaming kernel, split fused
+    (1, 8, 61, 67, 2, 8),      # ragged width (pitch padded, scalar tail stores)
+    (2, 5, 40, 45, 4, 1),      # p = 4 streaming
+    (1, 6, 30, 33, 2, 1),      # p = 2, d = 1: pool.cu kernel + split pass
+])
+def test_maxpool_forward_split(shape):
+    """dp_maxpool_forward_split: y and the argmax codes bit-identical to dp_maxpool_forward,
+    the split equal to dp_split_f16 of y (fused or as a second pass), pad columns untouched."""
+    import torch
+    from paper_1412_4526_b200 import _lib
+    from paper_1412_4526_b200.engine import ops
+    n, c, h, w, p, d = shape
+    e = (p - 1) * d + 1
+    ho, wo = h - e + 1, w - e + 1
+    rng = np.random.default_rng(sum(shape))
+    x = _t(rng.normal(size=(n, c, h, w)).astype(np.float32))
+    y1 = torch.empty((n, c, ho, wo), device="cuda")
+    a1 = torch.empty((n, c, ho, wo), dtype=torch.uint8, device="cuda")
+    ops.maxpool_forward(x, y1, a1, p, d, _lib.DP_TANH_FAST)
+    wp = (wo + 7) // 8 * 8
+    y2, a2 = torch.empty_like(y1), torch.empty_like(a1)
+    kw16 = {"dtype": torch.float16, "device": "cuda"}
+    hi = torch.full((n, c, ho, wp), 7.0, **kw16)
+    lo = torch.full((n, c, ho, wp), 7.0, **kw16)
+    ops.maxpool_forward_split(x, y2, a2, p, d, _lib.DP_TANH_FAST, hi, lo)
+    hr, lr = torch.zeros_like(hi), torch.zeros_like(lo)
+    ops.split_f16(y1, hr, lr)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(a1, a2)
+    assert torch.equal(hi[..., :wo], hr[..., :wo]) and torch.equal(lo[..., :wo], lr[..., :wo])

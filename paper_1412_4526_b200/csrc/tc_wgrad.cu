@@ -816,8 +816,11 @@ int wg_stage_x_taps(const float *x, float *xs, int n, int cin, int hi, int wi, i
 int wg_stage_dy(const float *dy, float *dys, int n, int cout, int ho, int wo, int wp, int lm,
                 cudaStream_t st, int src_pitch, const int *exit_unless) {
     const long long quads = (long long)n * cout * ho * (wp / 4);
-    tc_stage_dy<<<stage_grid(quads), 256, 0, st>>>(dy, dys, cout, ho, wo, wp, lm, quads,
-                                                   src_pitch > 0 ? src_pitch : wo, exit_unless);
+    // a gated fallback usually exits at once: a small grid-stride grid keeps that ~3 us
+    // (the full grid measured 22 us of block launches that only read the flag)
+    const int grid = exit_unless ? std::min(stage_grid(quads), 2 * wg_num_sms()) : stage_grid(quads);
+    tc_stage_dy<<<grid, 256, 0, st>>>(dy, dys, cout, ho, wo, wp, lm, quads,
+                                      src_pitch > 0 ? src_pitch : wo, exit_unless);
     return check_launch("tc_stage_dy");
 }
 

@@ -24,8 +24,10 @@ SEQ = [("tc_relayout_pk", "00:conv_forward_tc"), ("tc_conv_flat_kernel<1, 0, 3",
        ("maxpool_fwd_stream", "03:maxpool_forward"),
        ("tc_relayout_f16<0>", "04:conv_forward_tc"), ("tc_conv_tap_kernel<0, 1>", "04:conv_forward_tc"),
        ("tc_conv_flat_kernel<1, 0, 0, 0>", "04:conv_forward_tc"),
-       ("mask_delta", "05:mask_delta"), ("tc_stage_dy", "06:conv_backward_kernel_tc"),
+       ("mask_delta", "05:mask_delta"), ("tc_stage_dy16", "06:conv_backward_kernel_tc"),
        ("tc_wgrad_ss", "06:conv_backward_kernel_tc"),
+       # the fp16 weight gradient's gated tf32 fallback (dy staging, kernel: exit at once)
+       ("tc_stage_dy", "06:conv_backward_kernel_tc"), ("tc_wgrad_ss", "06:conv_backward_kernel_tc"),
        ("tc_relayout_f16_pk<1>", "07:conv_backward_data_tc"),
        ("tc_conv_flat_kernel<1, 1, 1, 1>", "07:conv_backward_data_tc"),
        ("tc_conv_flat_kernel<1, 1, 0, 0>", "07:conv_backward_data_tc"),

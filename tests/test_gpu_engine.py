@@ -522,3 +522,51 @@ def test_engine_step_with_softmax_xent(dp):
             assert np.abs(ke[k]).max() > 0
             assert rel_err(kf[k], ke[k]) < 1e-4
             assert rel_err(bf[k], be[k]) < 1e-4
+
+
+_C3 = ("input channels=3\n"
+       "conv out=50 in=3 k=6 stride=1 weights=seed:0\n"
+       "pool kind=max k=4 stride=4\nnonlin kind=tanh\n"
+       "conv out=50 in=50 k=3 stride=1 weights=seed:3\n"
+       "pool kind=max k=2 stride=2\nnonlin kind=tanh\n"
+       "conv out=8 in=50 k=7 stride=1 weights=seed:6\n")
+
+
+@pytest.mark.parametrize("target_scale", [1.0, 1e6])
+def test_engine_fp16_weight_gradient_and_its_guard(dp, monkeypatch, target_scale):
+    """c3 widths (the head's weight gradient on the fp16 split, its input split in the pool2
+    forward) vs the same engine with DP_WG_F16=0 (3xTF32 weight gradients): within 1e-4 at
+    ordinary deltas; with deltas beyond fp16's range the device flag sends that layer to its
+    tf32 launches, which then give bit-identical gradients."""
+    import torch
+    from paper_1412_4526_b200.engine import DenseNet
+    spec = dp.parse_spec(_C3)
+    plan = dp.compile_plan(spec)
+    side, batch = 96, 2
+    rng = np.random.default_rng(5)
+    imgs = torch.from_numpy(rng.uniform(-0.5, 0.5, (batch, 3, side, side)).astype(np.float32))
+    tgt = torch.from_numpy((rng.uniform(-1, 1, (batch, 8, side, side)) * target_scale)
+                           .astype(np.float32))
+    grads, plans = {}, {}
+    for mode in ("f16", "tf32"):
+        if mode == "tf32":
+            monkeypatch.setenv("DP_WG_F16", "0")
+        e = DenseNet(plan, batch, side, side, dtype=torch.float32, precision="fast")
+        e.set_input(imgs.cuda())
+        e.forward()
+        e.target.copy_(tgt)
+        e.mask.fill_(1)
+        e.loss_delta()
+        e.backward()
+        torch.cuda.synchronize()
+        grads[mode] = e.grad_flat.clone()
+        plans[mode] = e.kernel_plan()
+    head = max(plans["f16"])
+    assert plans["f16"][head]["weight_grad"] == "tcgen05-fp16x3-offset"
+    assert plans["tf32"][head]["weight_grad"] == "tcgen05-3xtf32"
+    g16, g32 = grads["f16"], grads["tf32"]
+    assert torch.isfinite(g16).all()
+    if target_scale > 1e5:
+        assert torch.equal(g16, g32)
+    else:
+        assert rel_err(g16.double().cpu().numpy(), g32.double().cpu().numpy()) < 1e-4

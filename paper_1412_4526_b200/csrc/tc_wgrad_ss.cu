@@ -781,7 +781,10 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     // the group's tap rows + SS - 1 + mirrors) does not fit -- then smaller groups (fewer
     // tap rows each; every group re-reads its rows), down to one tile.
     p.SS = 0;
-    for (int G = std::min(std::min(p.n_tiles, 512 / acc_cols), WS_MAX_G); G >= 1 && !p.SS; --G) {
+    int g_max = std::min(std::min(p.n_tiles, 512 / acc_cols), WS_MAX_G);
+    if (const char *e = getenv("DP_WG_GMAX"))  // experiments: smaller tile groups, more stages
+        g_max = std::max(1, std::min(g_max, atoi(e)));
+    for (int G = g_max; G >= 1 && !p.SS; --G) {
         p.n_groups = (p.n_tiles + G - 1) / G;
         p.G = (p.n_tiles + p.n_groups - 1) / p.n_groups;
         // tap rows per group and the ring slots a 128-line tile can span

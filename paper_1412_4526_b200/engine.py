@@ -759,7 +759,8 @@ class DenseNet:
                     ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
             elif isinstance(op, DilatedPool):
                 if (op.base.kind == "max" and s16 is not None and not s16["shift"] and
-                        self.args[gi].dtype == torch.uint8 and x.dtype == torch.float32):
+                        self.args[gi].dtype == torch.uint8 and x.dtype == torch.float32 and
+                        not os.environ.get("DP_NO_SPLIT_FUSE")):
                     # the next conv's fp16 weight-gradient operand, written with the output
                     ops.maxpool_forward_split(x, y, self.args[gi], op.base.kernel_size,
                                               op.dilation, act, s16["hi"], s16["lo"])

@@ -532,12 +532,16 @@ _C3 = ("input channels=3\n"
        "conv out=8 in=50 k=7 stride=1 weights=seed:6\n")
 
 
+@pytest.mark.parametrize("split", ["fused", "pass"])
 @pytest.mark.parametrize("target_scale", [1.0, 1e6])
-def test_engine_fp16_weight_gradient_and_its_guard(dp, monkeypatch, target_scale):
+def test_engine_fp16_weight_gradient_and_its_guard(dp, monkeypatch, target_scale, split):
     """c3 widths (the head's weight gradient on the fp16 split, its input split in the pool2
-    forward) vs the same engine with DP_WG_F16=0 (3xTF32 weight gradients): within 1e-4 at
-    ordinary deltas; with deltas beyond fp16's range the device flag sends that layer to its
-    tf32 launches, which then give bit-identical gradients."""
+    forward -- or by a separate split pass, DP_NO_SPLIT_FUSE) vs the same engine with
+    DP_WG_F16=0 (3xTF32 weight gradients): within 1e-4 at ordinary deltas; with deltas beyond
+    fp16's range the device flag sends that layer to its tf32 launches, which then give
+    bit-identical gradients."""
+    if split == "pass":
+        monkeypatch.setenv("DP_NO_SPLIT_FUSE", "1")
     import torch
     from paper_1412_4526_b200.engine import DenseNet
     spec = dp.parse_spec(_C3)

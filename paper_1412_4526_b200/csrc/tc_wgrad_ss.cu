@@ -104,6 +104,11 @@ struct WsArgs {
     int no_m64;   // DP_WG_NO_M64: run a short last tile as M = 128 (experiments)
     int pf;       // L2 prefetch distance in K blocks (DP_WG_PF, 0 = off)
     int f16;      // fp16-split operands: tm_x1 = x lo', tm_xp = dy lo' (offset split, 2^11)
+    int dycomb;   // fp16: ONE dy box {64, Q, J, row, hl} brings B_hi and B_lo' (tm_dy; rows
+                  // n*Ho + u); B_lo' then starts at row LO = J*Q (else two boxes, LO = NB)
+    int LO;       // B row (and accumulator column) offset of the lo' half
+    int dy_rows;  // dycomb: n * Ho folded rows (a row past Ho -- a column phase running past
+                  // the image -- is sent to this out-of-range row: TMA zero fill)
     unsigned long long *trace;  // DP_WG_TRACE: per-K-block clock64 stamps of CTA 0
     const int *exit_if;         // fp16 kernel: exit when its operands tripped the range flag
     const int *exit_unless;     // its tf32 fallback: run only when they did
@@ -218,13 +223,18 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         for (int kl = 0; kl < nkb; ++kl, sc.next(), pf.next()) {
             if (a.pf && lane == 0 && kl + a.pf < nkb) {
                 const int pv0 = pf.vb * (a.f16 ? 64 : 32);
-                if (a.J == 1)
+                const int prow = pf.u < a.Ho ? pf.img * a.Ho + pf.u : a.dy_rows;
+                if (a.dycomb && a.J == 1)
+                    ptx::tma_prefetch_l2_4d(&tm_dy, pv0, 0, prow, 0);
+                else if (a.dycomb)
+                    ptx::tma_prefetch_l2_5d(&tm_dy, pv0, 0, 0, prow, 0);
+                else if (a.J == 1)
                     ptx::tma_prefetch_l2_4d(&tm_dy, pv0, pf.u, 0, pf.img);
                 else
                     ptx::tma_prefetch_l2_5d(&tm_dy, pv0, 0, 0, pf.u, pf.img);
-                if (a.f16 && a.J == 1)
+                if (a.f16 && !a.dycomb && a.J == 1)
                     ptx::tma_prefetch_l2_4d(&tm_xp, pv0, pf.u, 0, pf.img);
-                else if (a.f16)
+                else if (a.f16 && !a.dycomb)
                     ptx::tma_prefetch_l2_5d(&tm_xp, pv0, 0, 0, pf.u, pf.img);
                 for (int k = pf.cstart ? 0 : n_i - 1; k < n_i; ++k) {
                     if (a.direct) {
@@ -281,14 +291,21 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 }
                 ptx::mbar_expect_tx(&sfull[s], f16x * ((uint32_t)(a.J * a.Q) * 128u +
                                                           (uint32_t)nbox_rows * a.box_tx_row));
-                if (a.f16) {  // B_lo' straight from the staged fp16 lo' rows
+                if (a.f16 && !a.dycomb) {  // B_lo' straight from the staged fp16 lo' rows
                     unsigned char *bl = smem + (size_t)s * a.b_bytes + (size_t)a.NB * 128;
                     if (a.J == 1)
                         ptx::tma_load_4d(bl, &tm_xp, v0, sc.u, 0, sc.img, &sfull[s]);
                     else
                         ptx::tma_load_5d(bl, &tm_xp, v0, 0, 0, sc.u, sc.img, &sfull[s]);
                 }
-                if (a.J == 1) {
+                const int drow = sc.u < a.Ho ? sc.img * a.Ho + sc.u : a.dy_rows;
+                if (a.dycomb && a.J == 1) {  // (w, o, row, hl): hi rows then lo' rows
+                    ptx::tma_load_4d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, 0, drow, 0,
+                                     &sfull[s]);
+                } else if (a.dycomb) {       // (w, o, jb', row, hl)
+                    ptx::tma_load_5d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, 0, 0, drow, 0,
+                                     &sfull[s]);
+                } else if (a.J == 1) {
                     ptx::tma_load_4d(smem + (size_t)s * a.b_bytes, &tm_dy, v0, sc.u, 0, sc.img,
                                      &sfull[s]);
                 } else {
@@ -344,11 +361,13 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         }
     } else if (warp == WS_MMA_WARP) {
         // ================================ MMA issuer ================================
-        const uint32_t idesc_2n =
-            a.f16 ? ptx::idesc_f16(128, 2 * a.NB) : ptx::idesc_tf32(128, 2 * a.NB);
+        // [B_hi | B_lo'] spans LO + NB rows... the stacked MMA's N: 2 NB, or 2 J Q when the
+        // halves come in one box (J Q a multiple of 8)
+        const int n2 = a.dycomb ? 2 * a.LO : 2 * a.NB;
+        const uint32_t idesc_2n = a.f16 ? ptx::idesc_f16(128, n2) : ptx::idesc_tf32(128, 2 * a.NB);
         const uint32_t idesc_n = a.f16 ? ptx::idesc_f16(128, a.NB) : ptx::idesc_tf32(128, a.NB);
         const uint32_t idesc_2n64 =
-            a.f16 ? ptx::idesc_f16(64, 2 * a.NB) : ptx::idesc_tf32(64, 2 * a.NB);
+            a.f16 ? ptx::idesc_f16(64, n2) : ptx::idesc_tf32(64, 2 * a.NB);
         const uint32_t idesc_n64 = a.f16 ? ptx::idesc_f16(64, a.NB) : ptx::idesc_tf32(64, a.NB);
         const uint32_t sbase = ptx::smem_u32(smem);
         const uint32_t hi_base = sbase + a.ring_hi, lo_base = sbase + a.ring_lo;
@@ -387,7 +406,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) {
                             ptx::mma_f16_ss(dcol, da + 2 * ks, bd0 + 2 * ks, i2, (kl | ks) > 0);
-                            ptx::mma_f16_ss(dcol + (uint32_t)a.NB, da + lo_units + 2 * ks,
+                            ptx::mma_f16_ss(dcol + (uint32_t)a.LO, da + lo_units + 2 * ks,
                                             bd0 + 2 * ks, i1, 1);
                         }
                     } else {
@@ -415,10 +434,12 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
         const int nchunks = a.NB * 8;    // 16-byte chunks of the dy tiles
         const int db0 = (a.J - 1) * a.Q * 8;  // the unshifted copy (jb' = J-1): db
         const int db1 = db0 + a.Q * 8;
-        // B rows past J*Q are never loaded: zero them once in every stage
+        // B rows past J*Q are never loaded: zero them once in every stage (combined fp16 dy
+        // box: the rows past both halves)
         for (int st_ = 0; st_ < a.SS; ++st_) {
             float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)st_ * a.b_bytes);
-            for (int idx = a.J * a.Q * 8 + tid; idx < nchunks; idx += WS_CONV_WARPS * 32)
+            const int z0 = (a.dycomb ? 2 : 1) * a.J * a.Q * 8, z1 = (a.dycomb ? 2 : 1) * nchunks;
+            for (int idx = z0 + tid; idx < z1; idx += WS_CONV_WARPS * 32)
                 bh[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -433,7 +454,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
             if (a.f16) {
                 // db from the staged split: dy = hi + lo' * 2^-11 (8 halves per chunk)
                 const uint4 *bh = reinterpret_cast<const uint4 *>(st);
-                const uint4 *bl = reinterpret_cast<const uint4 *>(st + (uint32_t)a.NB * 128);
+                const uint4 *bl = reinterpret_cast<const uint4 *>(st + (uint32_t)a.LO * 128);
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const int idx = tid + 256 * m;
@@ -541,7 +562,7 @@ tc_wgrad_ss_kernel(const __grid_constant__ CUtensorMap tm_x0,
                 if (nkb > 0) {
                     const uint32_t dcol = tmem + lane_off + (uint32_t)(t * acc_cols + o0);
                     ptx::tmem_ld16(dcol, h);
-                    ptx::tmem_ld16(dcol + a.NB, l2);
+                    ptx::tmem_ld16(dcol + a.LO, l2);
                     ptx::tmem_wait_ld();
                 }
 #pragma unroll
@@ -1033,6 +1054,9 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     a.NB = p.NB;
     a.tma_mirror = getenv("DP_WG_TMA_MIRROR") ? 1 : 0;
     a.f16 = 0;
+    a.dycomb = 0;
+    a.LO = p.NB;
+    a.dy_rows = 0;
     a.pair = p.pair;
     a.direct = p.direct;
     a.n_tiles = p.n_tiles;
@@ -1171,6 +1195,26 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
         }
         if (rc) return rc;
     }
+    // one box for both halves when J*Q is a multiple of 8 (the stacked MMA's N = 2 J Q then a
+    // multiple of 16): the staged rows (n, h) fold into one dimension, the hi -> lo' distance
+    // is a fifth (DP_WG_DY2BOX=1: two boxes)
+    const int dycomb = ((p.J * cout) % 8 == 0 && !getenv("DP_WG_DY2BOX")) ? 1 : 0;
+    if (dycomb) {
+        const cuuint64_t hlb = (cuuint64_t)((unsigned char *)dlo - (unsigned char *)dhi);
+        const cuuint64_t rows = (cuuint64_t)n * p.ho;
+        if (p.J == 1) {
+            cuuint64_t dims[4] = {(cuuint64_t)p.wo, (cuuint64_t)cout, rows, 2};
+            cuuint64_t str[3] = {rowb, rowb * cout, hlb};
+            cuuint32_t box[4] = {64, (cuuint32_t)cout, 1, 2};
+            rc = wg_make_map16(&mdy, dhi, 4, dims, str, box);
+        } else {
+            cuuint64_t dims[5] = {(cuuint64_t)p.wp_dy, (cuuint64_t)cout, (cuuint64_t)p.J, rows, 2};
+            cuuint64_t str[4] = {rowb, (cuuint64_t)p.sb * 2, rowb * cout, hlb};
+            cuuint32_t box[5] = {64, (cuuint32_t)cout, (cuuint32_t)p.J, 1, 2};
+            rc = wg_make_map16(&mdy, dhi, 5, dims, str, box);
+        }
+        if (rc) return rc;
+    }
     // residue rb's views: mx[2 rb] (hi), mx[2 rb + 1] (lo')
     for (int m = 0; m < 4; ++m) {
         const int rb = std::min(m / 2, p.rs.n_b - 1), hl = m & 1;
@@ -1198,6 +1242,9 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
     a.pair = 0;
     a.direct = 1;
     a.f16 = 1;
+    a.dycomb = dycomb;
+    a.LO = dycomb ? p.J * cout : p.NB;
+    a.dy_rows = n * p.ho;
     a.n_tiles = p.n_tiles;
     a.G = p.G;
     a.n_groups = p.n_groups;

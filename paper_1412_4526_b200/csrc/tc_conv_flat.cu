@@ -590,12 +590,14 @@ __global__ void tc_relayout_f16(const float *__restrict__ in, uint4 *__restrict_
 // [hi s0-3 | hi s4-7 | lo s0-3 | lo s4-7], hi = raw fp32 bits, lo = x - trunc_tf32(x).
 // The packed chunk's loaders were the limit of the 3-channel first layers (ncu, c3 conv1:
 // 28 % of the instructions at the record loads, 10 % at the flat-index divide).
+// (R a template parameter: with a runtime R the slot index t*R + c put v[] on the stack)
+template <int R>
 __global__ void __launch_bounds__(256) tc_relayout_pk(const float *__restrict__ in,
-                                                      float4 *__restrict__ xr, int R, int Hin,
+                                                      float4 *__restrict__ xr, int Hin,
                                                       int Win, int Wv, int pad, int d,
                                                       long long plane_recs, long long vrecs,
                                                       long long total) {
-    const int TP = 8 / R;
+    constexpr int TP = 8 / R;
     const long long cs = (long long)Hin * Win;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -619,8 +621,7 @@ __global__ void __launch_bounds__(256) tc_relayout_pk(const float *__restrict__ 
             if (!(y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
             const float *src = in + n * R * cs + (long long)y * Win + x;
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (c < R) v[t * R + c] = __ldg(src + c * cs);
+            for (int c = 0; c < R; ++c) v[t * R + c] = __ldg(src + c * cs);
         }
         float4 *dst = xr + n * 4 * plane_recs + f;
         dst[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -638,15 +639,15 @@ __global__ void __launch_bounds__(256) tc_relayout_pk(const float *__restrict__ 
 // flag as tc_relayout_f16
 // (the LAST chunk of a wider input when n_rc > 1: channels c_base .. c_base + rp of the R,
 // written to chunk n_rc - 1 of each image's planes)
-template <bool SCALED>
+template <bool SCALED, int R>
 __global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restrict__ in,
                                                           uint4 *__restrict__ xr, int R_all,
-                                                          int R, int c_base, int n_rc,
+                                                          int c_base, int n_rc,
                                                           int Hin, int Win, int Wv, int pad,
                                                           int d, long long plane_recs,
                                                           long long vrecs, long long total,
                                                           int *flag) {
-    const int TP = 16 / R;
+    constexpr int TP = 16 / R;
     const long long cs = (long long)Hin * Win;
     bool bad = false;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -669,8 +670,8 @@ __global__ void __launch_bounds__(256) tc_relayout_f16_pk(const float *__restric
             if (!(y >= 0 && y < Hin && x >= 0 && x < Win)) continue;
             const float *src = in + (n * R_all + c_base) * cs + (long long)y * Win + x;
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (c < R && t * R + c < 16) v[t * R + c] = __ldg(src + c * cs);
+            for (int c = 0; c < R; ++c)
+                if (t * R + c < 16) v[t * R + c] = __ldg(src + c * cs);
         }
         uint32_t hw[8], lw[8];
 #pragma unroll
@@ -954,14 +955,28 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
                 const long long gp = (tp_ + 255) / 256;
                 const int ggp = (int)(gp < 148 * 64 ? gp : 148 * 64);
                 const int c_base = (p.n_rc - 1) * 16;
-                if (bwd)
-                    tc_relayout_f16_pk<true><<<ggp, 256, 0, st>>>(
-                        in, (uint4 *)xr, R, p.rp, c_base, p.n_rc, Hin, Win, Wv, pad, d,
-                        plane_recs, vrecs, tp_, flag);
-                else
-                    tc_relayout_f16_pk<false><<<ggp, 256, 0, st>>>(
-                        in, (uint4 *)xr, R, p.rp, c_base, p.n_rc, Hin, Win, Wv, pad, d,
-                        plane_recs, vrecs, tp_, flag);
+#define DP_PK16(S, RR)                                                                  \
+    tc_relayout_f16_pk<S, RR><<<ggp, 256, 0, st>>>(in, (uint4 *)xr, R, c_base, p.n_rc, Hin,  \
+                                                   Win, Wv, pad, d, plane_recs, vrecs, tp_,  \
+                                                   flag)
+#define DP_PK16_R(S)                                                                    \
+    switch (p.rp) {                                                                     \
+        case 1: DP_PK16(S, 1); break;                                                   \
+        case 2: DP_PK16(S, 2); break;                                                   \
+        case 3: DP_PK16(S, 3); break;                                                   \
+        case 4: DP_PK16(S, 4); break;                                                   \
+        case 5: DP_PK16(S, 5); break;                                                   \
+        case 6: DP_PK16(S, 6); break;                                                   \
+        case 7: DP_PK16(S, 7); break;                                                   \
+        default: DP_PK16(S, 8); break;                                                  \
+    }
+                if (bwd) {
+                    DP_PK16_R(true)
+                } else {
+                    DP_PK16_R(false)
+                }
+#undef DP_PK16_R
+#undef DP_PK16
             }
             (void)gg;
             rc = check_launch("tc_relayout_f16");
@@ -989,10 +1004,17 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
             const long long total = (long long)n * q.n_rc * plane_recs;
             const long long g = (total + 255) / 256;
             const int gg = (int)(g < 148 * 64 ? g : 148 * 64);
-            if (q.rp)
-                tc_relayout_pk<<<gg, 256, 0, st>>>(in, xr, R, Hin, Win, Wv, pad, d, plane_recs,
-                                                   vrecs, total);
-            else
+            if (q.rp) {
+#define DP_PK32(RR) \
+    tc_relayout_pk<RR><<<gg, 256, 0, st>>>(in, xr, Hin, Win, Wv, pad, d, plane_recs, vrecs, total)
+                switch (R) {
+                    case 1: DP_PK32(1); break;
+                    case 2: DP_PK32(2); break;
+                    case 3: DP_PK32(3); break;
+                    default: DP_PK32(4); break;
+                }
+#undef DP_PK32
+            } else
                 tc_relayout<<<gg, 256, 0, st>>>(in, xr, R, Hin, Win, Wv, pad, q.n_rc, plane_recs,
                                                 vrecs, total);
             rc = check_launch("tc_relayout");

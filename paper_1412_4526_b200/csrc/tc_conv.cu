@@ -168,9 +168,9 @@ __global__ void tc_pack_weights_f16(const float *__restrict__ w, __half *__restr
             j = ks % l, i = (ks / l) % l, c = (ks / (l * l)) * 16 + k;
         }
         float v = 0.f;
-        if (n < Q && c < R && slot_ok)
-            v = bwd ? w[(((long long)c * Q + n) * l + (l - 1 - i)) * l + (l - 1 - j)]
-                    : w[(((long long)n * R + c) * l + i) * l + j];
+        if (n < Q && c < R && slot_ok)  // bwd 1: rotated + offset split, 2: offset split only
+            v = bwd == 1 ? w[(((long long)c * Q + n) * l + (l - 1 - i)) * l + (l - 1 - j)]
+                         : w[(((long long)n * R + c) * l + i) * l + j];
         if (!(fabsf(v) < ptx::F16_SPLIT_MAX)) atomicOr(flag, 1);
         __half hi, lo;
         if (bwd) {

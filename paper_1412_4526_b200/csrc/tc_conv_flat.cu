@@ -120,7 +120,10 @@ struct IntTag {
 // [hi c0-7 | hi c8-15 | lo c0-7 | lo c8-15] (8 halves per 16-byte core-matrix row, the same
 // byte geometry as the tf32 records, so descriptors are unchanged) -- half the record and
 // weight bytes and half the MMAs per channel.  Forward only (bounded activations).
-template <bool STACKED, bool BWD, int RP, bool HALF = false>
+// OFS: a forward with the data gradient's offset split (lo' scaled 2^11, cross products in
+// the second accumulator half): single tap-packed chunks (first layers), whose small inputs
+// would leave an unscaled fp16 lo subnormal
+template <bool STACKED, bool BWD, int RP, bool HALF = false, bool OFS = false>
 __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArgs a) {
     constexpr int TP = RP ? 8 / RP : 1;
     constexpr int CH = HALF ? 16 : 8;  // channels per chunk (one K step per tap)
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                                     uint32_t hw[8], lw2[8];
 #pragma unroll
                                     for (int q = 0; q < 8; ++q) {
-                                        if (BWD)  // deltas: the offset split
+                                        if (BWD || OFS)  // deltas: the offset split
                                             ptx::f16_split2_scaled(v[u][2 * q], v[u][2 * q + 1],
                                                                    hw[q], lw2[q]);
                                         else
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                         for (int mt = 0; mt < MT; ++mt) {
                             const uint64_t ad = a0 + (uint64_t)(mt * 128 + j * step);
                             const uint32_t dd = dbase + (uint32_t)(mt * a.acc_cols);
-                            if (HALF && STACKED && BWD) {
+                            if (HALF && STACKED && (BWD || OFS)) {
                                 // offset split: [hi*hi | hi*lo'] + lo'*hi into the lo' half
                                 ptx::mma_f16_ss(dd, ad, bj, idesc_2n, acc);
                                 ptx::mma_f16_ss(dd + a.Npad, ad + lo_units, bj, idesc_n, 1);
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tc_conv_flat_kernel(const TfArg
                     for (int t = 0; t < 16; ++t) {
                         if (t >= nq) break;
                         float val = __uint_as_float(r[t]);
-                        if (STACKED && HALF && BWD)
+                        if (STACKED && HALF && (BWD || OFS))
                             val += __uint_as_float(r2[t]) * (1.f / ptx::F16_LO_SCALE);
                         else if (STACKED)
                             val += __uint_as_float(r2[t]);
@@ -716,10 +719,11 @@ static bool tf_r32_relayout(const TfPlan &q) {
 // that runs instead when an operand is outside the split's range (|x| >= 2^15, inf, NaN):
 // c4's relu outputs errors exceeded fp16's 65504.
 static bool tf_half(int R, int l, bool bwd, bool f16_ok) {
-    // <= 8 channels: tap-packed, data gradient only by default -- a packed fp16 first layer
-    // gained little (c3 conv1 0.645 -> 0.630 ms, c1 conv1 slower) and its input split (lo
-    // subnormal below |x| = 1/8) doubled the unforced c4 output error and with it the relu /
-    // max-pool flips (dw2 2.1e-4 against the exact tier's 4.5e-5); DP_TF_F16_PACK_FWD=1 opts in
+    // <= 8 channels: tap-packed, data gradient only by default.  A packed fp16 first-layer
+    // forward (DP_TF_F16_PACK_FWD=1; the offset split since round 2 -- the unscaled one left lo
+    // subnormal below |x| = 1/8) is faster (c3 conv1 0.65 -> 0.57 ms, step -1 %), but on the
+    // relu net c4 it moves the unforced dw2 error to 2.3e-4 against the exact tier's 4.5e-5
+    // (relu / max-pool flips amplify any operand rounding), past the 3x parity bar
     if (R < 16 && (R > 8 || getenv("DP_TF_NOPACK") || (!bwd && !getenv("DP_TF_F16_PACK_FWD"))))
         return false;
     // (and >= 5 taps a row: c4's 3x3 8-channel head data gradient measured 0.513 ms in tf32
@@ -778,7 +782,7 @@ size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d
 static int g_tf_sms = 0;
 
 // one launch of plan p (fp16 records when half; TMA-fed from xr when given), weights at wp
-static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, const float *bias,
+static int tf_run(const TfPlan &p, int half, const float *in, const void *wp, const float *bias,
                   float *out, const float *gate, int n, int R, int Hin, int Win, int Q, int Ho,
                   int Wo, int l, int d, int pad, int act, int gate_kind, bool bwd,
                   const unsigned char *xr, long long plane_recs, const int *exit_if,
@@ -844,6 +848,8 @@ static int tf_run(const TfPlan &p, bool half, const float *in, const void *wp, c
     if (half && bwd)
         kern = p.rp ? tc_conv_flat_kernel<true, true, 1, true>
                     : tc_conv_flat_kernel<true, true, 0, true>;
+    else if (half == 2)  // (offset split: stacked only)
+        kern = tc_conv_flat_kernel<true, false, 1, true, true>;
     else if (half && p.rp)
         kern = p.stacked ? tc_conv_flat_kernel<true, false, 1, true>
                          : tc_conv_flat_kernel<false, false, 1, true>;
@@ -923,13 +929,18 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
         const size_t wb16 = p.ok ? al256(tf_weight_bytes(p, l)) : 0;
         const size_t wb32 = al256(tf_weight_bytes(q, l));
         const size_t need = wb16 + wb32 + 256 + (size_t)n * p.n_rc * 4 * plane_recs * 16;
-        if (p.ok && ws_bytes >= need && plane_recs < 0x7fffffffLL) {
+        // (a single packed forward chunk needs the stacked accumulator for its offset split)
+        const bool pk_fwd_ok = bwd || !p.rp || p.n_rc > 1 || p.stacked;
+        if (p.ok && pk_fwd_ok && ws_bytes >= need && plane_recs < 0x7fffffffLL) {
             unsigned char *w8 = (unsigned char *)ws;
             int *flag = (int *)(w8 + wb16 + wb32);
             const unsigned char *xr = w8 + wb16 + wb32 + 256;
             if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess)
                 return set_error(DP_ERR_CUDA, "flat conv: flag reset failed");
-            int rc = tc_pack_f16(w, w8, Q, R, l, bwd ? 1 : 0, flag, st, p.rp);
+            // single tap-packed forward chunk: the offset split too (tf_half)
+            const bool ofs = !bwd && p.rp && p.n_rc == 1 && p.stacked &&
+                             !getenv("DP_TF_F16_PACK_FWD_UNSCALED");
+            int rc = tc_pack_f16(w, w8, Q, R, l, bwd ? 1 : ofs ? 2 : 0, flag, st, p.rp);
             if (rc) return rc;
             const long long vrecs = (long long)(Hin + 2 * pad) * Wv;
             const long long total = (long long)n * p.n_rc * plane_recs;
@@ -970,7 +981,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
         case 7: DP_PK16(S, 7); break;                                                   \
         default: DP_PK16(S, 8); break;                                                  \
     }
-                if (bwd) {
+                if (bwd || ofs) {
                     DP_PK16_R(true)
                 } else {
                     DP_PK16_R(false)
@@ -983,7 +994,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
             if (rc) return rc;
             rc = tc_pack(w, (float *)(w8 + wb16), Q, R, l, bwd ? 1 : 0, q.rp, st);
             if (rc) return rc;
-            rc = tf_run(p, true, in, w8, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d, pad,
+            rc = tf_run(p, ofs ? 2 : 1, in, w8, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo, l, d, pad,
                         act, gate_kind, bwd, xr, plane_recs, flag, nullptr, st);
             if (rc) return rc;
             return tf_run(q, false, in, w8 + wb16, bias, out, gate, n, R, Hin, Win, Q, Ho, Wo,

@@ -141,7 +141,10 @@ int dp_conv_forward_fast(const float *x, const float *wt, const float *b, float 
  * inside the fp16 range (tanh outputs, images), which allows the fp16-split forward (hi =
  * RN_fp16(x), lo = RN_fp16(x - hi), kind::f16, fp32 accumulation: ~2^-22 relative, half the
  * operand feed of 3xTF32).  Without it (and in dp_conv_forward_fast) the forward is 3xTF32. */
-enum dp_fast_flags { DP_FAST_INPUT_FP16_RANGE = 1 };
+/* DP_FAST_PACK_FWD (ABI 6, with DP_FAST_INPUT_FP16_RANGE): <= 8-channel inputs also take the
+ * fp16 offset split (tap-packed) -- faster, slightly larger rounding; the engine sets it when
+ * the conv feeds a tanh (relu nets amplify first-layer rounding into relu / argmax flips) */
+enum dp_fast_flags { DP_FAST_INPUT_FP16_RANGE = 1, DP_FAST_PACK_FWD = 2 };
 int dp_conv_forward_fast_ex(const float *x, const float *wt, const float *b, float *y, int n,
                             int cin, int h, int w, int cout, int k, int d, int nonlin, int flags,
                             void *workspace, size_t workspace_bytes, void *stream);

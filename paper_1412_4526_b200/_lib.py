@@ -22,7 +22,7 @@ DP_IDENTITY, DP_TANH, DP_RELU, DP_TANH_FAST = 0, 1, 2, 3
 DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED = 0, 1, 2, 3
 NONLIN_CODE = {"identity": DP_IDENTITY, "tanh": DP_TANH, "relu": DP_RELU}
 DP_POOL_MAX, DP_POOL_AVG = 0, 1  # enum dp_pool_kind
-DP_FAST_INPUT_FP16_RANGE = 1  # enum dp_fast_flags
+DP_FAST_INPUT_FP16_RANGE, DP_FAST_PACK_FWD = 1, 2  # enum dp_fast_flags
 ABI_VERSION = 6
 
 _vp, _i, _i64, _sz, _d = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double

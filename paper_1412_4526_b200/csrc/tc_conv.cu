@@ -219,7 +219,7 @@ bool tf_conv_supported(int R, int Q, int l, int d);
 size_t tf_relayout_workspace(int n, int R, int Hin, int Win, int Q, int l, int d, int pad,
                              int Ho, int Wo, bool bwd);
 int tf_conv_forward(const float *, const float *, const float *, float *, int, int, int, int, int,
-                    int, int, int, void *, size_t, cudaStream_t, bool f16_ok);
+                    int, int, int, void *, size_t, cudaStream_t, int f16_ok);
 int tf_conv_backward_data(const float *, const float *, float *, int, int, int, int, int, int,
                           int, const float *, int, void *, size_t, cudaStream_t);
 
@@ -849,7 +849,7 @@ int tc_conv_forward(const float *x, const float *w, const float *b, float *y, in
     }
     if (tf_conv_supported(cin, cout, k, d))
         return tf_conv_forward(x, w, b, y, n, cin, h, wd, cout, k, d, act, ws, ws_bytes, st,
-                               f16);
+                               f16 ? (flags & 3) : 0);
     int e = (k - 1) * d + 1;
     return launch_tc(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k, d, 0, act,
                      0, false, ws, ws_bytes, st);

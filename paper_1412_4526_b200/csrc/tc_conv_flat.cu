@@ -718,23 +718,25 @@ static bool tf_r32_relayout(const TfPlan &q) {
 // (DP_TF_HALF_BWD=0: never).  Always TMA-fed and always paired with a tf32 fallback launch
 // that runs instead when an operand is outside the split's range (|x| >= 2^15, inf, NaN):
 // c4's relu outputs errors exceeded fp16's 65504.
-static bool tf_half(int R, int l, bool bwd, bool f16_ok) {
+// f16_ok: DP_FAST_INPUT_FP16_RANGE (1) | DP_FAST_PACK_FWD (2) from the caller
+static bool tf_half(int R, int l, bool bwd, int f16_ok) {
     // <= 8 channels: tap-packed, data gradient only by default.  A packed fp16 first-layer
     // forward (DP_TF_F16_PACK_FWD=1; the offset split since round 2 -- the unscaled one left lo
     // subnormal below |x| = 1/8) is faster (c3 conv1 0.65 -> 0.57 ms, step -1 %), but on the
     // relu net c4 it moves the unforced dw2 error to 2.3e-4 against the exact tier's 4.5e-5
     // (relu / max-pool flips amplify any operand rounding), past the 3x parity bar
-    if (R < 16 && (R > 8 || getenv("DP_TF_NOPACK") || (!bwd && !getenv("DP_TF_F16_PACK_FWD"))))
-        return false;
+    // (the engine sets DP_FAST_PACK_FWD on tanh nets: c3 unforced parity unchanged)
+    const bool pack_fwd = (f16_ok & 2) || getenv("DP_TF_F16_PACK_FWD");
+    if (R < 16 && (R > 8 || getenv("DP_TF_NOPACK") || (!bwd && !pack_fwd))) return false;
     // (and >= 5 taps a row: c4's 3x3 8-channel head data gradient measured 0.513 ms in tf32
     // against 0.553 packed, c3's 7x7 one 1.24 -> 0.94)
     if (R < 16 && bwd && l < 5) return false;
     const char *he = getenv(bwd ? "DP_TF_HALF_BWD" : "DP_TF_HALF");
     if (he && he[0] == '0') return false;
-    return bwd || f16_ok;
+    return bwd || (f16_ok & 1);
 }
 
-static bool tf_relayout_mode(int R, int l, bool bwd, bool f16_ok) {
+static bool tf_relayout_mode(int R, int l, bool bwd, int f16_ok) {
     const char *re = getenv("DP_TF_RELAYOUT");
     return tf_half(R, l, bwd, f16_ok) && !(re && re[0] == '0');
 }
@@ -911,7 +913,7 @@ int tf_fallback(const float *in, const float *w, const float *bias, float *out, 
 static int tf_launch(const float *in, const float *w, const float *bias, float *out,
                      const float *gate, int n, int R, int Hin, int Win, int Q, int Ho, int Wo,
                      int l, int d, int pad, int act, int gate_kind, bool bwd, void *ws,
-                     size_t ws_bytes, cudaStream_t st, bool f16_ok = false) {
+                     size_t ws_bytes, cudaStream_t st, int f16_ok = 0) {
     const int Wv = Win + 2 * pad;
     const long long flat_len = (long long)(Ho - 1) * Wv + Wo;
     // short images: fewer M tiles per CTA tile
@@ -1046,7 +1048,7 @@ static int tf_launch(const float *in, const float *w, const float *bias, float *
 
 int tf_conv_forward(const float *x, const float *w, const float *b, float *y, int n, int cin,
                     int h, int wd, int cout, int k, int d, int act, void *ws, size_t ws_bytes,
-                    cudaStream_t st, bool f16_ok) {
+                    cudaStream_t st, int f16_ok) {
     int e = (k - 1) * d + 1;
     return tf_launch(x, w, b, y, nullptr, n, cin, h, wd, cout, h - e + 1, wd - e + 1, k, d, 0, act,
                      0, false, ws, ws_bytes, st, f16_ok);

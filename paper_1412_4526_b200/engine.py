@@ -141,12 +141,15 @@ class ops:
         return int(_lib_dev().dp_conv_backward_data_fast_workspace(n, co, ho, wo, ci, k, d))
 
     @staticmethod
-    def conv_forward_fast(x, w, b, y, k, d, nonlin, ws, fp16_range=False):
+    def conv_forward_fast(x, w, b, y, k, d, nonlin, ws, fp16_range=False, pack_fwd=False):
         """fp16_range: the caller vouches |x| stays well inside fp16 range (tanh outputs,
-        images) -- allows the fp16-split forward (DP_FAST_INPUT_FP16_RANGE)."""
+        images) -- allows the fp16-split forward (DP_FAST_INPUT_FP16_RANGE); pack_fwd: also for
+        <= 8-channel inputs (DP_FAST_PACK_FWD, offset split)."""
         with _Rec('conv_forward_tc', 2, 'tensor', 2 * y.numel() * x.shape[1] * k * k):
             n, ci, h, wd = x.shape
             flags = _lib.DP_FAST_INPUT_FP16_RANGE if fp16_range else 0
+            if fp16_range and pack_fwd:
+                flags |= _lib.DP_FAST_PACK_FWD
             _lib.check(_lib_dev().dp_conv_forward_fast_ex(
                 _ptr(x), _ptr(w), _ptr(b), _ptr(y), n, ci, h, wd, w.shape[0], k, d, nonlin,
                 flags, _ptr(ws), ws.numel() * ws.element_size(), _stream()),
@@ -669,9 +672,10 @@ class DenseNet:
                 # fp16-split (3 passes, tf32 fallback launch when an operand leaves fp16's
                 # range): inputs of >= 16 channels declared in range; deltas of >= 16
                 # channels, or <= 8 tap-packed at >= 5 taps a row (tc_conv_flat.cu tf_half)
-                f16f = ci >= 16 and self._fp16_input(gi)
+                f16f = (ci >= 16 or (ci <= 8 and self._feeds_tanh(gi))) and self._fp16_input(gi)
                 f16b = co >= 16 or (co <= 8 and kk >= 5)
-                fwd = ("tcgen05-fp16x3" if f16f else "tcgen05-3xtf32") if f_ok else "exact"
+                fwd = ("tcgen05-3xtf32" if not f16f else "tcgen05-fp16x3-offset" if ci <= 8
+                       else "tcgen05-fp16x3") if f_ok else "exact"
                 dg = ("tcgen05-fp16x3-offset" if f16b else "tcgen05-3xtf32") if b_ok else "exact"
                 if gi == 0:
                     dg = "not needed"  # layer 0's input delta is not computed (backward.py:208)
@@ -705,6 +709,22 @@ class DenseNet:
         if prev.act == "tanh":
             return True
         return isinstance(prev.op, NonlinLayerSpec) and prev.op.kind == "tanh"
+
+    def _feeds_tanh(self, gi):
+        """Does conv group gi's output reach a tanh before any other nonlinearity (directly,
+        or through pools)?  Then its <= 8-channel input may take the fp16 offset split
+        (DP_FAST_PACK_FWD): on relu nets the extra rounding turned into relu / argmax flips
+        past the parity bar (c4), on tanh nets it did not (c3)."""
+        if os.environ.get("DP_NO_PACK_FWD"):
+            return False
+        for g in self.groups[gi:]:
+            if g.act != "identity":
+                return g.act == "tanh"
+            if isinstance(g.op, NonlinLayerSpec):
+                return g.op.kind == "tanh"
+            if g is not self.groups[gi] and isinstance(g.op, DilatedConv):
+                return False
+        return False
 
     def _view(self, buf, shape):
         n = int(np.prod(shape))
@@ -754,7 +774,8 @@ class DenseNet:
                 wt, b = self.params[g.first]
                 if self.tc.get(gi, (False, False))[0]:
                     ops.conv_forward_fast(x, wt, b, y, op.base.kernel_size, op.dilation, act,
-                                          self._tc_ws, fp16_range=self._fp16_input(gi))
+                                          self._tc_ws, fp16_range=self._fp16_input(gi),
+                                          pack_fwd=self._feeds_tanh(gi))
                 else:
                     ops.conv_forward(x, wt, b, y, op.base.kernel_size, op.dilation, act)
             elif isinstance(op, DilatedPool):

@@ -9,7 +9,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 2 --warmup 3 $ARGS > $OUT/ncu_launch.log 2>&1
 # warm-up steps are eager too: skip the first steps' launches of our kernels
 timeout 1500 ncu --set full --clock-control none --import-source on \
-   -k "regex:tc_conv|tc_wgrad|maxpool|tc_stage|tc_relayout|mask" -s 40 -c 30 \
+   -k "regex:tc_conv|tc_wgrad|maxpool|tc_stage|tc_relayout|mask" -s 40 -c 31 \
    -o $OUT/full_step python bench.py --steps 1 --warmup 3 $ARGS > $OUT/ncu_full.log 2>&1
 ncu -i $OUT/full_step.ncu-rep --page raw --csv > $OUT/full_step_raw.csv 2>/dev/null
 python tools/step_traffic.py $OUT/full_step.ncu-rep $OUT/traffic_c3.json $OUT/ncu_c3.md \

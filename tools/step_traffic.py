@@ -16,26 +16,28 @@ import sys
 # reductions are outside the capture's kernel filter, an fp16-split layer's tf32 fallback
 # launch (which exits at once) is inside.  The capture starts anywhere in a step; the
 # sequence is matched cyclically against it.
-SEQ = [("tc_relayout_pk", "00:conv_forward_tc"), ("tc_conv_flat_kernel<1, 0, 3", "00:conv_forward_tc"),
+SEQ = [("tc_relayout_f16_pk<1, 3", "00:conv_forward_tc"),
+       ("tc_conv_flat_kernel<1, 0, 1, 1, 1>", "00:conv_forward_tc"),
+       ("tc_conv_flat_kernel<1, 0, 3, 0, 0>", "00:conv_forward_tc"),
        ("maxpool_fwd_stream", "01:maxpool_forward"),
        ("tc_relayout_f16<0>", "02:conv_forward_tc"), ("tc_relayout_f16_pk<0,", "02:conv_forward_tc"),
-       ("tc_conv_flat_kernel<0, 0, 1, 1>", "02:conv_forward_tc"),
-       ("tc_conv_flat_kernel<0, 0, 0, 0>", "02:conv_forward_tc"),
+       ("tc_conv_flat_kernel<0, 0, 1, 1, 0>", "02:conv_forward_tc"),
+       ("tc_conv_flat_kernel<0, 0, 0, 0, 0>", "02:conv_forward_tc"),
        ("maxpool_fwd_stream", "03:maxpool_forward"),
        ("tc_relayout_f16<0>", "04:conv_forward_tc"), ("tc_conv_tap_kernel<0, 1>", "04:conv_forward_tc"),
-       ("tc_conv_flat_kernel<1, 0, 0, 0>", "04:conv_forward_tc"),
+       ("tc_conv_flat_kernel<1, 0, 0, 0, 0>", "04:conv_forward_tc"),
        ("mask_delta", "05:mask_delta"), ("tc_stage_dy16", "06:conv_backward_kernel_tc"),
        ("tc_wgrad_ss", "06:conv_backward_kernel_tc"),
        # the fp16 weight gradient's gated tf32 fallback (dy staging, kernel: exit at once)
        ("tc_stage_dy", "06:conv_backward_kernel_tc"), ("tc_wgrad_ss", "06:conv_backward_kernel_tc"),
        ("tc_relayout_f16_pk<1,", "07:conv_backward_data_tc"),
-       ("tc_conv_flat_kernel<1, 1, 1, 1>", "07:conv_backward_data_tc"),
-       ("tc_conv_flat_kernel<1, 1, 0, 0>", "07:conv_backward_data_tc"),
+       ("tc_conv_flat_kernel<1, 1, 1, 1, 0>", "07:conv_backward_data_tc"),
+       ("tc_conv_flat_kernel<1, 1, 0, 0, 0>", "07:conv_backward_data_tc"),
        ("maxpool_bwd_stream", "08:maxpool_backward"), ("tc_wgrad_ss", "09:conv_backward_kernel_tc"),
        ("tc_relayout_f16<1>", "10:conv_backward_data_tc"),
        ("tc_relayout_f16_pk<1,", "10:conv_backward_data_tc"),
-       ("tc_conv_flat_kernel<1, 1, 1, 1>", "10:conv_backward_data_tc"),
-       ("tc_conv_flat_kernel<0, 1, 0, 0>", "10:conv_backward_data_tc"),
+       ("tc_conv_flat_kernel<1, 1, 1, 1, 0>", "10:conv_backward_data_tc"),
+       ("tc_conv_flat_kernel<0, 1, 0, 0, 0>", "10:conv_backward_data_tc"),
        ("maxpool_bwd_stream", "11:maxpool_backward"), ("tc_stage_x_taps", "12:conv_backward_kernel_tc"),
        ("tc_wgrad_ss", "12:conv_backward_kernel_tc")]
 

@@ -579,3 +579,38 @@ def test_maxpool_forward_split(shape):
     torch.cuda.synchronize()
     assert torch.equal(y1, y2) and torch.equal(a1, a2)
     assert torch.equal(hi[..., :wo], hr[..., :wo]) and torch.equal(lo[..., :wo], lr[..., :wo])
+
+
+def test_fp16_split_and_weight_gradient_errors():
+    """The ABI-6 entry points fail loudly (DP_ERR_ARG -> ValueError) on bad layouts instead of
+    computing garbage."""
+    import torch
+    from paper_1412_4526_b200.engine import SLACK_BYTES, _slack_zeros, ops
+    x = torch.rand((1, 8, 40, 48), device="cuda")
+    kw16 = {"dtype": torch.float16, "device": "cuda"}
+    bad = torch.zeros((1, 8, 40, 50), **kw16)  # pitch 50: not a multiple of 8 halves
+    with pytest.raises(ValueError, match="pitch"):
+        ops.split_f16(x, bad, bad.clone())
+    short = torch.zeros((1, 8, 40, 40), **kw16)  # pitch < width
+    with pytest.raises(ValueError, match="pitch"):
+        ops.split_f16(x, short, short.clone())
+    # fp16 weight gradient: a workspace one byte short, then an unsupported dy pitch
+    co, k, d = 16, 3, 8
+    nb = ops.wgrad_f16_workspace(x, co, k, d)
+    assert nb > 0
+    xh, xl = _slack_zeros((1, 8, 40, 48), kw16), _slack_zeros((1, 8, 40, 48), kw16)
+    ops.split_f16(x, xh, xl)
+    dy = torch.rand((1, co, 40 - 16, 48 - 16), device="cuda")
+    dw = torch.empty((co, 8, k, k), device="cuda")
+    db = torch.empty((co,), device="cuda")
+    ws = torch.empty(nb - 1, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="workspace"):
+        ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, SLACK_BYTES)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="pitch"):
+        ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, SLACK_BYTES,
+                                          dy_pitch=3)
+    # and the good call still works after the errors
+    ops.conv_backward_kernel_fast_f16(x, xh, xl, dy, dw, db, k, d, ws, SLACK_BYTES)
+    torch.cuda.synchronize()
+    assert torch.isfinite(dw).all()

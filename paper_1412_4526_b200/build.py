@@ -40,6 +40,8 @@ def _flags(ptxas_verbose: bool):
                 "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if ptxas_verbose:
         f += ["-Xptxas", "-v"]
+    # experiments: extra nvcc flags (e.g. -DDP_MS_NBF=3); a forced rebuild picks them up
+    f += os.environ.get("DP_NVCC_EXTRA", "").split()
     return f
 
 

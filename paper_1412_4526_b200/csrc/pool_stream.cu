@@ -30,7 +30,10 @@ namespace dp {
 
 // staged rows in flight per warp (powers of two): occupancy, not prefetch depth, set the pace
 // (c3 pool1 fwd 679 / 650 / 648 us and pool2 bwd 638 / 603 / 587 us at 8 / 4 / 2 rows)
-constexpr int MS_NBF = 4;    // forward
+#ifndef DP_MS_NBF
+#define DP_MS_NBF 4
+#endif
+constexpr int MS_NBF = DP_MS_NBF;  // forward (DP_NVCC_EXTRA=-DDP_MS_NBF=<n>: experiments)
 constexpr int MS_NBB = 2;    // backward
 constexpr int MS_RS = 64;    // output (forward) / pixel (backward) rows per work item
 constexpr int MS_WARPS = 4;  // independent warps per CTA

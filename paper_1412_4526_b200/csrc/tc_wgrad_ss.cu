@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
     ws_reduce(const float *__restrict__ part, const float *__restrict__ pdb, float *__restrict__ dw,
               float *__restrict__ db, int Q, int C, int l, int Ls, int Npad, int J, int Ja,
               int splits, int rows_pad, WsResidues rs, const int *exit_if,
-              const int *exit_unless) {
+              const int *exit_unless, int ilv) {
     if ((exit_if && *(volatile const int *)exit_if) ||
         (exit_unless && !*(volatile const int *)exit_unless))
         return;
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
                 c = off / rs.n[rb];
                 const int jj = off - c * rs.n[rb];
                 const int ja = rs.tapcopy ? jj : rs.j0[rb] + jj * rs.step;
-                j = jb * Ja + ja;  // >= l: padding tap of the last column group
+                j = ilv ? ja * J + jb : jb * Ja + ja;  // >= l: a padding tap
                 if (rb == 0 && jj >= rs.nreal0) j = l;  // box-padding tap line
             }
         }
@@ -662,6 +662,8 @@ __global__ void __launch_bounds__(32 * WR_GROUPS)
 // --------------------------------------------------------------------------------
 struct WsPlan {
     int pair, direct, f16;
+    int ilv;  // fp16 interleaved taps: j = ja*J + jb, x taps J*d apart, J staged dy copies
+              // shifted by jb*d (copies, not an overlapping view: d*2 bytes is no 16-byte step)
     int J, kc, dc, sb, NB;  // J dy copies (B), kc = Ja column taps in the x lines (A), step dc = d
     int Cpad, Npad, Ls, n_tiles, G, n_groups, splits, SS, R, NM, max_ni;
     int ho, wo, nvb, T, wp_x, wp_dy, lm_dy, mask;
@@ -735,6 +737,20 @@ static bool ws_plan(int n, int cin, int hi, int wi, int cout, int k, int d, WsPl
             ok = true;
         }
     }
+    // fp16 with tap offsets in two or more 16-byte classes (c3 conv2: d = 4): the interleaved
+    // mode instead -- x taps J*d apart (one class, in place), J dy copies shifted by jb*d.
+    // Opt-in (DP_WG_F16_ILV=1): c3 conv2 measured 2.66 ms against 1.86 on 3xTF32 (224 TMEM
+    // columns per tile leave 2-tile groups, so every K block is fed twice, plus J staging passes)
+    if (f16 && (!ok || p.rs.n_b > 1 || p.rs.tapcopy) && getenv("DP_WG_F16_ILV")) {
+        int g = 8;
+        while (d % g) g >>= 1;
+        WsPlan q;
+        if (8 / g >= 2 && ws_plan_j(n, cin, hi, wi, cout, k, d, -(8 / g), q, f16) &&
+            q.rs.n_b == 1 && !q.rs.tapcopy) {
+            p = q;
+            ok = true;
+        }
+    }
     return ok;
 }
 
@@ -753,15 +769,21 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     if (p.ho < 1 || p.wo < 1 || k > 64) return false;
     p.Npad = (cout + 15) / 16 * 16;
     if (p.Npad > 128) return false;
+    // Ja < 0: the fp16 interleaved mode with J = -Ja dy copies (ws_plan)
+    p.ilv = Ja < 0 ? 1 : 0;
+    if (p.ilv) {
+        if (!f16 || -Ja < 2 || -Ja > k) return false;
+        Ja = (k + (-Ja) - 1) / (-Ja);  // x taps per group
+    }
     if (Ja < 1 || Ja > k) return false;
     const int J = (k + Ja - 1) / Ja;
     p.J = J;
     p.NB = (J * cout + 15) / 16 * 16;
     if (2 * p.NB > 256) return false;
     p.kc = Ja;
-    p.dc = d;
-    p.sb = p.kc * d;
-    if (J > 1 && (p.sb & (f16 ? 7 : 3))) return false;
+    p.dc = p.ilv ? J * d : d;  // column step between the x lines' taps
+    p.sb = p.ilv ? d : p.kc * d;
+    if (J > 1 && !p.ilv && (p.sb & (f16 ? 7 : 3))) return false;
     const int kc = p.kc, dc = p.dc;
     const int RM = f16 ? 8 : 4;  // residue modulus: elements per 16 bytes
     p.Cpad = (cin + 7) / 8 * 8;
@@ -898,6 +920,7 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     // to the last K block's reach, so the overlapping-view box never leaves the row
     p.lm_dy = (J - 1) * p.sb;
     p.wp_dy = J > 1 ? p.nvb * KB + p.lm_dy : (f16 ? (p.wo + 7) / 8 * 8 : (p.wo + 3) / 4 * 4);
+    if (p.ilv) p.wp_dy = (p.wp_dy + 7) / 8 * 8;  // (margins of d halves: keep 16-byte rows)
     p.stage_dy = f16 || J > 1 || p.wp_dy != p.wo;
     if ((long long)n * hi > (1LL << 31)) return false;
     p.part_bytes = ws_align256((size_t)p.splits * p.n_tiles * 128 * p.NB * 4);
@@ -908,7 +931,7 @@ static bool ws_plan_j(int n, int cin, int hi, int wi, int cout, int k, int d, in
     p.x_bytes = f16 ? 0 : (size_t)(p.rs.tapcopy ? kc : p.rs.n_b) * p.copy_bytes;
     // f16: dy staged as two fp16 tensors (hi, lo')
     p.dy_bytes = !p.stage_dy ? 0
-                 : f16 ? 2 * ws_align256((size_t)n * cout * p.ho * p.wp_dy * 2)
+                 : f16 ? 2 * (p.ilv ? J : 1) * ws_align256((size_t)n * cout * p.ho * p.wp_dy * 2)
                        : ws_align256((size_t)n * cout * p.ho * p.wp_dy * 4);
     p.total_bytes = p.part_bytes + p.pdb_bytes + p.x_bytes + p.dy_bytes;
     return true;
@@ -1102,7 +1125,7 @@ int ws_conv_backward_kernel(const float *x, const float *dy, float *dw, float *d
     const long long total = (long long)k * p.Ls * p.NB + cout;
     ws_reduce<<<ceil_div(total, 32), 32 * WR_GROUPS, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
                                                     p.Npad, p.J, p.kc, p.splits, p.n_tiles * 128,
-                                                    p.rs, nullptr, exit_unless);
+                                                    p.rs, nullptr, exit_unless, 0);
     return check_launch("ws_reduce");
 }
 
@@ -1122,7 +1145,8 @@ static bool ws_f16_inplace(const WsPlan &p) {
 static size_t ws_f16_overrun(const WsPlan &p, int d) {  // bytes the tap views read past x
     size_t m = 0;
     for (int rb = 0; rb < p.rs.n_b; ++rb)
-        m = std::max(m, (size_t)(p.rs.n[rb] - 1) * p.rs.step * d);
+        m = std::max(m, (size_t)(p.rs.n[rb] - 1) * p.rs.step * p.dc);
+    (void)d;
     return (m + 64) * 2;
 }
 
@@ -1174,8 +1198,20 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
     unsigned char *dhi = w8 + p.part_bytes + p.pdb_bytes;
     unsigned char *dlo = dhi + p.dy_bytes / 2;
     const int pitch = dy_pitch > 0 ? dy_pitch : p.wo;
-    int rc = wg_stage_dy16(dy, dhi, dlo, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st, pitch, flag);
-    if (rc) return rc;
+    int rc = DP_OK;
+    const size_t copyb = ws_align256((size_t)n * cout * p.ho * p.wp_dy * 2);
+    if (p.ilv) {
+        // interleaved taps: J dy copies, copy jb' = dy shifted right by (J-1-jb') d (the
+        // rows jb'*Q + o of B, as the overlapping view would give them)
+        for (int jb = 0; jb < p.J; ++jb) {
+            rc = wg_stage_dy16(dy, dhi + jb * copyb, dlo + jb * copyb, n, cout, p.ho, p.wo,
+                               p.wp_dy, (p.J - 1 - jb) * p.sb, st, pitch, flag);
+            if (rc) return rc;
+        }
+    } else {
+        rc = wg_stage_dy16(dy, dhi, dlo, n, cout, p.ho, p.wo, p.wp_dy, p.lm_dy, st, pitch, flag);
+        if (rc) return rc;
+    }
     CUtensorMap mx[4], mdy, mdyl;
     const cuuint64_t rowb = (cuuint64_t)p.wp_dy * 2;
     for (int hl = 0; hl < 2; ++hl) {
@@ -1189,7 +1225,9 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
         } else {
             cuuint64_t dims[5] = {(cuuint64_t)p.wp_dy, (cuuint64_t)cout, (cuuint64_t)p.J,
                                   (cuuint64_t)p.ho, (cuuint64_t)n};
-            cuuint64_t str[4] = {rowb, (cuuint64_t)p.sb * 2, rowb * cout, rowb * cout * p.ho};
+            // (interleaved taps: the J copies, copyb apart; else the overlapping view)
+            cuuint64_t str[4] = {rowb, p.ilv ? (cuuint64_t)copyb : (cuuint64_t)p.sb * 2,
+                                 rowb * cout, rowb * cout * p.ho};
             cuuint32_t box[5] = {64, (cuuint32_t)cout, (cuuint32_t)p.J, 1, 1};
             rc = wg_make_map16(m, base, 5, dims, str, box);
         }
@@ -1198,7 +1236,7 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
     // one box for both halves when J*Q is a multiple of 8 (the stacked MMA's N = 2 J Q then a
     // multiple of 16): the staged rows (n, h) fold into one dimension, the hi -> lo' distance
     // is a fifth (DP_WG_DY2BOX=1: two boxes)
-    const int dycomb = ((p.J * cout) % 8 == 0 && !getenv("DP_WG_DY2BOX")) ? 1 : 0;
+    const int dycomb = (!p.ilv && (p.J * cout) % 8 == 0 && !getenv("DP_WG_DY2BOX")) ? 1 : 0;
     if (dycomb) {
         const cuuint64_t hlb = (cuuint64_t)((unsigned char *)dlo - (unsigned char *)dhi);
         const cuuint64_t rows = (cuuint64_t)n * p.ho;
@@ -1286,7 +1324,7 @@ int ws_conv_backward_kernel_f16(const float *x, size_t x_slack, const void *x_hi
     const long long total = (long long)k * p.Ls * p.NB + cout;
     ws_reduce<<<ceil_div(total, 32), 32 * WR_GROUPS, 0, st>>>(a.part, a.pdb, dw, db, cout, cin, k, p.Ls,
                                                     p.Npad, p.J, p.kc, p.splits, p.n_tiles * 128,
-                                                    p.rs, flag, nullptr);
+                                                    p.rs, flag, nullptr, p.ilv);
     rc = check_launch("ws_reduce");
     if (rc) return rc;
     // the tf32 fallback, every launch gated on the flag

@@ -302,15 +302,20 @@ def _f16_case(shape, seed):
 
 
 @pytest.mark.parametrize("scale", [1.0, 1e-3, 1e4])
-@pytest.mark.parametrize("kernel", ["ss", "ss_j1", "ss_j2", "ss_j3"])
+@pytest.mark.parametrize("kernel", ["ss", "ss_j1", "ss_j2", "ss_j3", "ilv"])
 @pytest.mark.parametrize("shape", F16_WGRAD_SHAPES)
 def test_tc_weight_gradient_fp16_split(shape, kernel, scale, force_env, monkeypatch):
     """dp_conv_backward_kernel_fast_f16 (x pre-split by dp_split_f16, dy split on the device,
     kind::f16 offset-split MMAs) vs the fp64 exact tier: tighter than the tf32 kernel's bound
     (fp16's 11-bit hi), deterministic, at dy magnitudes across the guarded range.  Two-residue
-    shapes (shifted copies) are opt-in in production (DP_WG_F16_RES2) and enabled here."""
+    shapes (shifted copies) are opt-in in production (DP_WG_F16_RES2) and enabled here;
+    kernel "ilv": the same layouts through interleaved taps + dy copies (DP_WG_F16_ILV)."""
     monkeypatch.setenv("DP_WG_F16_RES2", "1")
-    force_env(kernel)
+    if kernel == "ilv":
+        monkeypatch.setenv("DP_WG_F16_ILV", "1")
+        monkeypatch.delenv("DP_WG_F16_RES2")
+    else:
+        force_env(kernel)
     import torch
     from paper_1412_4526_b200.engine import ops
     n, ci, co, k, d, h, w = shape
